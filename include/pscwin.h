@@ -1,0 +1,160 @@
+/* pscwin.h — C ABI of libpscwin.so, the B200 (sm_100a) PSCWin layer of HRSAM (arXiv 2407.02109).
+ *
+ * Citations: P:Lx = PAPER.md line x (section / equation alongside); Qn = reading n in DESIGN.md "Readings".
+ *
+ * Conventions for every call below
+ *   - Tensor pointers are DEVICE pointers unless the argument says "host". They are row-major, contiguous,
+ *     16-byte aligned (TMA requirement; violations return PSCWIN_ERR_ALIGN) and owned by the caller.
+ *     The library never allocates device memory inside these calls; scratch comes from a caller-provided
+ *     workspace sized by the matching *_workspace_bytes() function.
+ *   - `stream` is a cudaStream_t passed as void*. Calls enqueue work on it and return immediately;
+ *     argument/contract validation is synchronous. A launch failure returns PSCWIN_ERR_CUDA; a fault inside a
+ *     kernel surfaces later through pscwin_last_async_error() or the next call.
+ *   - No exceptions or C++ types cross the boundary. Calls are reentrant; the only global state is a cached
+ *     SM count and per-kernel attribute flags.
+ *   - dtype PSCWIN_BF16: activations and GEMM weights are bf16; LayerNorm parameters, biases, conv, dt_proj,
+ *     A_log, D_skip are f32. PSCWIN_F32 (all f32) is accepted by the partition / merge / layer-norm calls;
+ *     the fused layer and attention calls currently require PSCWIN_BF16 (PSCWIN_ERR_UNSUPPORTED otherwise).
+ */
+#ifndef PSCWIN_H_
+#define PSCWIN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PSCWIN_OK = 0,
+  PSCWIN_ERR_SHAPE = 1,       /* non-positive or inconsistent sizes */
+  PSCWIN_ERR_CONTRACT = 2,    /* violates the layer's definition (see each call) */
+  PSCWIN_ERR_ALIGN = 3,       /* pointer not 16-byte aligned */
+  PSCWIN_ERR_WORKSPACE = 4,   /* workspace missing or too small */
+  PSCWIN_ERR_CUDA = 5,        /* CUDA launch / driver error */
+  PSCWIN_ERR_UNSUPPORTED = 6  /* valid per the paper but not implemented on this path (e.g. d_head 128) */
+} pscwin_status;
+
+typedef enum { PSCWIN_BF16 = 0, PSCWIN_F32 = 1 } pscwin_dtype;
+/* Q5: LEARNABLE = the paper's Pad Swin (pad slots hold the projected learnable token p);
+ *     MASKED = pad keys get -inf logits (= vanilla shifted windows of different sizes). */
+typedef enum { PSCWIN_PAD_LEARNABLE = 0, PSCWIN_PAD_MASKED = 1 } pscwin_pad_mode;
+/* Q13: order in which the cycle scan walks the token grid (row-major raster by default). */
+typedef enum { PSCWIN_SCAN_ROW_MAJOR = 0, PSCWIN_SCAN_COL_MAJOR = 1, PSCWIN_SCAN_WINDOW_MAJOR = 2 } pscwin_scan_order;
+/* Q11: B_bar rule. ZOH = Eq. 3 B_bar = (e^{Delta A} - 1)/A * B;  EULER = Delta * B. */
+typedef enum { PSCWIN_BBAR_ZOH = 0, PSCWIN_BBAR_EULER = 1 } pscwin_bbar_mode;
+
+/* One PSCWin layer. Token grid H x W = image / 16. */
+typedef struct {
+  int32_t B, H, W, C, heads;          /* d_head = C / heads; d_head in {32, 64} on this path          */
+  int32_t window;                     /* w; power of two in [4, 64]                            */
+  int32_t shift_x, shift_y;           /* in [0, w); (0,0) = plain window attention (Q7)          */
+  int32_t pad_mode;                   /* pscwin_pad_mode                                                */
+  int32_t rope;                       /* 0 off, 1 axial 2-D RoPE base 10000 on q,k (Q6)         */
+  int32_t cycle_scan;                 /* 1: run the cycle-scan module before attention     */
+  int32_t ssm_state;                  /* N (32); N <= 64                                        */
+  int32_t ssm_expand;                 /* E, D = E*C (Mamba default 2, Q9)                              */
+  int32_t ssm_dt_rank;                /* R; 0 => ceil(C/16)                                              */
+  int32_t ssm_conv;                   /* causal depthwise conv width k (Mamba default 4, Q9)            */
+  int32_t scan_order;                 /* pscwin_scan_order (row-major only on this path)                */
+  int32_t bbar_mode;                  /* pscwin_bbar_mode                                               */
+  int32_t dtype;                      /* pscwin_dtype                                                   */
+  float ln_eps;                       /* LayerNorm eps (Q15: 1e-6)                                      */
+} pscwin_layer_desc;
+
+/* Weights of one layer. Linear weights are nn.Linear-style [out, in], bf16 (dtype BF16).
+ * Attention (a4-a7): ln1_g, ln1_b [C] f32; w_qkv [3C, C]; b_qkv [3C] f32 (Q = rows [0,C), K = [C,2C),
+ * V = [2C,3C), head-contiguous, Q3); pad [C] = learnable pad token p; w_o [C, C]; b_o [C] f32.
+ * Cycle scan (a1-a3, Mamba-1 block, Q9): lns_g, lns_b [C] f32; w_in [2D, C] (x-branch rows [0,D), z rows
+ * [D,2D)); conv_w [D, k] f32; conv_b [D] f32; w_x [R+2N, D] (delta_low, B, C); w_dt [D, R] f32; b_dt [D] f32;
+ * a_log [D, N] f32 (A = -exp(a_log)); d_skip [D] f32; w_out [C, D]. Unused pointers may be NULL. */
+typedef struct {
+  const void *ln1_g, *ln1_b, *w_qkv, *b_qkv, *pad, *w_o, *b_o;
+  const void *lns_g, *lns_b, *w_in, *conv_w, *conv_b, *w_x, *w_dt, *b_dt, *w_out;
+  const float *a_log, *d_skip;
+} pscwin_layer_weights;
+
+/* ------------------------------------------------------------------------------------------------ info */
+const char* pscwin_version(void);
+const char* pscwin_status_string(int status);
+/* Returns PSCWIN_ERR_CUDA if an asynchronous kernel fault is pending on the device (cudaGetLastError /
+ * cudaPeekAtLastError), else PSCWIN_OK. */
+int pscwin_last_async_error(void);
+
+/* ------------------------------------------------------------------------------- a5: window geometry */
+/* Number of windows per image. Plain (sx = sy = 0): H, W must be divisible by w else
+ * ERR_CONTRACT. Shifted: pad left/top = (w - s) mod w (Q7), right/bottom minimal. */
+int pscwin_window_count(int32_t H, int32_t W, int32_t window, int32_t shift_x, int32_t shift_y,
+                        int32_t* n_windows /* host, out */);
+/* Host-side index map (App. C): for destination slot s = win*w*w + iy*w + ix (windows
+ * row-major over (wy,wx), Q4) the source token y*W + x, or 0xFFFFFFFF (PAD) outside the grid.
+ * host_map must hold n_windows*w*w entries. Pure host computation; no GPU needed. */
+int pscwin_index_map(int32_t H, int32_t W, int32_t window, int32_t shift_x, int32_t shift_y, uint32_t* host_map);
+
+/* Plain window partition F -> F_w: x [B,H,W,Cx] -> out [B*nW, w*w, Cx]. Bit-exact copy. */
+int pscwin_window_partition(const void* x, int32_t B, int32_t H, int32_t W, int32_t Cx, int32_t window,
+                            int32_t dtype, void* out, void* stream);
+/* Padding-shifted partition: out [B*nWp, w*w, Cx]; pad slots receive pad_row [Cx]
+ * (required: ERR_CONTRACT if NULL and the layout has pad slots). Bit-exact copy. */
+int pscwin_shifted_pad_partition(const void* x, const void* pad_row, int32_t B, int32_t H, int32_t W, int32_t Cx,
+                                 int32_t window, int32_t shift_x, int32_t shift_y, int32_t dtype, void* out,
+                                 void* stream);
+/* Merge / crop / un-shift ("paddings are discarded"): out[b,y,x] = win[b, window(y,x), slot(y,x)]
+ * (+ residual[b,y,x] when residual != NULL, added in f32 and rounded once). win [B*nW, w*w, Cx]. */
+int pscwin_window_merge(const void* win, int32_t B, int32_t H, int32_t W, int32_t Cx, int32_t window,
+                        int32_t shift_x, int32_t shift_y, const void* residual, int32_t dtype, void* out,
+                        void* stream);
+
+/* ---------------------------------------------------------------------------------- step entry points */
+/* LayerNorm over the last axis (Q15): out = (x - mean)/sqrt(var + eps) * g + b. x, out [rows, C]. */
+int pscwin_layer_norm(const void* x, int64_t rows, int32_t C, const float* g, const float* b, float eps,
+                      int32_t dtype, void* out, void* stream);
+/* out[M, N] = A[M, K] . Wt[N, K]^T (+ bias[N]) (+ residual[M, N]); bf16 in, f32 accumulate on tcgen05,
+ * out bf16 (out_f32 = 0) or f32 (out_f32 = 1, no residual). K % 8 == 0. (Projection step of a1/a3/a4/a7.) */
+int pscwin_linear(const void* A, int64_t M, int32_t K, const void* Wt, int32_t N, const float* bias,
+                  const void* residual, int32_t out_f32, void* out, void* stream);
+/* a4: u = LN1(x); qkv = u W_qkv^T + b_qkv with 2-D RoPE applied to q and k at each token's grid coordinate
+ * (Q6) -> qkv [B,H,W,3C] bf16; qkv_pad = p W_qkv^T + b_qkv [3C] f32 (unrotated).
+ * Workspace: pscwin_workspace_bytes(desc). */
+int pscwin_qkv_project(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x, void* qkv,
+                       float* qkv_pad, void* workspace, size_t ws_bytes, void* stream);
+/* a5 + a6 + crop: window attention core. qkv [B,H,W,3C] bf16 (q,k already rotated), qkv_pad [3C] f32
+ * (required for shifted LEARNABLE layers, else may be NULL) -> O [B,H,W,C] bf16, heads contiguous.
+ * Softmax over all w^2 slots (LEARNABLE) or over real slots only (MASKED). Pad query rows never written.
+ * Workspace: pscwin_workspace_bytes(desc). */
+int pscwin_window_attention(const pscwin_layer_desc* desc, const void* qkv, const float* qkv_pad, void* O,
+                            void* workspace, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------------ a2: the cycle scan */
+typedef struct {
+  int32_t B, H, W;             /* L = H*W tokens per image, walked in scan_order                        */
+  int32_t D, N, R, conv_k;     /* channels, SSM state (N <= 64), dt rank, conv width (L >= conv_k - 1)   */
+  int32_t scan_order, bbar_mode, dtype;
+} pscwin_scan_desc;
+/* Cycle scan: per image the token sequence (in scan order) is repeated three times, the Mamba
+ * selective SSM (block internals Q9) scans the 3L sequence, the three output segments are summed:
+ *   v = SiLU(causal_conv(xin)) over the cycled sequence (copy 1 sees zero history, copies 2-3 the tail, Q10)
+ *   (delta_low, B, C) = v W_x^T;  Delta = softplus(delta_low W_dt^T + b_dt);  A = -exp(a_log)
+ *   h_j = exp(Delta A) h_{j-1} + B_bar v_j (Eq. 3-4);  y_j = C_j . h_j + d_skip * v_j
+ *   out_t = sum_{c=0..2} y_{cL+t} * SiLU(z_t)   (no gate when z == NULL)
+ * xin, z, out [B, L, D] bf16 in grid (row-major token) order. Computed exactly (up to rounding) by a
+ * two-pass chunked closed form. Workspace: pscwin_scan_workspace_bytes. */
+int pscwin_cycle_scan(const pscwin_scan_desc* desc, const void* xin, const void* z, const float* conv_w,
+                      const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
+                      const float* a_log, const float* d_skip, void* out, void* workspace, size_t ws_bytes,
+                      void* stream);
+size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* desc);
+
+/* ----------------------------------------------------------------------------------- the whole layer */
+/* One PSCWin layer: [cycle-scan module: x += (cycle_scan(in_proj(LN_s(x)))) W_out^T] then
+ * x_out = x + window_attention(qkv_project(x)) W_o^T + b_o. x_in, x_out [B,H,W,C] bf16; x_out may alias
+ * x_in. Workspace: pscwin_workspace_bytes(desc). */
+size_t pscwin_workspace_bytes(const pscwin_layer_desc* desc);
+int pscwin_forward(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
+                   void* workspace, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSCWIN_H_ */

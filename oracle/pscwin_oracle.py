@@ -215,7 +215,7 @@ def flash_attention_tiled(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: fl
 # =============================================================================================
 
 def attention_core_padded(qkv: np.ndarray, qkv_p: np.ndarray, H: int, W: int, heads: int, w: int,
-                          sx: int, sy: int, pad_mode: int, rope: int) -> np.ndarray:
+                          sx: int, sy: int, pad_mode: int, rope: int, window_rows=None) -> np.ndarray:
     """Window attention over the materialised padded grid (a5 + a6 + crop of a7).
 
     qkv  [B,H,W,3C] projected tokens (Q = cols [0,C), K = [C,2C), V = [2C,3C); head-contiguous, Q3)
@@ -223,7 +223,9 @@ def attention_core_padded(qkv: np.ndarray, qkv_p: np.ndarray, H: int, W: int, he
     Builds the padded grid whose pad cells hold COPIES of qkv_p ("replicated"), applies RoPE at
     every cell's global coordinate (pad cells at their geometric coordinates, Q6), runs softmax attention
     inside every w x w window over all w^2 keys (LEARNABLE) or over real keys only (MASKED, Q5), and keeps
-    only real cells ("the paddings are discarded"). Returns O [B,H,W,C]."""
+    only real cells ("the paddings are discarded"). Returns O [B,H,W,C].
+    window_rows: optional subset of padded-grid window rows to evaluate (sampling at full size; the other
+    cells are NaN). Each window depends only on its own cells, so a subset is exact for those windows."""
     B = qkv.shape[0]
     C3 = qkv.shape[-1]
     C = C3 // 3
@@ -245,9 +247,9 @@ def attention_core_padded(qkv: np.ndarray, qkv_p: np.ndarray, H: int, W: int, he
         q = rope_2d(q, X[None, :, :, None], Y[None, :, :, None])
         k = rope_2d(k, X[None, :, :, None], Y[None, :, :, None])
     nwy, nwx = Hp // w, Wp // w
-    out = np.empty((B, Hp, Wp, heads, d))
+    out = np.full((B, Hp, Wp, heads, d), np.nan)
     scale = 1.0 / math.sqrt(d)
-    for wy in range(nwy):  # one window row at a time bounds memory at 4096^2
+    for wy in (range(nwy) if window_rows is None else window_rows):  # one window row at a time bounds memory
         ys = slice(wy * w, (wy + 1) * w)
 
         def win(t):  # [B, w, Wp, heads, d] -> [B, nwx, heads, w*w, d]

@@ -1,0 +1,133 @@
+"""ctypes binding of libpscwin.so (include/pscwin.h). Argument marshalling only: every step of the path runs
+in the CUDA library. PyTorch provides device memory and the current stream.
+
+The library is REQUIRED: there is no CPU or eager fallback. `lib()` raises if libpscwin.so is missing or
+cannot be loaded, and every call raises PscwinError on a non-zero status.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpscwin.so")
+
+OK, ERR_SHAPE, ERR_CONTRACT, ERR_ALIGN, ERR_WORKSPACE, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+BF16, F32 = 0, 1
+PAD_LEARNABLE, PAD_MASKED = 0, 1
+
+# every symbol include/pscwin.h declares (checked by tests/test_abi_cpu.py)
+EXPORTS = [
+    "pscwin_version", "pscwin_status_string", "pscwin_last_async_error", "pscwin_window_count",
+    "pscwin_index_map", "pscwin_window_partition", "pscwin_shifted_pad_partition", "pscwin_window_merge",
+    "pscwin_layer_norm", "pscwin_linear", "pscwin_qkv_project", "pscwin_window_attention", "pscwin_cycle_scan",
+    "pscwin_scan_workspace_bytes", "pscwin_workspace_bytes", "pscwin_forward",
+]
+
+
+class PscwinError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = _LIB.pscwin_status_string(status).decode() if _LIB is not None else str(status)
+        super().__init__(f"{where}: {msg} (status {status})")
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "B", "H", "W", "C", "heads", "window", "shift_x", "shift_y", "pad_mode", "rope", "cycle_scan",
+        "ssm_state", "ssm_expand", "ssm_dt_rank", "ssm_conv", "scan_order", "bbar_mode", "dtype")] + \
+        [("ln_eps", ctypes.c_float)]
+
+    @classmethod
+    def from_config(cls, cfg) -> "LayerDesc":
+        d = cls()
+        for name, _ in cls._fields_:
+            if name == "dtype":
+                d.dtype = BF16 if getattr(cfg, "dtype", "bf16") == "bf16" else F32
+            elif name == "ssm_dt_rank":
+                d.ssm_dt_rank = getattr(cfg, "R", 0)
+            else:
+                setattr(d, name, getattr(cfg, name))
+        return d
+
+
+class LayerWeights(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "ln1_g", "ln1_b", "w_qkv", "b_qkv", "pad", "w_o", "b_o",
+        "lns_g", "lns_b", "w_in", "conv_w", "conv_b", "w_x", "w_dt", "b_dt", "w_out", "a_log", "d_skip")]
+
+    @classmethod
+    def from_tensors(cls, t: Dict[str, "torch.Tensor"]) -> "LayerWeights":
+        w = cls()
+        for name, _ in cls._fields_:
+            if name in t and t[name] is not None:
+                setattr(w, name, t[name].data_ptr())
+        return w
+
+
+class ScanDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("B", "H", "W", "D", "N", "R", "conv_k", "scan_order", "bbar_mode",
+                                              "dtype")]
+
+
+_LIB: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, f32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+    sig = {
+        "pscwin_version": ([], ctypes.c_char_p),
+        "pscwin_status_string": ([ctypes.c_int], ctypes.c_char_p),
+        "pscwin_last_async_error": ([], ctypes.c_int),
+        "pscwin_window_count": ([i32, i32, i32, i32, i32, ctypes.POINTER(i32)], ctypes.c_int),
+        "pscwin_index_map": ([i32, i32, i32, i32, i32, vp], ctypes.c_int),
+        "pscwin_window_partition": ([vp, i32, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
+        "pscwin_shifted_pad_partition": ([vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
+        "pscwin_window_merge": ([vp, i32, i32, i32, i32, i32, i32, i32, vp, i32, vp, vp], ctypes.c_int),
+        "pscwin_layer_norm": ([vp, i64, i32, vp, vp, f32, i32, vp, vp], ctypes.c_int),
+        "pscwin_linear": ([vp, i64, i32, vp, i32, vp, vp, i32, vp, vp], ctypes.c_int),
+        "pscwin_qkv_project": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, vp, sz, vp],
+                               ctypes.c_int),
+        "pscwin_window_attention": ([ctypes.POINTER(LayerDesc), vp, vp, vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_cycle_scan": ([ctypes.POINTER(ScanDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
+                              ctypes.c_int),
+        "pscwin_scan_workspace_bytes": ([ctypes.POINTER(ScanDesc)], sz),
+        "pscwin_workspace_bytes": ([ctypes.POINTER(LayerDesc)], sz),
+        "pscwin_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
+                           ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = L
+    return L
+
+
+def check(status: int, where: str) -> None:
+    if status != OK:
+        raise PscwinError(status, where)
+
+
+# ------------------------------------------------------------------------------------------------ host helpers
+
+def window_count(H: int, W: int, window: int, sx: int = 0, sy: int = 0) -> int:
+    n = ctypes.c_int32()
+    check(lib().pscwin_window_count(H, W, window, sx, sy, ctypes.byref(n)), "window_count")
+    return n.value
+
+
+def index_map(H: int, W: int, window: int, sx: int = 0, sy: int = 0) -> np.ndarray:
+    n = window_count(H, W, window, sx, sy)
+    out = np.empty(n * window * window, dtype=np.uint32)
+    check(lib().pscwin_index_map(H, W, window, sx, sy, out.ctypes.data), "index_map")
+    return out

@@ -1,0 +1,418 @@
+// C-ABI entry points of libpscwin.so (declared and documented in include/pscwin.h): argument / contract
+// validation, workspace planning, TMA descriptor encoding and the per-layer launch sequence.
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/pscwin.h"
+#include "common.cuh"
+#include "pscwin_internal.h"
+
+namespace pscwin {
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return -10;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -11;
+}
+
+int make_tmap_5d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const uint64_t dims_in[5],
+                 const uint64_t strides_in[4], const uint32_t box_in[5], CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return -10;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    dims[i] = dims_in[i];
+    box[i] = box_in[i];
+  }
+  for (int i = 0; i < 4; ++i) strides[i] = strides_in[i];
+  CUresult r = fn(m, dt, 5, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -11;
+}
+
+}  // namespace pscwin
+
+using namespace pscwin;
+
+namespace {
+
+inline bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline int status_from(int rc) {
+  if (rc == 0) return PSCWIN_OK;
+  if (rc == -2) return PSCWIN_ERR_UNSUPPORTED;
+  if (rc == -3) return PSCWIN_ERR_CONTRACT;
+  return PSCWIN_ERR_CUDA;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Geo {
+  int pt, pl, pb, pr, nw;
+};
+
+int geometry(int H, int W, int w, int sx, int sy, Geo* g) {
+  if (H <= 0 || W <= 0 || w <= 0) return PSCWIN_ERR_SHAPE;
+  if (sx < 0 || sy < 0 || sx >= w || sy >= w) return PSCWIN_ERR_CONTRACT;
+  if (sx == 0 && sy == 0 && (H % w || W % w)) return PSCWIN_ERR_CONTRACT;
+  g->pl = (w - sx) % w;
+  g->pt = (w - sy) % w;
+  g->pr = ((-(g->pl + W)) % w + w) % w;
+  g->pb = ((-(g->pt + H)) % w + w) % w;
+  g->nw = ((g->pt + H + g->pb) / w) * ((g->pl + W + g->pr) / w);
+  return PSCWIN_OK;
+}
+
+int check_layer(const pscwin_layer_desc* d) {
+  if (!d) return PSCWIN_ERR_SHAPE;
+  if (d->B <= 0 || d->H <= 0 || d->W <= 0 || d->C <= 0 || d->heads <= 0) return PSCWIN_ERR_SHAPE;
+  if (d->C % d->heads) return PSCWIN_ERR_CONTRACT;
+  Geo g;
+  int rc = geometry(d->H, d->W, d->window, d->shift_x, d->shift_y, &g);
+  if (rc) return rc;
+  const int dh = d->C / d->heads;
+  if (d->rope && dh % 4) return PSCWIN_ERR_CONTRACT;
+  if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
+  if (!(dh == 32 || dh == 64)) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->window < 4 || d->window > 64 || (d->window & (d->window - 1))) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->pad_mode != PSCWIN_PAD_LEARNABLE && d->pad_mode != PSCWIN_PAD_MASKED) return PSCWIN_ERR_CONTRACT;
+  if (d->C % 64) return PSCWIN_ERR_UNSUPPORTED;  // GEMM K tiles
+  return PSCWIN_OK;
+}
+
+// Workspace layout shared by qkv_project / window_attention / forward.
+struct LayerWs {
+  size_t u, qkv, qkv_pad, O, pad_tab, rope_tab, xz, g, scan, total;
+  int rope_n_pos, rope_off;
+};
+
+LayerWs plan_layer(const pscwin_layer_desc* d) {
+  LayerWs w;
+  const size_t T = (size_t)d->B * d->H * d->W;
+  const size_t C = d->C;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.u = take(T * C * 2);
+  w.qkv = take(T * 3 * C * 2);
+  w.qkv_pad = take(3 * C * 4);
+  w.O = take(T * C * 2);
+  w.pad_tab = take(attn_pad_table_bytes(d->H, d->W, d->C, d->window));
+  w.rope_off = d->window;
+  w.rope_n_pos = (d->H > d->W ? d->H : d->W) + 2 * d->window;
+  const int dh = d->C / d->heads;
+  w.rope_tab = take((size_t)w.rope_n_pos * (dh / 4) * 8);
+  w.xz = w.g = w.scan = 0;
+  if (d->cycle_scan) {
+    const size_t D = (size_t)d->ssm_expand * C;
+    w.xz = take(T * 2 * D * 2);
+    w.g = take(T * D * 2);
+    pscwin_scan_desc sd;
+    sd.B = d->B;
+    sd.H = d->H;
+    sd.W = d->W;
+    sd.D = (int)D;
+    sd.N = d->ssm_state;
+    sd.R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (d->C + 15) / 16;
+    sd.conv_k = d->ssm_conv;
+    sd.scan_order = d->scan_order;
+    sd.bbar_mode = d->bbar_mode;
+    sd.dtype = d->dtype;
+    w.scan = take(pscwin_scan_workspace_bytes(&sd));
+  }
+  w.total = off;
+  return w;
+}
+
+uint8_t* wsp(void* base, size_t off) { return reinterpret_cast<uint8_t*>(base) + off; }
+
+int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x, void* qkv,
+                     float* qkv_pad, void* ws, const LayerWs& L, cudaStream_t s) {
+  const long long T = (long long)d->B * d->H * d->W;
+  const int C = d->C;
+  void* u = wsp(ws, L.u);
+  float2* rope_tab = reinterpret_cast<float2*>(wsp(ws, L.rope_tab));
+  int rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, 0, u, s);
+  if (rc) return rc;
+  const int dh = C / d->heads;
+  if (d->rope) {
+    rc = launch_rope_table(rope_tab, L.rope_n_pos, L.rope_off, dh, s);
+    if (rc) return rc;
+  }
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)T;
+  a.N = 3 * C;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = qkv;
+  a.ldo = 3 * C;
+  a.epi = EPI_QKV_ROPE;
+  a.bias = (const float*)wt->b_qkv;
+  a.rope = d->rope;
+  a.HW = d->H * d->W;
+  a.Wgrid = d->W;
+  a.C = C;
+  a.d_head = dh;
+  a.rope_off = L.rope_off;
+  a.rope_tab = rope_tab;
+  rc = launch_gemm_bf16(u, wt->w_qkv, a, s);
+  if (rc) return rc;
+  if (qkv_pad && wt->pad) {
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, s);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv_pad, void* O, void* ws,
+                   const LayerWs& L, cudaStream_t s) {
+  AttnArgs a;
+  a.B = d->B;
+  a.H = d->H;
+  a.W = d->W;
+  a.C = d->C;
+  a.heads = d->heads;
+  a.d = d->C / d->heads;
+  a.w = d->window;
+  a.sx = d->shift_x;
+  a.sy = d->shift_y;
+  a.pad_mode = d->pad_mode;
+  a.rope = d->rope;
+  a.qkv = qkv;
+  a.qkv_pad = qkv_pad;
+  a.out = O;
+  a.rope_tab = reinterpret_cast<const float2*>(wsp(ws, L.rope_tab));
+  a.rope_off = L.rope_off;
+  a.pad_tab = wsp(ws, L.pad_tab);
+  if (d->rope) {
+    int rc = launch_rope_table(reinterpret_cast<float2*>(wsp(ws, L.rope_tab)), L.rope_n_pos, L.rope_off, a.d, s);
+    if (rc) return rc;
+  }
+  return launch_window_attention(a, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pscwin_version(void) { return "pscwin-b200 0.1 (sm_100a)"; }
+
+const char* pscwin_status_string(int st) {
+  switch (st) {
+    case PSCWIN_OK: return "ok";
+    case PSCWIN_ERR_SHAPE: return "shape error";
+    case PSCWIN_ERR_CONTRACT: return "contract violation";
+    case PSCWIN_ERR_ALIGN: return "pointer not 16-byte aligned";
+    case PSCWIN_ERR_WORKSPACE: return "workspace too small";
+    case PSCWIN_ERR_CUDA: return "CUDA error";
+    case PSCWIN_ERR_UNSUPPORTED: return "unsupported on this path";
+    default: return "unknown status";
+  }
+}
+
+int pscwin_last_async_error(void) { return cudaGetLastError() == cudaSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA; }
+
+int pscwin_window_count(int32_t H, int32_t W, int32_t window, int32_t sx, int32_t sy, int32_t* n) {
+  Geo g;
+  int rc = geometry(H, W, window, sx, sy, &g);
+  if (rc) return rc;
+  if (n) *n = g.nw;
+  return PSCWIN_OK;
+}
+
+int pscwin_index_map(int32_t H, int32_t W, int32_t w, int32_t sx, int32_t sy, uint32_t* map) {
+  Geo g;
+  int rc = geometry(H, W, w, sx, sy, &g);
+  if (rc) return rc;
+  if (!map) return PSCWIN_ERR_SHAPE;
+  const int nwx = (g.pl + W + g.pr) / w;
+  for (int win = 0; win < g.nw; ++win) {
+    const int wy = win / nwx, wx = win % nwx;
+    for (int iy = 0; iy < w; ++iy)
+      for (int ix = 0; ix < w; ++ix) {
+        const int y = wy * w + iy - g.pt, x = wx * w + ix - g.pl;
+        map[((size_t)win * w + iy) * w + ix] =
+            (y >= 0 && y < H && x >= 0 && x < W) ? (uint32_t)(y * W + x) : 0xFFFFFFFFu;
+      }
+  }
+  return PSCWIN_OK;
+}
+
+int pscwin_window_partition(const void* x, int32_t B, int32_t H, int32_t W, int32_t Cx, int32_t window,
+                            int32_t dtype, void* out, void* stream) {
+  return pscwin_shifted_pad_partition(x, nullptr, B, H, W, Cx, window, 0, 0, dtype, out, stream);
+}
+
+int pscwin_shifted_pad_partition(const void* x, const void* pad_row, int32_t B, int32_t H, int32_t W, int32_t Cx,
+                                 int32_t window, int32_t sx, int32_t sy, int32_t dtype, void* out, void* stream) {
+  if (B <= 0 || Cx <= 0) return PSCWIN_ERR_SHAPE;
+  if (dtype != PSCWIN_BF16 && dtype != PSCWIN_F32) return PSCWIN_ERR_CONTRACT;
+  Geo g;
+  int rc = geometry(H, W, window, sx, sy, &g);
+  if (rc) return rc;
+  const bool has_pad = (long long)g.nw * window * window != (long long)H * W;
+  if (has_pad && !pad_row) return PSCWIN_ERR_CONTRACT;
+  if (!x || !out) return PSCWIN_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(out) || !aligned16(pad_row)) return PSCWIN_ERR_ALIGN;
+  const int esize = dtype == PSCWIN_F32 ? 4 : 2;
+  return status_from(launch_partition(x, has_pad ? pad_row : nullptr, B, H, W, Cx, window, sx, sy, esize, out,
+                                      (cudaStream_t)stream));
+}
+
+int pscwin_window_merge(const void* win, int32_t B, int32_t H, int32_t W, int32_t Cx, int32_t window, int32_t sx,
+                        int32_t sy, const void* residual, int32_t dtype, void* out, void* stream) {
+  if (B <= 0 || Cx <= 0) return PSCWIN_ERR_SHAPE;
+  if (dtype != PSCWIN_BF16 && dtype != PSCWIN_F32) return PSCWIN_ERR_CONTRACT;
+  Geo g;
+  int rc = geometry(H, W, window, sx, sy, &g);
+  if (rc) return rc;
+  if (!win || !out) return PSCWIN_ERR_SHAPE;
+  if (!aligned16(win) || !aligned16(out) || !aligned16(residual)) return PSCWIN_ERR_ALIGN;
+  return status_from(launch_merge(win, B, H, W, Cx, window, sx, sy, residual, dtype == PSCWIN_F32, out,
+                                  (cudaStream_t)stream));
+}
+
+int pscwin_layer_norm(const void* x, int64_t rows, int32_t C, const float* g, const float* b, float eps,
+                      int32_t dtype, void* out, void* stream) {
+  if (rows < 0 || C <= 0 || !x || !out || !g || !b) return PSCWIN_ERR_SHAPE;
+  if (!aligned16(x) || !aligned16(out)) return PSCWIN_ERR_ALIGN;
+  int rc = launch_layer_norm(x, rows, C, g, b, eps, dtype == PSCWIN_F32, out, (cudaStream_t)stream);
+  return rc == -1 ? PSCWIN_ERR_UNSUPPORTED : status_from(rc);
+}
+
+int pscwin_linear(const void* A, int64_t M, int32_t K, const void* Wt, int32_t N, const float* bias,
+                  const void* residual, int32_t out_f32, void* out, void* stream) {
+  if (M < 0 || K <= 0 || N <= 0 || !A || !Wt || !out) return PSCWIN_ERR_SHAPE;
+  if (K % 8) return PSCWIN_ERR_UNSUPPORTED;
+  if (!aligned16(A) || !aligned16(Wt) || !aligned16(out) || !aligned16(residual)) return PSCWIN_ERR_ALIGN;
+  if (out_f32 && residual) return PSCWIN_ERR_CONTRACT;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)M;
+  a.N = N;
+  a.K = K;
+  a.lda = K;
+  a.ldb = K;
+  a.out = out;
+  a.ldo = N;
+  a.epi = out_f32 ? EPI_STORE_F32 : (residual ? EPI_RESID_BF16 : EPI_STORE_BF16);
+  a.bias = bias;
+  a.residual = residual;
+  a.ldr = N;
+  return status_from(launch_gemm_bf16(A, Wt, a, (cudaStream_t)stream));
+}
+
+size_t pscwin_workspace_bytes(const pscwin_layer_desc* d) {
+  if (check_layer(d) != PSCWIN_OK) return 0;
+  return plan_layer(d).total;
+}
+
+int pscwin_qkv_project(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x, void* qkv,
+                       float* qkv_pad, void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_layer(d);
+  if (rc) return rc;
+  if (!wt || !x || !qkv || !wt->w_qkv || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv) return PSCWIN_ERR_SHAPE;
+  LayerWs L = plan_layer(d);
+  if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x) || !aligned16(qkv) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  return status_from(qkv_project_impl(d, wt, x, qkv, qkv_pad, ws, L, (cudaStream_t)stream));
+}
+
+int pscwin_window_attention(const pscwin_layer_desc* d, const void* qkv, const float* qkv_pad, void* O, void* ws,
+                            size_t ws_bytes, void* stream) {
+  int rc = check_layer(d);
+  if (rc) return rc;
+  if (!qkv || !O) return PSCWIN_ERR_SHAPE;
+  const bool shifted = d->shift_x || d->shift_y;
+  if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !qkv_pad) return PSCWIN_ERR_CONTRACT;
+  LayerWs L = plan_layer(d);
+  if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(qkv) || !aligned16(O) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  return status_from(attention_impl(d, qkv, qkv_pad, O, ws, L, (cudaStream_t)stream));
+}
+
+int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x_in, void* x_out,
+                   void* ws, size_t ws_bytes, void* stream) {
+  int rc = check_layer(d);
+  if (rc) return rc;
+  if (!wt || !x_in || !x_out) return PSCWIN_ERR_SHAPE;
+  const bool shifted = d->shift_x || d->shift_y;
+  if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !wt->pad) return PSCWIN_ERR_CONTRACT;
+  if (!wt->w_qkv || !wt->w_o || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  LayerWs L = plan_layer(d);
+  if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)d->B * d->H * d->W;
+  const int C = d->C;
+  const void* x = x_in;
+  if (d->cycle_scan) {
+    rc = cycle_scan_module(d, wt, x_in, x_out, ws, L.u, L.xz, L.g, L.scan, L.total - L.scan, s);
+    if (rc) return rc;
+    x = x_out;
+  }
+  void* qkv = wsp(ws, L.qkv);
+  float* qkv_pad = reinterpret_cast<float*>(wsp(ws, L.qkv_pad));
+  void* O = wsp(ws, L.O);
+  rc = qkv_project_impl(d, wt, x, qkv, (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE) ? qkv_pad : nullptr, ws, L,
+                        s);
+  if (rc) return status_from(rc);
+  rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s);
+  if (rc) return status_from(rc);
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)T;
+  a.N = C;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = x_out;
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.bias = (const float*)wt->b_o;
+  a.residual = x;
+  a.ldr = C;
+  return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// Internal (non-ABI) declarations shared by the .cu translation units of libpscwin.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace pscwin {
+
+enum GemmEpilogue { EPI_STORE_BF16 = 0, EPI_STORE_F32 = 1, EPI_QKV_ROPE = 2, EPI_RESID_BF16 = 3 };
+
+struct GemmArgs {
+  int M, N, K;
+  int lda, ldb;          // elements (row strides of A [M,K] and B [N,K])
+  void* out;
+  int ldo;               // elements
+  int epi;               // GemmEpilogue
+  int BN;                // 0 = auto
+  const float* bias;     // [N] or null
+  const void* residual;  // bf16 [M, ldr] or null
+  int ldr;
+  // QKV + RoPE epilogue
+  int rope, HW, Wgrid, C, d_head, rope_off;
+  const float2* rope_tab;
+};
+
+// host helpers (abi.cu)
+int num_sms();
+int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
+int make_tmap_5d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const uint64_t dims[5],
+                 const uint64_t strides_bytes[4], const uint32_t box[5], CUtensorMapSwizzle swz);
+
+// launchers (return 0 or a cudaError_t / negative internal code)
+int launch_partition(const void* x, const void* pad_row, int B, int H, int W, int Cx, int w, int sx, int sy,
+                     int esize, void* out, cudaStream_t stream);
+int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, int sy, const void* residual,
+                 int is_f32, void* out, cudaStream_t stream);
+int launch_gemm_bf16(const void* A, const void* B, const GemmArgs& args, cudaStream_t stream);
+int launch_rope_table(float2* tab, int n_pos, int off, int d, cudaStream_t stream);
+int launch_layer_norm(const void* x, long long rows, int C, const float* g, const float* b, float eps, int is_f32,
+                      void* out, cudaStream_t stream);
+int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C, int is_f32, float* out,
+                   cudaStream_t stream);
+
+struct AttnArgs {
+  int B, H, W, C, heads, d, w, sx, sy, pad_mode, rope;
+  const void* qkv;       // [B,H,W,3C] bf16 (q,k rotated at their grid coordinates)
+  const float* qkv_pad;  // [3C] f32 projection of p (unrotated) or null (plain / masked)
+  void* out;             // [B,H,W,C] bf16
+  const float2* rope_tab;
+  int rope_off;
+  void* pad_tab;         // workspace for rotated pad K halves + V (bf16)
+};
+size_t attn_pad_table_bytes(int H, int W, int C, int w);
+int launch_window_attention(const AttnArgs& a, cudaStream_t stream);
+
+}  // namespace pscwin
+
+
+namespace pscwin {
+// cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
+int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
+                      size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);
+}  // namespace pscwin

@@ -1,0 +1,126 @@
+// Row-wise helper kernels: LayerNorm (pre-norm of a4 and a1; eps 1e-6, reading Q15) and the one-row
+// projection of the learnable pad token p through the QKV linear ("F and the learnable padding
+// embedding p are both projected through the attention's QKV-linear layer"; p is not normalised, reading Q14).
+#include "common.cuh"
+#include "pscwin_internal.h"
+
+namespace pscwin {
+
+// One warp per row; up to 8 x 32 vectors (C <= 2048 bf16 / 1024 f32) kept in registers (two-pass mean/var).
+template <typename T>
+__global__ void layer_norm_kernel(const T* __restrict__ x, long long rows, int C, const float* __restrict__ g,
+                                  const float* __restrict__ b, float eps, T* __restrict__ out) {
+  constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte vector
+  long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int nvec = C / EPV;
+  const uint4* src = reinterpret_cast<const uint4*>(x + row * C);
+  uint4 v[8];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int i = lane + 32 * k;
+    if (i < nvec) {
+      v[k] = src[i];
+      const T* e = reinterpret_cast<const T*>(&v[k]);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) {
+        float f;
+        if constexpr (sizeof(T) == 2) f = __bfloat162float(e[j]); else f = e[j];
+        sum += f;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / C;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int i = lane + 32 * k;
+    if (i < nvec) {
+      const T* e = reinterpret_cast<const T*>(&v[k]);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) {
+        float f;
+        if constexpr (sizeof(T) == 2) f = __bfloat162float(e[j]); else f = e[j];
+        sq += (f - mean) * (f - mean);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const float rstd = rsqrtf(sq / C + eps);
+  uint4* dst = reinterpret_cast<uint4*>(out + row * C);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int i = lane + 32 * k;
+    if (i < nvec) {
+      uint4 w;
+      const T* e = reinterpret_cast<const T*>(&v[k]);
+      T* o = reinterpret_cast<T*>(&w);
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) {
+        int c = i * EPV + j;
+        float f;
+        if constexpr (sizeof(T) == 2) f = __bfloat162float(e[j]); else f = e[j];
+        float y = (f - mean) * rstd * g[c] + b[c];
+        if constexpr (sizeof(T) == 2) o[j] = __float2bfloat16_rn(y); else o[j] = y;
+      }
+      dst[i] = w;
+    }
+  }
+}
+
+int launch_layer_norm(const void* x, long long rows, int C, const float* g, const float* b, float eps, int is_f32,
+                      void* out, cudaStream_t stream) {
+  if (rows == 0) return 0;
+  unsigned grid = (unsigned)((rows + 7) / 8);
+  if (is_f32) {
+    if (C % 4 || C > 1024) return -1;
+    layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, rows, C, g, b, eps, (float*)out);
+  } else {
+    if (C % 8 || C > 2048) return -1;
+    layer_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, rows, C, g, b, eps,
+                                                               (__nv_bfloat16*)out);
+  }
+  return (int)cudaGetLastError();
+}
+
+// qkv_p[j] = sum_c p[c] W_qkv[j, c] + b_qkv[j]  (f32 accumulate, f32 result), one warp per output j
+template <typename T>
+__global__ void pad_qkv_kernel(const T* __restrict__ pad, const T* __restrict__ w, const float* __restrict__ bias,
+                               int C, float* __restrict__ out) {
+  int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= 3 * C) return;
+  int lane = threadIdx.x & 31;
+  float acc = 0.f;
+  for (int c = lane; c < C; c += 32) {
+    float a, bw;
+    if constexpr (sizeof(T) == 2) {
+      a = __bfloat162float(pad[c]);
+      bw = __bfloat162float(w[(size_t)j * C + c]);
+    } else {
+      a = pad[c];
+      bw = w[(size_t)j * C + c];
+    }
+    acc = fmaf(a, bw, acc);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[j] = acc + (bias ? bias[j] : 0.f);
+}
+
+int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C, int is_f32, float* out,
+                   cudaStream_t stream) {
+  unsigned grid = (unsigned)((3 * C + 7) / 8);
+  if (is_f32)
+    pad_qkv_kernel<float><<<grid, 256, 0, stream>>>((const float*)pad, (const float*)w_qkv, b_qkv, C, out);
+  else
+    pad_qkv_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)pad,
+                                                            (const __nv_bfloat16*)w_qkv, b_qkv, C, out);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace pscwin

@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same seeded inputs.
+
+Bar: partition / merge / index work bit-exact; floating point within
+max|g - o| / max|o| <= 2e-2 for the bf16 path (north star). Sizes span several tiles and ragged tails; the
+full-size cases (4096^2 grid) compare sampled windows the oracle computes one window row at a time.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2407_02109_b200 as p
+    return p
+
+
+def _sync():
+    import torch
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------------------------------- a5 / a7
+
+@pytest.mark.parametrize("B,H,W,C,w,sx,sy,dtype", [
+    (2, 12, 20, 768, 4, 0, 0, "bf16"), (2, 12, 20, 768, 4, 1, 3, "bf16"), (1, 64, 64, 2304, 16, 8, 8, "bf16"),
+    (1, 16, 16, 64, 8, 4, 4, "f32"), (1, 7, 9, 12, 4, 2, 1, "bf16"), (1, 256, 256, 64, 16, 8, 8, "bf16"),
+    (3, 5, 6, 10, 4, 3, 1, "f32")])
+def test_partition_merge_bit_exact(pl, B, H, W, C, w, sx, sy, dtype):
+    x = synth._store(synth.normal(synth.stream_seed(B, H, W), B * H * W * C).reshape(B, H, W, C), "mat",
+                     synth.tiny(dtype=dtype))
+    pad = synth._store(synth.normal(synth.stream_seed(9, C), C), "mat", synth.tiny(dtype=dtype))
+    xt, pt_ = dev(x, dtype), dev(pad, dtype)
+    if sx == 0 and sy == 0:
+        got = pl.window_partition(xt, w)
+        ref = oracle.window_partition(x, w)
+    else:
+        got = pl.shifted_pad_partition(xt, pt_, w, sx, sy)
+        ref = oracle.shifted_pad_partition(x, pad, w, sx, sy)
+    _sync()
+    assert np.array_equal(host(got), ref)
+    back = pl.window_merge(got, B, H, W, w, sx, sy)
+    res = synth._store(synth.normal(synth.stream_seed(5, B, C), B * H * W * C).reshape(B, H, W, C), "mat",
+                       synth.tiny(dtype=dtype))
+    back_res = pl.window_merge(got, B, H, W, w, sx, sy, residual=dev(res, dtype))
+    _sync()
+    assert np.array_equal(host(back), x)
+    ref_res = oracle.window_merge(ref, B, H, W, w, sx, sy, res)
+    ref_res = synth.round_bf16(ref_res) if dtype == "bf16" else synth.round_f32(ref_res)
+    assert np.array_equal(host(back_res), ref_res)
+
+
+# ------------------------------------------------------------------------------------------- LN, GEMM
+
+def test_layer_norm(pl):
+    cfg = synth.vitb(64)
+    x = synth.make_input(cfg)
+    w = synth.make_weights(cfg)
+    got = pl.layer_norm(dev(x), dev(w["ln1_g"], "f32"), dev(w["ln1_b"], "f32"), 1e-6)
+    ref = oracle.layer_norm(x, w["ln1_g"], w["ln1_b"], 1e-6)
+    _sync()
+    assert rel_err(host(got), ref) < 1e-2
+
+
+@pytest.mark.parametrize("M,K,N,bias,resid,f32", [
+    (4096, 768, 2304, True, False, False), (4173, 768, 768, True, True, False), (100, 1536, 112, False, False, True),
+    (1, 64, 36, False, False, True), (300, 64, 192, True, False, False), (4096, 768, 3072, False, False, False),
+    (777, 1536, 768, False, True, False), (130, 128, 256, True, True, False)])
+def test_linear(pl, M, K, N, bias, resid, f32):
+    g = lambda s, n: synth.round_bf16(synth.normal(synth.stream_seed(s, M, K, N), n))
+    A = g(1, M * K).reshape(M, K)
+    Wt = g(2, N * K).reshape(N, K) * 0.05
+    b = synth.round_f32(g(3, N) * 0.1) if bias else None
+    r = g(4, M * N).reshape(M, N) if resid else None
+    got = pl.linear(dev(A), dev(Wt), dev(b, "f32") if bias else None, dev(r) if resid else None, out_f32=f32)
+    ref = A @ Wt.T + (b if bias else 0) + (r if resid else 0)
+    _sync()
+    assert rel_err(host(got), ref) < (1e-5 if f32 else 8e-3)
+
+
+# ------------------------------------------------------------------------------------------- a4
+
+def _rotated(qkv, C, heads, H, W):
+    """round_bf16(RoPE(q), RoPE(k)) at grid coordinates — the a4 output convention the attention ABI takes."""
+    d = C // heads
+    B = qkv.shape[0]
+    g = qkv.reshape(B, H, W, 3, heads, d).copy()
+    yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    for i in (0, 1):
+        g[:, :, :, i] = oracle.rope_2d(g[:, :, :, i], xx[None, :, :, None], yy[None, :, :, None])
+    return synth.round_bf16(g.reshape(qkv.shape))
+
+
+@pytest.mark.parametrize("cfg", [synth.tiny(), synth.vitb(64, shift_x=0, shift_y=0), synth.tiny(rope=0, H=8, W=24)])
+def test_qkv_project(pl, cfg):
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    desc = pl.LayerDesc.from_config(cfg)
+    qkv, qkv_pad = pl.qkv_project(desc, dev_weights(w, cfg), dev(x))
+    u = oracle.layer_norm(x, w["ln1_g"], w["ln1_b"], cfg.ln_eps)
+    ref = u @ w["w_qkv"].T + w["b_qkv"]
+    if cfg.rope:
+        ref = _rotated(ref, cfg.C, cfg.heads, cfg.H, cfg.W)
+    ref_pad = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
+    _sync()
+    assert rel_err(host(qkv), ref) < BF16_TOL
+    assert rel_err(host(qkv_pad), ref_pad) < 1e-5
+
+
+# ------------------------------------------------------------------------------------------- a5 + a6
+
+ATTN_CASES = [
+    synth.tiny(shift_x=0, shift_y=0, rope=0),
+    synth.tiny(shift_x=0, shift_y=0),
+    synth.tiny(),                                                   # shifted, LEARNABLE
+    synth.tiny(pad_mode=synth.PAD_MASKED),
+    synth.tiny(window=16, shift_x=0, shift_y=0),                    # P1: window = whole grid (2 key tiles)
+    synth.tiny(H=12, W=20, window=8, shift_x=3, shift_y=5),         # ragged grid, asymmetric shift
+    synth.tiny(H=12, W=20, window=8, shift_x=3, shift_y=5, pad_mode=synth.PAD_MASKED),
+    synth.tiny(H=9, W=11, C=128, heads=2, window=4, shift_x=1, shift_y=2),   # d=64, w=4 (16-slot tiles)
+    synth.vitb(64, B=2),                                            # 1024^2 shifted LEARNABLE, batch 2
+    synth.vitb(64, pad_mode=synth.PAD_MASKED),
+    synth.vitb(64, shift_x=0, shift_y=0),
+    synth.tiny(H=64, W=64, C=128, heads=2, window=32, shift_x=16, shift_y=16),  # w=32: 4 q x 4 kv tiles
+]
+
+
+def _attn_inputs(cfg):
+    qkv = synth.make_qkv(cfg)
+    qkv_p = synth.make_pad_qkv(cfg)
+    gpu_qkv = _rotated(qkv, cfg.C, cfg.heads, cfg.H, cfg.W) if cfg.rope else qkv
+    return qkv, qkv_p, gpu_qkv
+
+
+@pytest.mark.parametrize("cfg", ATTN_CASES, ids=lambda c: f"{c.B}x{c.H}x{c.W}C{c.C}h{c.heads}w{c.window}"
+                         f"s{c.shift_x},{c.shift_y}m{c.pad_mode}r{c.rope}")
+def test_window_attention(pl, cfg):
+    qkv, qkv_p, gpu_qkv = _attn_inputs(cfg)
+    desc = pl.LayerDesc.from_config(cfg)
+    O = pl.window_attention(desc, dev(gpu_qkv), dev(qkv_p, "f32"))
+    ref = oracle.attention_core_padded(qkv, qkv_p, cfg.H, cfg.W, cfg.heads, cfg.window, cfg.shift_x, cfg.shift_y,
+                                       cfg.pad_mode, cfg.rope)
+    _sync()
+    assert rel_err(host(O), ref) < BF16_TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("mode", [synth.PAD_LEARNABLE, synth.PAD_MASKED])
+def test_window_attention_4096_sampled(pl, mode):
+    cfg = synth.vitb(256, pad_mode=mode)
+    qkv, qkv_p, gpu_qkv = _attn_inputs(cfg)
+    O = host(pl.window_attention(pl.LayerDesc.from_config(cfg), dev(gpu_qkv), dev(qkv_p, "f32")))
+    rows = [0, 7, 16]  # first (half pad), interior, last (half pad) window rows of the 272^2 padded grid
+    ref = oracle.attention_core_padded(qkv, qkv_p, cfg.H, cfg.W, cfg.heads, cfg.window, cfg.shift_x, cfg.shift_y,
+                                       cfg.pad_mode, cfg.rope, window_rows=rows)
+    sel = ~np.isnan(ref)
+    assert sel.sum() > 0
+    assert np.all(np.isfinite(O))
+    assert float(np.max(np.abs(O[sel] - ref[sel])) / np.max(np.abs(ref[sel]))) < BF16_TOL
+
+
+def test_attention_guard_and_invariants(pl):
+    import torch
+    cfg = synth.vitb(64)
+    qkv, qkv_p, gpu_qkv = _attn_inputs(cfg)
+    desc = pl.LayerDesc.from_config(cfg)
+    n = cfg.B * cfg.H * cfg.W * cfg.C
+    # canary guard bands around O: pad query rows / out-of-grid rows are never written
+    buf = torch.full((n + 2 * 4096,), 12345.0, dtype=torch.bfloat16, device="cuda")
+    O = buf[4096:4096 + n].view(cfg.B, cfg.H, cfg.W, cfg.C)
+    pl.window_attention(desc, dev(gpu_qkv), dev(qkv_p, "f32"), out=O)
+    _sync()
+    assert torch.all(buf[:4096] == 12345.0) and torch.all(buf[-4096:] == 12345.0)
+    # MASKED: pad token never influences real tokens (bit-exact)
+    dm = pl.LayerDesc.from_config(cfg.replace(pad_mode=synth.PAD_MASKED))
+    a = pl.window_attention(dm, dev(gpu_qkv), dev(qkv_p, "f32"))
+    b = pl.window_attention(dm, dev(gpu_qkv), dev(qkv_p * -3.0 + 1.0, "f32"))
+    # LEARNABLE: windows with no pad slot ignore p (bit-exact): padded-grid rows/cols 16..63 are interior
+    c = pl.window_attention(desc, dev(gpu_qkv), dev(qkv_p * 2.0, "f32"))
+    _sync()
+    assert torch.equal(a, b)
+    inner = (slice(None), slice(8, 56), slice(8, 56))
+    assert torch.equal(O[inner], c[inner])
+    assert not torch.equal(O[:, :8], c[:, :8])
+    # shift 0 == plain (P2): pad mode / pad token are irrelevant without pads
+    p0 = pl.LayerDesc.from_config(cfg.replace(shift_x=0, shift_y=0))
+    p1 = pl.LayerDesc.from_config(cfg.replace(shift_x=0, shift_y=0, pad_mode=synth.PAD_MASKED))
+    e = pl.window_attention(p0, dev(gpu_qkv), dev(qkv_p, "f32"))
+    f = pl.window_attention(p1, dev(gpu_qkv), None)
+    _sync()
+    assert torch.equal(e, f)
+
+
+# ------------------------------------------------------------------------------------------- layer
+
+LAYER_CASES = [synth.tiny(shift_x=0, shift_y=0), synth.tiny(), synth.tiny(pad_mode=synth.PAD_MASKED),
+               synth.vitb(64), synth.vitb(64, shift_x=0, shift_y=0)]
+
+
+@pytest.mark.parametrize("cfg", LAYER_CASES, ids=lambda c: f"{c.H}C{c.C}s{c.shift_x}m{c.pad_mode}cs{c.cycle_scan}")
+def test_layer_forward(pl, cfg):
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))
+    got = host(layer(dev(x)))
+    ref = oracle.pscwin_layer(x, w, cfg)
+    _sync()
+    assert rel_err(got, ref) < BF16_TOL
+    # the sub-layer increment itself (x_out - x), scaled by its own magnitude, minus bf16 output rounding
+    inc = ref - x
+    assert float(np.max(np.abs((got - x) - inc))) < BF16_TOL * np.max(np.abs(inc)) + 2.0 ** -8 * np.max(np.abs(ref))
