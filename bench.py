@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""bench.py — PSCWin layer latency on B200 (BASELINE.json metric: "PSCWin encoder-layer latency ms/image").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload 1024|2048|4096] [--impl ours|reference]
+
+A step is one pass of the whole hot path over one batch of synthetic input: at the default workload
+(configs[1], 1024^2 input) the three layers of HRSAM stage 1 under the global-alternation reading
+(Q8): plain window attention (P), padded-shift window attention (S, LEARNABLE pad) and the
+cycle-scan module + plain attention (CS+P), ViT-B (C=768, 12 heads, w=16, shift 8, N=32, E=2), bf16,
+B=1 image per rank. Under torchrun each rank processes its own image (weak scaling; no data-path
+collective). Inputs are resident in HBM before timing; L2 is flushed (256 MiB write) before every
+timed step, and each step is timed with CUDA events on the launching stream; max over ranks.
+
+Also reported: e2e (same metric through the public API with pinned-host input/output copies in the timed
+region), the dominant kernel's roofline (per-kernel CUDA-event timing inside the library), the fp64 CPU
+oracle as cpu_baseline (rank 0, N=1), clocks sampled by nvidia-smi during the timed region, and the number
+of library kernel launches inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+F32_KEYS = {"ln1_g", "ln1_b", "b_qkv", "b_o", "lns_g", "lns_b", "conv_w", "conv_b", "w_dt", "b_dt", "a_log",
+            "d_skip"}
+METRIC = "PSCWin encoder-layer latency ms/image"
+
+
+def workload(name: str):
+    """(label, B per rank, [LayerConfig per layer])."""
+    if name == "1024":
+        side, B, n_layers = 64, 1, 3
+        label = "1024^2 (64x64 tokens) HRSAM stage 1: P, S(pad learnable), CS+P; ViT-B bf16"
+    elif name == "2048":
+        side, B, n_layers = 128, 8, 12
+        label = "2048^2 (128x128 tokens) full 12-layer PSCWin stack (6 P, 6 S, 4 CS); ViT-B bf16"
+    elif name == "4096":
+        side, B, n_layers = 256, 1, 12
+        label = "4096^2 (256x256 tokens) full 12-layer PSCWin stack, one image per GPU; ViT-B bf16"
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    cfgs = []
+    for i in range(n_layers):
+        shifted, cs = synth.stack_layer_kind(i)
+        cfgs.append(synth.vitb(side, B=B, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0,
+                               cycle_scan=int(cs)))
+    return label, B, cfgs
+
+
+# ----------------------------------------------------------------------------------------------- roofline
+def kernel_work(label: str, cfgs, launches_per_step: int):
+    """Algorithmic work of ONE launch of a kernel label:
+    returns (bound, amount, unit_scale, unit)."""
+    c = cfgs[0]
+    T = c.B * c.H * c.W
+    C, D, N, R = c.C, c.D, c.N, c.R
+    if label == "window_attention":
+        return "hbm", 8.0 * T * C, 1e9, "GB/s"                    # Q,K,V read + O write, bf16, real tokens
+    if label in ("scan_pass1", "scan_pass2"):
+        return "alu", 1.0 * T * D * N, 1e9, "Gexp/s"              # one ex2 per (token, channel, state)
+    if label == "gemm_qkv_rope":
+        return "tensor", 2.0 * T * C * 3 * C, 1e12, "TFLOP/s"
+    if label == "gemm_out_proj":
+        return "tensor", 2.0 * T * C * C, 1e12, "TFLOP/s"
+    if label == "gemm_in_proj":
+        return "tensor", 2.0 * T * C * 2 * D, 1e12, "TFLOP/s"
+    if label == "gemm_out_proj_scan":
+        return "tensor", 2.0 * T * D * C, 1e12, "TFLOP/s"
+    if label == "gemm_x_proj":
+        return "tensor", 2.0 * (T + 3) * D * (R + 2 * N), 1e12, "TFLOP/s"
+    if label == "layer_norm":
+        return "hbm", 4.0 * T * C, 1e9, "GB/s"
+    if label == "conv_silu":
+        return "hbm", 2.0 * T * 2 * D * 0 + 2.0 * T * D * 2, 1e9, "GB/s"
+    return None
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update(hbm_gbs=m["hbm_gbs"], bf16_tflops=m["bf16_tflops"],
+                 bf16_tflops_sustained=m.get("bf16_tflops_sustained", m["bf16_tflops"]), src="measured",
+                 sm_max_mhz=m.get("sm_max_mhz", 1965.0))
+    except Exception:
+        p["sm_max_mhz"] = 1965.0
+    # MUFU ex2: 16 / clk / SM (B200: 148 SMs), at the max SM clock
+    p["ex2_gps"] = 16 * 148 * p["sm_max_mhz"] * 1e6 / 1e9
+    return p
+
+
+def traffic_table():
+    path = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.out = self.proc.communicate(timeout=5)[0]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2407_02109_b200 as pl
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    label, B, cfgs = workload(args.workload)
+    layers = []
+    for i, cfg in enumerate(cfgs):
+        w = synth.make_weights(cfg, layer=i)
+        dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+              for k, v in w.items()}
+        layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dw))
+    x_host = synth.make_input(cfgs[0], layer=rank)
+    x0 = torch.tensor(x_host, dtype=torch.bfloat16, device=dev)
+    bufs = [torch.empty_like(x0), torch.empty_like(x0)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(x):
+        cur = x
+        for j, layer in enumerate(layers):
+            nxt = bufs[j & 1]
+            layer(cur, out=nxt)
+            cur = nxt
+        return cur
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        step(x0)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed before each, CUDA events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    n0 = pl.launch_count()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step(x0)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = pl.launch_count() - n0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    per_step = [a.elapsed_time(b) for a, b in ev]
+
+    # ---- per-layer breakdown (untimed for value): each layer timed alone after an L2 flush
+    layer_ms = []
+    for j, layer in enumerate(layers):
+        ts = []
+        for _ in range(max(3, min(20, args.steps))):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            layer(x0, out=bufs[0])
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        layer_ms.append(float(np.median(ts)))
+
+    # ---- e2e: public API with pinned host buffers, copies inside the timed region
+    x_pin = torch.empty(x0.shape, dtype=torch.bfloat16, pin_memory=True)
+    x_pin.copy_(x0.cpu())
+    y_pin = torch.empty_like(x_pin).pin_memory()
+    x_dev = torch.empty_like(x0)
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        e2e_ev[i][0].record(stream)
+        x_dev.copy_(x_pin, non_blocking=True)
+        out = step(x_dev)
+        y_pin.copy_(out, non_blocking=True)
+        e2e_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+
+    # ---- per-kernel timing (library CUDA events on the launching stream), separate pass
+    pl.profile_enable(True)
+    for i in range(args.steps):
+        flush.zero_()
+        step(x0)
+    torch.cuda.synchronize()
+    prof = pl.profile_read()
+    pl.profile_enable(False)
+
+    # ---- max over ranks
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+    images = args.steps * B * world
+    result = dict(total_ms=total_ms, e2e_ms=e2e_ms, images=images, per_step=per_step, layer_ms=layer_ms,
+                  prof=prof, launches=launches, clocks=clk.summary(), label=label, B=B, cfgs=cfgs,
+                  h2d=x0.numel() * 2 * B // B, d2h=x0.numel() * 2)
+    return result
+
+
+def roofline(res, args):
+    pk = peaks()
+    steps = args.steps
+    rows = []
+    for lab, (ms, cnt) in res["prof"].items():
+        per_launch = ms / max(cnt, 1)
+        w = kernel_work(lab, res["cfgs"], cnt // max(steps, 1))
+        share = ms / max(sum(v[0] for v in res["prof"].values()), 1e-12)
+        row = {"kernel": lab, "ms_per_launch": per_launch, "launches": cnt, "share": share}
+        if w:
+            bound, amount, scale, unit = w
+            achieved = amount / (per_launch * 1e-3) / scale
+            if bound == "hbm":
+                peak = pk["hbm_gbs"]
+            elif bound == "tensor":
+                peak = pk["bf16_tflops"]
+            else:
+                peak = pk["ex2_gps"]
+            row.update(bound=bound, achieved=achieved, peak=peak, unit=unit, frac=achieved / peak)
+        rows.append(row)
+    rows.sort(key=lambda r: -r["share"])
+    dom = next((r for r in rows if "bound" in r), None)
+    traffic = traffic_table()
+    out = None
+    if dom:
+        tr = traffic.get(dom["kernel"])
+        out = {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": round(dom["achieved"], 2),
+               "peak": round(dom["peak"], 2), "unit": dom["unit"], "frac": round(dom["frac"], 4),
+               "traffic": tr, "share_of_step": round(dom["share"], 4),
+               "peak_src": pk["src"] if dom["bound"] != "alu" else "derived: 16 ex2/clk/SM x 148 SMs x max SM clock"}
+    return out, rows
+
+
+# ----------------------------------------------------------------------------------------------- oracle (CPU)
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else os.cpu_count()
+    except Exception:
+        return os.cpu_count()
+
+
+def time_oracle_layer(cfg, layer_idx):
+    import oracle
+    x = synth.make_input(cfg, layer=0)
+    w = synth.make_weights(cfg, layer=layer_idx)
+    t0 = time.perf_counter()
+    oracle.pscwin_layer(x, w, cfg)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(args):
+    """The fp64 oracle as it stands, timed on this host: one full step of the workload (one image through
+    every layer) when that is affordable, else one layer of each kind (summed per image)."""
+    label, B, cfgs = workload(args.workload)
+    one = [c.replace(B=1) for c in cfgs]
+    kinds = {}
+    for i, c in enumerate(one):
+        key = (c.shift_x != 0, c.cycle_scan)
+        kinds.setdefault(key, []).append(i)
+    t_kind = {k: time_oracle_layer(one[idx[0]], idx[0]) for k, idx in kinds.items()}
+    ms_per_image = 1e3 * sum(t_kind[k] * len(idx) for k, idx in kinds.items())
+    sample = (f"one image; one layer of each kind timed once ({', '.join(f'{len(v)}x' for v in kinds.values())}) "
+              f"summed over the {len(one)} layers")
+    return {"value": round(ms_per_image, 1), "unit": "ms/image", "cores": oracle_threads(), "kind": "oracle",
+            "sample": sample}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle timed as the reference arm, same metric/config; each step one
+    layer of the workload (round-robin over the layers), value = mean layer time x layers per image."""
+    label, B, cfgs = workload(args.workload)
+    one = [c.replace(B=1) for c in cfgs]
+    for i in range(args.warmup):
+        time_oracle_layer(one[i % len(one)], i % len(one))
+    times = []
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        times.append(time_oracle_layer(one[i % len(one)], i % len(one)))
+    wall = time.perf_counter() - t0
+    per_layer = {}
+    for i, t in enumerate(times):
+        per_layer.setdefault(i % len(one), []).append(t)
+    ms_img = 1e3 * sum(np.mean(per_layer.get(j, [np.mean(times)])) for j in range(len(one)))
+    cores = oracle_threads()
+    sample = f"{args.steps} single-layer steps round-robin over the {len(one)} layers of one image"
+    line = {"metric": METRIC, "value": round(ms_img, 2), "unit": "ms/image", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(args.steps, 1), 2),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": label, "images_per_rank": 1, "layers": len(one)},
+            "cpu_baseline": {"value": round(ms_img, 2), "unit": "ms/image", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(ms_img, 2), "unit": "ms/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="1024", choices=["1024", "2048", "4096"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", help="also print the per-kernel table to stderr")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        rl, rows = roofline(res, args)
+        ms_img = res["total_ms"] / res["images"]
+        e2e_img = res["e2e_ms"] / res["images"]
+        c0 = res["cfgs"][0]
+        line = {
+            "metric": METRIC, "value": round(ms_img, 4), "unit": "ms/image", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(res["total_ms"] / args.steps, 4),
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded splitmix64; random-init ViT-B PSCWin weights)",
+            "config": {"workload": res["label"], "grid": f"{c0.H}x{c0.W}", "images_per_rank": res["B"],
+                       "layers": ["CS+" if c.cycle_scan else "" + ("S" if c.shift_x else "P") for c in res["cfgs"]],
+                       "C": c0.C, "heads": c0.heads, "window": c0.window, "shift": 8, "ssm_state": c0.N,
+                       "ssm_expand": c0.ssm_expand, "pad_mode": "learnable", "parallelism": f"images x{world}",
+                       "l2": "flushed before every timed step (256 MiB write)",
+                       "per_layer_ms": [round(t, 4) for t in res["layer_ms"]]},
+            "e2e": {"value": round(e2e_img, 4), "unit": "ms/image", "h2d_bytes_per_step": int(res["h2d"]),
+                    "d2h_bytes_per_step": int(res["d2h"])},
+            "gpu_launches": int(res["launches"]),
+            "clocks": res["clocks"],
+            "roofline": rl,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args)
+        if args.breakdown:
+            for r in rows:
+                print(json.dumps({k: (round(v, 5) if isinstance(v, float) else v) for k, v in r.items()}),
+                      file=sys.stderr)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

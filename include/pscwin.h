@@ -154,6 +154,17 @@ size_t pscwin_workspace_bytes(const pscwin_layer_desc* desc);
 int pscwin_forward(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
                    void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------------------ instrumentation */
+/* Kernel launches issued by this library since it was loaded (every launcher counts itself). */
+int64_t pscwin_launch_count(void);
+/* on != 0: from now on every launch records a CUDA event pair on its own stream (bench.py per-kernel
+ * timing); any call clears the records collected so far. Not thread-safe against concurrent reads. */
+void pscwin_profile_enable(int on);
+/* Synchronises on the recorded events and aggregates them by kernel label. Writes up to max_entries labels
+ * ('\n'-separated, NUL-terminated, into names[names_len]), their summed milliseconds and launch counts
+ * (host arrays). Returns the number of labels written. */
+int pscwin_profile_read(char* names, size_t names_len, double* total_ms, int32_t* counts, int32_t max_entries);
+
 #ifdef __cplusplus
 }
 #endif

@@ -361,53 +361,44 @@ def scan_permutation(H: int, W: int, order: int, window: int = 0) -> np.ndarray:
     raise ValueError(order)
 
 
-def cycle_ssm_3L(xin3: np.ndarray, z3: np.ndarray, wt: Dict[str, np.ndarray], bbar_mode: int) -> np.ndarray:
+def cycle_ssm_3L(xin3: np.ndarray, z3: Optional[np.ndarray], wt: Dict[str, np.ndarray], bbar_mode: int,
+                 channels=None) -> np.ndarray:
     """The Mamba SSM operator over the literal cycled sequence of 3L tokens ("repeats the image
     token sequence three times and connects them sequentially. The Mamba SSM operator then scans the
     tokens in this order"). Mamba-1 block internals per reading Q9:
       v = SiLU(causal_conv(xin));  (delta_low, B, C) = v W_x^T;  Delta = softplus(delta_low W_dt^T + b_dt);
-      A = -exp(A_log);  y = selective scan (Eqs. 3-4) + D_skip v;  g = y * SiLU(z).
-    xin3, z3 [3L, D]. Returns g3 [3L, D]."""
+      A = -exp(A_log);  y = selective scan (Eqs. 3-4) + D_skip v;  g = y * SiLU(z)  (no gate if z3 is None).
+    xin3, z3 [3L, D]. Returns g3 [3L, D] (or [3L, len(channels)]: channels are independent, so a
+    subset is exact for those channels — used to sample full-size cases)."""
     R = wt["w_dt"].shape[1]
     N = wt["a_log"].shape[1]
     v = silu(causal_conv1d(xin3, wt["conv_w"], wt["conv_b"]))
     dbc = v @ wt["w_x"].T
     delta_low, Bm, Cm = dbc[:, :R], dbc[:, R:R + N], dbc[:, R + N:R + 2 * N]
-    delta = softplus(delta_low @ wt["w_dt"].T + wt["b_dt"])
-    A = -np.exp(wt["a_log"])
-    y = selective_scan_sequential(v, delta, A, Bm, Cm, wt["d_skip"], bbar_mode)
-    return y * silu(z3)
+    ch = slice(None) if channels is None else np.asarray(channels)
+    delta = softplus(delta_low @ wt["w_dt"][ch].T + wt["b_dt"][ch])
+    A = -np.exp(wt["a_log"][ch])
+    y = selective_scan_sequential(v[:, ch], delta, A, Bm, Cm, wt["d_skip"][ch], bbar_mode)
+    return y if z3 is None else y * silu(z3[:, ch])
 
 
 def cycle_scan(xin: np.ndarray, z: Optional[np.ndarray], wt: Dict[str, np.ndarray], H: int, W: int,
-               scan_order: int = SCAN_ROW_MAJOR, bbar_mode: int = BBAR_ZOH, window: int = 0) -> np.ndarray:
+               scan_order: int = SCAN_ROW_MAJOR, bbar_mode: int = BBAR_ZOH, window: int = 0,
+               channels=None) -> np.ndarray:
     """ABI-level cycle scan (pscwin_cycle_scan): xin, z [B,L,D] in grid (row-major token) order.
     Per image: flatten in scan order, replicate three times, run the SSM over 3L (cycle_ssm_3L),
     "split into the corresponding three sequences and ... merged through summation" (P:L165).
-    z None => no SiLU(z) gate. Returns g [B,L,D] in grid order."""
+    z None => no SiLU(z) gate. Returns g [B,L,D] (or [B,L,len(channels)]) in grid order."""
     B, L, D = xin.shape
     pi = scan_permutation(H, W, scan_order, window)
-    out = np.empty((B, L, D))
+    nd = D if channels is None else len(channels)
+    out = np.empty((B, L, nd))
     for b in range(B):
         s = xin[b][pi]
-        xin3 = np.concatenate([s, s, s])
-        if z is None:
-            g3 = _cycle_ssm_nogate(xin3, wt, bbar_mode)
-        else:
-            zz = z[b][pi]
-            g3 = cycle_ssm_3L(xin3, np.concatenate([zz, zz, zz]), wt, bbar_mode)
-        g = g3[:L] + g3[L:2 * L] + g3[2 * L:]
-        out[b][pi] = g
+        z3 = None if z is None else np.concatenate([z[b][pi]] * 3)
+        g3 = cycle_ssm_3L(np.concatenate([s, s, s]), z3, wt, bbar_mode, channels)
+        out[b][pi] = g3[:L] + g3[L:2 * L] + g3[2 * L:]
     return out
-
-
-def _cycle_ssm_nogate(xin3, wt, bbar_mode):
-    R = wt["w_dt"].shape[1]
-    N = wt["a_log"].shape[1]
-    v = silu(causal_conv1d(xin3, wt["conv_w"], wt["conv_b"]))
-    dbc = v @ wt["w_x"].T
-    delta = softplus(dbc[:, :R] @ wt["w_dt"].T + wt["b_dt"])
-    return selective_scan_sequential(v, delta, -np.exp(wt["a_log"]), dbc[:, R:R + N], dbc[:, R + N:], wt["d_skip"], bbar_mode)
 
 
 def cycle_scan_module(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False):

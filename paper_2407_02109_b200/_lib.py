@@ -25,6 +25,7 @@ EXPORTS = [
     "pscwin_index_map", "pscwin_window_partition", "pscwin_shifted_pad_partition", "pscwin_window_merge",
     "pscwin_layer_norm", "pscwin_linear", "pscwin_qkv_project", "pscwin_window_attention", "pscwin_cycle_scan",
     "pscwin_scan_workspace_bytes", "pscwin_workspace_bytes", "pscwin_forward",
+    "pscwin_launch_count", "pscwin_profile_enable", "pscwin_profile_read",
 ]
 
 
@@ -104,6 +105,10 @@ def lib() -> ctypes.CDLL:
         "pscwin_workspace_bytes": ([ctypes.POINTER(LayerDesc)], sz),
         "pscwin_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
                            ctypes.c_int),
+        "pscwin_launch_count": ([], ctypes.c_int64),
+        "pscwin_profile_enable": ([ctypes.c_int], None),
+        "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],
+                                ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -124,6 +129,24 @@ def window_count(H: int, W: int, window: int, sx: int = 0, sy: int = 0) -> int:
     n = ctypes.c_int32()
     check(lib().pscwin_window_count(H, W, window, sx, sy, ctypes.byref(n)), "window_count")
     return n.value
+
+
+def launch_count() -> int:
+    return int(lib().pscwin_launch_count())
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().pscwin_profile_enable(int(on))
+
+
+def profile_read(max_entries: int = 64) -> Dict[str, tuple]:
+    """{kernel label: (total_ms, launches)} for the launches recorded since profile_enable()."""
+    names = ctypes.create_string_buffer(8192)
+    ms = (ctypes.c_double * max_entries)()
+    cnt = (ctypes.c_int32 * max_entries)()
+    n = lib().pscwin_profile_read(names, 8192, ms, cnt, max_entries)
+    labels = names.value.decode().split("\n")[:n]
+    return {labels[i]: (ms[i], cnt[i]) for i in range(n)}
 
 
 def index_map(H: int, W: int, window: int, sx: int = 0, sy: int = 0) -> np.ndarray:

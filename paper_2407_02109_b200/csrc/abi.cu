@@ -187,6 +187,7 @@ int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt,
   a.out = qkv;
   a.ldo = 3 * C;
   a.epi = EPI_QKV_ROPE;
+  a.prof_name = "gemm_qkv_rope";
   a.bias = (const float*)wt->b_qkv;
   a.rope = d->rope;
   a.HW = d->H * d->W;
@@ -409,6 +410,7 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   a.out = x_out;
   a.ldo = C;
   a.epi = EPI_RESID_BF16;
+  a.prof_name = "gemm_out_proj";
   a.bias = (const float*)wt->b_o;
   a.residual = x;
   a.ldr = C;

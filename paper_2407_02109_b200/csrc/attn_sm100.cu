@@ -11,8 +11,7 @@
 // (shifted windows) are zero-filled by TMA and the pad rows are patched in shared memory from tiny per-layer
 // tables (rotated k_p halves per x / y coordinate, v_p). S = Q K^T accumulates in TMEM (fp32), softmax runs
 // one row per thread in fp32 (exp2 with log2(e)/sqrt(d) folded), P is written bf16 to swizzled smem, O = P V
-// accumulates in TMEM, and the merge/crop is a TMA store of the same box shape (out-of-grid rows are clipped
-// by the hardware). No L^2 buffer exists anywhere (App. A.6).
+// accumulates in TMEM, and the merge/crop writes each real row straight to the [B,H,W,C] grid (pad rows dropped). No L^2 buffer exists anywhere (App. A.6).
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -32,12 +31,12 @@ struct AttnKArgs {
   const __nv_bfloat16* ky;  // [Hp][heads][d/2]  rotated second half at y = Y (index Y + pt)
   const __nv_bfloat16* vp;  // [heads][d]
   int Wp, Hp;
+  __nv_bfloat16* out;       // [B,H,W,C]
 };
 
 template <int D>
 __global__ void __launch_bounds__(ATT_THREADS, 2)
-    window_attn_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmO,
-                       AttnKArgs p) {
+    window_attn_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnKArgs p) {
   constexpr int ROWB = D * 2;                 // bytes per row of Q/K/V/O (64 or 128)
   constexpr int TILE_BYTES = 128 * ROWB;      // smem rows allocated per operand
   constexpr uint32_t LAYOUT = ROWB == 128 ? kLayoutSW128 : kLayoutSW64;
@@ -234,24 +233,26 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
     }
   }
 
-  // ---- normalise, stage bf16 rows (swizzled like the store map) in sQ, TMA-store the box (clips pad rows)
-  const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+  // ---- normalise and write this thread's row straight to the grid (merge/crop: pad query rows are dropped).
+  // (A TMA tensor store would clip the box, but box origins left of / above the grid are illegal for stores.)
+  {
+    const int iy = qt * p.rpt + tid / w, ix = tid % w;
+    const int Y = Y0 + iy, X = X0 + ix;
+    if (tid < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
 #pragma unroll
-  for (int c = 0; c < D / 8; ++c) {
-    uint4 v;
-    v.x = pack_bf16(o_acc[c * 8 + 0] * inv, o_acc[c * 8 + 1] * inv);
-    v.y = pack_bf16(o_acc[c * 8 + 2] * inv, o_acc[c * 8 + 3] * inv);
-    v.z = pack_bf16(o_acc[c * 8 + 4] * inv, o_acc[c * 8 + 5] * inv);
-    v.w = pack_bf16(o_acc[c * 8 + 6] * inv, o_acc[c * 8 + 7] * inv);
-    *reinterpret_cast<uint4*>(sQ + swz_offset(tid, c, ROWB)) = v;
+      for (int c = 0; c < D / 8; ++c) {
+        uint4 v;
+        v.x = pack_bf16(o_acc[c * 8 + 0] * inv, o_acc[c * 8 + 1] * inv);
+        v.y = pack_bf16(o_acc[c * 8 + 2] * inv, o_acc[c * 8 + 3] * inv);
+        v.z = pack_bf16(o_acc[c * 8 + 4] * inv, o_acc[c * 8 + 5] * inv);
+        v.w = pack_bf16(o_acc[c * 8 + 6] * inv, o_acc[c * 8 + 7] * inv);
+        dst[c] = v;
+      }
+    }
   }
-  fence_proxy_async_smem();
-  __syncthreads();
-  if (tid == 0) {
-    tma_store_5d(&tmO, sQ, 0, h, X0, Y0 + qt * p.rpt, b);
-    bulk_commit();
-    bulk_wait0();
-  }
+  tc_fence_before();
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -334,10 +335,11 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
     p.ky = ky;
     p.vp = vp;
     int n = (p.Wp + p.Hp) * a.C / 2 + a.C;
+    PSCWIN_PROF("pad_tables", stream);
     pad_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
                                                            a.rope_tab, a.rope_off, kx, ky, vp);
   }
-  CUtensorMap tmQKV, tmO;
+  CUtensorMap tmQKV;
   const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
   const uint64_t sq[4] = {(uint64_t)d * 2, (uint64_t)3 * a.C * 2, (uint64_t)a.W * 3 * a.C * 2,
                           (uint64_t)a.H * a.W * 3 * a.C * 2};
@@ -345,26 +347,24 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
   const CUtensorMapSwizzle swz = d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   int rc = make_tmap_5d(&tmQKV, a.qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dq, sq, box, swz);
   if (rc) return rc;
-  const uint64_t dout[5] = {(uint64_t)d, (uint64_t)a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
-  const uint64_t sout[4] = {(uint64_t)d * 2, (uint64_t)a.C * 2, (uint64_t)a.W * a.C * 2, (uint64_t)a.H * a.W * a.C * 2};
-  rc = make_tmap_5d(&tmO, a.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dout, sout, box, swz);
-  if (rc) return rc;
+  p.out = reinterpret_cast<__nv_bfloat16*>(a.out);
   const size_t smem = 1024 + 3 * 128 * d * 2 + 128 * 256 + 64;
   dim3 grid(p.n_tiles, a.heads, a.B * p.nw);
+  PSCWIN_PROF("window_attention", stream);
   if (d == 64) {
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(window_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       set = true;
     }
-    window_attn_kernel<64><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, tmO, p);
+    window_attn_kernel<64><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, p);
   } else {
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(window_attn_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       set = true;
     }
-    window_attn_kernel<32><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, tmO, p);
+    window_attn_kernel<32><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, p);
   }
   return (int)cudaGetLastError();
 }

@@ -1,17 +1,557 @@
-// Cycle scan — placeholder until the chunked closed-form kernels land.
+// Cycle-scan module (§3.3 Eqs. 2-4, Mamba selective SSM P:L161,
+// cycle scan P:L165 "repeats the image token sequence three times ... scans ... split into the corresponding
+// three sequences and ... merged through summation"; Mamba-1 block internals = DESIGN.md reading Q9).
+//
+// The literal method scans 3L tokens sequentially. The three copies see identical per-token parameters except
+// for the first P = k-1 tokens of copy 1, whose causal conv sees zero history (reading Q10). With diagonal A the
+// summed output obeys (pinned in fp64 by tests/test_oracle_pins.py):
+//   prefix t < P : per copy, h^(c)_t from c_1 = 0, c_2 = end of copy 1, c_3 = end of copy 2
+//   body  t >= P : H_t = A_bar_t H_{t-1} + 3 B_bar_t v_t ,  y_t = C_t . H_t + 3 D v_t ,  H_{P-1} = sum_c h^(c)_{P-1}
+// so the GPU runs two chunk-parallel passes over L instead of one sequential pass over 3L:
+//   conv      : v = SiLU(causal conv) for the copy-2/3 stream (history = sequence tail) + the P copy-1 rows
+//   x_proj    : (delta_low, B, C) = v W_x^T on tcgen05 (f32 out)
+//   pass 1    : per (chunk, channel): Delta = softplus(delta_low W_dt^T + b_dt) (stored for pass 2), chunk sum
+//               of Delta and the chunk-end state from zero (b_c)       — thread per channel, N states in registers
+//   carry     : per (image, channel) warp, lane = state: copy prefixes, fold of (exp(A sum Delta), b_c) over the
+//               chunks, c_2, c_3, the prefix outputs, and every chunk's entry state H_in
+//   pass 2    : per (chunk, channel): the summed recurrence from H_in, y, gate SiLU(z), bf16 store
+// Transcendentals: ex2.approx on the MUFU pipe (A pre-scaled by log2 e); everything else FP32.
+#include <math.h>
+#include <string.h>
+
 #include "../../include/pscwin.h"
+#include "common.cuh"
 #include "pscwin_internal.h"
 
 namespace pscwin {
-int cycle_scan_module(const void*, const void*, const void*, void*, void*, size_t, size_t, size_t, size_t, size_t,
-                      cudaStream_t) {
-  return PSCWIN_ERR_UNSUPPORTED;
+
+namespace {
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int TS = 32;  // tokens staged per smem round in the passes
 }
+
+struct ScanParams {
+  int B, L, D, N, R, k, P, Lc, n_chunks, bbar;
+  const __nv_bfloat16* xin;
+  long long ld_x;
+  const __nv_bfloat16* z;
+  long long ld_z;
+  const float *conv_w, *conv_b, *w_dt, *b_dt, *a_log, *d_skip;
+  __nv_bfloat16* v;  // [B, L+P, D]
+  float* dbc;        // [B, L+P, R+2N]
+  float* delta;      // [B, L+P, D]
+  float* sumdt;      // [B, n_chunks, D]
+  float* hs;         // [B, n_chunks, D, N]
+  __nv_bfloat16* out;
+  long long ld_out;
+};
+
+__device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
+__device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log1pf(__expf(x)); }
+
+// ------------------------------------------------------------------------------------------------- conv
+// v rows [0, L): copy-2/3 stream (tap index wraps to the sequence tail); rows [L, L+P): copy-1 tokens 0..P-1
+// (taps before the sequence start contribute 0). 8 channels per thread.
+__global__ void conv_silu_kernel(ScanParams p) {
+  const int dv = p.D / 8;
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long rows = (long long)p.B * (p.L + p.P);
+  if (idx >= rows * dv) return;
+  const int d0 = (int)(idx % dv) * 8;
+  const long long row = idx / dv;
+  const int b = (int)(row / (p.L + p.P));
+  const int r = (int)(row - (long long)b * (p.L + p.P));
+  const bool copy1 = r >= p.L;
+  const int t = copy1 ? r - p.L : r;
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = p.conv_b[d0 + j];
+  for (int i = 0; i < p.k; ++i) {
+    int j = t - (p.k - 1) + i;
+    if (j < 0) {
+      if (copy1) continue;
+      j += p.L;
+    }
+    const uint4 xv = *reinterpret_cast<const uint4*>(p.xin + ((long long)b * p.L + j) * p.ld_x + d0);
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      acc[2 * q] = fmaf(p.conv_w[(d0 + 2 * q) * p.k + i], bf16_lo(xw[q]), acc[2 * q]);
+      acc[2 * q + 1] = fmaf(p.conv_w[(d0 + 2 * q + 1) * p.k + i], bf16_hi(xw[q]), acc[2 * q + 1]);
+    }
+  }
+  uint4 o;
+  uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ow[q] = pack_bf16(silu_f(acc[2 * q]), silu_f(acc[2 * q + 1]));
+  *reinterpret_cast<uint4*>(p.v + row * p.D + d0) = o;
+}
+
+// ------------------------------------------------------------------------------------------------- pass 1
+template <int N, int RMAX>
+__global__ void __launch_bounds__(128) scan_pass1_kernel(ScanParams p) {
+  extern __shared__ float s_dbc[];  // [TS][R+2N]
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int b = blockIdx.z;
+  const int W = p.R + 2 * N;
+  const long long rbase = (long long)b * (p.L + p.P);
+  float A2[N], invA[N], h[N], wdt[RMAX];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    const float A = -__expf(p.a_log[d * N + n]);
+    A2[n] = A * kLog2e;
+    invA[n] = 1.f / A;
+    h[n] = 0.f;
+  }
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) wdt[r] = r < p.R ? p.w_dt[d * p.R + r] : 0.f;
+  const float bdt = p.b_dt[d];
+  const bool zoh = p.bbar == 0;
+
+  auto compute_dt = [&](const float* drow) {
+    float acc = bdt;
+#pragma unroll
+    for (int r = 0; r < RMAX; ++r)
+      if (r < p.R) acc = fmaf(drow[r], wdt[r], acc);
+    return softplus_f(acc);
+  };
+
+  const int t0 = chunk * p.Lc;
+  const int t1 = min(p.L, t0 + p.Lc);
+  // chunk 0 also produces Delta of the P prefix tokens of both streams (used by the carry kernel)
+  if (chunk == 0) {
+    for (int q = 0; q < 2 * p.P; ++q) {
+      const long long row = rbase + (q < p.P ? q : p.L + (q - p.P));
+      const float dt = compute_dt(p.dbc + row * W);
+      p.delta[row * p.D + d] = dt;
+    }
+  }
+  const int tb = max(t0, p.P);
+  float sdt = 0.f;
+  for (int ts = tb; ts < t1; ts += TS) {
+    const int nt = min(TS, t1 - ts);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * W / 4; i += blockDim.x)
+      reinterpret_cast<float4*>(s_dbc)[i] = reinterpret_cast<const float4*>(p.dbc + (rbase + ts) * W)[i];
+    __syncthreads();
+    for (int j = 0; j < nt; ++j) {
+      const long long row = rbase + ts + j;
+      const float* drow = s_dbc + j * W;
+      const float v = __bfloat162float(p.v[row * p.D + d]);
+      const float dt = compute_dt(drow);
+      p.delta[row * p.D + d] = dt;
+      sdt += dt;
+      const float* Bt = drow + p.R;
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float dA = ex2_approx(dt * A2[n]);
+        const float dBv = zoh ? (dA - 1.f) * invA[n] * Bt[n] * v : dt * Bt[n] * v;
+        h[n] = fmaf(dA, h[n], dBv);
+      }
+    }
+  }
+  p.sumdt[((long long)b * p.n_chunks + chunk) * p.D + d] = sdt;
+  float4* dst = reinterpret_cast<float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
+#pragma unroll
+  for (int n = 0; n < N; n += 4) dst[n / 4] = make_float4(h[n], h[n + 1], h[n + 2], h[n + 3]);
+}
+
+// ------------------------------------------------------------------------------------------------- carry
+// One warp per (image, channel); lane owns states n = lane + 32 j. Produces the prefix outputs and every chunk's
+// entry state (overwriting the pass-1 chunk-end states in place).
+template <int N>
+__global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
+  constexpr int NPL = (N + 31) / 32;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp_global >= p.B * p.D) return;
+  const int b = warp_global / p.D;
+  const int d = warp_global - b * p.D;
+  const int W = p.R + 2 * N;
+  const long long rbase = (long long)b * (p.L + p.P);
+  const bool zoh = p.bbar == 0;
+  float A2[NPL], invA[NPL];
+  bool act[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int n = lane + 32 * j;
+    act[j] = n < N;
+    const float A = act[j] ? -__expf(p.a_log[d * N + n]) : -1.f;
+    A2[j] = A * kLog2e;
+    invA[j] = 1.f / A;
+  }
+  auto step = [&](float (&h)[NPL], long long row) {
+    const float dt = p.delta[row * p.D + d];
+    const float v = __bfloat162float(p.v[row * p.D + d]);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      if (!act[j]) continue;
+      const float Bn = p.dbc[row * W + p.R + lane + 32 * j];
+      const float dA = ex2_approx(dt * A2[j]);
+      const float dBv = zoh ? (dA - 1.f) * invA[j] * Bn * v : dt * Bn * v;
+      h[j] = fmaf(dA, h[j], dBv);
+    }
+  };
+  // prefix end states: copy 1 from zero (stream rows L..L+P-1); copy-2/3 stream rows 0..P-1 as alpha*c + beta
+  float beta1[NPL], beta2[NPL], alpha2[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) beta1[j] = beta2[j] = 0.f;
+  float sdt2 = 0.f;
+  for (int t = 0; t < p.P; ++t) {
+    step(beta1, rbase + p.L + t);
+    step(beta2, rbase + t);
+    sdt2 += p.delta[(rbase + t) * p.D + d];
+  }
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) alpha2[j] = ex2_approx(sdt2 * A2[j]);
+  // body fold over chunks: (A_body, B_body) with a_c = exp(A sum_c Delta)
+  const float* sd = p.sumdt + (long long)b * p.n_chunks * p.D + d;
+  float* hs = p.hs + ((long long)b * p.n_chunks * p.D + d) * N;
+  float Bb[NPL], sall = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) Bb[j] = 0.f;
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const float s = sd[(long long)c * p.D];
+    sall += s;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) Bb[j] = fmaf(ex2_approx(s * A2[j]), Bb[j], hs[(long long)c * p.D * N + lane + 32 * j]);
+  }
+  float c2[NPL], c3[NPL], H[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const float Ab = ex2_approx(sall * A2[j]);
+    c2[j] = fmaf(Ab, beta1[j], Bb[j]);
+    const float e2 = fmaf(alpha2[j], c2[j], beta2[j]);
+    c3[j] = fmaf(Ab, e2, Bb[j]);
+    const float e3 = fmaf(alpha2[j], c3[j], beta2[j]);
+    H[j] = beta1[j] + e2 + e3;
+  }
+  // prefix outputs: out_t = (sum_copies C^(c)_t . h^(c)_t + D (v1_t + 2 v2_t)) * SiLU(z_t)
+  {
+    float h1[NPL], h2[NPL], h3[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      h1[j] = 0.f;
+      h2[j] = c2[j];
+      h3[j] = c3[j];
+    }
+    const float Ds = p.d_skip[d];
+    for (int t = 0; t < p.P; ++t) {
+      const long long r1 = rbase + p.L + t, r2 = rbase + t;
+      step(h1, r1);
+      step(h2, r2);
+      step(h3, r2);
+      float y = 0.f;
+#pragma unroll
+      for (int j = 0; j < NPL; ++j)
+        if (act[j]) {
+          const int n = lane + 32 * j;
+          y += p.dbc[r1 * W + p.R + N + n] * h1[j] + p.dbc[r2 * W + p.R + N + n] * (h2[j] + h3[j]);
+        }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (lane == 0) {
+        y += Ds * (__bfloat162float(p.v[r1 * p.D + d]) + 2.f * __bfloat162float(p.v[r2 * p.D + d]));
+        const long long tok = (long long)b * p.L + t;
+        const float g = p.z ? silu_f(__bfloat162float(p.z[tok * p.ld_z + d])) : 1.f;
+        p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
+      }
+    }
+  }
+  // chunk entry states of the summed recurrence (input x3): H_in(0) = H_{P-1}; H_in(c+1) = a_c H_in(c) + 3 b_c
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const float s = sd[(long long)c * p.D];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) {
+        float* slot = hs + (long long)c * p.D * N + lane + 32 * j;
+        const float bc = *slot;
+        *slot = H[j];
+        H[j] = fmaf(ex2_approx(s * A2[j]), H[j], 3.f * bc);
+      }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------- pass 2
+template <int N>
+__global__ void __launch_bounds__(128) scan_pass2_kernel(ScanParams p) {
+  extern __shared__ float s_dbc[];
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  const int chunk = blockIdx.y;
+  const int b = blockIdx.z;
+  const int W = p.R + 2 * N;
+  const long long rbase = (long long)b * (p.L + p.P);
+  float A2[N], invA[N], h[N];
+  const float4* src = reinterpret_cast<const float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
+#pragma unroll
+  for (int n = 0; n < N; n += 4) {
+    const float4 q = src[n / 4];
+    h[n] = q.x;
+    h[n + 1] = q.y;
+    h[n + 2] = q.z;
+    h[n + 3] = q.w;
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    const float A = -__expf(p.a_log[d * N + n]);
+    A2[n] = A * kLog2e;
+    invA[n] = 1.f / A;
+  }
+  const float D3 = 3.f * p.d_skip[d];
+  const bool zoh = p.bbar == 0;
+  const int t0 = chunk * p.Lc;
+  const int t1 = min(p.L, t0 + p.Lc);
+  const int tb = max(t0, p.P);
+  for (int ts = tb; ts < t1; ts += TS) {
+    const int nt = min(TS, t1 - ts);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * W / 4; i += blockDim.x)
+      reinterpret_cast<float4*>(s_dbc)[i] = reinterpret_cast<const float4*>(p.dbc + (rbase + ts) * W)[i];
+    __syncthreads();
+    for (int j = 0; j < nt; ++j) {
+      const long long row = rbase + ts + j;
+      const float* Bt = s_dbc + j * W + p.R;
+      const float* Ct = Bt + N;
+      const float v = __bfloat162float(p.v[row * p.D + d]);
+      const float dt = p.delta[row * p.D + d];
+      const float v3 = 3.f * v;
+      float y = D3 * v;
+#pragma unroll
+      for (int n = 0; n < N; ++n) {
+        const float dA = ex2_approx(dt * A2[n]);
+        const float dBv = zoh ? (dA - 1.f) * invA[n] * Bt[n] * v3 : dt * Bt[n] * v3;
+        h[n] = fmaf(dA, h[n], dBv);
+        y = fmaf(Ct[n], h[n], y);
+      }
+      const long long tok = (long long)b * p.L + ts + j;
+      const float g = p.z ? silu_f(__bfloat162float(p.z[tok * p.ld_z + d])) : 1.f;
+      p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------- host
+struct ScanPlan {
+  int P, Lc, n_chunks, W;
+  size_t v, dbc, delta, sumdt, hs, total;
+};
+
+static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static int choose_chunk(int B, int L, int D) {
+  // aim for >= ~4 waves of 128-channel CTAs over 148 SMs; chunk length a multiple of TS
+  const long long ctas_per_chunk = (long long)B * (D / 128 > 0 ? D / 128 : 1);
+  long long target_chunks = (4LL * 148 + ctas_per_chunk - 1) / ctas_per_chunk;
+  long long lc = (L + target_chunks - 1) / target_chunks;
+  lc = ((lc + TS - 1) / TS) * TS;
+  if (lc < TS) lc = TS;
+  return (int)lc;
+}
+
+static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
+  ScanPlan s;
+  s.P = k - 1;
+  s.Lc = choose_chunk(B, L, D);
+  s.n_chunks = (L + s.Lc - 1) / s.Lc;
+  s.W = R + 2 * N;
+  const size_t rows = (size_t)B * (L + s.P);
+  size_t off = 0;
+  s.v = off;
+  off += al256(rows * D * 2);
+  s.dbc = off;
+  off += al256(rows * s.W * 4);
+  s.delta = off;
+  off += al256(rows * (size_t)D * 4);
+  s.sumdt = off;
+  off += al256((size_t)B * s.n_chunks * D * 4);
+  s.hs = off;
+  off += al256((size_t)B * s.n_chunks * D * N * 4);
+  s.total = off;
+  return s;
+}
+
+static int check_scan(int B, int L, int D, int N, int R, int k) {
+  if (B <= 0 || L <= 0 || D <= 0 || N <= 0 || R <= 0 || k <= 0) return PSCWIN_ERR_SHAPE;
+  if (L < k - 1) return PSCWIN_ERR_CONTRACT;  // copies 2 and 3 must see a full history
+  if (!(N == 16 || N == 32 || N == 64)) return PSCWIN_ERR_UNSUPPORTED;
+  if (R > 64 || (R + 2 * N) % 4) return PSCWIN_ERR_UNSUPPORTED;
+  if (D % 128 && D % 32) return PSCWIN_ERR_UNSUPPORTED;
+  if (D % 64) return PSCWIN_ERR_UNSUPPORTED;  // x_proj GEMM K tiles
+  return PSCWIN_OK;
+}
+
+template <int N>
+static int launch_passes(ScanParams& p, cudaStream_t s) {
+  const int tpb = p.D % 128 == 0 ? 128 : (p.D % 64 == 0 ? 64 : 32);
+  dim3 grid(p.D / tpb, p.n_chunks, p.B);
+  const size_t smem = (size_t)TS * (p.R + 2 * N) * 4;
+  {
+  PSCWIN_PROF("scan_pass1", s);
+  if (p.R <= 16)
+    scan_pass1_kernel<N, 16><<<grid, tpb, smem, s>>>(p);
+  else if (p.R <= 48)
+    scan_pass1_kernel<N, 48><<<grid, tpb, smem, s>>>(p);
+  else
+    scan_pass1_kernel<N, 64><<<grid, tpb, smem, s>>>(p);
+  }
+  const int warps = p.B * p.D;
+  {
+    PSCWIN_PROF("scan_carry", s);
+    scan_carry_kernel<N><<<(warps + 7) / 8, 256, 0, s>>>(p);
+  }
+  {
+    PSCWIN_PROF("scan_pass2", s);
+    scan_pass2_kernel<N><<<grid, tpb, smem, s>>>(p);
+  }
+  return (int)cudaGetLastError();
+}
+
+// Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out).
+static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, const __nv_bfloat16* xin,
+                          long long ld_x, const __nv_bfloat16* z, long long ld_z, const float* conv_w,
+                          const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
+                          const float* a_log, const float* d_skip, __nv_bfloat16* out, long long ld_out, void* ws,
+                          size_t ws_bytes, cudaStream_t s) {
+  ScanPlan pl = plan_scan(B, L, D, N, R, k);
+  if (ws_bytes < pl.total) return PSCWIN_ERR_WORKSPACE;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  ScanParams p;
+  p.B = B;
+  p.L = L;
+  p.D = D;
+  p.N = N;
+  p.R = R;
+  p.k = k;
+  p.P = pl.P;
+  p.Lc = pl.Lc;
+  p.n_chunks = pl.n_chunks;
+  p.bbar = bbar;
+  p.xin = xin;
+  p.ld_x = ld_x;
+  p.z = z;
+  p.ld_z = ld_z;
+  p.conv_w = conv_w;
+  p.conv_b = conv_b;
+  p.w_dt = w_dt;
+  p.b_dt = b_dt;
+  p.a_log = a_log;
+  p.d_skip = d_skip;
+  p.v = reinterpret_cast<__nv_bfloat16*>(base + pl.v);
+  p.dbc = reinterpret_cast<float*>(base + pl.dbc);
+  p.delta = reinterpret_cast<float*>(base + pl.delta);
+  p.sumdt = reinterpret_cast<float*>(base + pl.sumdt);
+  p.hs = reinterpret_cast<float*>(base + pl.hs);
+  p.out = out;
+  p.ld_out = ld_out;
+  const long long rows = (long long)B * (L + pl.P);
+  const long long nthreads = rows * (D / 8);
+  {
+    PSCWIN_PROF("conv_silu", s);
+    conv_silu_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p);
+  }
+  GemmArgs g;
+  memset(&g, 0, sizeof(g));
+  g.prof_name = "gemm_x_proj";
+  g.M = (int)rows;
+  g.N = pl.W;
+  g.K = D;
+  g.lda = D;
+  g.ldb = D;
+  g.out = p.dbc;
+  g.ldo = pl.W;
+  g.epi = EPI_STORE_F32;
+  int rc = launch_gemm_bf16(p.v, w_x, g, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  if (N == 16) rc = launch_passes<16>(p, s);
+  else if (N == 32) rc = launch_passes<32>(p, s);
+  else rc = launch_passes<64>(p, s);
+  return rc ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
+size_t scan_ws_bytes(int B, int L, int D, int N, int R, int k) { return plan_scan(B, L, D, N, R, k).total; }
+
+int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, void* x_out, void* ws, size_t off_u,
+                      size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s) {
+  const pscwin_layer_desc* d = reinterpret_cast<const pscwin_layer_desc*>(desc_v);
+  const pscwin_layer_weights* w = reinterpret_cast<const pscwin_layer_weights*>(wts_v);
+  if (!w->lns_g || !w->lns_b || !w->w_in || !w->conv_w || !w->conv_b || !w->w_x || !w->w_dt || !w->b_dt ||
+      !w->a_log || !w->d_skip || !w->w_out)
+    return PSCWIN_ERR_SHAPE;
+  if (d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_UNSUPPORTED;
+  const int C = d->C, D = d->ssm_expand * C, N = d->ssm_state;
+  const int R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (C + 15) / 16;
+  const int L = d->H * d->W;
+  int rc = check_scan(d->B, L, D, N, R, d->ssm_conv);
+  if (rc) return rc;
+  const long long T = (long long)d->B * L;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(base + off_u);
+  __nv_bfloat16* xz = reinterpret_cast<__nv_bfloat16*>(base + off_xz);
+  __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(base + off_g);
+  // a1: u0 = LN_s(x); [xin, z] = u0 W_in^T
+  rc = launch_layer_norm(x_in, T, C, (const float*)w->lns_g, (const float*)w->lns_b, d->ln_eps, 0, u, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_in_proj";
+  a.M = (int)T;
+  a.N = 2 * D;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = xz;
+  a.ldo = 2 * D;
+  a.epi = EPI_STORE_BF16;
+  rc = launch_gemm_bf16(u, w->w_in, a, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  // a2: cycle scan -> g = sum over copies of y * SiLU(z)
+  rc = run_cycle_scan(d->B, L, D, N, R, d->ssm_conv, d->bbar_mode, xz, 2 * D, xz + D, 2 * D,
+                      (const float*)w->conv_w, (const float*)w->conv_b, w->w_x, (const float*)w->w_dt,
+                      (const float*)w->b_dt, w->a_log, w->d_skip, g, D, base + off_scan, scan_bytes, s);
+  if (rc) return rc;
+  // a3: x_out = x_in + g W_out^T (the sum over copies commutes with the bias-free out_proj)
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_out_proj_scan";
+  a.M = (int)T;
+  a.N = C;
+  a.K = D;
+  a.lda = D;
+  a.ldb = D;
+  a.out = x_out;
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.residual = x_in;
+  a.ldr = C;
+  rc = launch_gemm_bf16(g, w->w_out, a, s);
+  return rc ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
 }  // namespace pscwin
 
-extern "C" size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc*) { return 256; }
-extern "C" int pscwin_cycle_scan(const pscwin_scan_desc*, const void*, const void*, const float*, const float*,
-                                 const void*, const float*, const float*, const float*, const float*, void*, void*,
-                                 size_t, void*) {
-  return PSCWIN_ERR_UNSUPPORTED;
+using namespace pscwin;
+
+extern "C" size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* d) {
+  if (!d) return 0;
+  const int L = d->H * d->W;
+  if (check_scan(d->B, L, d->D, d->N, d->R, d->conv_k) != PSCWIN_OK) return 0;
+  return scan_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k);
+}
+
+extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, const void* z, const float* conv_w,
+                                 const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
+                                 const float* a_log, const float* d_skip, void* out, void* ws, size_t ws_bytes,
+                                 void* stream) {
+  if (!d || !xin || !conv_w || !conv_b || !w_x || !w_dt || !b_dt || !a_log || !d_skip || !out)
+    return PSCWIN_ERR_SHAPE;
+  if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_UNSUPPORTED;
+  const int L = d->H * d->W;
+  int rc = check_scan(d->B, L, d->D, d->N, d->R, d->conv_k);
+  if (rc) return rc;
+  if (((uintptr_t)xin | (uintptr_t)z | (uintptr_t)out | (uintptr_t)ws | (uintptr_t)w_x) & 15) return PSCWIN_ERR_ALIGN;
+  return run_cycle_scan(d->B, L, d->D, d->N, d->R, d->conv_k, d->bbar_mode, (const __nv_bfloat16*)xin, d->D,
+                        (const __nv_bfloat16*)z, d->D, conv_w, conv_b, w_x, w_dt, b_dt, a_log, d_skip,
+                        (__nv_bfloat16*)out, d->D, ws, ws_bytes, (cudaStream_t)stream);
 }

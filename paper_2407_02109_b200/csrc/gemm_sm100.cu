@@ -234,6 +234,7 @@ __global__ void rope_table_kernel(float2* tab, int n_pos, int off, int d) {
 
 int launch_rope_table(float2* tab, int n_pos, int off, int d, cudaStream_t stream) {
   int n = n_pos * (d / 4);
+  PSCWIN_PROF("rope_table", stream);
   rope_table_kernel<<<(n + 255) / 256, 256, 0, stream>>>(tab, n_pos, off, d);
   return (int)cudaGetLastError();
 }
@@ -258,6 +259,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   }
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
+  PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
   gemm_bf16_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, tmB, p);
   return (int)cudaGetLastError();
 }

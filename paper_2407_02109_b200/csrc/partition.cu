@@ -111,6 +111,7 @@ int launch_partition(const void* x, const void* pad_row, int B, int H, int W, in
   size_t row_bytes = (size_t)Cx * esize;
   bool vec16 = row_bytes % 16 == 0 && ((uintptr_t)x % 16 == 0) && ((uintptr_t)out % 16 == 0) &&
                (pad_row == nullptr || (uintptr_t)pad_row % 16 == 0);
+  PSCWIN_PROF("partition", stream);
   if (vec16) {
     partition_kernel<uint4><<<grid, 256, 0, stream>>>((const uint4*)x, (const uint4*)pad_row, (uint4*)out, g,
                                                       (int)(row_bytes / 16), n_rows);
@@ -130,6 +131,7 @@ int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, in
   long long n_rows = (long long)B * H * W;
   if (n_rows == 0) return 0;
   unsigned grid = (unsigned)((n_rows + 7) / 8);
+  PSCWIN_PROF("merge", stream);
   if (is_f32) {
     merge_kernel<float><<<grid, 256, 0, stream>>>((const float*)win, (const float*)residual, (float*)out, g, Cx,
                                                   n_rows);

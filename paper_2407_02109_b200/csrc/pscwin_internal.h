@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "prof.h"
+
 namespace pscwin {
 
 enum GemmEpilogue { EPI_STORE_BF16 = 0, EPI_STORE_F32 = 1, EPI_QKV_ROPE = 2, EPI_RESID_BF16 = 3 };
@@ -22,6 +24,7 @@ struct GemmArgs {
   // QKV + RoPE epilogue
   int rope, HW, Wgrid, C, d_head, rope_off;
   const float2* rope_tab;
+  const char* prof_name;  // kernel label for pscwin_profile_read
 };
 
 // host helpers (abi.cu)

@@ -77,6 +77,7 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
                       void* out, cudaStream_t stream) {
   if (rows == 0) return 0;
   unsigned grid = (unsigned)((rows + 7) / 8);
+  PSCWIN_PROF("layer_norm", stream);
   if (is_f32) {
     if (C % 4 || C > 1024) return -1;
     layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, rows, C, g, b, eps, (float*)out);
@@ -115,6 +116,7 @@ __global__ void pad_qkv_kernel(const T* __restrict__ pad, const T* __restrict__ 
 int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C, int is_f32, float* out,
                    cudaStream_t stream) {
   unsigned grid = (unsigned)((3 * C + 7) / 8);
+  PSCWIN_PROF("pad_qkv", stream);
   if (is_f32)
     pad_qkv_kernel<float><<<grid, 256, 0, stream>>>((const float*)pad, (const float*)w_qkv, b_qkv, C, out);
   else

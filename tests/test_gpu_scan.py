@@ -1,0 +1,99 @@
+"""GPU parity of the cycle scan (a2, via pscwin_cycle_scan) and the cycle-scan layer (a1-a3 + attention, via
+pscwin_forward) against the oracle's literal 3L sequential recurrence (Eq. 4)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2407_02109_b200 as p
+    return p
+
+
+def _scan_inputs(cfg, seed=3):
+    B, L, D = cfg.B, cfg.H * cfg.W, cfg.D
+    xin = synth.round_bf16(0.6 * synth.normal(synth.stream_seed(seed, 1), B * L * D).reshape(B, L, D))
+    z = synth.round_bf16(synth.normal(synth.stream_seed(seed, 2), B * L * D).reshape(B, L, D))
+    return xin, z
+
+
+def _desc(pl, cfg):
+    sd = pl.ScanDesc()
+    sd.B, sd.H, sd.W, sd.D, sd.N, sd.R, sd.conv_k = cfg.B, cfg.H, cfg.W, cfg.D, cfg.N, cfg.R, cfg.ssm_conv
+    sd.scan_order, sd.bbar_mode, sd.dtype = cfg.scan_order, cfg.bbar_mode, 0
+    return sd
+
+
+SCAN_CASES = [
+    synth.tiny(),                                  # D=128, N=16, R=4, L=256
+    synth.tiny(H=10, W=13),                        # ragged L = 130 (partial last chunk)
+    synth.tiny(B=3, H=5, W=7),                     # batch, L = 35
+    synth.tiny(bbar_mode=synth.BBAR_EULER),
+    synth.tiny(H=1, W=3),                          # L = k - 1: empty body, prefix only
+    synth.tiny(C=128, ssm_state=32, ssm_dt_rank=8, H=24, W=24),
+    synth.vitb(64),                                # 1024^2: D=1536, N=32, R=48, L=4096
+]
+
+
+@pytest.mark.parametrize("cfg", SCAN_CASES, ids=lambda c: f"B{c.B}L{c.H}x{c.W}D{c.D}N{c.N}R{c.R}b{c.bbar_mode}")
+def test_cycle_scan(pl, cfg):
+    xin, z = _scan_inputs(cfg)
+    w = synth.make_weights(cfg)
+    dw = dev_weights(w, cfg)
+    got = host(pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dw))
+    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W, bbar_mode=cfg.bbar_mode)
+    assert rel_err(got, ref) < BF16_TOL
+
+
+def test_cycle_scan_no_gate(pl):
+    cfg = synth.tiny(H=8, W=8)
+    xin, _ = _scan_inputs(cfg)
+    w = synth.make_weights(cfg)
+    got = host(pl.cycle_scan(_desc(pl, cfg), dev(xin), None, dev_weights(w, cfg)))
+    ref = oracle.cycle_scan(xin, None, w, cfg.H, cfg.W)
+    assert rel_err(got, ref) < BF16_TOL
+
+
+@pytest.mark.slow
+def test_cycle_scan_4096_sampled_channels(pl):
+    # full 4096^2 sequence (L = 65536, 3L = 196608 sequential oracle steps) on a sample of channels:
+    # channels are independent given (v, Delta, B, C), so the oracle evaluates only those.
+    cfg = synth.vitb(256)
+    xin, z = _scan_inputs(cfg)
+    w = synth.make_weights(cfg)
+    got = host(pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(w, cfg)))
+    ch = [0, 1, 511, 777, 1535]
+    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W, channels=ch)
+    assert rel_err(got[:, :, ch], ref) < BF16_TOL
+
+
+def test_cycle_scan_contract(pl):
+    from paper_2407_02109_b200._lib import PscwinError
+    cfg = synth.tiny(H=1, W=2)  # L = 2 < k - 1: copies 2 and 3 would differ, rejected
+    xin, z = _scan_inputs(cfg)
+    with pytest.raises(PscwinError):
+        pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(synth.make_weights(cfg), cfg))
+
+
+CS_LAYERS = [synth.tiny(cycle_scan=1, shift_x=0, shift_y=0), synth.tiny(cycle_scan=1),
+             synth.vitb(64, cycle_scan=1, shift_x=0, shift_y=0)]
+
+
+@pytest.mark.parametrize("cfg", CS_LAYERS, ids=lambda c: f"{c.H}C{c.C}s{c.shift_x}")
+def test_cycle_scan_layer_forward(pl, cfg):
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))
+    got = host(layer(dev(x)))
+    ref = oracle.pscwin_layer(x, w, cfg)
+    assert rel_err(got, ref) < BF16_TOL
+    inc = ref - x
+    assert float(np.max(np.abs((got - x) - inc))) < BF16_TOL * np.max(np.abs(inc)) + 2.0 ** -8 * np.max(np.abs(ref))
