@@ -191,6 +191,16 @@ PSCWIN_DEVICE void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
 }
 PSCWIN_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ---------------------------------------------------------------------------------------------- cp.async
+PSCWIN_DEVICE void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+PSCWIN_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+PSCWIN_DEVICE void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------------------------------------- numerics
 PSCWIN_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -213,4 +223,11 @@ PSCWIN_DEVICE uint32_t swz_offset(uint32_t row, uint32_t chunk, uint32_t row_byt
   return off ^ (((off >> 7) & 3u) << 4);
 }
 
+}  // namespace pscwin
+
+namespace pscwin {
+PSCWIN_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+PSCWIN_DEVICE void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 }  // namespace pscwin

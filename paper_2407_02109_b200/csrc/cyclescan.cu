@@ -27,7 +27,7 @@ namespace pscwin {
 
 namespace {
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int TS = 32;  // tokens staged per smem round in the passes
+constexpr int TS = 32;  // chunk length granularity
 }
 
 struct ScanParams {
@@ -51,105 +51,214 @@ __device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log
 
 // ------------------------------------------------------------------------------------------------- conv
 // v rows [0, L): copy-2/3 stream (tap index wraps to the sequence tail); rows [L, L+P): copy-1 tokens 0..P-1
-// (taps before the sequence start contribute 0). 8 channels per thread.
+// (taps before the sequence start contribute 0). A thread owns 8 channels x CONV_T consecutive rows and slides
+// the k-tap window along them, so each input vector is loaded once per thread (k <= KMAX).
+constexpr int CONV_T = 8;
+constexpr int KMAX = 4;  // conv width supported by the register window (Mamba default 4)
 __global__ void conv_silu_kernel(ScanParams p) {
   const int dv = p.D / 8;
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long rows = (long long)p.B * (p.L + p.P);
-  if (idx >= rows * dv) return;
-  const int d0 = (int)(idx % dv) * 8;
-  const long long row = idx / dv;
-  const int b = (int)(row / (p.L + p.P));
-  const int r = (int)(row - (long long)b * (p.L + p.P));
-  const bool copy1 = r >= p.L;
-  const int t = copy1 ? r - p.L : r;
-  float acc[8];
+  const int rows_img = p.L + p.P;
+  const int groups_img = (rows_img + CONV_T - 1) / CONV_T;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= p.B * groups_img * dv) return;
+  const int d0 = (idx % dv) * 8;
+  const int grp = idx / dv;
+  const int b = grp / groups_img;
+  const int r0 = (grp - b * groups_img) * CONV_T;
+  float wk[8][KMAX], bias[8];
 #pragma unroll
-  for (int j = 0; j < 8; ++j) acc[j] = p.conv_b[d0 + j];
-  for (int i = 0; i < p.k; ++i) {
-    int j = t - (p.k - 1) + i;
-    if (j < 0) {
-      if (copy1) continue;
-      j += p.L;
+  for (int c = 0; c < 8; ++c) {
+    bias[c] = p.conv_b[d0 + c];
+#pragma unroll
+    for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? p.conv_w[(d0 + c) * p.k + i] : 0.f;
+  }
+  const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
+  float win[KMAX][8];  // the k most recent inputs (slot k-1 = newest)
+  auto load = [&](int r, int j, float (&dst)[8]) {  // input feeding stream row r at tap offset j (j <= 0)
+    const bool copy1 = r >= p.L;
+    int t = (copy1 ? r - p.L : r) + j;
+    if (t < 0) {
+      if (copy1) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dst[c] = 0.f;
+        return;
+      }
+      t += p.L;
     }
-    const uint4 xv = *reinterpret_cast<const uint4*>(p.xin + ((long long)b * p.L + j) * p.ld_x + d0);
+    const uint4 xv = *reinterpret_cast<const uint4*>(xb + (long long)t * p.ld_x);
     const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      acc[2 * q] = fmaf(p.conv_w[(d0 + 2 * q) * p.k + i], bf16_lo(xw[q]), acc[2 * q]);
-      acc[2 * q + 1] = fmaf(p.conv_w[(d0 + 2 * q + 1) * p.k + i], bf16_hi(xw[q]), acc[2 * q + 1]);
+      dst[2 * q] = bf16_lo(xw[q]);
+      dst[2 * q + 1] = bf16_hi(xw[q]);
     }
-  }
-  uint4 o;
-  uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+  };
+  for (int rr = 0; rr < CONV_T; ++rr) {
+    const int r = r0 + rr;
+    if (r >= rows_img) break;
+    const bool fresh = rr == 0 || r == p.L;  // window restarts at the group start and at the copy-1 rows
+    if (fresh) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) ow[q] = pack_bf16(silu_f(acc[2 * q]), silu_f(acc[2 * q + 1]));
-  *reinterpret_cast<uint4*>(p.v + row * p.D + d0) = o;
+      for (int i = 0; i < KMAX; ++i)
+        if (i < p.k) load(r, i - (p.k - 1), win[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < KMAX - 1; ++i)
+        if (i + 1 < p.k) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) win[i][c] = win[i + 1][c];
+        }
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (i == p.k - 1) load(r, 0, win[i]);
+    }
+    float acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      acc[c] = bias[c];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i)
+        if (i < p.k) acc[c] = fmaf(wk[c][i], win[i][c], acc[c]);
+    }
+    uint4 o;
+    uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) ow[q] = pack_bf16(silu_f(acc[2 * q]), silu_f(acc[2 * q + 1]));
+    *reinterpret_cast<uint4*>(p.v + ((long long)b * rows_img + r) * p.D + d0) = o;
+  }
 }
 
+// ------------------------------------------------------------------------------------------------- staging
+// Per-chunk token loop with cp.async double buffering: every per-token operand (the shared (delta_low, B, C)
+// row, and this CTA's slice of v, Delta, z) lands in shared memory one sub-chunk ahead of its use, so the
+// sequential recurrence never waits on a global load. The state is kept scaled, h~ = A h (per (d, n) constant),
+// which turns the ZOH update into h~ <- dA (h~ + w) - w with w = B_t[n] v_t (no 1/A per element).
+template <int DPB, bool PASS2>
+struct Stage {
+  static constexpr int TSUB = 16;
+  float* dbc;              // [TSUB][W]
+  __nv_bfloat16* v;        // [TSUB][DPB]
+  float* dt;               // [TSUB][DPB] (pass 2)
+  __nv_bfloat16* z;        // [TSUB][DPB] (pass 2)
+  __host__ __device__ static size_t bytes(int W) {
+    size_t b = (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 2;
+    if (PASS2) b += (size_t)TSUB * DPB * 4 + (size_t)TSUB * DPB * 2;
+    return (b + 127) & ~size_t(127);
+  }
+  __device__ void carve(uint8_t* base, int W) {
+    dbc = reinterpret_cast<float*>(base);
+    v = reinterpret_cast<__nv_bfloat16*>(base + (size_t)TSUB * W * 4);
+    dt = reinterpret_cast<float*>(base + (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 2);
+    z = reinterpret_cast<__nv_bfloat16*>(base + (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 6);
+  }
+  // issue cp.async for tokens [t, t + nt) of image row base rbase / token base tbase
+  __device__ void load(const ScanParams& p, int W, long long rbase, long long tok0, int t, int nt, int d0) {
+    const int tid = threadIdx.x;
+    const float* gd = p.dbc + (rbase + t) * W;
+    for (int i = tid; i < nt * W / 4; i += DPB) cp_async16(dbc + 4 * i, gd + 4 * i);
+    constexpr int VPR = DPB / 8;  // 16-byte chunks per token row of bf16
+    for (int i = tid; i < nt * VPR; i += DPB) {
+      const int j = i / VPR, c = i - j * VPR;
+      cp_async16(v + j * DPB + c * 8, p.v + (rbase + t + j) * p.D + d0 + c * 8);
+      if (PASS2 && p.z) cp_async16(z + j * DPB + c * 8, p.z + (tok0 + t + j) * p.ld_z + d0 + c * 8);
+    }
+    if (PASS2) {
+      constexpr int FPR = DPB / 4;
+      for (int i = tid; i < nt * FPR; i += DPB) {
+        const int j = i / FPR, c = i - j * FPR;
+        cp_async16(dt + j * DPB + c * 4, p.delta + (rbase + t + j) * p.D + d0 + c * 4);
+      }
+    }
+  }
+};
+
 // ------------------------------------------------------------------------------------------------- pass 1
-template <int N, int RMAX>
-__global__ void __launch_bounds__(128) scan_pass1_kernel(ScanParams p) {
-  extern __shared__ float s_dbc[];  // [TS][R+2N]
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+template <int N, int RMAX, int DPB>
+__global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
+  using St = Stage<DPB, false>;
+  extern __shared__ __align__(128) uint8_t s_raw[];
+  const int W = p.R + 2 * N;
+  St st[2];
+  st[0].carve(s_raw, W);
+  st[1].carve(s_raw + St::bytes(W), W);
+  const int d0 = blockIdx.x * DPB;
+  const int d = d0 + threadIdx.x;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
-  const int W = p.R + 2 * N;
   const long long rbase = (long long)b * (p.L + p.P);
-  float A2[N], invA[N], h[N], wdt[RMAX];
+  float A2[N], h[N], wdt[RMAX];
 #pragma unroll
   for (int n = 0; n < N; ++n) {
-    const float A = -__expf(p.a_log[d * N + n]);
-    A2[n] = A * kLog2e;
-    invA[n] = 1.f / A;
+    A2[n] = -__expf(p.a_log[d * N + n]) * kLog2e;
     h[n] = 0.f;
   }
 #pragma unroll
   for (int r = 0; r < RMAX; ++r) wdt[r] = r < p.R ? p.w_dt[d * p.R + r] : 0.f;
   const float bdt = p.b_dt[d];
   const bool zoh = p.bbar == 0;
-
   auto compute_dt = [&](const float* drow) {
     float acc = bdt;
+    const float4* d4 = reinterpret_cast<const float4*>(drow);
 #pragma unroll
-    for (int r = 0; r < RMAX; ++r)
-      if (r < p.R) acc = fmaf(drow[r], wdt[r], acc);
+    for (int r = 0; r < RMAX; r += 4)
+      if (r < p.R) {
+        const float4 q = d4[r / 4];
+        acc = fmaf(q.x, wdt[r], acc);
+        acc = fmaf(q.y, wdt[r + 1], acc);
+        acc = fmaf(q.z, wdt[r + 2], acc);
+        acc = fmaf(q.w, wdt[r + 3], acc);
+      }
     return softplus_f(acc);
   };
-
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
-  // chunk 0 also produces Delta of the P prefix tokens of both streams (used by the carry kernel)
-  if (chunk == 0) {
+  if (chunk == 0) {  // Delta of the P prefix tokens of both streams (for the carry kernel)
     for (int q = 0; q < 2 * p.P; ++q) {
       const long long row = rbase + (q < p.P ? q : p.L + (q - p.P));
-      const float dt = compute_dt(p.dbc + row * W);
-      p.delta[row * p.D + d] = dt;
+      p.delta[row * p.D + d] = compute_dt(p.dbc + row * W);
     }
   }
   const int tb = max(t0, p.P);
+  const int nsub = (t1 - tb + St::TSUB - 1) / St::TSUB;
   float sdt = 0.f;
-  for (int ts = tb; ts < t1; ts += TS) {
-    const int nt = min(TS, t1 - ts);
+  if (nsub > 0) {
+    st[0].load(p, W, rbase, 0, tb, min(St::TSUB, t1 - tb), d0);
+    cp_async_commit();
+  }
+  for (int sc = 0; sc < nsub; ++sc) {
+    const int ts = tb + sc * St::TSUB;
+    const int nt = min(St::TSUB, t1 - ts);
+    if (sc + 1 < nsub) {
+      st[(sc + 1) & 1].load(p, W, rbase, 0, ts + St::TSUB, min(St::TSUB, t1 - ts - St::TSUB), d0);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    for (int i = threadIdx.x; i < nt * W / 4; i += blockDim.x)
-      reinterpret_cast<float4*>(s_dbc)[i] = reinterpret_cast<const float4*>(p.dbc + (rbase + ts) * W)[i];
-    __syncthreads();
+    const St& S = st[sc & 1];
     for (int j = 0; j < nt; ++j) {
-      const long long row = rbase + ts + j;
-      const float* drow = s_dbc + j * W;
-      const float v = __bfloat162float(p.v[row * p.D + d]);
+      const float* drow = S.dbc + j * W;
+      const float v = __bfloat162float(S.v[j * DPB + threadIdx.x]);
       const float dt = compute_dt(drow);
-      p.delta[row * p.D + d] = dt;
+      p.delta[(rbase + ts + j) * p.D + d] = dt;
       sdt += dt;
-      const float* Bt = drow + p.R;
+      const float4* b4 = reinterpret_cast<const float4*>(drow + p.R);
 #pragma unroll
       for (int n = 0; n < N; ++n) {
-        const float dA = ex2_approx(dt * A2[n]);
-        const float dBv = zoh ? (dA - 1.f) * invA[n] * Bt[n] * v : dt * Bt[n] * v;
-        h[n] = fmaf(dA, h[n], dBv);
+        const float4 qb = b4[n / 4];
+        const float bn = (n & 3) == 0 ? qb.x : (n & 3) == 1 ? qb.y : (n & 3) == 2 ? qb.z : qb.w;
+        const float x = dt * A2[n];
+        const float dA = ex2_approx(x);
+        const float w = bn * v;
+        if (zoh) {
+          h[n] = fmaf(dA, h[n] + w, -w);                    // h~ = dA h~ + (dA - 1) B v
+        } else {
+          h[n] = fmaf(dA, h[n], x * 0.69314718055994531f * w);  // h~ = dA h~ + (Delta A) B v
+        }
       }
     }
+    __syncthreads();
   }
   p.sumdt[((long long)b * p.n_chunks + chunk) * p.D + d] = sdt;
   float4* dst = reinterpret_cast<float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
@@ -158,8 +267,8 @@ __global__ void __launch_bounds__(128) scan_pass1_kernel(ScanParams p) {
 }
 
 // ------------------------------------------------------------------------------------------------- carry
-// One warp per (image, channel); lane owns states n = lane + 32 j. Produces the prefix outputs and every chunk's
-// entry state (overwriting the pass-1 chunk-end states in place).
+// One warp per (image, channel); lane owns states n = lane + 32 j (scaled states h~ = A h throughout).
+// Produces the prefix outputs and every chunk's entry state (overwriting the pass-1 chunk-end states).
 template <int N>
 __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   constexpr int NPL = (N + 31) / 32;
@@ -187,13 +296,12 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
       if (!act[j]) continue;
-      const float Bn = p.dbc[row * W + p.R + lane + 32 * j];
-      const float dA = ex2_approx(dt * A2[j]);
-      const float dBv = zoh ? (dA - 1.f) * invA[j] * Bn * v : dt * Bn * v;
-      h[j] = fmaf(dA, h[j], dBv);
+      const float w = p.dbc[row * W + p.R + lane + 32 * j] * v;
+      const float x = dt * A2[j];
+      const float dA = ex2_approx(x);
+      h[j] = zoh ? fmaf(dA, h[j] + w, -w) : fmaf(dA, h[j], x * 0.69314718055994531f * w);
     }
   };
-  // prefix end states: copy 1 from zero (stream rows L..L+P-1); copy-2/3 stream rows 0..P-1 as alpha*c + beta
   float beta1[NPL], beta2[NPL], alpha2[NPL];
 #pragma unroll
   for (int j = 0; j < NPL; ++j) beta1[j] = beta2[j] = 0.f;
@@ -205,7 +313,6 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   }
 #pragma unroll
   for (int j = 0; j < NPL; ++j) alpha2[j] = ex2_approx(sdt2 * A2[j]);
-  // body fold over chunks: (A_body, B_body) with a_c = exp(A sum_c Delta)
   const float* sd = p.sumdt + (long long)b * p.n_chunks * p.D + d;
   float* hs = p.hs + ((long long)b * p.n_chunks * p.D + d) * N;
   float Bb[NPL], sall = 0.f;
@@ -228,8 +335,7 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
     const float e3 = fmaf(alpha2[j], c3[j], beta2[j]);
     H[j] = beta1[j] + e2 + e3;
   }
-  // prefix outputs: out_t = (sum_copies C^(c)_t . h^(c)_t + D (v1_t + 2 v2_t)) * SiLU(z_t)
-  {
+  {  // prefix outputs: out_t = (sum_copies C^(c)_t . h^(c)_t + D (v1_t + 2 v2_t)) * SiLU(z_t)
     float h1[NPL], h2[NPL], h3[NPL];
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
@@ -248,7 +354,7 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
       for (int j = 0; j < NPL; ++j)
         if (act[j]) {
           const int n = lane + 32 * j;
-          y += p.dbc[r1 * W + p.R + N + n] * h1[j] + p.dbc[r2 * W + p.R + N + n] * (h2[j] + h3[j]);
+          y += invA[j] * (p.dbc[r1 * W + p.R + N + n] * h1[j] + p.dbc[r2 * W + p.R + N + n] * (h2[j] + h3[j]));
         }
 #pragma unroll
       for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
@@ -275,14 +381,20 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
-template <int N>
-__global__ void __launch_bounds__(128) scan_pass2_kernel(ScanParams p) {
-  extern __shared__ float s_dbc[];
-  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+template <int N, int DPB>
+__global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
+  using St = Stage<DPB, true>;
+  extern __shared__ __align__(128) uint8_t s_raw[];
+  const int W = p.R + 2 * N;
+  St st[2];
+  st[0].carve(s_raw, W);
+  st[1].carve(s_raw + St::bytes(W), W);
+  const int d0 = blockIdx.x * DPB;
+  const int d = d0 + threadIdx.x;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
-  const int W = p.R + 2 * N;
   const long long rbase = (long long)b * (p.L + p.P);
+  const long long tok0 = (long long)b * p.L;
   float A2[N], invA[N], h[N];
   const float4* src = reinterpret_cast<const float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
 #pragma unroll
@@ -304,31 +416,48 @@ __global__ void __launch_bounds__(128) scan_pass2_kernel(ScanParams p) {
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
   const int tb = max(t0, p.P);
-  for (int ts = tb; ts < t1; ts += TS) {
-    const int nt = min(TS, t1 - ts);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nt * W / 4; i += blockDim.x)
-      reinterpret_cast<float4*>(s_dbc)[i] = reinterpret_cast<const float4*>(p.dbc + (rbase + ts) * W)[i];
-    __syncthreads();
-    for (int j = 0; j < nt; ++j) {
-      const long long row = rbase + ts + j;
-      const float* Bt = s_dbc + j * W + p.R;
-      const float* Ct = Bt + N;
-      const float v = __bfloat162float(p.v[row * p.D + d]);
-      const float dt = p.delta[row * p.D + d];
-      const float v3 = 3.f * v;
-      float y = D3 * v;
-#pragma unroll
-      for (int n = 0; n < N; ++n) {
-        const float dA = ex2_approx(dt * A2[n]);
-        const float dBv = zoh ? (dA - 1.f) * invA[n] * Bt[n] * v3 : dt * Bt[n] * v3;
-        h[n] = fmaf(dA, h[n], dBv);
-        y = fmaf(Ct[n], h[n], y);
-      }
-      const long long tok = (long long)b * p.L + ts + j;
-      const float g = p.z ? silu_f(__bfloat162float(p.z[tok * p.ld_z + d])) : 1.f;
-      p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
+  const int nsub = (t1 - tb + St::TSUB - 1) / St::TSUB;
+  if (nsub > 0) {
+    st[0].load(p, W, rbase, tok0, tb, min(St::TSUB, t1 - tb), d0);
+    cp_async_commit();
+  }
+  for (int sc = 0; sc < nsub; ++sc) {
+    const int ts = tb + sc * St::TSUB;
+    const int nt = min(St::TSUB, t1 - ts);
+    if (sc + 1 < nsub) {
+      st[(sc + 1) & 1].load(p, W, rbase, tok0, ts + St::TSUB, min(St::TSUB, t1 - ts - St::TSUB), d0);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const St& S = st[sc & 1];
+    for (int j = 0; j < nt; ++j) {
+      const float4* b4 = reinterpret_cast<const float4*>(S.dbc + j * W + p.R);
+      const float v = __bfloat162float(S.v[j * DPB + threadIdx.x]);
+      const float dt = S.dt[j * DPB + threadIdx.x];
+      const float v3 = 3.f * v;
+      float y = 0.f;
+#pragma unroll
+      for (int n4 = 0; n4 < N; n4 += 4) {
+        const float4 qb = b4[n4 / 4], qc = b4[N / 4 + n4 / 4];
+        const float bt[4] = {qb.x, qb.y, qb.z, qb.w}, ct[4] = {qc.x, qc.y, qc.z, qc.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int n = n4 + e;
+          const float x = dt * A2[n];
+          const float dA = ex2_approx(x);
+          const float w = bt[e] * v3;
+          h[n] = zoh ? fmaf(dA, h[n] + w, -w) : fmaf(dA, h[n], x * 0.69314718055994531f * w);
+          y = fmaf(ct[e] * invA[n], h[n], y);
+        }
+      }
+      y = fmaf(D3, v, y);
+      const float g = p.z ? silu_f(__bfloat162float(S.z[j * DPB + threadIdx.x])) : 1.f;
+      p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
+    }
+    __syncthreads();
   }
 }
 
@@ -376,36 +505,43 @@ static int check_scan(int B, int L, int D, int N, int R, int k) {
   if (B <= 0 || L <= 0 || D <= 0 || N <= 0 || R <= 0 || k <= 0) return PSCWIN_ERR_SHAPE;
   if (L < k - 1) return PSCWIN_ERR_CONTRACT;  // copies 2 and 3 must see a full history
   if (!(N == 16 || N == 32 || N == 64)) return PSCWIN_ERR_UNSUPPORTED;
-  if (R > 64 || (R + 2 * N) % 4) return PSCWIN_ERR_UNSUPPORTED;
+  if (R > 64 || R % 4 || k > 4) return PSCWIN_ERR_UNSUPPORTED;  // float4 smem rows, register conv window
   if (D % 128 && D % 32) return PSCWIN_ERR_UNSUPPORTED;
   if (D % 64) return PSCWIN_ERR_UNSUPPORTED;  // x_proj GEMM K tiles
   return PSCWIN_OK;
 }
 
-template <int N>
-static int launch_passes(ScanParams& p, cudaStream_t s) {
-  const int tpb = p.D % 128 == 0 ? 128 : (p.D % 64 == 0 ? 64 : 32);
-  dim3 grid(p.D / tpb, p.n_chunks, p.B);
-  const size_t smem = (size_t)TS * (p.R + 2 * N) * 4;
+template <int N, int DPB>
+static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
+  dim3 grid(p.D / DPB, p.n_chunks, p.B);
+  const int W = p.R + 2 * N;
+  const size_t smem1 = 2 * Stage<DPB, false>::bytes(W);
+  const size_t smem2 = 2 * Stage<DPB, true>::bytes(W);
   {
-  PSCWIN_PROF("scan_pass1", s);
-  if (p.R <= 16)
-    scan_pass1_kernel<N, 16><<<grid, tpb, smem, s>>>(p);
-  else if (p.R <= 48)
-    scan_pass1_kernel<N, 48><<<grid, tpb, smem, s>>>(p);
-  else
-    scan_pass1_kernel<N, 64><<<grid, tpb, smem, s>>>(p);
+    PSCWIN_PROF("scan_pass1", s);
+    if (p.R <= 16)
+      scan_pass1_kernel<N, 16, DPB><<<grid, DPB, smem1, s>>>(p);
+    else if (p.R <= 48)
+      scan_pass1_kernel<N, 48, DPB><<<grid, DPB, smem1, s>>>(p);
+    else
+      scan_pass1_kernel<N, 64, DPB><<<grid, DPB, smem1, s>>>(p);
   }
-  const int warps = p.B * p.D;
   {
     PSCWIN_PROF("scan_carry", s);
+    const int warps = p.B * p.D;
     scan_carry_kernel<N><<<(warps + 7) / 8, 256, 0, s>>>(p);
   }
   {
     PSCWIN_PROF("scan_pass2", s);
-    scan_pass2_kernel<N><<<grid, tpb, smem, s>>>(p);
+    scan_pass2_kernel<N, DPB><<<grid, DPB, smem2, s>>>(p);
   }
   return (int)cudaGetLastError();
+}
+
+template <int N>
+static int launch_passes(ScanParams& p, cudaStream_t s) {
+  if (p.D % 128 == 0) return launch_passes_dpb<N, 128>(p, s);
+  return launch_passes_dpb<N, 64>(p, s);
 }
 
 // Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out).
@@ -446,7 +582,7 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.out = out;
   p.ld_out = ld_out;
   const long long rows = (long long)B * (L + pl.P);
-  const long long nthreads = rows * (D / 8);
+  const long long nthreads = (long long)B * ((L + pl.P + CONV_T - 1) / CONV_T) * (D / 8);
   {
     PSCWIN_PROF("conv_silu", s);
     conv_silu_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p);

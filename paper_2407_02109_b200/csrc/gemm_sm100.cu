@@ -7,8 +7,10 @@
 // Structure (B200-native): persistent grid (one CTA per SM), warp-specialised —
 //   warp 0: TMA producer (128B-swizzled A/B k-blocks of 64, 4-stage mbarrier ring)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256, K=16 per instruction)
-//   warps 2-5: epilogue (tcgen05.ld 32x32b -> registers -> fused op -> global), double-buffered TMEM
-//   accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+//   warps 2-9: epilogue (tcgen05.ld 32x32b -> registers -> fused op -> swizzled smem -> TMA tensor store),
+//   double-buffered TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <string.h>
+
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -20,8 +22,9 @@ constexpr int BK = 64;
 constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;       // 16 KB
 constexpr int B_STAGE_BYTES = 256 * BK * 2;      // 32 KB (max BN)
-constexpr int GEMM_THREADS = 192;
-constexpr size_t GEMM_SMEM = 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 256;
+constexpr int STAGE_OUT_BYTES = BM * 64 * 2;   // one 128x64 bf16 output chunk
+constexpr int GEMM_THREADS = 64 + 256;      // TMA warp, MMA warp, 8 epilogue warps
+constexpr size_t GEMM_SMEM = 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGE_OUT_BYTES + 256;
 }  // namespace
 
 __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) {
@@ -32,12 +35,14 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
 }
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs p) {
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmOut, GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE_BYTES);
+  uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + 2 * STAGE_OUT_BYTES);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -53,13 +58,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (p.epi != EPI_STORE_F32) tma_prefetch_desc(&tmOut);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 256);
     }
     fence_barrier_init();
   }
@@ -125,85 +131,119 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
-    // ------------------------------------------------------------------ epilogue warps 2..5
-    const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+    // ------------------------------------------------------------------ epilogue warps 2..9
+    // Two warps per TMEM lane quarter (rows), each taking 32 of every 64 accumulator columns. bf16 outputs are
+    // staged in 128B-swizzled smem (two 128x64 buffers) and written by TMA tensor stores (coalesced, async);
+    // f32 outputs are stored directly.
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int lane = lane_id();
+    const int etid = threadIdx.x - 64;                 // 0..255
+    const bool issuer = etid == 0;
+    const bool tma_out = p.epi != EPI_STORE_F32;
+    const int row_local = quarter * 32 + lane;
+    const int nch = (BN + 63) / 64;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int gseq = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
       const int m0 = (tile / n_tiles_n) * BM;
       const int n0 = (tile % n_tiles_n) * BN;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const int row = m0 + quarter * 32 + lane;
+      const int row = m0 + row_local;
       const bool row_ok = row < p.M;
-      // RoPE coordinates of this token (QKV epilogue): row = b*H*W + y*W + x
       int px = 0, py = 0;
       if (p.epi == EPI_QKV_ROPE && p.rope) {
-        int t = row % p.HW;
+        const int t = row % p.HW;
         py = t / p.Wgrid;
         px = t - py * p.Wgrid;
       }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
       const uint32_t t_row = tmem_base + acc * 256 + ((uint32_t)(quarter * 32) << 16);
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(t_row + c0, r);
-        tmem_wait_ld();
-        const int col0 = n0 + c0;
-        if (!row_ok || col0 >= p.N) continue;
-        float v[16];
+      for (int cc = 0; cc < nch; ++cc, ++gseq) {
+        const int cl = cc * 64 + half * 32;            // tile-local first column of this thread's 32
+        const int col0 = n0 + cl;
+        // residual prefetch (bf16, 4 x 16B) before the TMEM load
+        uint4 res[4];
+        const bool use_res = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
+        if (use_res) {
+          const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.residual) +
+                                                           (size_t)row * p.ldr + col0);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        const int ncols = min(16, p.N - col0);
+          for (int q = 0; q < 4; ++q)
+            res[q] = (row_ok && cl < BN && col0 + 8 * q < p.N) ? rp[q] : make_uint4(0, 0, 0, 0);
+        }
+        uint8_t* stg = s_stage + (gseq & 1) * STAGE_OUT_BYTES;
+        if (tma_out) {
+          if (issuer && gseq >= 2) bulk_wait_read1();
+          named_bar_sync(1, 256);
+        }
+        uint32_t r[32];
+        if (cl < BN) {
+          tmem_ld32(t_row + cl, r);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        }
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
         if (p.bias) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j < ncols) v[j] += p.bias[col0 + j];
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < p.N) v[j] += __ldg(p.bias + col0 + j);
         }
         if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {
-          // columns [0,C) = q, [C,2C) = k; head-local index i = col % d; half = i / (d/2); pair j = (i % (d/2))/2
+          // q = cols [0,C), k = [C,2C); head-local index i; half hf = i / (d/2); rotation pair fj = (i % (d/2)) / 2
           const int d = p.d_head;
 #pragma unroll
-          for (int j = 0; j < 16; j += 2) {
+          for (int j = 0; j < 32; j += 2) {
             const int i = (col0 + j) % d;
-            const int half = i / (d >> 1);
-            const int fj = (i - half * (d >> 1)) >> 1;
-            const int pos = half ? py : px;
-            const float2 cs = p.rope_tab[(pos + p.rope_off) * (d >> 2) + fj];
+            const int hf = i / (d >> 1);
+            const int fj = (i - hf * (d >> 1)) >> 1;
+            const float2 cs = __ldg(p.rope_tab + ((hf ? py : px) + p.rope_off) * (d >> 2) + fj);
             rope_pair(v[j], v[j + 1], cs.x, cs.y);
           }
         }
-        if (p.epi == EPI_RESID_BF16 && p.residual) {
-          const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(p.residual) + (size_t)row * p.ldr + col0;
+        if (use_res) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j < ncols) v[j] += __bfloat162float(res[j]);
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t* rw = reinterpret_cast<const uint32_t*>(&res[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * q + 2 * e] += bf16_lo(rw[e]);
+              v[8 * q + 2 * e + 1] += bf16_hi(rw[e]);
+            }
+          }
         }
-        if (p.epi == EPI_STORE_F32) {
-          float* o = reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0;
-          if (ncols == 16 && (p.ldo % 4) == 0) {
+        if (tma_out) {
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-            for (int j = 0; j < ncols; ++j) o[j] = v[j];
+          for (int q = 0; q < 4; ++q) {
+            uint4 w;
+            w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+            w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+            w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+            w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+            *reinterpret_cast<uint4*>(stg + swz_offset(row_local, half * 4 + q, 128)) = w;
           }
-        } else {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + (size_t)row * p.ldo + col0;
-          if (ncols == 16 && (p.ldo % 8) == 0) {
-            uint4 w0, w1;
-            w0.x = pack_bf16(v[0], v[1]);
-            w0.y = pack_bf16(v[2], v[3]);
-            w0.z = pack_bf16(v[4], v[5]);
-            w0.w = pack_bf16(v[6], v[7]);
-            w1.x = pack_bf16(v[8], v[9]);
-            w1.y = pack_bf16(v[10], v[11]);
-            w1.z = pack_bf16(v[12], v[13]);
-            w1.w = pack_bf16(v[14], v[15]);
-            reinterpret_cast<uint4*>(o)[0] = w0;
-            reinterpret_cast<uint4*>(o)[1] = w1;
-          } else {
-            for (int j = 0; j < ncols; ++j) o[j] = __float2bfloat16_rn(v[j]);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 256);
+          if (issuer) {
+            tma_store_2d(&tmOut, stg, n0 + cc * 64, m0);
+            bulk_commit();
           }
+        } else if (row_ok && cl < BN) {
+          float* o = reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            if (col0 + j < p.N) {
+              if (col0 + j + 4 <= p.N && (p.ldo % 4) == 0) {
+                *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              } else {
+                for (int e = 0; e < 4 && col0 + j + e < p.N; ++e) o[j + e] = v[j + e];
+              }
+            }
         }
       }
       tc_fence_before();
@@ -211,6 +251,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (issuer && tma_out) bulk_wait0();
   }
   __syncthreads();
   if (warp == 1) {
@@ -243,15 +284,29 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   GemmArgs p = args_in;
   if (p.M <= 0 || p.N <= 0) return 0;
   if (p.K % 8 != 0) return -1;
-  // tile N: 256 when N is large, else N rounded up to 16
-  if (p.BN <= 0) p.BN = p.N >= 256 ? 256 : ((p.N + 15) / 16) * 16;
-  CUtensorMap tmA, tmB;
+  // tile N: a single tile when N <= 256; else 256, or 128 when 256-wide tiles would leave SMs idle
+  if (p.BN <= 0) {
+    if (p.N <= 256) {
+      p.BN = ((p.N + 15) / 16) * 16;
+    } else {
+      const long long t256 = (long long)((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
+      p.BN = t256 >= 2LL * num_sms() ? 256 : 128;
+    }
+  }
+  CUtensorMap tmA, tmB, tmOut;
   int rc = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.M, (uint64_t)p.lda * 2, BK, BM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   rc = make_tmap_2d(&tmB, Bw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.N, (uint64_t)p.ldb * 2, BK, p.BN,
                     CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
+  memset(&tmOut, 0, sizeof(tmOut));
+  if (p.epi != EPI_STORE_F32) {
+    if ((p.ldo * 2) % 16) return -1;
+    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldo * 2, 64, BM,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
@@ -260,7 +315,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   int tiles = ((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
-  gemm_bf16_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, tmB, p);
+  gemm_bf16_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, tmB, tmOut, p);
   return (int)cudaGetLastError();
 }
 
