@@ -132,83 +132,85 @@ __global__ void conv_silu_kernel(ScanParams p) {
 // Per-chunk token loop with cp.async double buffering: every per-token operand (the shared (delta_low, B, C)
 // row, and this CTA's slice of v, Delta, z) lands in shared memory one sub-chunk ahead of its use, so the
 // sequential recurrence never waits on a global load. The state is kept scaled, h~ = A h (per (d, n) constant),
-// which turns the ZOH update into h~ <- dA (h~ + w) - w with w = B_t[n] v_t (no 1/A per element).
+// which turns the ZOH update into h~ <- dA (h~ + w) - w with w = B_t[n] v_t (no 1/A per element), and pairs of
+// states are updated with packed fp32x2 instructions (FFMA2 / FMUL2 on sm_100a).
+constexpr int TSUB = 16;
 template <int DPB, bool PASS2>
-struct Stage {
-  static constexpr int TSUB = 16;
-  float* dbc;              // [TSUB][W]
-  __nv_bfloat16* v;        // [TSUB][DPB]
-  float* dt;               // [TSUB][DPB] (pass 2)
-  __nv_bfloat16* z;        // [TSUB][DPB] (pass 2)
+struct StageLayout {
+  // byte offsets inside one stage buffer
+  __host__ __device__ static size_t off_v(int W) { return (size_t)TSUB * W * 4; }
+  __host__ __device__ static size_t off_dt(int W) { return off_v(W) + (size_t)TSUB * DPB * 2; }
+  __host__ __device__ static size_t off_z(int W) { return off_dt(W) + (PASS2 ? (size_t)TSUB * DPB * 4 : 0); }
   __host__ __device__ static size_t bytes(int W) {
-    size_t b = (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 2;
-    if (PASS2) b += (size_t)TSUB * DPB * 4 + (size_t)TSUB * DPB * 2;
+    size_t b = off_z(W) + (PASS2 ? (size_t)TSUB * DPB * 2 : 0);
     return (b + 127) & ~size_t(127);
   }
-  __device__ void carve(uint8_t* base, int W) {
-    dbc = reinterpret_cast<float*>(base);
-    v = reinterpret_cast<__nv_bfloat16*>(base + (size_t)TSUB * W * 4);
-    dt = reinterpret_cast<float*>(base + (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 2);
-    z = reinterpret_cast<__nv_bfloat16*>(base + (size_t)TSUB * W * 4 + (size_t)TSUB * DPB * 6);
-  }
-  // issue cp.async for tokens [t, t + nt) of image row base rbase / token base tbase
-  __device__ void load(const ScanParams& p, int W, long long rbase, long long tok0, int t, int nt, int d0) {
+  // issue cp.async for tokens [t, t + nt) into stage buffer `buf`
+  __device__ static void load(uint8_t* buf, const ScanParams& p, int W, long long rbase, long long tok0, int t, int nt,
+                              int d0) {
     const int tid = threadIdx.x;
+    float* sd = reinterpret_cast<float*>(buf);
+    __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(buf + off_v(W));
     const float* gd = p.dbc + (rbase + t) * W;
-    for (int i = tid; i < nt * W / 4; i += DPB) cp_async16(dbc + 4 * i, gd + 4 * i);
+    for (int i = tid; i < nt * W / 4; i += DPB) cp_async16(sd + 4 * i, gd + 4 * i);
     constexpr int VPR = DPB / 8;  // 16-byte chunks per token row of bf16
     for (int i = tid; i < nt * VPR; i += DPB) {
-      const int j = i / VPR, c = i - j * VPR;
-      cp_async16(v + j * DPB + c * 8, p.v + (rbase + t + j) * p.D + d0 + c * 8);
-      if (PASS2 && p.z) cp_async16(z + j * DPB + c * 8, p.z + (tok0 + t + j) * p.ld_z + d0 + c * 8);
+      const int j = i / VPR, cc = i - j * VPR;
+      cp_async16(sv + j * DPB + cc * 8, p.v + (rbase + t + j) * p.D + d0 + cc * 8);
     }
     if (PASS2) {
+      float* sdt = reinterpret_cast<float*>(buf + off_dt(W));
+      __nv_bfloat16* sz = reinterpret_cast<__nv_bfloat16*>(buf + off_z(W));
       constexpr int FPR = DPB / 4;
       for (int i = tid; i < nt * FPR; i += DPB) {
-        const int j = i / FPR, c = i - j * FPR;
-        cp_async16(dt + j * DPB + c * 4, p.delta + (rbase + t + j) * p.D + d0 + c * 4);
+        const int j = i / FPR, cc = i - j * FPR;
+        cp_async16(sdt + j * DPB + cc * 4, p.delta + (rbase + t + j) * p.D + d0 + cc * 4);
       }
+      if (p.z)
+        for (int i = tid; i < nt * VPR; i += DPB) {
+          const int j = i / VPR, cc = i - j * VPR;
+          cp_async16(sz + j * DPB + cc * 8, p.z + (tok0 + t + j) * p.ld_z + d0 + cc * 8);
+        }
     }
   }
 };
 
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
 // ------------------------------------------------------------------------------------------------- pass 1
 template <int N, int RMAX, int DPB>
 __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
-  using St = Stage<DPB, false>;
+  using St = StageLayout<DPB, false>;
   extern __shared__ __align__(128) uint8_t s_raw[];
   const int W = p.R + 2 * N;
-  St st[2];
-  st[0].carve(s_raw, W);
-  st[1].carve(s_raw + St::bytes(W), W);
+  const size_t SB = St::bytes(W);
   const int d0 = blockIdx.x * DPB;
   const int d = d0 + threadIdx.x;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
   const long long rbase = (long long)b * (p.L + p.P);
-  float A2[N], h[N], wdt[RMAX];
+  float2 A2[N / 2], h[N / 2], wdt[RMAX / 2];
 #pragma unroll
-  for (int n = 0; n < N; ++n) {
-    A2[n] = -__expf(p.a_log[d * N + n]) * kLog2e;
-    h[n] = 0.f;
+  for (int k = 0; k < N / 2; ++k) {
+    A2[k] = make_float2(-__expf(p.a_log[d * N + 2 * k]) * kLog2e, -__expf(p.a_log[d * N + 2 * k + 1]) * kLog2e);
+    h[k] = make_float2(0.f, 0.f);
   }
 #pragma unroll
-  for (int r = 0; r < RMAX; ++r) wdt[r] = r < p.R ? p.w_dt[d * p.R + r] : 0.f;
+  for (int r = 0; r < RMAX / 2; ++r)
+    wdt[r] = 2 * r < p.R ? make_float2(p.w_dt[d * p.R + 2 * r], p.w_dt[d * p.R + 2 * r + 1]) : make_float2(0.f, 0.f);
   const float bdt = p.b_dt[d];
   const bool zoh = p.bbar == 0;
   auto compute_dt = [&](const float* drow) {
-    float acc = bdt;
+    float2 acc = make_float2(bdt, 0.f);
     const float4* d4 = reinterpret_cast<const float4*>(drow);
 #pragma unroll
     for (int r = 0; r < RMAX; r += 4)
       if (r < p.R) {
         const float4 q = d4[r / 4];
-        acc = fmaf(q.x, wdt[r], acc);
-        acc = fmaf(q.y, wdt[r + 1], acc);
-        acc = fmaf(q.z, wdt[r + 2], acc);
-        acc = fmaf(q.w, wdt[r + 3], acc);
+        acc = __ffma2_rn(make_float2(q.x, q.y), wdt[r / 2], acc);
+        acc = __ffma2_rn(make_float2(q.z, q.w), wdt[r / 2 + 1], acc);
       }
-    return softplus_f(acc);
+    return softplus_f(acc.x + acc.y);
   };
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
@@ -219,42 +221,46 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
     }
   }
   const int tb = max(t0, p.P);
-  const int nsub = (t1 - tb + St::TSUB - 1) / St::TSUB;
+  const int nsub = (t1 - tb + TSUB - 1) / TSUB;
   float sdt = 0.f;
   if (nsub > 0) {
-    st[0].load(p, W, rbase, 0, tb, min(St::TSUB, t1 - tb), d0);
+    St::load(s_raw, p, W, rbase, 0, tb, min(TSUB, t1 - tb), d0);
     cp_async_commit();
   }
+  const float2 m1 = f2(-1.f);
   for (int sc = 0; sc < nsub; ++sc) {
-    const int ts = tb + sc * St::TSUB;
-    const int nt = min(St::TSUB, t1 - ts);
+    const int ts = tb + sc * TSUB;
+    const int nt = min(TSUB, t1 - ts);
     if (sc + 1 < nsub) {
-      st[(sc + 1) & 1].load(p, W, rbase, 0, ts + St::TSUB, min(St::TSUB, t1 - ts - St::TSUB), d0);
+      St::load(s_raw + ((sc + 1) & 1) * SB, p, W, rbase, 0, ts + TSUB, min(TSUB, t1 - ts - TSUB), d0);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const St& S = st[sc & 1];
+    const uint8_t* buf = s_raw + (sc & 1) * SB;
+    const float* sdbc = reinterpret_cast<const float*>(buf);
+    const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     for (int j = 0; j < nt; ++j) {
-      const float* drow = S.dbc + j * W;
-      const float v = __bfloat162float(S.v[j * DPB + threadIdx.x]);
+      const float* drow = sdbc + j * W;
+      const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
       const float dt = compute_dt(drow);
       p.delta[(rbase + ts + j) * p.D + d] = dt;
       sdt += dt;
-      const float4* b4 = reinterpret_cast<const float4*>(drow + p.R);
+      const float2* b2 = reinterpret_cast<const float2*>(drow + p.R);
+      const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
-      for (int n = 0; n < N; ++n) {
-        const float4 qb = b4[n / 4];
-        const float bn = (n & 3) == 0 ? qb.x : (n & 3) == 1 ? qb.y : (n & 3) == 2 ? qb.z : qb.w;
-        const float x = dt * A2[n];
-        const float dA = ex2_approx(x);
-        const float w = bn * v;
+      for (int k = 0; k < N / 2; ++k) {
+        const float2 x = __fmul2_rn(dt2, A2[k]);
+        const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 wn = __fmul2_rn(b2[k], nv2);                 // -w = -B v
         if (zoh) {
-          h[n] = fmaf(dA, h[n] + w, -w);                    // h~ = dA h~ + (dA - 1) B v
+          const float2 t = __ffma2_rn(wn, m1, h[k]);               // h~ + w
+          h[k] = __ffma2_rn(dA, t, wn);                            // dA (h~ + w) - w
         } else {
-          h[n] = fmaf(dA, h[n], x * 0.69314718055994531f * w);  // h~ = dA h~ + (Delta A) B v
+          const float2 u = __fmul2_rn(__fmul2_rn(x, f2(0.69314718055994531f)), wn);  // -(Delta A) B v
+          h[k] = __ffma2_rn(dA, h[k], __fmul2_rn(u, m1));
         }
       }
     }
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
   p.sumdt[((long long)b * p.n_chunks + chunk) * p.D + d] = sdt;
   float4* dst = reinterpret_cast<float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
 #pragma unroll
-  for (int n = 0; n < N; n += 4) dst[n / 4] = make_float4(h[n], h[n + 1], h[n + 2], h[n + 3]);
+  for (int k = 0; k < N / 2; k += 2) dst[k / 2] = make_float4(h[k].x, h[k].y, h[k + 1].x, h[k + 1].y);
 }
 
 // ------------------------------------------------------------------------------------------------- carry
@@ -383,78 +389,80 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
 // ------------------------------------------------------------------------------------------------- pass 2
 template <int N, int DPB>
 __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
-  using St = Stage<DPB, true>;
+  using St = StageLayout<DPB, true>;
   extern __shared__ __align__(128) uint8_t s_raw[];
   const int W = p.R + 2 * N;
-  St st[2];
-  st[0].carve(s_raw, W);
-  st[1].carve(s_raw + St::bytes(W), W);
+  const size_t SB = St::bytes(W);
   const int d0 = blockIdx.x * DPB;
   const int d = d0 + threadIdx.x;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
   const long long rbase = (long long)b * (p.L + p.P);
   const long long tok0 = (long long)b * p.L;
-  float A2[N], invA[N], h[N];
+  float2 A2[N / 2], invA[N / 2], h[N / 2];
   const float4* src = reinterpret_cast<const float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
 #pragma unroll
-  for (int n = 0; n < N; n += 4) {
-    const float4 q = src[n / 4];
-    h[n] = q.x;
-    h[n + 1] = q.y;
-    h[n + 2] = q.z;
-    h[n + 3] = q.w;
+  for (int k = 0; k < N / 2; k += 2) {
+    const float4 q = src[k / 2];
+    h[k] = make_float2(q.x, q.y);
+    h[k + 1] = make_float2(q.z, q.w);
   }
 #pragma unroll
-  for (int n = 0; n < N; ++n) {
-    const float A = -__expf(p.a_log[d * N + n]);
-    A2[n] = A * kLog2e;
-    invA[n] = 1.f / A;
+  for (int k = 0; k < N / 2; ++k) {
+    const float a0 = -__expf(p.a_log[d * N + 2 * k]), a1 = -__expf(p.a_log[d * N + 2 * k + 1]);
+    A2[k] = make_float2(a0 * kLog2e, a1 * kLog2e);
+    invA[k] = make_float2(1.f / a0, 1.f / a1);
   }
   const float D3 = 3.f * p.d_skip[d];
   const bool zoh = p.bbar == 0;
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
   const int tb = max(t0, p.P);
-  const int nsub = (t1 - tb + St::TSUB - 1) / St::TSUB;
+  const int nsub = (t1 - tb + TSUB - 1) / TSUB;
   if (nsub > 0) {
-    st[0].load(p, W, rbase, tok0, tb, min(St::TSUB, t1 - tb), d0);
+    St::load(s_raw, p, W, rbase, tok0, tb, min(TSUB, t1 - tb), d0);
     cp_async_commit();
   }
+  const float2 m1 = f2(-1.f);
   for (int sc = 0; sc < nsub; ++sc) {
-    const int ts = tb + sc * St::TSUB;
-    const int nt = min(St::TSUB, t1 - ts);
+    const int ts = tb + sc * TSUB;
+    const int nt = min(TSUB, t1 - ts);
     if (sc + 1 < nsub) {
-      st[(sc + 1) & 1].load(p, W, rbase, tok0, ts + St::TSUB, min(St::TSUB, t1 - ts - St::TSUB), d0);
+      St::load(s_raw + ((sc + 1) & 1) * SB, p, W, rbase, tok0, ts + TSUB, min(TSUB, t1 - ts - TSUB), d0);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const St& S = st[sc & 1];
+    const uint8_t* buf = s_raw + (sc & 1) * SB;
+    const float* sdbc = reinterpret_cast<const float*>(buf);
+    const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
+    const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
+    const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
     for (int j = 0; j < nt; ++j) {
-      const float4* b4 = reinterpret_cast<const float4*>(S.dbc + j * W + p.R);
-      const float v = __bfloat162float(S.v[j * DPB + threadIdx.x]);
-      const float dt = S.dt[j * DPB + threadIdx.x];
-      const float v3 = 3.f * v;
-      float y = 0.f;
+      const float2* b2 = reinterpret_cast<const float2*>(sdbc + j * W + p.R);
+      const float2* c2 = b2 + N / 2;
+      const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
+      const float dt = sdt[j * DPB + threadIdx.x];
+      const float2 dt2 = f2(dt), nv3 = f2(-3.f * v);
+      float2 y2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int n4 = 0; n4 < N; n4 += 4) {
-        const float4 qb = b4[n4 / 4], qc = b4[N / 4 + n4 / 4];
-        const float bt[4] = {qb.x, qb.y, qb.z, qb.w}, ct[4] = {qc.x, qc.y, qc.z, qc.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int n = n4 + e;
-          const float x = dt * A2[n];
-          const float dA = ex2_approx(x);
-          const float w = bt[e] * v3;
-          h[n] = zoh ? fmaf(dA, h[n] + w, -w) : fmaf(dA, h[n], x * 0.69314718055994531f * w);
-          y = fmaf(ct[e] * invA[n], h[n], y);
+      for (int k = 0; k < N / 2; ++k) {
+        const float2 x = __fmul2_rn(dt2, A2[k]);
+        const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 wn = __fmul2_rn(b2[k], nv3);                 // -3 B v
+        if (zoh) {
+          const float2 t = __ffma2_rn(wn, m1, h[k]);
+          h[k] = __ffma2_rn(dA, t, wn);
+        } else {
+          const float2 u = __fmul2_rn(__fmul2_rn(x, f2(0.69314718055994531f)), wn);
+          h[k] = __ffma2_rn(dA, h[k], __fmul2_rn(u, m1));
         }
+        y2 = __ffma2_rn(__fmul2_rn(c2[k], invA[k]), h[k], y2);  // C . h = C . (h~ / A)
       }
-      y = fmaf(D3, v, y);
-      const float g = p.z ? silu_f(__bfloat162float(S.z[j * DPB + threadIdx.x])) : 1.f;
+      const float y = fmaf(D3, v, y2.x + y2.y);
+      const float g = p.z ? silu_f(__bfloat162float(sz[j * DPB + threadIdx.x])) : 1.f;
       p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
     }
     __syncthreads();
@@ -515,8 +523,8 @@ template <int N, int DPB>
 static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
   dim3 grid(p.D / DPB, p.n_chunks, p.B);
   const int W = p.R + 2 * N;
-  const size_t smem1 = 2 * Stage<DPB, false>::bytes(W);
-  const size_t smem2 = 2 * Stage<DPB, true>::bytes(W);
+  const size_t smem1 = 2 * StageLayout<DPB, false>::bytes(W);
+  const size_t smem2 = 2 * StageLayout<DPB, true>::bytes(W);
   {
     PSCWIN_PROF("scan_pass1", s);
     if (p.R <= 16)
