@@ -180,8 +180,14 @@ def run_ours(args, rank, world, local_rank):
     x0 = torch.tensor(x_host, dtype=torch.bfloat16, device=dev)
     bufs = [torch.empty_like(x0), torch.empty_like(x0)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    # the public API's multi-layer step: all kernels of all layers captured once into a CUDA graph
+    stack = pl.PSCWinStack(layers, tuple(x0.shape), device=dev, graph=not args.no_graph)
+    stack.x_in.copy_(x0)
 
-    def step(x):
+    def step(x=None):
+        return stack.replay()
+
+    def step_eager(x):
         cur = x
         for j, layer in enumerate(layers):
             nxt = bufs[j & 1]
@@ -195,23 +201,22 @@ def run_ours(args, rank, world, local_rank):
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        step(x0)
+        step()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, L2 flushed before each, CUDA events on the launching stream
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
-    n0 = pl.launch_count()
     with ClockSampler(local_rank) as clk:
         for i in range(args.steps):
             flush.zero_()
             ev[i][0].record(stream)
-            step(x0)
+            step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     barrier()
-    launches = pl.launch_count() - n0
+    launches = stack.launches_per_step * args.steps  # library kernels per step (graph nodes) x steps
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     per_step = [a.elapsed_time(b) for a, b in ev]
 
@@ -233,16 +238,14 @@ def run_ours(args, rank, world, local_rank):
     x_pin = torch.empty(x0.shape, dtype=torch.bfloat16, pin_memory=True)
     x_pin.copy_(x0.cpu())
     y_pin = torch.empty_like(x_pin).pin_memory()
-    x_dev = torch.empty_like(x0)
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     for i in range(args.steps):
         flush.zero_()
         e2e_ev[i][0].record(stream)
-        x_dev.copy_(x_pin, non_blocking=True)
-        out = step(x_dev)
-        y_pin.copy_(out, non_blocking=True)
+        out = stack(x_pin)                        # H2D copy into the static input + graph replay
+        y_pin.copy_(out, non_blocking=True)       # D2H of the result
         e2e_ev[i][1].record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -252,7 +255,7 @@ def run_ours(args, rank, world, local_rank):
     pl.profile_enable(True)
     for i in range(args.steps):
         flush.zero_()
-        step(x0)
+        step_eager(x0)
     torch.cuda.synchronize()
     prof = pl.profile_read()
     pl.profile_enable(False)
@@ -377,6 +380,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="also print the per-kernel table to stderr")
+    ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -409,6 +413,7 @@ def main():
                        "C": c0.C, "heads": c0.heads, "window": c0.window, "shift": 8, "ssm_state": c0.N,
                        "ssm_expand": c0.ssm_expand, "pad_mode": "learnable", "parallelism": f"images x{world}",
                        "l2": "flushed before every timed step (256 MiB write)",
+                       "launch": "eager" if args.no_graph else "CUDA graph of the whole step",
                        "per_layer_ms": [round(t, 4) for t in res["layer_ms"]]},
             "e2e": {"value": round(e2e_img, 4), "unit": "ms/image", "h2d_bytes_per_step": int(res["h2d"]),
                     "d2h_bytes_per_step": int(res["d2h"])},

@@ -5,7 +5,7 @@ binding with the same call names. Importing it loads the library and fails loudl
 """
 from ._lib import (LIB_PATH, LayerDesc, LayerWeights, PscwinError, ScanDesc, launch_count, lib,  # noqa: F401
                    profile_enable, profile_read)
-from .api import (PSCWinLayer, Workspace, cycle_scan, forward, index_map, layer_norm, linear,  # noqa: F401
+from .api import (PSCWinLayer, PSCWinStack, Workspace, cycle_scan, forward, index_map, layer_norm, linear,  # noqa: F401
                   qkv_project, scan_workspace_bytes, shifted_pad_partition, window_attention, window_count,
                   window_merge, window_partition, workspace_bytes)
 

@@ -162,3 +162,50 @@ class PSCWinLayer:
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         return forward(self.desc, self.weights, x, out=out, ws=self.ws, wts=self.wts)
+
+
+class PSCWinStack:
+    """A sequence of PSCWin layers with static device buffers, optionally captured once into a CUDA graph and
+    replayed (all kernels of all layers become one graph launch; shapes are fixed per resolution).
+
+        stack = PSCWinStack(layers, x_shape)
+        y = stack(x)            # copies x into the static input, replays, returns the static output
+    """
+
+    def __init__(self, layers, x_shape, device="cuda", graph: bool = True):
+        self.layers = list(layers)
+        self.x_in = torch.empty(x_shape, dtype=torch.bfloat16, device=device)
+        self.bufs = [torch.empty_like(self.x_in), torch.empty_like(self.x_in)]
+        self.graph = None
+        self.out = self.bufs[(len(self.layers) - 1) & 1] if self.layers else self.x_in
+        self.launches_per_step = 0
+        # eager warm-up (sets kernel attributes; counts launches)
+        from ._lib import launch_count
+        n0 = launch_count()
+        self._run()
+        torch.cuda.synchronize()
+        self.launches_per_step = launch_count() - n0
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._run()
+            torch.cuda.synchronize()
+            self.graph = g
+
+    def _run(self):
+        cur = self.x_in
+        for j, layer in enumerate(self.layers):
+            layer(cur, out=self.bufs[j & 1])
+            cur = self.bufs[j & 1]
+        return cur
+
+    def replay(self) -> torch.Tensor:
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._run()
+        return self.out
+
+    def __call__(self, x: torch.Tensor) -> torch.Tensor:
+        self.x_in.copy_(x, non_blocking=True)
+        return self.replay()

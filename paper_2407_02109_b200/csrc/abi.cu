@@ -117,8 +117,7 @@ int check_layer(const pscwin_layer_desc* d) {
 
 // Workspace layout shared by qkv_project / window_attention / forward.
 struct LayerWs {
-  size_t u, qkv, qkv_pad, O, pad_tab, rope_tab, xz, g, scan, total;
-  int rope_n_pos, rope_off;
+  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, scan, total;
 };
 
 LayerWs plan_layer(const pscwin_layer_desc* d) {
@@ -136,10 +135,6 @@ LayerWs plan_layer(const pscwin_layer_desc* d) {
   w.qkv_pad = take(3 * C * 4);
   w.O = take(T * C * 2);
   w.pad_tab = take(attn_pad_table_bytes(d->H, d->W, d->C, d->window));
-  w.rope_off = d->window;
-  w.rope_n_pos = (d->H > d->W ? d->H : d->W) + 2 * d->window;
-  const int dh = d->C / d->heads;
-  w.rope_tab = take((size_t)w.rope_n_pos * (dh / 4) * 8);
   w.xz = w.g = w.scan = 0;
   if (d->cycle_scan) {
     const size_t D = (size_t)d->ssm_expand * C;
@@ -169,14 +164,9 @@ int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt,
   const long long T = (long long)d->B * d->H * d->W;
   const int C = d->C;
   void* u = wsp(ws, L.u);
-  float2* rope_tab = reinterpret_cast<float2*>(wsp(ws, L.rope_tab));
   int rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, 0, u, s);
   if (rc) return rc;
   const int dh = C / d->heads;
-  if (d->rope) {
-    rc = launch_rope_table(rope_tab, L.rope_n_pos, L.rope_off, dh, s);
-    if (rc) return rc;
-  }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = (int)T;
@@ -194,8 +184,6 @@ int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt,
   a.Wgrid = d->W;
   a.C = C;
   a.d_head = dh;
-  a.rope_off = L.rope_off;
-  a.rope_tab = rope_tab;
   rc = launch_gemm_bf16(u, wt->w_qkv, a, s);
   if (rc) return rc;
   if (qkv_pad && wt->pad) {
@@ -222,13 +210,7 @@ int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv
   a.qkv = qkv;
   a.qkv_pad = qkv_pad;
   a.out = O;
-  a.rope_tab = reinterpret_cast<const float2*>(wsp(ws, L.rope_tab));
-  a.rope_off = L.rope_off;
   a.pad_tab = wsp(ws, L.pad_tab);
-  if (d->rope) {
-    int rc = launch_rope_table(reinterpret_cast<float2*>(wsp(ws, L.rope_tab)), L.rope_n_pos, L.rope_off, a.d, s);
-    if (rc) return rc;
-  }
   return launch_window_attention(a, s);
 }
 

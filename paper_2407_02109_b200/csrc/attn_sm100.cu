@@ -12,6 +12,8 @@
 // tables (rotated k_p halves per x / y coordinate, v_p). S = Q K^T accumulates in TMEM (fp32), softmax runs
 // one row per thread in fp32 (exp2 with log2(e)/sqrt(d) folded), P is written bf16 to swizzled smem, O = P V
 // accumulates in TMEM, and the merge/crop writes each real row straight to the [B,H,W,C] grid (pad rows dropped). No L^2 buffer exists anywhere (App. A.6).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -263,8 +265,7 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
 // Pad tables for the LEARNABLE patch: kx[X+pl][h][0:d/2] = rot_X(k_p[h][0:d/2]), ky[Y+pt][h][0:d/2] =
 // rot_Y(k_p[h][d/2:d]), vp[h][:] = v_p[h][:]  (bf16; rotation in f32 from the f32 projection of p).
 __global__ void pad_tables_kernel(const float* __restrict__ qkv_pad, int C, int heads, int d, int Wp, int Hp, int pl,
-                                  int pt, int rope, const float2* __restrict__ rope_tab, int rope_off,
-                                  __nv_bfloat16* kx, __nv_bfloat16* ky, __nv_bfloat16* vp) {
+                                  int pt, int rope, __nv_bfloat16* kx, __nv_bfloat16* ky, __nv_bfloat16* vp) {
   const int half = d / 2;
   const int nx = Wp * heads * half, ny = Hp * heads * half, nv = heads * d;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -279,9 +280,10 @@ __global__ void pad_tables_kernel(const float* __restrict__ qkv_pad, int C, int 
     float val;
     if (rope) {
       const int jpair = e >> 1;
-      const float2 cs = rope_tab[(pos + rope_off) * (d / 4) + jpair];
+      float c, sn;
+      rope_cs(pos, jpair, d, c, sn);
       const float a = kp[jpair * 2], bb = kp[jpair * 2 + 1];
-      val = (e & 1) ? (a * cs.y + bb * cs.x) : (a * cs.x - bb * cs.y);
+      val = (e & 1) ? (a * sn + bb * c) : (a * c - bb * sn);
     } else {
       val = kp[e];
     }
@@ -337,8 +339,13 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
     int n = (p.Wp + p.Hp) * a.C / 2 + a.C;
     PSCWIN_PROF("pad_tables", stream);
     pad_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
-                                                           a.rope_tab, a.rope_off, kx, ky, vp);
+                                                           kx, ky, vp);
   }
+  // windows of <= 256 slots: persistent warp-specialised kernel (attn_sm100_ws.cu); PSCWIN_ATTN_V1=1 forces this
+  // file's one-CTA-per-(q tile, head, window) kernel, which also serves larger windows.
+  const char* force_v1 = getenv("PSCWIN_ATTN_V1");
+  if (p.n_tiles <= 2 && !(force_v1 && force_v1[0] == '1'))
+    return launch_window_attention_ws(a, p.kx, p.ky, p.vp, p.patch, stream);
   CUtensorMap tmQKV;
   const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
   const uint64_t sq[4] = {(uint64_t)d * 2, (uint64_t)3 * a.C * 2, (uint64_t)a.W * 3 * a.C * 2,

@@ -1,0 +1,374 @@
+// Window attention core, persistent warp-specialised tcgen05 kernel for windows of <= 256 slots (w <= 16).
+// Same math as attn_sm100.cu (§3.2; App. A.5; readings Q1, Q5, Q6):
+// O = softmax(q k^T / sqrt(d)) v per (window, head), pad slots LEARNABLE (projected p, K rotated at the slot's
+// geometric coordinate) or MASKED (-inf), only real rows written back to the [B,H,W,C] grid.
+//
+// Roles (320 threads, one CTA per SM, loops over (image, window, head) work items):
+//   warp 0     TMA: Q, K, V tiles of the item (5-D boxes straight from QKV [B,H,W,3,heads,d]; off-grid rows
+//              zero-filled) into one of two shared-memory stages (prefetch of item i+1 overlaps item i)
+//   warp 1     TMEM allocation + single-thread tcgen05.mma issue: S_a = Q_a K_t^T, O_a = P_a V_t (P from TMEM)
+//   warps 2-5  softmax warpgroup for q-tile 0, warps 6-9 for q-tile 1 (one query row per thread): fp32 online
+//              softmax over each key tile, P written back to TMEM as bf16 (aliasing S), running output in registers
+// TMEM per warpgroup a: S/P at columns [256a, 256a+128), O tile at [256a+128, 256a+128+d).
+#include "common.cuh"
+#include "pscwin_internal.h"
+
+namespace pscwin {
+
+namespace {
+constexpr int WS_THREADS = 320;
+}
+
+struct AttnWsArgs {
+  int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
+  int rpt, n_tiles, tile_slots, n_items;
+  float sl2;
+  const __nv_bfloat16 *kx, *ky, *vp;
+  __nv_bfloat16* out;
+};
+
+template <int D>
+__global__ void __launch_bounds__(WS_THREADS, 1)
+    window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnWsArgs p) {
+  constexpr int ROWB = D * 2;
+  constexpr int TILE = 128 * ROWB;           // smem bytes reserved per 128-slot tile
+  constexpr int STAGE = 6 * TILE;            // Q0 Q1 K0 K1 V0 V1
+  constexpr uint32_t LAYOUT = ROWB == 128 ? kLayoutSW128 : kLayoutSW64;
+  constexpr uint32_t SBO = 8 * ROWB;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  uint64_t* ld_full = bars + 0;      // [2]
+  uint64_t* ld_empty = bars + 2;     // [2]
+  uint64_t* patch_done = bars + 4;   // [2]
+  uint64_t* s_full = bars + 6;       // [2] per warpgroup
+  uint64_t* p_full = bars + 8;       // [2]
+  uint64_t* o_full = bars + 10;      // [2]
+  uint64_t* o_free = bars + 12;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int warp = warp_id();
+  const int nt = p.n_tiles;
+  const uint32_t tile_tx = (uint32_t)(p.tile_slots * ROWB);
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQKV);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&ld_full[i], 1);
+      mbar_init(&ld_empty[i], 1);
+      mbar_init(&patch_done[i], 256);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_free[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto decode = [&](int item, int& b, int& h, int& X0, int& Y0) {
+    h = item % p.heads;
+    const int r = item / p.heads;
+    const int win = r % p.nw;
+    b = r / p.nw;
+    const int wy = win / p.nwx, wx = win - wy * p.nwx;
+    X0 = wx * p.w - p.pl;
+    Y0 = wy * p.w - p.pt;
+  };
+  // q tile a of an item has at least one real query row
+  auto q_active = [&](int a, int Y0) {
+    if (a >= nt) return false;
+    const int ylo = Y0 + a * p.rpt;
+    return ylo + p.rpt > 0 && ylo < p.H;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t pol = policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        int b, h, X0, Y0;
+        decode(item, b, h, X0, Y0);
+        mbar_wait(&ld_empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&ld_full[stage], 3 * nt * tile_tx);
+        uint8_t* st = smem + stage * STAGE;
+        for (int t = 0; t < nt; ++t) {
+          const int y = Y0 + t * p.rpt;
+          tma_load_5d(st + t * TILE, &tmQKV, &ld_full[stage], 0, h, X0, y, b, pol);
+          tma_load_5d(st + (2 + t) * TILE, &tmQKV, &ld_full[stage], 0, p.heads + h, X0, y, b, pol);
+          tma_load_5d(st + (4 + t) * TILE, &tmQKV, &ld_full[stage], 0, 2 * p.heads + h, X0, y, b, pol);
+        }
+        if (++stage == 2) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------------------------------ MMA issuer
+    const uint32_t idesc_s = make_idesc_bf16(128, p.tile_slots, 0, 0);
+    const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t ph_p[2] = {0, 0}, ph_of[2] = {0, 0};
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      int b, h, X0, Y0;
+      decode(item, b, h, X0, Y0);
+      const bool act[2] = {q_active(0, Y0), q_active(1, Y0)};
+      mbar_wait(&ld_full[stage], phase);
+      if (p.patch) mbar_wait(&patch_done[stage], phase);
+      tc_fence_after();
+      const uint32_t sb = smem_u32(smem + stage * STAGE);
+      for (int kt = 0; kt < nt; ++kt) {
+        for (int a = 0; a < 2; ++a) {
+          if (!act[a]) continue;
+          if (elect_one()) {
+            const uint32_t qa = sb + a * TILE, ka = sb + (2 + kt) * TILE;
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k)
+              umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
+                      idesc_s, k > 0);
+            umma_commit(&s_full[a]);
+          }
+          __syncwarp();
+        }
+        for (int a = 0; a < 2; ++a) {
+          if (!act[a]) continue;
+          mbar_wait(&p_full[a], ph_p[a]);
+          ph_p[a] ^= 1;
+          mbar_wait(&o_free[a], ph_of[a] ^ 1);
+          ph_of[a] ^= 1;
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t va = sb + (4 + kt) * TILE;
+            for (int ks = 0; ks < p.tile_slots / 16; ++ks)
+              umma_ts(tmem + 256 * a + 128, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
+                      idesc_o, ks > 0);
+            umma_commit(&o_full[a]);
+          }
+          __syncwarp();
+        }
+      }
+      if (elect_one()) umma_commit(&ld_empty[stage]);  // all MMAs reading this stage are done -> TMA may refill
+      __syncwarp();
+      if (++stage == 2) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------------------------------ softmax WGs
+    const int a = (warp - 2) >> 2;           // q tile / warpgroup
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane_id();  // query slot within the q tile (= TMEM lane)
+    const int wtid = (warp - 2) * 32 + lane_id();  // 0..255 over both warpgroups
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + 256 * a + lane_base;
+    const uint32_t tO = tmem + 256 * a + 128 + lane_base;
+    const bool masked = p.pad_mode == 1;
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t ph_s = 0, ph_o = 0;
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      int b, h, X0, Y0;
+      decode(item, b, h, X0, Y0);
+      const bool active = q_active(a, Y0);
+      if (p.patch) {
+        // LEARNABLE pad patch of K/V rows outside the grid; thread wtid patches slot (wtid & 127) of key tile wtid>>7
+        mbar_wait(&ld_full[stage], phase);
+        const int kt = wtid >> 7, r = wtid & 127;
+        if (kt < nt && r < p.tile_slots) {
+          const int Y = Y0 + kt * p.rpt + (r >> p.lw), X = X0 + (r & (p.w - 1));
+          if (Y < 0 || Y >= p.H || X < 0 || X >= p.W) {
+            uint8_t* sK = smem + stage * STAGE + (2 + kt) * TILE;
+            uint8_t* sV = smem + stage * STAGE + (4 + kt) * TILE;
+            const uint4* kx = reinterpret_cast<const uint4*>(p.kx + ((size_t)(X + p.pl) * p.heads + h) * (D / 2));
+            const uint4* ky = reinterpret_cast<const uint4*>(p.ky + ((size_t)(Y + p.pt) * p.heads + h) * (D / 2));
+            const uint4* vp = reinterpret_cast<const uint4*>(p.vp + (size_t)h * D);
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) {
+              *reinterpret_cast<uint4*>(sK + swz_offset(r, c, ROWB)) = kx[c];
+              *reinterpret_cast<uint4*>(sK + swz_offset(r, c + D / 16, ROWB)) = ky[c];
+            }
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4*>(sV + swz_offset(r, c, ROWB)) = vp[c];
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&patch_done[stage]);
+      }
+      if (active) {
+        float o_acc[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) o_acc[j] = 0.f;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int kt = 0; kt < nt; ++kt) {
+          // valid-key bitmask per 32-column chunk (MASKED: real slots only). Rows of the key tile: rpt; cols: w.
+          uint32_t xmask = 0xFFFFFFFFu;
+          int iy_lo = 0, iy_hi = 1 << 30;
+          if (masked) {
+            const int xl = max(0, -X0), xh = min(p.w, p.W - X0);
+            xmask = (xh > xl) ? (((1u << (xh - xl)) - 1u) << xl) : 0u;
+            iy_lo = -(Y0 + kt * p.rpt);
+            iy_hi = p.H - (Y0 + kt * p.rpt);
+          }
+          mbar_wait(&s_full[a], ph_s);
+          ph_s ^= 1;
+          tc_fence_after();
+          auto chunk_mask = [&](int c0) -> uint32_t {
+            if (!masked) return 0xFFFFFFFFu;
+            uint32_t m = 0;
+            const int rows = 32 >> p.lw;
+#pragma unroll 8
+            for (int rr = 0; rr < rows; ++rr) {
+              const int iy = (c0 >> p.lw) + rr;
+              if (iy >= iy_lo && iy < iy_hi) m |= (p.w == 32 ? xmask : (xmask & ((1u << p.w) - 1u))) << (rr * p.w);
+            }
+            return m;
+          };
+          float mx = -INFINITY;
+          for (int c0 = 0; c0 < p.tile_slots; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tS + c0, r);
+            tmem_wait_ld();
+            const uint32_t m = chunk_mask(c0);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if ((m >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r[j]));
+          }
+          const float m_new = fmaxf(m_run, mx * p.sl2);
+          const float base = (m_new == -INFINITY) ? 0.f : m_new;
+          const float corr = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - base);
+          float lsum = 0.f;
+          for (int c0 = 0; c0 < p.tile_slots; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tS + c0, r);
+            tmem_wait_ld();
+            const uint32_t m = chunk_mask(c0);
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float e0 = ((m >> j) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j]), p.sl2, -base)) : 0.f;
+              const float e1 = ((m >> (j + 1)) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j + 1]), p.sl2, -base)) : 0.f;
+              lsum += e0 + e1;
+              pk[j / 2] = pack_bf16(e0, e1);
+            }
+            tmem_st16(tS + c0 / 2, pk);  // P (bf16 pairs) over the already-consumed S columns
+          }
+          tmem_wait_st();
+          l_run = l_run * corr + lsum;
+          m_run = m_new;
+          tc_fence_before();
+          mbar_arrive(&p_full[a]);
+          mbar_wait(&o_full[a], ph_o);
+          ph_o ^= 1;
+          tc_fence_after();
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32(tO + c0, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) o_acc[c0 + j] = fmaf(o_acc[c0 + j], corr, __uint_as_float(r[j]));
+          }
+          tc_fence_before();
+          mbar_arrive(&o_free[a]);
+        }
+        // normalise; write real query rows to the grid (merge / crop)
+        const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
+        const int Y = Y0 + iy, X = X0 + ix;
+        if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+          const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+          uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) {
+            uint4 v;
+            v.x = pack_bf16(o_acc[c * 8 + 0] * inv, o_acc[c * 8 + 1] * inv);
+            v.y = pack_bf16(o_acc[c * 8 + 2] * inv, o_acc[c * 8 + 3] * inv);
+            v.z = pack_bf16(o_acc[c * 8 + 4] * inv, o_acc[c * 8 + 5] * inv);
+            v.w = pack_bf16(o_acc[c * 8 + 6] * inv, o_acc[c * 8 + 7] * inv);
+            dst[c] = v;
+          }
+        }
+      }
+      if (++stage == 2) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky, const void* vp, int patch,
+                               cudaStream_t stream) {
+  const int d = a.d, w = a.w;
+  AttnWsArgs p;
+  p.B = a.B;
+  p.H = a.H;
+  p.W = a.W;
+  p.C = a.C;
+  p.heads = a.heads;
+  p.w = w;
+  p.lw = 0;
+  while ((1 << p.lw) < w) ++p.lw;
+  p.pl = (w - a.sx) % w;
+  p.pt = (w - a.sy) % w;
+  const int pr = ((-(p.pl + a.W)) % w + w) % w;
+  const int pb = ((-(p.pt + a.H)) % w + w) % w;
+  p.nwx = (p.pl + a.W + pr) / w;
+  p.nw = ((p.pt + a.H + pb) / w) * p.nwx;
+  p.pad_mode = a.pad_mode;
+  p.patch = patch;
+  p.rpt = w * w <= 128 ? w : 128 / w;
+  p.n_tiles = w / p.rpt;
+  p.tile_slots = w * p.rpt;
+  p.n_items = a.B * p.nw * a.heads;
+  p.sl2 = 1.4426950408889634f / sqrtf((float)d);
+  p.kx = reinterpret_cast<const __nv_bfloat16*>(kx);
+  p.ky = reinterpret_cast<const __nv_bfloat16*>(ky);
+  p.vp = reinterpret_cast<const __nv_bfloat16*>(vp);
+  p.out = reinterpret_cast<__nv_bfloat16*>(a.out);
+  if (p.n_tiles > 2 || p.tile_slots < 16) return -2;
+  CUtensorMap tmQKV;
+  const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
+  const uint64_t sq[4] = {(uint64_t)d * 2, (uint64_t)3 * a.C * 2, (uint64_t)a.W * 3 * a.C * 2,
+                          (uint64_t)a.H * a.W * 3 * a.C * 2};
+  const uint32_t box[5] = {(uint32_t)d, 1, (uint32_t)w, (uint32_t)p.rpt, 1};
+  int rc = make_tmap_5d(&tmQKV, a.qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dq, sq, box,
+                        d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+  if (rc) return rc;
+  const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8;
+  const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
+  PSCWIN_PROF("window_attention", stream);
+  if (d == 64) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(window_attn_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set = true;
+    }
+    window_attn_ws_kernel<64><<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
+  } else {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(window_attn_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      set = true;
+    }
+    window_attn_ws_kernel<32><<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
+  }
+  return (int)cudaGetLastError();
+}
+
+}  // namespace pscwin

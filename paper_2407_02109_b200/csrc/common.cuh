@@ -231,3 +231,19 @@ PSCWIN_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
 }
 PSCWIN_DEVICE void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 }  // namespace pscwin
+
+namespace pscwin {
+// RoPE frequencies in turns: kRopeTurns64[j] = 10000^(-j/16) / (2 pi)  (theta_j = 10000^(-4j/d) for d = 64;
+// for d = 32 use index 2j). DESIGN.md reading Q6.
+__device__ __constant__ float kRopeTurns64[16] = {
+    1.591549431e-01f, 8.949940161e-02f, 5.032921210e-02f, 2.830219583e-02f, 1.591549431e-02f, 8.949940161e-03f,
+    5.032921210e-03f, 2.830219583e-03f, 1.591549431e-03f, 8.949940161e-04f, 5.032921210e-04f, 2.830219583e-04f,
+    1.591549431e-04f, 8.949940161e-05f, 5.032921210e-05f, 2.830219583e-05f};
+// cos/sin of pos * theta_fj (head dim d in {32, 64}): reduce to a fraction of a turn, then MUFU sin/cos on
+// [-pi, pi] (absolute error ~2e-5 rad at |pos| <= 300, far below bf16 resolution).
+PSCWIN_DEVICE void rope_cs(int pos, int fj, int d, float& c, float& s) {
+  const float turns = (float)pos * kRopeTurns64[fj * (64 / d)];
+  const float f = turns - rintf(turns);
+  __sincosf(f * 6.283185307179586f, &s, &c);
+}
+}  // namespace pscwin

@@ -17,6 +17,7 @@
 //   pass 2    : per (chunk, channel): the summed recurrence from H_in, y, gate SiLU(z), bf16 store
 // Transcendentals: ex2.approx on the MUFU pipe (A pre-scaled by log2 e); everything else FP32.
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/pscwin.h"
@@ -478,9 +479,16 @@ struct ScanPlan {
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static int choose_chunk(int B, int L, int D) {
-  // aim for >= ~4 waves of 128-channel CTAs over 148 SMs; chunk length a multiple of TS
+  // aim for ~`waves` x 148 CTAs of 128 channels (several resident per SM); chunk length a multiple of TS.
+  // PSCWIN_SCAN_WAVES overrides the target (tuning knob; the result is identical for any chunking).
+  static int waves = 0;
+  if (!waves) {
+    const char* e = getenv("PSCWIN_SCAN_WAVES");
+    waves = e ? atoi(e) : 4;
+    if (waves <= 0) waves = 4;
+  }
   const long long ctas_per_chunk = (long long)B * (D / 128 > 0 ? D / 128 : 1);
-  long long target_chunks = (4LL * 148 + ctas_per_chunk - 1) / ctas_per_chunk;
+  long long target_chunks = ((long long)waves * 148 + ctas_per_chunk - 1) / ctas_per_chunk;
   long long lc = (L + target_chunks - 1) / target_chunks;
   lc = ((lc + TS - 1) / TS) * TS;
   if (lc < TS) lc = TS;

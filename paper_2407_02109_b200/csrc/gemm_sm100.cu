@@ -151,11 +151,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int n0 = (tile % n_tiles_n) * BN;
       const int row = m0 + row_local;
       const bool row_ok = row < p.M;
-      int px = 0, py = 0;
+      // RoPE of this row (QKV epilogue): this thread's 32 columns of every 64-column chunk are one half of a head
+      // (d = 64: axis = half, pair jj -> frequency jj) or one whole head (d = 32: pairs 0-7 x, 8-15 y).
+      float rc[16], rs[16];
       if (p.epi == EPI_QKV_ROPE && p.rope) {
         const int t = row % p.HW;
-        py = t / p.Wgrid;
-        px = t - py * p.Wgrid;
+        const int py = t / p.Wgrid, px = t - py * p.Wgrid;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int axis = p.d_head == 64 ? half : (jj >= 8);
+          const int fj = p.d_head == 64 ? jj : (jj & 7);
+          rope_cs(axis ? py : px, fj, p.d_head, rc[jj], rs[jj]);
+        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -194,17 +201,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             if (col0 + j < p.N) v[j] += __ldg(p.bias + col0 + j);
         }
-        if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {
-          // q = cols [0,C), k = [C,2C); head-local index i; half hf = i / (d/2); rotation pair fj = (i % (d/2)) / 2
-          const int d = p.d_head;
+        if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const int i = (col0 + j) % d;
-            const int hf = i / (d >> 1);
-            const int fj = (i - hf * (d >> 1)) >> 1;
-            const float2 cs = __ldg(p.rope_tab + ((hf ? py : px) + p.rope_off) * (d >> 2) + fj);
-            rope_pair(v[j], v[j + 1], cs.x, cs.y);
-          }
+          for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
         }
         if (use_res) {
 #pragma unroll
@@ -260,30 +259,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-// RoPE table: tab[(pos + off) * (d/4) + j] = (cos, sin)(pos * 10000^(-4j/d)), pos in [-off, n - off).
-__global__ void rope_table_kernel(float2* tab, int n_pos, int off, int d) {
-  int q = d / 4;
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_pos * q) return;
-  int pos = i / q - off;
-  int j = i % q;
-  double theta = pow(10000.0, -4.0 * j / d);
-  double s, c;
-  sincos((double)pos * theta, &s, &c);
-  tab[i] = make_float2((float)c, (float)s);
-}
-
-int launch_rope_table(float2* tab, int n_pos, int off, int d, cudaStream_t stream) {
-  int n = n_pos * (d / 4);
-  PSCWIN_PROF("rope_table", stream);
-  rope_table_kernel<<<(n + 255) / 256, 256, 0, stream>>>(tab, n_pos, off, d);
-  return (int)cudaGetLastError();
-}
-
 int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cudaStream_t stream) {
   GemmArgs p = args_in;
   if (p.M <= 0 || p.N <= 0) return 0;
   if (p.K % 8 != 0) return -1;
+  if (p.epi == EPI_QKV_ROPE && p.rope && !(p.d_head == 32 || p.d_head == 64)) return -2;
   // tile N: a single tile when N <= 256; else 256, or 128 when 256-wide tiles would leave SMs idle
   if (p.BN <= 0) {
     if (p.N <= 256) {

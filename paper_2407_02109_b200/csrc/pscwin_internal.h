@@ -22,8 +22,7 @@ struct GemmArgs {
   const void* residual;  // bf16 [M, ldr] or null
   int ldr;
   // QKV + RoPE epilogue
-  int rope, HW, Wgrid, C, d_head, rope_off;
-  const float2* rope_tab;
+  int rope, HW, Wgrid, C, d_head;
   const char* prof_name;  // kernel label for pscwin_profile_read
 };
 
@@ -40,7 +39,6 @@ int launch_partition(const void* x, const void* pad_row, int B, int H, int W, in
 int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, int sy, const void* residual,
                  int is_f32, void* out, cudaStream_t stream);
 int launch_gemm_bf16(const void* A, const void* B, const GemmArgs& args, cudaStream_t stream);
-int launch_rope_table(float2* tab, int n_pos, int off, int d, cudaStream_t stream);
 int launch_layer_norm(const void* x, long long rows, int C, const float* g, const float* b, float eps, int is_f32,
                       void* out, cudaStream_t stream);
 int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C, int is_f32, float* out,
@@ -51,12 +49,12 @@ struct AttnArgs {
   const void* qkv;       // [B,H,W,3C] bf16 (q,k rotated at their grid coordinates)
   const float* qkv_pad;  // [3C] f32 projection of p (unrotated) or null (plain / masked)
   void* out;             // [B,H,W,C] bf16
-  const float2* rope_tab;
-  int rope_off;
   void* pad_tab;         // workspace for rotated pad K halves + V (bf16)
 };
 size_t attn_pad_table_bytes(int H, int W, int C, int w);
 int launch_window_attention(const AttnArgs& a, cudaStream_t stream);
+int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky, const void* vp, int patch,
+                               cudaStream_t stream);
 
 }  // namespace pscwin
 

@@ -84,6 +84,30 @@ def test_cycle_scan_contract(pl):
         pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(synth.make_weights(cfg), cfg))
 
 
+def test_stack_graph_replay_equals_eager(pl):
+    # PSCWinStack captures every kernel of the P, S, CS+P layers into one CUDA graph; replay must be bit-identical
+    # to eager layer-by-layer execution and match the oracle.
+    import torch
+    cfgs = [synth.tiny(shift_x=0, shift_y=0), synth.tiny(), synth.tiny(shift_x=0, shift_y=0, cycle_scan=1)]
+    layers = [pl.PSCWinLayer(pl.LayerDesc.from_config(c), dev_weights(synth.make_weights(c, layer=i), c))
+              for i, c in enumerate(cfgs)]
+    x = synth.make_input(cfgs[0])
+    xd = dev(x)
+    stack = pl.PSCWinStack(layers, tuple(xd.shape), graph=True)
+    assert stack.launches_per_step >= 15
+    g1 = stack(xd).clone()
+    g2 = stack(xd).clone()
+    cur = xd
+    for layer in layers:
+        cur = layer(cur)
+    torch.cuda.synchronize()
+    assert torch.equal(g1, g2) and torch.equal(g1, cur)
+    ref = x
+    for i, c in enumerate(cfgs):
+        ref = oracle.pscwin_layer(ref, synth.make_weights(c, layer=i), c)
+    assert rel_err(host(g1), ref) < BF16_TOL
+
+
 CS_LAYERS = [synth.tiny(cycle_scan=1, shift_x=0, shift_y=0), synth.tiny(cycle_scan=1),
              synth.vitb(64, cycle_scan=1, shift_x=0, shift_y=0)]
 
