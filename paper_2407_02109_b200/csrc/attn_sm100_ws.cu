@@ -7,9 +7,11 @@
 //   warp 0     TMA: Q, K, V tiles of the item (5-D boxes straight from QKV [B,H,W,3,heads,d]; off-grid rows
 //              zero-filled) into one of two shared-memory stages (prefetch of item i+1 overlaps item i)
 //   warp 1     TMEM allocation + single-thread tcgen05.mma issue: S_a = Q_a K_t^T, O_a = P_a V_t (P from TMEM)
-//   warps 2-5  softmax warpgroup for q-tile 0, warps 6-9 for q-tile 1 (one query row per thread): fp32 online
-//              softmax over each key tile, P written back to TMEM as bf16 (aliasing S), running output in registers
-// TMEM per warpgroup a: S/P at columns [256a, 256a+128), O tile at [256a+128, 256a+128+d).
+//   warps 2-5  softmax warpgroup for q-tile 0, warps 6-9 for q-tile 1 (one query row per thread): the whole
+//              window (w^2 <= 256 keys) is ONE key tile, so softmax is a single exact pass (max, exp2, sum) in fp32;
+//              P is written back to TMEM as bf16 over the consumed S columns
+// TMEM per warpgroup a (256 columns): S at [256a, 256a+w^2), then P at [256a, 256a+w^2/2) and O at
+// [256a+128, 256a+128+d) (both alias S columns that were already read).
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -113,7 +115,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------------------------------ MMA issuer
-    const uint32_t idesc_s = make_idesc_bf16(128, p.tile_slots, 0, 0);
+    const int NK = nt * p.tile_slots;
+    const uint32_t idesc_s = make_idesc_bf16(128, NK, 0, 0);
     const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
     int stage = 0;
     uint32_t phase = 0;
@@ -126,35 +129,35 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       if (p.patch) mbar_wait(&patch_done[stage], phase);
       tc_fence_after();
       const uint32_t sb = smem_u32(smem + stage * STAGE);
-      for (int kt = 0; kt < nt; ++kt) {
-        for (int a = 0; a < 2; ++a) {
-          if (!act[a]) continue;
-          if (elect_one()) {
-            const uint32_t qa = sb + a * TILE, ka = sb + (2 + kt) * TILE;
+      // the whole window (NK = w^2 <= 256 keys) is one key tile: K0|K1 and V0|V1 are contiguous in shared memory
+      for (int a = 0; a < 2; ++a) {
+        if (!act[a]) continue;
+        mbar_wait(&o_free[a], ph_of[a] ^ 1);  // the previous item's O (aliasing S columns) has been read
+        ph_of[a] ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t qa = sb + a * TILE, ka = sb + 2 * TILE;
 #pragma unroll
-            for (int k = 0; k < D / 16; ++k)
-              umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
-                      idesc_s, k > 0);
-            umma_commit(&s_full[a]);
-          }
-          __syncwarp();
+          for (int k = 0; k < D / 16; ++k)
+            umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
+                    idesc_s, k > 0);
+          umma_commit(&s_full[a]);
         }
-        for (int a = 0; a < 2; ++a) {
-          if (!act[a]) continue;
-          mbar_wait(&p_full[a], ph_p[a]);
-          ph_p[a] ^= 1;
-          mbar_wait(&o_free[a], ph_of[a] ^ 1);
-          ph_of[a] ^= 1;
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t va = sb + (4 + kt) * TILE;
-            for (int ks = 0; ks < p.tile_slots / 16; ++ks)
-              umma_ts(tmem + 256 * a + 128, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
-                      idesc_o, ks > 0);
-            umma_commit(&o_full[a]);
-          }
-          __syncwarp();
+        __syncwarp();
+      }
+      for (int a = 0; a < 2; ++a) {
+        if (!act[a]) continue;
+        mbar_wait(&p_full[a], ph_p[a]);
+        ph_p[a] ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t va = sb + 4 * TILE;
+          for (int ks = 0; ks < NK / 16; ++ks)
+            umma_ts(tmem + 256 * a + 128, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
+                    idesc_o, ks > 0);
+          umma_commit(&o_full[a]);
         }
+        __syncwarp();
       }
       if (elect_one()) umma_commit(&ld_empty[stage]);  // all MMAs reading this stage are done -> TMA may refill
       __syncwarp();
@@ -205,98 +208,90 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         mbar_arrive(&patch_done[stage]);
       }
       if (active) {
-        float o_acc[D];
-#pragma unroll
-        for (int j = 0; j < D; ++j) o_acc[j] = 0.f;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int kt = 0; kt < nt; ++kt) {
-          // valid-key bitmask per 32-column chunk (MASKED: real slots only). Rows of the key tile: rpt; cols: w.
-          uint32_t xmask = 0xFFFFFFFFu;
-          int iy_lo = 0, iy_hi = 1 << 30;
-          if (masked) {
-            const int xl = max(0, -X0), xh = min(p.w, p.W - X0);
-            xmask = (xh > xl) ? (((1u << (xh - xl)) - 1u) << xl) : 0u;
-            iy_lo = -(Y0 + kt * p.rpt);
-            iy_hi = p.H - (Y0 + kt * p.rpt);
-          }
-          mbar_wait(&s_full[a], ph_s);
-          ph_s ^= 1;
-          tc_fence_after();
-          auto chunk_mask = [&](int c0) -> uint32_t {
-            if (!masked) return 0xFFFFFFFFu;
-            uint32_t m = 0;
-            const int rows = 32 >> p.lw;
-#pragma unroll 8
-            for (int rr = 0; rr < rows; ++rr) {
-              const int iy = (c0 >> p.lw) + rr;
-              if (iy >= iy_lo && iy < iy_hi) m |= (p.w == 32 ? xmask : (xmask & ((1u << p.w) - 1u))) << (rr * p.w);
-            }
-            return m;
-          };
-          float mx = -INFINITY;
-          for (int c0 = 0; c0 < p.tile_slots; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tS + c0, r);
-            tmem_wait_ld();
-            const uint32_t m = chunk_mask(c0);
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if ((m >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r[j]));
-          }
-          const float m_new = fmaxf(m_run, mx * p.sl2);
-          const float base = (m_new == -INFINITY) ? 0.f : m_new;
-          const float corr = (m_run == -INFINITY) ? 0.f : ex2_approx(m_run - base);
-          float lsum = 0.f;
-          for (int c0 = 0; c0 < p.tile_slots; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tS + c0, r);
-            tmem_wait_ld();
-            const uint32_t m = chunk_mask(c0);
-            uint32_t pk[16];
-#pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const float e0 = ((m >> j) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j]), p.sl2, -base)) : 0.f;
-              const float e1 = ((m >> (j + 1)) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j + 1]), p.sl2, -base)) : 0.f;
-              lsum += e0 + e1;
-              pk[j / 2] = pack_bf16(e0, e1);
-            }
-            tmem_st16(tS + c0 / 2, pk);  // P (bf16 pairs) over the already-consumed S columns
-          }
-          tmem_wait_st();
-          l_run = l_run * corr + lsum;
-          m_run = m_new;
-          tc_fence_before();
-          mbar_arrive(&p_full[a]);
-          mbar_wait(&o_full[a], ph_o);
-          ph_o ^= 1;
-          tc_fence_after();
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t r[32];
-            tmem_ld32(tO + c0, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) o_acc[c0 + j] = fmaf(o_acc[c0 + j], corr, __uint_as_float(r[j]));
-          }
-          tc_fence_before();
-          mbar_arrive(&o_free[a]);
+        const int NK = nt * p.tile_slots;  // keys of the window (one S tile)
+        // valid-key bitmask per 32-column chunk (MASKED: real slots only; all: columns inside the window)
+        uint32_t xmask = 0xFFFFFFFFu;
+        int iy_lo = 0, iy_hi = 1 << 30;
+        if (masked) {
+          const int xl = max(0, -X0), xh = min(p.w, p.W - X0);
+          xmask = (xh > xl) ? (((1u << (xh - xl)) - 1u) << xl) : 0u;
+          iy_lo = -Y0;
+          iy_hi = p.H - Y0;
         }
-        // normalise; write real query rows to the grid (merge / crop)
+        auto chunk_mask = [&](int c0) -> uint32_t {
+          const uint32_t in_tile = NK - c0 >= 32 ? 0xFFFFFFFFu : ((1u << (NK - c0)) - 1u);
+          if (!masked) return in_tile;
+          uint32_t m = 0;
+          const int rows = 32 >> p.lw;
+#pragma unroll 8
+          for (int rr = 0; rr < rows; ++rr) {
+            const int iy = (c0 >> p.lw) + rr;
+            if (iy >= iy_lo && iy < iy_hi) m |= (xmask & ((1u << p.w) - 1u)) << (rr * p.w);
+          }
+          return m & in_tile;
+        };
+        mbar_wait(&s_full[a], ph_s);
+        ph_s ^= 1;
+        tc_fence_after();
+        float mx = -INFINITY;
+        for (int c0 = 0; c0 < NK; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tS + c0, r);
+          tmem_wait_ld();
+          const uint32_t m = chunk_mask(c0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((m >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r[j]));
+        }
+        const float base = (mx == -INFINITY) ? 0.f : mx * p.sl2;
+        float lsum = 0.f;
+        for (int c0 = 0; c0 < NK; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tS + c0, r);
+          tmem_wait_ld();
+          const uint32_t m = chunk_mask(c0);
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float e0 = ((m >> j) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j]), p.sl2, -base)) : 0.f;
+            const float e1 = ((m >> (j + 1)) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j + 1]), p.sl2, -base)) : 0.f;
+            lsum += e0 + e1;
+            pk[j / 2] = pack_bf16(e0, e1);
+          }
+          tmem_st16(tS + c0 / 2, pk);  // P (bf16 pairs) over the already-consumed S columns
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[a]);
+        // O = P V lands in columns [128, 128 + d) (S columns already consumed); normalise and write the real
+        // query rows to the grid (merge / crop)
+        mbar_wait(&o_full[a], ph_o);
+        ph_o ^= 1;
+        tc_fence_after();
         const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
         const int Y = Y0 + iy, X = X0 + ix;
-        if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
-          const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-          uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
+        const bool write = row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W;
+        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
 #pragma unroll
-          for (int c = 0; c < D / 8; ++c) {
-            uint4 v;
-            v.x = pack_bf16(o_acc[c * 8 + 0] * inv, o_acc[c * 8 + 1] * inv);
-            v.y = pack_bf16(o_acc[c * 8 + 2] * inv, o_acc[c * 8 + 3] * inv);
-            v.z = pack_bf16(o_acc[c * 8 + 4] * inv, o_acc[c * 8 + 5] * inv);
-            v.w = pack_bf16(o_acc[c * 8 + 6] * inv, o_acc[c * 8 + 7] * inv);
-            dst[c] = v;
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tO + c0, r);
+          tmem_wait_ld();
+          if (write) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(r[c * 8 + 0]) * inv, __uint_as_float(r[c * 8 + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(r[c * 8 + 2]) * inv, __uint_as_float(r[c * 8 + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(r[c * 8 + 4]) * inv, __uint_as_float(r[c * 8 + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(r[c * 8 + 6]) * inv, __uint_as_float(r[c * 8 + 7]) * inv);
+              dst[c0 / 8 + c] = v;
+            }
           }
         }
+        tc_fence_before();
+        mbar_arrive(&o_free[a]);
       }
       if (++stage == 2) {
         stage = 0;

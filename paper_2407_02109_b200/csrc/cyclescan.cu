@@ -43,6 +43,7 @@ struct ScanParams {
   float* delta;      // [B, L+P, D]
   float* sumdt;      // [B, n_chunks, D]
   float* hs;         // [B, n_chunks, D, N]
+  __nv_bfloat16* gz;  // [B, L, D] SiLU(z) (written by the conv kernel when z != NULL)
   __nv_bfloat16* out;
   long long ld_out;
 };
@@ -67,11 +68,23 @@ __global__ void conv_silu_kernel(ScanParams p) {
   const int b = grp / groups_img;
   const int r0 = (grp - b * groups_img) * CONV_T;
   float wk[8][KMAX], bias[8];
+  {
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.conv_b + d0));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.conv_b + d0 + 4));
+    bias[0] = b0.x; bias[1] = b0.y; bias[2] = b0.z; bias[3] = b0.w;
+    bias[4] = b1.x; bias[5] = b1.y; bias[6] = b1.z; bias[7] = b1.w;
+  }
+  if (p.k == 4) {  // the 8 channels' taps are 32 contiguous floats
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    bias[c] = p.conv_b[d0 + c];
+    for (int c = 0; c < 8; ++c) {
+      const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.conv_w + (d0 + c) * 4));
+      wk[c][0] = w4.x; wk[c][1] = w4.y; wk[c][2] = w4.z; wk[c][3] = w4.w;
+    }
+  } else {
 #pragma unroll
-    for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? p.conv_w[(d0 + c) * p.k + i] : 0.f;
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? p.conv_w[(d0 + c) * p.k + i] : 0.f;
   }
   const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
   float win[KMAX][8];  // the k most recent inputs (slot k-1 = newest)
@@ -126,6 +139,15 @@ __global__ void conv_silu_kernel(ScanParams p) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) ow[q] = pack_bf16(silu_f(acc[2 * q]), silu_f(acc[2 * q + 1]));
     *reinterpret_cast<uint4*>(p.v + ((long long)b * rows_img + r) * p.D + d0) = o;
+    if (p.z && r < p.L) {  // output gate SiLU(z_t), once per token (used by the carry prefix and pass 2)
+      const uint4 zv = *reinterpret_cast<const uint4*>(p.z + ((long long)b * p.L + r) * p.ld_z + d0);
+      const uint32_t* zw = reinterpret_cast<const uint32_t*>(&zv);
+      uint4 g;
+      uint32_t* gw = reinterpret_cast<uint32_t*>(&g);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) gw[q] = pack_bf16(silu_f(bf16_lo(zw[q])), silu_f(bf16_hi(zw[q])));
+      *reinterpret_cast<uint4*>(p.gz + ((long long)b * p.L + r) * p.D + d0) = g;
+    }
   }
 }
 
@@ -170,7 +192,7 @@ struct StageLayout {
       if (p.z)
         for (int i = tid; i < nt * VPR; i += DPB) {
           const int j = i / VPR, cc = i - j * VPR;
-          cp_async16(sz + j * DPB + cc * 8, p.z + (tok0 + t + j) * p.ld_z + d0 + cc * 8);
+          cp_async16(sz + j * DPB + cc * 8, p.gz + (tok0 + t + j) * p.D + d0 + cc * 8);
         }
     }
   }
@@ -249,13 +271,15 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
       const float dt = compute_dt(drow);
       p.delta[(rbase + ts + j) * p.D + d] = dt;
       sdt += dt;
-      const float2* b2 = reinterpret_cast<const float2*>(drow + p.R);
+      const float4* b4 = reinterpret_cast<const float4*>(drow + p.R);  // two state pairs per 16-byte load
       const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
       for (int k = 0; k < N / 2; ++k) {
+        const float4 bq = b4[k / 2];
+        const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
         const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-        const float2 wn = __fmul2_rn(b2[k], nv2);                 // -w = -B v
+        const float2 wn = __fmul2_rn(bk, nv2);                    // -w = -B v
         if (zoh) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);               // h~ + w
           h[k] = __ffma2_rn(dA, t, wn);                            // dA (h~ + w) - w
@@ -325,12 +349,24 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   float Bb[NPL], sall = 0.f;
 #pragma unroll
   for (int j = 0; j < NPL; ++j) Bb[j] = 0.f;
-  for (int c = 0; c < p.n_chunks; ++c) {
-    const float s = sd[(long long)c * p.D];
-    sall += s;
+  constexpr int CB = 8;  // chunk summaries loaded in batches (independent loads, one round trip per batch)
+  for (int c0 = 0; c0 < p.n_chunks; c0 += CB) {
+    float sb[CB], hb[CB][NPL];
 #pragma unroll
-    for (int j = 0; j < NPL; ++j)
-      if (act[j]) Bb[j] = fmaf(ex2_approx(s * A2[j]), Bb[j], hs[(long long)c * p.D * N + lane + 32 * j]);
+    for (int i = 0; i < CB; ++i) {
+      const int c = c0 + i < p.n_chunks ? c0 + i : p.n_chunks - 1;
+      sb[i] = sd[(long long)c * p.D];
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) hb[i][j] = act[j] ? hs[(long long)c * p.D * N + lane + 32 * j] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      if (c0 + i >= p.n_chunks) break;
+      sall += sb[i];
+#pragma unroll
+      for (int j = 0; j < NPL; ++j)
+        if (act[j]) Bb[j] = fmaf(ex2_approx(sb[i] * A2[j]), Bb[j], hb[i][j]);
+    }
   }
   float c2[NPL], c3[NPL], H[NPL];
 #pragma unroll
@@ -368,22 +404,31 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
       if (lane == 0) {
         y += Ds * (__bfloat162float(p.v[r1 * p.D + d]) + 2.f * __bfloat162float(p.v[r2 * p.D + d]));
         const long long tok = (long long)b * p.L + t;
-        const float g = p.z ? silu_f(__bfloat162float(p.z[tok * p.ld_z + d])) : 1.f;
+        const float g = p.z ? __bfloat162float(p.gz[tok * p.D + d]) : 1.f;
         p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
       }
     }
   }
   // chunk entry states of the summed recurrence (input x3): H_in(0) = H_{P-1}; H_in(c+1) = a_c H_in(c) + 3 b_c
-  for (int c = 0; c < p.n_chunks; ++c) {
-    const float s = sd[(long long)c * p.D];
+  for (int c0 = 0; c0 < p.n_chunks; c0 += CB) {
+    float sb[CB], hb[CB][NPL];
 #pragma unroll
-    for (int j = 0; j < NPL; ++j)
-      if (act[j]) {
-        float* slot = hs + (long long)c * p.D * N + lane + 32 * j;
-        const float bc = *slot;
-        *slot = H[j];
-        H[j] = fmaf(ex2_approx(s * A2[j]), H[j], 3.f * bc);
-      }
+    for (int i = 0; i < CB; ++i) {
+      const int c = c0 + i < p.n_chunks ? c0 + i : p.n_chunks - 1;
+      sb[i] = sd[(long long)c * p.D];
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) hb[i][j] = act[j] ? hs[(long long)c * p.D * N + lane + 32 * j] : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < CB; ++i) {
+      if (c0 + i >= p.n_chunks) break;
+#pragma unroll
+      for (int j = 0; j < NPL; ++j)
+        if (act[j]) {
+          hs[(long long)(c0 + i) * p.D * N + lane + 32 * j] = H[j];
+          H[j] = fmaf(ex2_approx(sb[i] * A2[j]), H[j], 3.f * hb[i][j]);
+        }
+    }
   }
 }
 
@@ -442,17 +487,19 @@ __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
     const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
     const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
     for (int j = 0; j < nt; ++j) {
-      const float2* b2 = reinterpret_cast<const float2*>(sdbc + j * W + p.R);
-      const float2* c2 = b2 + N / 2;
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R);  // B pairs, then C pairs
       const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
       const float dt = sdt[j * DPB + threadIdx.x];
       const float2 dt2 = f2(dt), nv3 = f2(-3.f * v);
       float2 y2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int k = 0; k < N / 2; ++k) {
+        const float4 bq = b4[k / 2], cq = b4[N / 4 + k / 2];
+        const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
+        const float2 ck = (k & 1) ? make_float2(cq.z, cq.w) : make_float2(cq.x, cq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
         const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-        const float2 wn = __fmul2_rn(b2[k], nv3);                 // -3 B v
+        const float2 wn = __fmul2_rn(bk, nv3);                    // -3 B v
         if (zoh) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);
           h[k] = __ffma2_rn(dA, t, wn);
@@ -460,10 +507,10 @@ __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
           const float2 u = __fmul2_rn(__fmul2_rn(x, f2(0.69314718055994531f)), wn);
           h[k] = __ffma2_rn(dA, h[k], __fmul2_rn(u, m1));
         }
-        y2 = __ffma2_rn(__fmul2_rn(c2[k], invA[k]), h[k], y2);  // C . h = C . (h~ / A)
+        y2 = __ffma2_rn(__fmul2_rn(ck, invA[k]), h[k], y2);     // C . h = C . (h~ / A)
       }
       const float y = fmaf(D3, v, y2.x + y2.y);
-      const float g = p.z ? silu_f(__bfloat162float(sz[j * DPB + threadIdx.x])) : 1.f;
+      const float g = p.z ? __bfloat162float(sz[j * DPB + threadIdx.x]) : 1.f;
       p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
     }
     __syncthreads();
@@ -472,8 +519,8 @@ __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
 
 // ------------------------------------------------------------------------------------------------- host
 struct ScanPlan {
-  int P, Lc, n_chunks, W;
-  size_t v, dbc, delta, sumdt, hs, total;
+  int P, Lc, n_chunks, W, xsplits;
+  size_t v, dbc, delta, sumdt, hs, gz, partial, sem, total;
 };
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -513,6 +560,19 @@ static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
   off += al256((size_t)B * s.n_chunks * D * 4);
   s.hs = off;
   off += al256((size_t)B * s.n_chunks * D * N * 4);
+  s.gz = off;
+  off += al256((size_t)B * L * D * 2);
+  // x_proj split-K: enough K splits for the (few) M tiles to cover the SMs, at least 4 k-blocks per split
+  const int m_tiles = (int)((rows + 127) / 128);
+  const int kblocks = (D + 63) / 64;
+  int sp = 148 / (m_tiles > 0 ? m_tiles : 1);
+  if (sp > 8) sp = 8;
+  if (sp > kblocks / 4) sp = kblocks / 4;
+  s.xsplits = sp > 1 ? sp : 1;
+  s.partial = off;
+  off += s.xsplits > 1 ? al256((size_t)s.xsplits * rows * s.W * 4) : 0;
+  s.sem = off;
+  off += al256((size_t)m_tiles * sizeof(int));
   s.total = off;
   return s;
 }
@@ -595,6 +655,7 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.delta = reinterpret_cast<float*>(base + pl.delta);
   p.sumdt = reinterpret_cast<float*>(base + pl.sumdt);
   p.hs = reinterpret_cast<float*>(base + pl.hs);
+  p.gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
   p.out = out;
   p.ld_out = ld_out;
   const long long rows = (long long)B * (L + pl.P);
@@ -614,6 +675,11 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   g.out = p.dbc;
   g.ldo = pl.W;
   g.epi = EPI_STORE_F32;
+  g.BN = ((pl.W + 15) / 16) * 16;  // one N tile (R + 2N <= 256)
+  g.splits = pl.xsplits;           // split-K when the M tiles alone cannot fill the SMs
+  g.partial = reinterpret_cast<float*>(base + pl.partial);
+  g.sem = reinterpret_cast<int*>(base + pl.sem);
+  if (g.splits > 1) cudaMemsetAsync(g.sem, 0, (size_t)((g.M + 127) / 128) * sizeof(int), s);
   int rc = launch_gemm_bf16(p.v, w_x, g, s);
   if (rc) return PSCWIN_ERR_CUDA;
   if (N == 16) rc = launch_passes<16>(p, s);

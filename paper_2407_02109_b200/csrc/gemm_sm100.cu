@@ -21,10 +21,15 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int STAGES = 4;
 constexpr int A_STAGE_BYTES = BM * BK * 2;       // 16 KB
-constexpr int B_STAGE_BYTES = 256 * BK * 2;      // 32 KB (max BN)
-constexpr int STAGE_OUT_BYTES = BM * 64 * 2;   // one 128x64 bf16 output chunk
-constexpr int GEMM_THREADS = 64 + 256;      // TMA warp, MMA warp, 8 epilogue warps
-constexpr size_t GEMM_SMEM = 1024 /*align slack*/ + STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + 2 * STAGE_OUT_BYTES + 256;
+constexpr int STAGE_OUT_BYTES = BM * 64 * 2;     // one 128x64 bf16 output / residual chunk (16 KB)
+constexpr int GEMM_THREADS = 64 + 256;           // TMA warp, MMA warp, 8 epilogue warps
+constexpr size_t GEMM_SMEM_MAX = 230656;         // 1024 + 4 x 48 KB + 32 KB + 256 (also = BN 128 + residual)
+// shared memory layout for a tile width BN (B stage = BN x 64 bf16; residual tiles double-buffered)
+__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid) {
+  const size_t nch = (size_t)(BN + 63) / 64;
+  return 1024 + (size_t)STAGES * (A_STAGE_BYTES + (size_t)BN * BK * 2) + 2 * STAGE_OUT_BYTES +
+         (resid ? 2 * nch * STAGE_OUT_BYTES : 0) + 256;
+}
 }  // namespace
 
 __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) {
@@ -36,24 +41,42 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmOut, GemmArgs p) {
+                     const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
+                     GemmArgs p) {
   extern __shared__ uint8_t smem_raw[];
+  const int BN = p.BN;
+  const int B_STAGE_BYTES = BN * BK * 2;
+  const bool resid_tma = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
+  const int nch = (BN + 63) / 64;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_stage + 2 * STAGE_OUT_BYTES);
+  uint8_t* s_res = s_stage + 2 * STAGE_OUT_BYTES;   // 2 x nch x 16 KB residual tiles (TMA-loaded)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : 0));
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
   uint64_t* tempty = bars + 2 * STAGES + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* rfull = bars + 2 * STAGES + 4;   // [2] residual tile landed
+  uint64_t* rempty = bars + 2 * STAGES + 6;  // [2] residual tile consumed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
+  int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = warp_id();
-  const int BN = p.BN;
   const int n_tiles_n = (p.N + BN - 1) / BN;
-  const int n_tiles = ((p.M + BM - 1) / BM) * n_tiles_n;
+  const int S = p.splits > 1 ? p.splits : 1;  // split-K factor (f32 outputs only)
+  const int n_tiles = ((p.M + BM - 1) / BM) * n_tiles_n * S;
   const int nk = (p.K + BK - 1) / BK;
+  // work tile -> output tile (m0, n0), k-block range [kb0, kb1) and split index
+  auto coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1, int& s) {
+    const int mn = tile / S;
+    s = tile - mn * S;
+    m0 = (mn / n_tiles_n) * BM;
+    n0 = (mn % n_tiles_n) * BN;
+    kb0 = (int)((long long)nk * s / S);
+    kb1 = (int)((long long)nk * (s + 1) / S);
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
@@ -66,7 +89,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 256);
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], 256);
     }
+    if (resid_tma) tma_prefetch_desc(&tmRes);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -81,10 +107,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      int rbuf = 0;
+      uint32_t rphase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile / n_tiles_n) * BM;
-        const int n0 = (tile % n_tiles_n) * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+        int m0, n0, kb0, kb1, s;
+        coords(tile, m0, n0, kb0, kb1, s);
+        if (resid_tma) {
+          // residual tile of this output tile (double-buffered, consumed by the epilogue), issued ahead of the k-loop
+          mbar_wait(&rempty[rbuf], rphase ^ 1);
+          mbar_arrive_expect_tx(&rfull[rbuf], nch * STAGE_OUT_BYTES);
+          for (int c = 0; c < nch; ++c)
+            tma_load_2d(s_res + (rbuf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[rbuf], n0 + c * 64, m0, pol_a);
+          if (++rbuf == 2) {
+            rbuf = 0;
+            rphase ^= 1;
+          }
+        }
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + BN * BK * 2);
           tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m0, pol_a);
@@ -103,10 +142,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int m0, n0, kb0, kb1, s;
+      coords(tile, m0, n0, kb0, kb1, s);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * 256;
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -116,10 +157,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, kLayoutSW128);
             uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, kLayoutSW128);
-            umma_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            umma_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
-          if (kb == nk - 1) umma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -142,13 +183,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool issuer = etid == 0;
     const bool tma_out = p.epi != EPI_STORE_F32;
     const int row_local = quarter * 32 + lane;
-    const int nch = (BN + 63) / 64;
     int acc = 0;
     uint32_t acc_phase = 0;
     int gseq = 0;
+    int rbuf = 0;
+    uint32_t rphase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const int m0 = (tile / n_tiles_n) * BM;
-      const int n0 = (tile % n_tiles_n) * BN;
+      int m0, n0, kb0, kb1, split;
+      coords(tile, m0, n0, kb0, kb1, split);
       const int row = m0 + row_local;
       const bool row_ok = row < p.M;
       // RoPE of this row (QKV epilogue): this thread's 32 columns of every 64-column chunk are one half of a head
@@ -166,19 +208,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (resid_tma) mbar_wait(&rfull[rbuf], rphase);
       const uint32_t t_row = tmem_base + acc * 256 + ((uint32_t)(quarter * 32) << 16);
       for (int cc = 0; cc < nch; ++cc, ++gseq) {
         const int cl = cc * 64 + half * 32;            // tile-local first column of this thread's 32
         const int col0 = n0 + cl;
-        // residual prefetch (bf16, 4 x 16B) before the TMEM load
+        // residual: this thread's 4 x 16B of the TMA-loaded tile (swizzled like the output staging)
         uint4 res[4];
-        const bool use_res = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
-        if (use_res) {
-          const uint4* rp = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(p.residual) +
-                                                           (size_t)row * p.ldr + col0);
+        if (resid_tma) {
+          const uint8_t* rt = s_res + (rbuf * nch + cc) * STAGE_OUT_BYTES;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            res[q] = (row_ok && cl < BN && col0 + 8 * q < p.N) ? rp[q] : make_uint4(0, 0, 0, 0);
+          for (int q = 0; q < 4; ++q) res[q] = *reinterpret_cast<const uint4*>(rt + swz_offset(row_local, half * 4 + q, 128));
         }
         uint8_t* stg = s_stage + (gseq & 1) * STAGE_OUT_BYTES;
         if (tma_out) {
@@ -196,16 +236,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.bias) {
+        if (p.bias) {  // 16-byte broadcast loads (every lane of the warp reads the same columns)
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < p.N) v[j] += __ldg(p.bias + col0 + j);
+          for (int j = 0; j < 32; j += 4)
+            if (col0 + j + 4 <= p.N) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            } else {
+              for (int e = 0; e < 4 && col0 + j + e < p.N; ++e) v[j + e] += __ldg(p.bias + col0 + j + e);
+            }
         }
         if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
         }
-        if (use_res) {
+        if (resid_tma) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const uint32_t* rw = reinterpret_cast<const uint32_t*>(&res[q]);
@@ -233,11 +278,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             bulk_commit();
           }
         } else if (row_ok && cl < BN) {
-          float* o = reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0;
+          // f32 output; with split-K each split first writes its partial tile ([S][M][N] workspace)
+          const int ld = S > 1 ? p.N : p.ldo;
+          float* o = (S > 1 ? p.partial + (size_t)split * p.M * p.N : reinterpret_cast<float*>(p.out)) +
+                     (size_t)row * ld + col0;
 #pragma unroll
           for (int j = 0; j < 32; j += 4)
             if (col0 + j < p.N) {
-              if (col0 + j + 4 <= p.N && (p.ldo % 4) == 0) {
+              if (col0 + j + 4 <= p.N && (ld % 4) == 0) {
                 *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
               } else {
                 for (int e = 0; e < 4 && col0 + j + e < p.N; ++e) o[j + e] = v[j + e];
@@ -249,6 +297,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+      if (resid_tma) {
+        mbar_arrive(&rempty[rbuf]);
+        if (++rbuf == 2) {
+          rbuf = 0;
+          rphase ^= 1;
+        }
+      }
+      if (S > 1) {
+        // deterministic split-K fix-up: the last split to finish this output tile sums the S partials in split
+        // order (no floating-point atomics) and resets the tile's counter for the next launch.
+        const int mn = tile / S;
+        __threadfence();
+        named_bar_sync(1, 256);
+        if (issuer) *s_flag = atomicAdd(&p.sem[mn], 1);
+        named_bar_sync(1, 256);
+        if (*s_flag == S - 1) {
+          __threadfence();
+          for (int cc = 0; cc < nch; ++cc) {
+            const int col0 = n0 + cc * 64 + half * 32;
+            if (!row_ok || cc * 64 + half * 32 >= BN) continue;
+            // 16-byte loads of all splits issued together, summed in split order (N % 4 == 0 checked on the host)
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              if (col0 + j >= p.N) break;
+              float4 part[8];
+#pragma unroll
+              for (int s2 = 0; s2 < 8; ++s2)
+                if (s2 < S)
+                  part[s2] = __ldcg(reinterpret_cast<const float4*>(p.partial + ((size_t)s2 * p.M + row) * p.N + col0 + j));
+              float4 sum = part[0];
+#pragma unroll
+              for (int s2 = 1; s2 < 8; ++s2)
+                if (s2 < S) {
+                  sum.x += part[s2].x; sum.y += part[s2].y; sum.z += part[s2].z; sum.w += part[s2].w;
+                }
+              *reinterpret_cast<float4*>(reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0 + j) = sum;
+            }
+          }
+          if (issuer) p.sem[mn] = 0;
+        }
+        named_bar_sync(1, 256);
+      }
     }
     if (issuer && tma_out) bulk_wait0();
   }
@@ -264,16 +354,21 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (p.M <= 0 || p.N <= 0) return 0;
   if (p.K % 8 != 0) return -1;
   if (p.epi == EPI_QKV_ROPE && p.rope && !(p.d_head == 32 || p.d_head == 64)) return -2;
-  // tile N: a single tile when N <= 256; else 256, or 128 when 256-wide tiles would leave SMs idle
+  const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
+  // tile N: a single tile when N <= 256; else 256, or 128 when 256-wide tiles would leave SMs idle. Residual
+  // epilogues stage the residual tile in shared memory, which fits next to the 4-stage ring only for BN <= 128.
   if (p.BN <= 0) {
-    if (p.N <= 256) {
+    if (p.N <= (resid ? 128 : 256)) {
       p.BN = ((p.N + 15) / 16) * 16;
     } else {
       const long long t256 = (long long)((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
-      p.BN = t256 >= 2LL * num_sms() ? 256 : 128;
+      p.BN = (!resid && t256 >= 2LL * num_sms()) ? 256 : 128;
     }
   }
-  CUtensorMap tmA, tmB, tmOut;
+  if (resid && p.BN > 128) return -2;
+  if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
+    return -3;
+  CUtensorMap tmA, tmB, tmOut, tmRes;
   int rc = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.M, (uint64_t)p.lda * 2, BK, BM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
@@ -287,15 +382,24 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
                       CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
+  memset(&tmRes, 0, sizeof(tmRes));
+  if (resid) {
+    if ((p.ldr * 2) % 16) return -1;
+    rc = make_tmap_2d(&tmRes, p.residual, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldr * 2, 64, BM,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+    cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
     attr_set = true;
   }
-  int tiles = ((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN);
-  int grid = tiles < num_sms() ? tiles : num_sms();
+  const size_t smem = gemm_smem_bytes(p.BN, resid);
+  if (smem > GEMM_SMEM_MAX) return -2;
+  const long long tiles = (long long)((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
+  const int grid = tiles < num_sms() ? (int)tiles : num_sms();
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
-  gemm_bf16_kernel<<<grid, GEMM_THREADS, GEMM_SMEM, stream>>>(tmA, tmB, tmOut, p);
+  gemm_bf16_kernel<<<grid, GEMM_THREADS, smem, stream>>>(tmA, tmB, tmOut, tmRes, p);
   return (int)cudaGetLastError();
 }
 

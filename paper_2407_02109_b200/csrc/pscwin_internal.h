@@ -24,6 +24,11 @@ struct GemmArgs {
   // QKV + RoPE epilogue
   int rope, HW, Wgrid, C, d_head;
   const char* prof_name;  // kernel label for pscwin_profile_read
+  // split-K (f32 output only): splits > 1 needs partial [splits][M][N] f32 and sem [m_tiles * n_tiles] ints that
+  // are zero before the first launch (the kernel leaves them zero again)
+  int splits;
+  float* partial;
+  int* sem;
 };
 
 // host helpers (abi.cu)

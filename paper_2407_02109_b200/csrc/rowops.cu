@@ -60,12 +60,19 @@ __global__ void layer_norm_kernel(const T* __restrict__ x, long long rows, int C
       uint4 w;
       const T* e = reinterpret_cast<const T*>(&v[k]);
       T* o = reinterpret_cast<T*>(&w);
+      float gg[EPV], bb[EPV];  // gamma / beta for this vector, 16-byte loads
+#pragma unroll
+      for (int j = 0; j < EPV; j += 4) {
+        const float4 g4 = __ldg(reinterpret_cast<const float4*>(g + i * EPV + j));
+        const float4 b4 = __ldg(reinterpret_cast<const float4*>(b + i * EPV + j));
+        gg[j] = g4.x; gg[j + 1] = g4.y; gg[j + 2] = g4.z; gg[j + 3] = g4.w;
+        bb[j] = b4.x; bb[j + 1] = b4.y; bb[j + 2] = b4.z; bb[j + 3] = b4.w;
+      }
 #pragma unroll
       for (int j = 0; j < EPV; ++j) {
-        int c = i * EPV + j;
         float f;
         if constexpr (sizeof(T) == 2) f = __bfloat162float(e[j]); else f = e[j];
-        float y = (f - mean) * rstd * g[c] + b[c];
+        float y = (f - mean) * rstd * gg[j] + bb[j];
         if constexpr (sizeof(T) == 2) o[j] = __float2bfloat16_rn(y); else o[j] = y;
       }
       dst[i] = w;
