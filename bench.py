@@ -255,6 +255,9 @@ def run_ours(args, rank, world, local_rank):
     pl.profile_enable(True)
     for i in range(args.steps):
         flush.zero_()
+        # park the stream ~1 ms so the host enqueues the whole eager step before the GPU reaches it: the per-kernel
+        # events then time back-to-back kernels, not host launch latency
+        torch.cuda._sleep(2_000_000)
         step_eager(x0)
     torch.cuda.synchronize()
     prof = pl.profile_read()

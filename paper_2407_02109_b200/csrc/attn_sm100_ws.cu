@@ -3,23 +3,37 @@
 // O = softmax(q k^T / sqrt(d)) v per (window, head), pad slots LEARNABLE (projected p, K rotated at the slot's
 // geometric coordinate) or MASKED (-inf), only real rows written back to the [B,H,W,C] grid.
 //
-// Roles (320 threads, one CTA per SM, loops over (image, window, head) work items):
+// Roles (576 threads, one CTA per SM, loops over (image, window, head) work items):
 //   warp 0     TMA: Q, K, V tiles of the item (5-D boxes straight from QKV [B,H,W,3,heads,d]; off-grid rows
 //              zero-filled) into one of two shared-memory stages (prefetch of item i+1 overlaps item i)
 //   warp 1     TMEM allocation + single-thread tcgen05.mma issue: S_a = Q_a K_t^T, O_a = P_a V_t (P from TMEM)
-//   warps 2-5  softmax warpgroup for q-tile 0, warps 6-9 for q-tile 1 (one query row per thread): the whole
-//              window (w^2 <= 256 keys) is ONE key tile, so softmax is a single exact pass (max, exp2, sum) in fp32;
-//              P is written back to TMEM as bf16 over the consumed S columns
-// TMEM per warpgroup a (256 columns): S at [256a, 256a+w^2), then P at [256a, 256a+w^2/2) and O at
-// [256a+128, 256a+128+d) (both alias S columns that were already read).
+//   warps 2-17 four softmax warpgroups: q tile a = 0/1, each query row split over two threads by key halves
+//              (row max / sum combined in shared memory). The whole window (w^2 <= 256 keys) is ONE key tile, so
+//              softmax is a single exact pass (max, exp2, sum) in fp32; P is written back to TMEM as bf16 over
+//              the consumed S columns
+// TMEM per q tile a (256 columns): S at [256a, 256a+w^2); then P of keys < 128 at [256a, 256a+64), P of keys
+// >= 128 at [256a+128, 256a+192) and O at [256a+192, 256a+192+d) (all alias S columns already consumed).
+#include <stdio.h>
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "pscwin_internal.h"
 
 namespace pscwin {
 
 namespace {
-constexpr int WS_THREADS = 320;
+constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroups
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
+}
+// debug timeline: role slot base (0 loader, 32 MMA, 64 WG0, 96 WG1), 32 events each per CTA
+#define ATT_TS(base, cnt)                                                                   \
+  do {                                                                                      \
+    if (p.dbg && lane_id() == 0) p.dbg[blockIdx.x * 128 + (base) + ((cnt)++ & 31)] = gtimer(); \
+  } while (0)
 
 struct AttnWsArgs {
   int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
@@ -27,9 +41,10 @@ struct AttnWsArgs {
   float sl2;
   const __nv_bfloat16 *kx, *ky, *vp;
   __nv_bfloat16* out;
+  unsigned long long* dbg;  // debug timeline (PSCWIN_ATTN_TIMELINE), else null
 };
 
-template <int D>
+template <int D, bool MASKED>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnWsArgs p) {
   constexpr int ROWB = D * 2;
@@ -49,6 +64,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   uint64_t* o_full = bars + 10;      // [2]
   uint64_t* o_free = bars + 12;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  float* s_red = reinterpret_cast<float*>(bars + 16);  // [2 q tiles][2 halves][128 rows] partial row max / sum
 
   const int warp = warp_id();
   const int nt = p.n_tiles;
@@ -59,11 +75,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ld_full[i], 1);
       mbar_init(&ld_empty[i], 1);
-      mbar_init(&patch_done[i], 256);
+      mbar_init(&patch_done[i], 512);
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
+      mbar_init(&p_full[i], 256);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], 128);
+      mbar_init(&o_free[i], 256);
     }
     fence_barrier_init();
   }
@@ -93,12 +109,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     // ------------------------------------------------------------------------------------------ TMA producer
     if (elect_one()) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
+      int stage = 0, ev = 0;
       uint32_t phase = 0;
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         int b, h, X0, Y0;
         decode(item, b, h, X0, Y0);
         mbar_wait(&ld_empty[stage], phase ^ 1);
+        ATT_TS(0, ev);
         mbar_arrive_expect_tx(&ld_full[stage], 3 * nt * tile_tx);
         uint8_t* st = smem + stage * STAGE;
         for (int t = 0; t < nt; ++t) {
@@ -121,12 +138,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     int stage = 0;
     uint32_t phase = 0;
     uint32_t ph_p[2] = {0, 0}, ph_of[2] = {0, 0};
+    int ev = 0;
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
       const bool act[2] = {q_active(0, Y0), q_active(1, Y0)};
       mbar_wait(&ld_full[stage], phase);
       if (p.patch) mbar_wait(&patch_done[stage], phase);
+      ATT_TS(32, ev);
       tc_fence_after();
       const uint32_t sb = smem_u32(smem + stage * STAGE);
       // the whole window (NK = w^2 <= 256 keys) is one key tile: K0|K1 and V0|V1 are contiguous in shared memory
@@ -149,12 +168,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         if (!act[a]) continue;
         mbar_wait(&p_full[a], ph_p[a]);
         ph_p[a] ^= 1;
+        ATT_TS(32, ev);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t va = sb + 4 * TILE;
-          for (int ks = 0; ks < NK / 16; ++ks)
-            umma_ts(tmem + 256 * a + 128, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
-                    idesc_o, ks > 0);
+          for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128)
+            umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (ks >= 8 ? 64 : 0),
+                    make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
           umma_commit(&o_full[a]);
         }
         __syncwarp();
@@ -168,17 +188,32 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------------------------------------ softmax WGs
-    const int a = (warp - 2) >> 2;           // q tile / warpgroup
+    // 16 warps: q tile a = sw >> 3, column half hc = (sw >> 2) & 1. The two warps of a q tile that share a TMEM
+    // lane quarter split each query row's keys in halves; row max / sum are combined through shared memory.
+    const int sw = warp - 2;
+    const int a = sw >> 3;
+    const int hc = (sw >> 2) & 1;
     const int quarter = warp & 3;
-    const int row = quarter * 32 + lane_id();  // query slot within the q tile (= TMEM lane)
-    const int wtid = (warp - 2) * 32 + lane_id();  // 0..255 over both warpgroups
+    const int row = quarter * 32 + lane_id();        // query slot within the q tile (= TMEM lane)
+    const int wtid = sw * 32 + lane_id();            // 0..511
+    const int gtid = (sw & 7) * 32 + lane_id();      // 0..255 within the q tile's two warpgroups
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tmem + 256 * a + lane_base;
-    const uint32_t tO = tmem + 256 * a + 128 + lane_base;
-    const bool masked = p.pad_mode == 1;
+    const uint32_t tO = tmem + 256 * a + 192 + lane_base;
+    float* red_max = s_red + (a * 2) * 128;          // [2][128]
+    float* red_sum = s_red + 512 + (a * 2) * 128;
     int stage = 0;
     uint32_t phase = 0;
     uint32_t ph_s = 0, ph_o = 0;
+    int ev = 0;
+    const int NK = nt * p.tile_slots;                // keys of the window (one S tile)
+    // keys are split between the two threads of a row only for 256-key windows (w = 16); smaller windows use one
+    const bool split = NK == 256;
+    const int half_cols = split ? 128 : NK;
+    const bool col_active = split || hc == 0;
+    const uint32_t tail_mask = NK >= 32 ? 0xFFFFFFFFu : ((1u << NK) - 1u);  // 16-key windows (w = 4)
+    const int c_lo = hc * half_cols;
+    const float2 sl2 = make_float2(p.sl2, p.sl2);
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
@@ -208,19 +243,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         mbar_arrive(&patch_done[stage]);
       }
       if (active) {
-        const int NK = nt * p.tile_slots;  // keys of the window (one S tile)
-        // valid-key bitmask per 32-column chunk (MASKED: real slots only; all: columns inside the window)
+        // MASKED: valid-key bitmask per 32-column chunk (real slots only); columns past the window are never read
         uint32_t xmask = 0xFFFFFFFFu;
         int iy_lo = 0, iy_hi = 1 << 30;
-        if (masked) {
+        if (MASKED) {
           const int xl = max(0, -X0), xh = min(p.w, p.W - X0);
           xmask = (xh > xl) ? (((1u << (xh - xl)) - 1u) << xl) : 0u;
           iy_lo = -Y0;
           iy_hi = p.H - Y0;
         }
         auto chunk_mask = [&](int c0) -> uint32_t {
-          const uint32_t in_tile = NK - c0 >= 32 ? 0xFFFFFFFFu : ((1u << (NK - c0)) - 1u);
-          if (!masked) return in_tile;
           uint32_t m = 0;
           const int rows = 32 >> p.lw;
 #pragma unroll 8
@@ -228,70 +260,115 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             const int iy = (c0 >> p.lw) + rr;
             if (iy >= iy_lo && iy < iy_hi) m |= (xmask & ((1u << p.w) - 1u)) << (rr * p.w);
           }
-          return m & in_tile;
+          return m;
         };
+        const int nc = col_active ? half_cols : 0;   // this thread's columns [c_lo, c_lo + nc)
         mbar_wait(&s_full[a], ph_s);
         ph_s ^= 1;
+        if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
         tc_fence_after();
+        // pass 1: partial row max (two TMEM loads per wait::ld)
         float mx = -INFINITY;
-        for (int c0 = 0; c0 < NK; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tS + c0, r);
+        for (int c0 = c_lo; c0 < c_lo + nc; c0 += 64) {
+          uint32_t r0[32], r1[32];
+          const bool two = c0 + 32 < c_lo + nc;
+          tmem_ld32(tS + c0, r0);
+          if (two) tmem_ld32(tS + c0 + 32, r1);
           tmem_wait_ld();
-          const uint32_t m = chunk_mask(c0);
+          if (MASKED || tail_mask != 0xFFFFFFFFu) {
+            const uint32_t m0 = (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask;
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if ((m >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r[j]));
+            for (int j = 0; j < 32; ++j)
+              if ((m0 >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r0[j]));
+            if (two) {
+              const uint32_t m1 = MASKED ? chunk_mask(c0 + 32) : 0xFFFFFFFFu;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((m1 >> j) & 1u) mx = fmaxf(mx, __uint_as_float(r1[j]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r0[j]));
+            if (two) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r1[j]));
+            }
+          }
         }
+        red_max[hc * 128 + row] = mx;
+        named_bar_sync(1 + a, 256);
+        mx = fmaxf(mx, red_max[(hc ^ 1) * 128 + row]);
         const float base = (mx == -INFINITY) ? 0.f : mx * p.sl2;
-        float lsum = 0.f;
-        for (int c0 = 0; c0 < NK; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tS + c0, r);
-          tmem_wait_ld();
-          const uint32_t m = chunk_mask(c0);
-          uint32_t pk[16];
+        const float2 nb = make_float2(-base, -base);
+        // pass 2: p = 2^(s log2(e)/sqrt(d) - base) (packed fp32x2 scale, MUFU ex2), partial sums, P (bf16 pairs)
+        // written over the consumed S columns
+        float2 ls = make_float2(0.f, 0.f);
+        auto exp_chunk = [&](const uint32_t (&r)[32], uint32_t m, uint32_t (&pk)[16]) {
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float e0 = ((m >> j) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j]), p.sl2, -base)) : 0.f;
-            const float e1 = ((m >> (j + 1)) & 1u) ? ex2_approx(fmaf(__uint_as_float(r[j + 1]), p.sl2, -base)) : 0.f;
-            lsum += e0 + e1;
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl2, nb);
+            float e0 = ex2_approx(x.x), e1 = ex2_approx(x.y);
+            if (MASKED || m != 0xFFFFFFFFu) {  // invalid keys, or stale columns past a 16-key window
+              e0 = ((m >> j) & 1u) ? e0 : 0.f;
+              e1 = ((m >> (j + 1)) & 1u) ? e1 : 0.f;
+            }
+            ls = __fadd2_rn(ls, make_float2(e0, e1));
             pk[j / 2] = pack_bf16(e0, e1);
           }
-          tmem_st16(tS + c0 / 2, pk);  // P (bf16 pairs) over the already-consumed S columns
+        };
+        // P for key k goes to TMEM column k/2 (keys < 128) or 64 + k/2 (keys >= 128): each thread overwrites only S
+        // columns it has already consumed (the PV MMA reads A from columns [0,64) and [128,192)).
+        const int p_off = (split && hc) ? 64 : 0;
+        for (int c0 = c_lo; c0 < c_lo + nc; c0 += 32) {
+          uint32_t r0[32], pk[16];
+          tmem_ld32(tS + c0, r0);
+          tmem_wait_ld();
+          exp_chunk(r0, (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask, pk);
+          tmem_st16(tS + p_off + c0 / 2, pk);
         }
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[a]);
-        // O = P V lands in columns [128, 128 + d) (S columns already consumed); normalise and write the real
-        // query rows to the grid (merge / crop)
+        red_sum[hc * 128 + row] = ls.x + ls.y;
+        if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
+        // O = P V lands in columns [192, 192 + d): this thread takes d/2 of them (its column half), copies them to
+        // registers, releases the TMEM columns (the next item's S may overwrite them), then normalises and writes
+        // its half of the real query row to the grid (merge / crop)
         mbar_wait(&o_full[a], ph_o);
         ph_o ^= 1;
+        if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
         tc_fence_after();
-        const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
-        const int Y = Y0 + iy, X = X0 + ix;
-        const bool write = row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W;
-        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
+        constexpr int DH = D / 2;
+        uint32_t o[32];
+        if (DH == 32) {
+          tmem_ld32(tO + hc * 32, o);
+        } else {
+          uint32_t o16[16];
+          tmem_ld16(tO + hc * 16, o16);
 #pragma unroll
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(tO + c0, r);
-          tmem_wait_ld();
-          if (write) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 v;
-              v.x = pack_bf16(__uint_as_float(r[c * 8 + 0]) * inv, __uint_as_float(r[c * 8 + 1]) * inv);
-              v.y = pack_bf16(__uint_as_float(r[c * 8 + 2]) * inv, __uint_as_float(r[c * 8 + 3]) * inv);
-              v.z = pack_bf16(__uint_as_float(r[c * 8 + 4]) * inv, __uint_as_float(r[c * 8 + 5]) * inv);
-              v.w = pack_bf16(__uint_as_float(r[c * 8 + 6]) * inv, __uint_as_float(r[c * 8 + 7]) * inv);
-              dst[c0 / 8 + c] = v;
-            }
-          }
+          for (int j = 0; j < 16; ++j) o[j] = o16[j];
         }
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(&o_free[a]);
+        named_bar_sync(1 + a, 256);  // partial sums of both halves are in shared memory
+        const float lsum = red_sum[row] + (split ? red_sum[128 + row] : 0.f);
+        const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
+        const int Y = Y0 + iy, X = X0 + ix;
+        if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+          const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+          uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D + hc * DH);
+#pragma unroll
+          for (int c = 0; c < DH / 8; ++c) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[c * 8 + 0]) * inv, __uint_as_float(o[c * 8 + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
+            dst[c] = v;
+          }
+        }
+        if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
       }
       if (++stage == 2) {
         stage = 0;
@@ -336,6 +413,14 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   p.ky = reinterpret_cast<const __nv_bfloat16*>(ky);
   p.vp = reinterpret_cast<const __nv_bfloat16*>(vp);
   p.out = reinterpret_cast<__nv_bfloat16*>(a.out);
+  p.dbg = nullptr;
+  static unsigned long long* dbg_buf = nullptr;
+  const char* tl = getenv("PSCWIN_ATTN_TIMELINE");
+  if (tl) {
+    if (!dbg_buf) cudaMalloc(&dbg_buf, 148 * 128 * sizeof(unsigned long long));
+    cudaMemsetAsync(dbg_buf, 0, 148 * 128 * sizeof(unsigned long long), stream);
+    p.dbg = dbg_buf;
+  }
   if (p.n_tiles > 2 || p.tile_slots < 16) return -2;
   CUtensorMap tmQKV;
   const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
@@ -345,23 +430,27 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   int rc = make_tmap_5d(&tmQKV, a.qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dq, sq, box,
                         d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
-  const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8;
+  const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8 + 1024 * 4;
   const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
   PSCWIN_PROF("window_attention", stream);
-  if (d == 64) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(window_attn_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
+  };
+  const bool masked = p.pad_mode == 1;
+  if (d == 64)
+    masked ? launch(window_attn_ws_kernel<64, true>) : launch(window_attn_ws_kernel<64, false>);
+  else
+    masked ? launch(window_attn_ws_kernel<32, true>) : launch(window_attn_ws_kernel<32, false>);
+  if (tl) {  // debug: dump the per-CTA phase timeline (globaltimer ns)
+    static unsigned long long host[148 * 128];
+    cudaMemcpyAsync(host, dbg_buf, sizeof(host), cudaMemcpyDeviceToHost, stream);
+    cudaStreamSynchronize(stream);
+    FILE* f = fopen(tl, "ab");
+    if (f) {
+      fwrite(host, sizeof(host), 1, f);
+      fclose(f);
     }
-    window_attn_ws_kernel<64><<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
-  } else {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(window_attn_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
-    }
-    window_attn_ws_kernel<32><<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
   }
   return (int)cudaGetLastError();
 }

@@ -10,8 +10,9 @@
 // so the GPU runs two chunk-parallel passes over L instead of one sequential pass over 3L:
 //   conv      : v = SiLU(causal conv) for the copy-2/3 stream (history = sequence tail) + the P copy-1 rows
 //   x_proj    : (delta_low, B, C) = v W_x^T on tcgen05 (f32 out)
-//   pass 1    : per (chunk, channel): Delta = softplus(delta_low W_dt^T + b_dt) (stored for pass 2), chunk sum
-//               of Delta and the chunk-end state from zero (b_c)       — thread per channel, N states in registers
+//   dt        : Delta = softplus(delta_low W_dt^T + b_dt) for every stream row (fp32, stored)
+//   pass 1    : per (chunk, channel): chunk sum of Delta and the chunk-end state from zero (b_c) — thread per
+//               channel, N states in registers
 //   carry     : per (image, channel) warp, lane = state: copy prefixes, fold of (exp(A sum Delta), b_c) over the
 //               chunks, c_2, c_3, the prefix outputs, and every chunk's entry state H_in
 //   pass 2    : per (chunk, channel): the summed recurrence from H_in, y, gate SiLU(z), bf16 store
@@ -163,7 +164,7 @@ struct StageLayout {
   // byte offsets inside one stage buffer
   __host__ __device__ static size_t off_v(int W) { return (size_t)TSUB * W * 4; }
   __host__ __device__ static size_t off_dt(int W) { return off_v(W) + (size_t)TSUB * DPB * 2; }
-  __host__ __device__ static size_t off_z(int W) { return off_dt(W) + (PASS2 ? (size_t)TSUB * DPB * 4 : 0); }
+  __host__ __device__ static size_t off_z(int W) { return off_dt(W) + (size_t)TSUB * DPB * 4; }
   __host__ __device__ static size_t bytes(int W) {
     size_t b = off_z(W) + (PASS2 ? (size_t)TSUB * DPB * 2 : 0);
     return (b + 127) & ~size_t(127);
@@ -181,14 +182,16 @@ struct StageLayout {
       const int j = i / VPR, cc = i - j * VPR;
       cp_async16(sv + j * DPB + cc * 8, p.v + (rbase + t + j) * p.D + d0 + cc * 8);
     }
-    if (PASS2) {
+    {
       float* sdt = reinterpret_cast<float*>(buf + off_dt(W));
-      __nv_bfloat16* sz = reinterpret_cast<__nv_bfloat16*>(buf + off_z(W));
       constexpr int FPR = DPB / 4;
       for (int i = tid; i < nt * FPR; i += DPB) {
         const int j = i / FPR, cc = i - j * FPR;
         cp_async16(sdt + j * DPB + cc * 4, p.delta + (rbase + t + j) * p.D + d0 + cc * 4);
       }
+    }
+    if (PASS2) {
+      __nv_bfloat16* sz = reinterpret_cast<__nv_bfloat16*>(buf + off_z(W));
       if (p.z)
         for (int i = tid; i < nt * VPR; i += DPB) {
           const int j = i / VPR, cc = i - j * VPR;
@@ -200,8 +203,58 @@ struct StageLayout {
 
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
+// ------------------------------------------------------------------------------------------------- dt
+// Delta[row, d] = softplus(delta_low[row] . W_dt[d] + b_dt[d]) for every stream row (copy-2/3 rows and the P copy-1
+// rows). Block = DPB channels x DT_ROWS rows; the rows' delta_low vectors are staged in shared memory, each thread
+// keeps its W_dt row in registers (fp32x2 FMAs).
+constexpr int DT_ROWS = 64;
+template <int RMAX>
+__global__ void __launch_bounds__(128) scan_dt_kernel(ScanParams p) {
+  extern __shared__ __align__(16) float s_dt_raw[];
+  float* s_w = s_dt_raw;                       // [DPB][R]   this block's W_dt rows (contiguous in global)
+  float* s_d = s_dt_raw + blockDim.x * RMAX;   // [DT_ROWS][RMAX] delta_low of the rows
+  const int W = p.R + 2 * p.N;
+  const int d0 = blockIdx.x * blockDim.x;
+  const int d = d0 + threadIdx.x;
+  const long long rows = (long long)p.B * (p.L + p.P);
+  const long long r0 = (long long)blockIdx.y * DT_ROWS;
+  const int nr = (int)min((long long)DT_ROWS, rows - r0);
+  const int R4 = p.R / 4;
+  {
+    const float4* gw = reinterpret_cast<const float4*>(p.w_dt + (size_t)d0 * p.R);
+    float4* sw4 = reinterpret_cast<float4*>(s_w);
+    for (int i = threadIdx.x; i < blockDim.x * R4; i += blockDim.x) sw4[i] = __ldg(gw + i);
+    for (int i = threadIdx.x; i < nr * R4; i += blockDim.x) {
+      const int j = i / R4, q = i - j * R4;
+      reinterpret_cast<float4*>(s_d + j * RMAX)[q] = __ldg(reinterpret_cast<const float4*>(p.dbc + (r0 + j) * W) + q);
+    }
+  }
+  __syncthreads();
+  float2 wdt[RMAX / 2];
+#pragma unroll
+  for (int r = 0; r < RMAX / 2; ++r)
+    wdt[r] = 2 * r < p.R ? make_float2(s_w[threadIdx.x * p.R + 2 * r], s_w[threadIdx.x * p.R + 2 * r + 1])
+                         : make_float2(0.f, 0.f);
+  const float bdt = p.b_dt[d];
+  for (int j = 0; j < nr; ++j) {
+    const float4* d4 = reinterpret_cast<const float4*>(s_d + j * RMAX);
+    float2 acc = make_float2(bdt, 0.f);
+#pragma unroll
+    for (int r = 0; r < RMAX; r += 4)
+      if (r < p.R) {
+        const float4 q = d4[r / 4];
+        acc = __ffma2_rn(make_float2(q.x, q.y), wdt[r / 2], acc);
+        acc = __ffma2_rn(make_float2(q.z, q.w), wdt[r / 2 + 1], acc);
+      }
+    const float x = acc.x + acc.y;
+    // softplus: log(1 + e^x); for x < -5 the series u - u^2/2 (u = e^x < 7e-3) avoids the rounding of 1 + u
+    const float u = __expf(x);
+    p.delta[(r0 + j) * p.D + d] = x > 20.f ? x : (x < -5.f ? u * (1.f - 0.5f * u) : __logf(1.f + u));
+  }
+}
+
 // ------------------------------------------------------------------------------------------------- pass 1
-template <int N, int RMAX, int DPB>
+template <int N, int DPB>
 __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
   using St = StageLayout<DPB, false>;
   extern __shared__ __align__(128) uint8_t s_raw[];
@@ -212,37 +265,15 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
   const long long rbase = (long long)b * (p.L + p.P);
-  float2 A2[N / 2], h[N / 2], wdt[RMAX / 2];
+  float2 A2[N / 2], h[N / 2];
 #pragma unroll
   for (int k = 0; k < N / 2; ++k) {
     A2[k] = make_float2(-__expf(p.a_log[d * N + 2 * k]) * kLog2e, -__expf(p.a_log[d * N + 2 * k + 1]) * kLog2e);
     h[k] = make_float2(0.f, 0.f);
   }
-#pragma unroll
-  for (int r = 0; r < RMAX / 2; ++r)
-    wdt[r] = 2 * r < p.R ? make_float2(p.w_dt[d * p.R + 2 * r], p.w_dt[d * p.R + 2 * r + 1]) : make_float2(0.f, 0.f);
-  const float bdt = p.b_dt[d];
   const bool zoh = p.bbar == 0;
-  auto compute_dt = [&](const float* drow) {
-    float2 acc = make_float2(bdt, 0.f);
-    const float4* d4 = reinterpret_cast<const float4*>(drow);
-#pragma unroll
-    for (int r = 0; r < RMAX; r += 4)
-      if (r < p.R) {
-        const float4 q = d4[r / 4];
-        acc = __ffma2_rn(make_float2(q.x, q.y), wdt[r / 2], acc);
-        acc = __ffma2_rn(make_float2(q.z, q.w), wdt[r / 2 + 1], acc);
-      }
-    return softplus_f(acc.x + acc.y);
-  };
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
-  if (chunk == 0) {  // Delta of the P prefix tokens of both streams (for the carry kernel)
-    for (int q = 0; q < 2 * p.P; ++q) {
-      const long long row = rbase + (q < p.P ? q : p.L + (q - p.P));
-      p.delta[row * p.D + d] = compute_dt(p.dbc + row * W);
-    }
-  }
   const int tb = max(t0, p.P);
   const int nsub = (t1 - tb + TSUB - 1) / TSUB;
   float sdt = 0.f;
@@ -265,13 +296,12 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
     const uint8_t* buf = s_raw + (sc & 1) * SB;
     const float* sdbc = reinterpret_cast<const float*>(buf);
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
+    const float* sdelta = reinterpret_cast<const float*>(buf + St::off_dt(W));
     for (int j = 0; j < nt; ++j) {
-      const float* drow = sdbc + j * W;
       const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
-      const float dt = compute_dt(drow);
-      p.delta[(rbase + ts + j) * p.D + d] = dt;
+      const float dt = sdelta[j * DPB + threadIdx.x];
       sdt += dt;
-      const float4* b4 = reinterpret_cast<const float4*>(drow + p.R);  // two state pairs per 16-byte load
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R);  // two state pairs per 16-byte load
       const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
       for (int k = 0; k < N / 2; ++k) {
@@ -594,13 +624,21 @@ static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
   const size_t smem1 = 2 * StageLayout<DPB, false>::bytes(W);
   const size_t smem2 = 2 * StageLayout<DPB, true>::bytes(W);
   {
-    PSCWIN_PROF("scan_pass1", s);
+    PSCWIN_PROF("scan_dt", s);
+    const long long rows = (long long)p.B * (p.L + p.P);
+    dim3 gdt(p.D / DPB, (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
+    const int rmax = p.R <= 16 ? 16 : (p.R <= 48 ? 48 : 64);
+    const size_t smem_dt = ((size_t)DPB * rmax + (size_t)DT_ROWS * rmax) * 4;  // s_w [DPB][<=RMAX], s_d [rows][RMAX]
     if (p.R <= 16)
-      scan_pass1_kernel<N, 16, DPB><<<grid, DPB, smem1, s>>>(p);
+      scan_dt_kernel<16><<<gdt, DPB, smem_dt, s>>>(p);
     else if (p.R <= 48)
-      scan_pass1_kernel<N, 48, DPB><<<grid, DPB, smem1, s>>>(p);
+      scan_dt_kernel<48><<<gdt, DPB, smem_dt, s>>>(p);
     else
-      scan_pass1_kernel<N, 64, DPB><<<grid, DPB, smem1, s>>>(p);
+      scan_dt_kernel<64><<<gdt, DPB, smem_dt, s>>>(p);
+  }
+  {
+    PSCWIN_PROF("scan_pass1", s);
+    scan_pass1_kernel<N, DPB><<<grid, DPB, smem1, s>>>(p);
   }
   {
     PSCWIN_PROF("scan_carry", s);

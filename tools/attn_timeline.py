@@ -1,0 +1,28 @@
+"""Run one attention layer with PSCWIN_ATTN_TIMELINE and print per-CTA phase timings (debug)."""
+import os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
+path = "/tmp/attn_tl.bin"
+if os.path.exists(path): os.remove(path)
+os.environ["PSCWIN_ATTN_TIMELINE"] = path
+import torch, synth
+import paper_2407_02109_b200 as pl
+from gpu_util import dev
+for shift in (0, 8):
+    cfg = synth.vitb(64, shift_x=shift, shift_y=shift)
+    qkv = dev(synth.make_qkv(cfg)); qp = dev(synth.make_pad_qkv(cfg), "f32")
+    d = pl.LayerDesc.from_config(cfg)
+    for _ in range(3):
+        pl.window_attention(d, qkv, qp)
+    torch.cuda.synchronize()
+raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 148, 128).astype(np.int64)
+for run in (2, 5):
+    t = raw[run]
+    t0 = t[t > 0].min()
+    print(f"--- run {run} (shift {'8' if run >= 3 else '0'}), kernel span {(t[t>0].max()-t0)/1e3:.1f} us")
+    for cta in (0, 1, 100, 147):
+        row = t[cta]
+        def ev(base):
+            v = row[base:base + 32]; v = v[v > 0]; return ((v - t0) / 1e3).round(2).tolist()
+        print(f"cta {cta}: load {ev(0)}\n   mma {ev(32)}\n   wg0 {ev(64)}\n   wg1 {ev(96)}")
