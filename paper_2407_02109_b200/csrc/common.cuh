@@ -195,6 +195,9 @@ PSCWIN_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;
 PSCWIN_DEVICE void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
+PSCWIN_DEVICE void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 PSCWIN_DEVICE void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 PSCWIN_DEVICE void cp_async_wait() {

@@ -29,22 +29,20 @@ namespace pscwin {
 
 namespace {
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int TS = 32;  // chunk length granularity
 }
 
 struct ScanParams {
   int B, L, D, N, R, k, P, Lc, n_chunks, bbar;
   const __nv_bfloat16* xin;
   long long ld_x;
-  const __nv_bfloat16* z;
-  long long ld_z;
+  const __nv_bfloat16* gz;  // output gate SiLU(z) [B, L] rows of stride ld_gz, or null (no gate)
+  long long ld_gz;
   const float *conv_w, *conv_b, *w_dt, *b_dt, *a_log, *d_skip;
   __nv_bfloat16* v;  // [B, L+P, D]
   float* dbc;        // [B, L+P, R+2N]
   float* delta;      // [B, L+P, D]
   float* sumdt;      // [B, n_chunks, D]
   float* hs;         // [B, n_chunks, D, N]
-  __nv_bfloat16* gz;  // [B, L, D] SiLU(z) (written by the conv kernel when z != NULL)
   __nv_bfloat16* out;
   long long ld_out;
 };
@@ -54,20 +52,24 @@ __device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log
 
 // ------------------------------------------------------------------------------------------------- conv
 // v rows [0, L): copy-2/3 stream (tap index wraps to the sequence tail); rows [L, L+P): copy-1 tokens 0..P-1
-// (taps before the sequence start contribute 0). A thread owns 8 channels x CONV_T consecutive rows and slides
-// the k-tap window along them, so each input vector is loaded once per thread (k <= KMAX).
+// (taps before the sequence start contribute 0). A thread owns 8 channels x CONV_T consecutive rows: it issues the
+// CONV_T + k - 1 input loads of its window up front (independent 16-byte loads, coalesced across the warp's channel
+// groups), keeps its 8 x k taps in registers, and slides the window in registers.
+constexpr int KMAX = 4;  // conv width supported (Mamba default 4)
 constexpr int CONV_T = 8;
-constexpr int KMAX = 4;  // conv width supported by the register window (Mamba default 4)
-__global__ void conv_silu_kernel(ScanParams p) {
+__global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
   const int dv = p.D / 8;
   const int rows_img = p.L + p.P;
   const int groups_img = (rows_img + CONV_T - 1) / CONV_T;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= p.B * groups_img * dv) return;
-  const int d0 = (idx % dv) * 8;
-  const int grp = idx / dv;
-  const int b = grp / groups_img;
-  const int r0 = (grp - b * groups_img) * CONV_T;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)p.B * groups_img * dv) return;
+  const int d0 = (int)(idx % dv) * 8;
+  const long long grp = idx / dv;
+  const int b = (int)(grp / groups_img);
+  const int r0 = (int)(grp - (long long)b * groups_img) * CONV_T;
+  const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
+  __nv_bfloat16* vb = p.v + (long long)b * rows_img * p.D + d0;
+  auto load_tok = [&](int tt) { return *reinterpret_cast<const uint4*>(xb + (long long)tt * p.ld_x); };
   float wk[8][KMAX], bias[8];
   {
     const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.conv_b + d0));
@@ -75,81 +77,92 @@ __global__ void conv_silu_kernel(ScanParams p) {
     bias[0] = b0.x; bias[1] = b0.y; bias[2] = b0.z; bias[3] = b0.w;
     bias[4] = b1.x; bias[5] = b1.y; bias[6] = b1.z; bias[7] = b1.w;
   }
-  if (p.k == 4) {  // the 8 channels' taps are 32 contiguous floats
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.conv_w + (d0 + c) * 4));
-      wk[c][0] = w4.x; wk[c][1] = w4.y; wk[c][2] = w4.z; wk[c][3] = w4.w;
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? p.conv_w[(d0 + c) * p.k + i] : 0.f;
-  }
-  const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
-  float win[KMAX][8];  // the k most recent inputs (slot k-1 = newest)
-  auto load = [&](int r, int j, float (&dst)[8]) {  // input feeding stream row r at tap offset j (j <= 0)
-    const bool copy1 = r >= p.L;
-    int t = (copy1 ? r - p.L : r) + j;
-    if (t < 0) {
-      if (copy1) {
-#pragma unroll
-        for (int c = 0; c < 8; ++c) dst[c] = 0.f;
-        return;
-      }
-      t += p.L;
-    }
-    const uint4 xv = *reinterpret_cast<const uint4*>(xb + (long long)t * p.ld_x);
-    const uint32_t* xw = reinterpret_cast<const uint32_t*>(&xv);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      dst[2 * q] = bf16_lo(xw[q]);
-      dst[2 * q + 1] = bf16_hi(xw[q]);
-    }
-  };
-  for (int rr = 0; rr < CONV_T; ++rr) {
-    const int r = r0 + rr;
-    if (r >= rows_img) break;
-    const bool fresh = rr == 0 || r == p.L;  // window restarts at the group start and at the copy-1 rows
-    if (fresh) {
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i)
-        if (i < p.k) load(r, i - (p.k - 1), win[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < KMAX - 1; ++i)
-        if (i + 1 < p.k) {
-#pragma unroll
-          for (int c = 0; c < 8; ++c) win[i][c] = win[i + 1][c];
-        }
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i)
-        if (i == p.k - 1) load(r, 0, win[i]);
-    }
-    float acc[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      acc[c] = bias[c];
-#pragma unroll
-      for (int i = 0; i < KMAX; ++i)
-        if (i < p.k) acc[c] = fmaf(wk[c][i], win[i][c], acc[c]);
-    }
+  auto emit = [&](int r, const uint4 (&xw)[KMAX]) {  // xw[i] = input of tap i (zeros where absent)
     uint4 o;
     uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) ow[q] = pack_bf16(silu_f(acc[2 * q]), silu_f(acc[2 * q + 1]));
-    *reinterpret_cast<uint4*>(p.v + ((long long)b * rows_img + r) * p.D + d0) = o;
-    if (p.z && r < p.L) {  // output gate SiLU(z_t), once per token (used by the carry prefix and pass 2)
-      const uint4 zv = *reinterpret_cast<const uint4*>(p.z + ((long long)b * p.L + r) * p.ld_z + d0);
-      const uint32_t* zw = reinterpret_cast<const uint32_t*>(&zv);
-      uint4 g;
-      uint32_t* gw = reinterpret_cast<uint32_t*>(&g);
+    for (int q = 0; q < 4; ++q) {
+      float a0 = bias[2 * q], a1 = bias[2 * q + 1];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) gw[q] = pack_bf16(silu_f(bf16_lo(zw[q])), silu_f(bf16_hi(zw[q])));
-      *reinterpret_cast<uint4*>(p.gz + ((long long)b * p.L + r) * p.D + d0) = g;
+      for (int i = 0; i < KMAX; ++i) {
+        const uint32_t u = reinterpret_cast<const uint32_t*>(&xw[i])[q];
+        a0 = fmaf(wk[2 * q][i], bf16_lo(u), a0);
+        a1 = fmaf(wk[2 * q + 1][i], bf16_hi(u), a1);
+      }
+      ow[q] = pack_bf16(silu_f(a0), silu_f(a1));
+    }
+    *reinterpret_cast<uint4*>(vb + (long long)r * p.D) = o;
+  };
+  if (r0 + CONV_T <= p.L) {
+    // body rows: the window is tokens r0-(k-1) .. r0+CONV_T-1 (negative indices wrap to the sequence tail)
+    uint4 xs[CONV_T + KMAX - 1];
+#pragma unroll
+    for (int m = 0; m < CONV_T + KMAX - 1; ++m) {
+      int tt = r0 - (p.k - 1) + m;
+      if (tt < 0) tt += p.L;
+      xs[m] = (m < CONV_T + p.k - 1) ? load_tok(tt) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (p.k == 4) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const float4 w4 = __ldg(reinterpret_cast<const float4*>(p.conv_w + (d0 + c) * 4));
+        wk[c][0] = w4.x; wk[c][1] = w4.y; wk[c][2] = w4.z; wk[c][3] = w4.w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+#pragma unroll
+        for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? __ldg(p.conv_w + (d0 + c) * p.k + i) : 0.f;
+    }
+#pragma unroll
+    for (int rr = 0; rr < CONV_T; ++rr) {
+      uint4 xw[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) xw[i] = xs[rr + i];  // tap i of row r0+rr is token r0+rr-(k-1)+i
+      emit(r0 + rr, xw);
+    }
+  } else {
+    // rows at the end of the body and the copy-1 rows: generic per-row taps
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) wk[c][i] = i < p.k ? __ldg(p.conv_w + (d0 + c) * p.k + i) : 0.f;
+    for (int rr = 0; rr < CONV_T; ++rr) {
+      const int r = r0 + rr;
+      if (r >= rows_img) break;
+      const bool copy1 = r >= p.L;
+      const int t = copy1 ? r - p.L : r;
+      uint4 xw[KMAX];
+#pragma unroll
+      for (int i = 0; i < KMAX; ++i) {
+        xw[i] = make_uint4(0u, 0u, 0u, 0u);
+        if (i < p.k) {
+          int tt = t - (p.k - 1) + i;
+          if (tt < 0 && !copy1) tt += p.L;
+          if (tt >= 0) xw[i] = load_tok(tt);
+        }
+      }
+      emit(r, xw);
     }
   }
+}
+
+// Output gate SiLU(z) for the standalone pscwin_cycle_scan entry point (raw z). The module path gets SiLU(z)
+// straight from the in_proj GEMM epilogue instead.
+__global__ void __launch_bounds__(256) silu_gate_kernel(const __nv_bfloat16* z, long long ld_z, long long T, int D,
+                                                        __nv_bfloat16* gz) {
+  const int dv = D / 8;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= T * dv) return;
+  const long long tok = idx / dv;
+  const int d0 = (int)(idx - tok * dv) * 8;
+  const uint4 zv = *reinterpret_cast<const uint4*>(z + tok * ld_z + d0);
+  const uint32_t* zw = reinterpret_cast<const uint32_t*>(&zv);
+  uint4 g;
+  uint32_t* gw = reinterpret_cast<uint32_t*>(&g);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) gw[q] = pack_bf16(silu_f(bf16_lo(zw[q])), silu_f(bf16_hi(zw[q])));
+  *reinterpret_cast<uint4*>(gz + tok * D + d0) = g;
 }
 
 // ------------------------------------------------------------------------------------------------- staging
@@ -159,7 +172,7 @@ __global__ void conv_silu_kernel(ScanParams p) {
 // which turns the ZOH update into h~ <- dA (h~ + w) - w with w = B_t[n] v_t (no 1/A per element), and pairs of
 // states are updated with packed fp32x2 instructions (FFMA2 / FMUL2 on sm_100a).
 constexpr int TSUB = 16;
-template <int DPB, bool PASS2>
+template <int DPB, int NT, bool PASS2>  // DPB channels per CTA, NT threads
 struct StageLayout {
   // byte offsets inside one stage buffer
   __host__ __device__ static size_t off_v(int W) { return (size_t)TSUB * W * 4; }
@@ -176,26 +189,26 @@ struct StageLayout {
     float* sd = reinterpret_cast<float*>(buf);
     __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(buf + off_v(W));
     const float* gd = p.dbc + (rbase + t) * W;
-    for (int i = tid; i < nt * W / 4; i += DPB) cp_async16(sd + 4 * i, gd + 4 * i);
+    for (int i = tid; i < nt * W / 4; i += NT) cp_async16(sd + 4 * i, gd + 4 * i);
     constexpr int VPR = DPB / 8;  // 16-byte chunks per token row of bf16
-    for (int i = tid; i < nt * VPR; i += DPB) {
+    for (int i = tid; i < nt * VPR; i += NT) {
       const int j = i / VPR, cc = i - j * VPR;
       cp_async16(sv + j * DPB + cc * 8, p.v + (rbase + t + j) * p.D + d0 + cc * 8);
     }
     {
       float* sdt = reinterpret_cast<float*>(buf + off_dt(W));
       constexpr int FPR = DPB / 4;
-      for (int i = tid; i < nt * FPR; i += DPB) {
+      for (int i = tid; i < nt * FPR; i += NT) {
         const int j = i / FPR, cc = i - j * FPR;
         cp_async16(sdt + j * DPB + cc * 4, p.delta + (rbase + t + j) * p.D + d0 + cc * 4);
       }
     }
     if (PASS2) {
       __nv_bfloat16* sz = reinterpret_cast<__nv_bfloat16*>(buf + off_z(W));
-      if (p.z)
-        for (int i = tid; i < nt * VPR; i += DPB) {
+      if (p.gz)
+        for (int i = tid; i < nt * VPR; i += NT) {
           const int j = i / VPR, cc = i - j * VPR;
-          cp_async16(sz + j * DPB + cc * 8, p.gz + (tok0 + t + j) * p.D + d0 + cc * 8);
+          cp_async16(sz + j * DPB + cc * 8, p.gz + (tok0 + t + j) * p.ld_gz + d0 + cc * 8);
         }
     }
   }
@@ -205,70 +218,111 @@ __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 
 // ------------------------------------------------------------------------------------------------- dt
 // Delta[row, d] = softplus(delta_low[row] . W_dt[d] + b_dt[d]) for every stream row (copy-2/3 rows and the P copy-1
-// rows). Block = DPB channels x DT_ROWS rows; the rows' delta_low vectors are staged in shared memory, each thread
-// keeps its W_dt row in registers (fp32x2 FMAs).
+// rows). Block = 64 threads x 2 channels x DT_ROWS rows: the rows' delta_low vectors are staged in shared memory
+// (read back as broadcasts), each thread keeps its two channels' W_dt rows in registers as (d, d+1) pairs, so one
+// packed fp32x2 FMA advances both channels, and four rows are accumulated at once (4 independent chains).
 constexpr int DT_ROWS = 64;
+constexpr int DT_THREADS = 64;
 template <int RMAX>
-__global__ void __launch_bounds__(128) scan_dt_kernel(ScanParams p) {
-  extern __shared__ __align__(16) float s_dt_raw[];
-  float* s_w = s_dt_raw;                       // [DPB][R]   this block's W_dt rows (contiguous in global)
-  float* s_d = s_dt_raw + blockDim.x * RMAX;   // [DT_ROWS][RMAX] delta_low of the rows
+__global__ void __launch_bounds__(DT_THREADS) scan_dt_kernel(ScanParams p) {
+  __shared__ float4 s_d4[DT_ROWS * (RMAX / 4)];
   const int W = p.R + 2 * p.N;
-  const int d0 = blockIdx.x * blockDim.x;
-  const int d = d0 + threadIdx.x;
+  const int d = blockIdx.x * (2 * DT_THREADS) + 2 * threadIdx.x;
   const long long rows = (long long)p.B * (p.L + p.P);
   const long long r0 = (long long)blockIdx.y * DT_ROWS;
   const int nr = (int)min((long long)DT_ROWS, rows - r0);
   const int R4 = p.R / 4;
-  {
-    const float4* gw = reinterpret_cast<const float4*>(p.w_dt + (size_t)d0 * p.R);
-    float4* sw4 = reinterpret_cast<float4*>(s_w);
-    for (int i = threadIdx.x; i < blockDim.x * R4; i += blockDim.x) sw4[i] = __ldg(gw + i);
-    for (int i = threadIdx.x; i < nr * R4; i += blockDim.x) {
-      const int j = i / R4, q = i - j * R4;
-      reinterpret_cast<float4*>(s_d + j * RMAX)[q] = __ldg(reinterpret_cast<const float4*>(p.dbc + (r0 + j) * W) + q);
+  for (int i = threadIdx.x; i < nr * R4; i += DT_THREADS) {
+    const int j = i / R4, q = i - j * R4;
+    s_d4[j * (RMAX / 4) + q] = __ldg(reinterpret_cast<const float4*>(p.dbc + (r0 + j) * W) + q);
+  }
+  float2 wp[RMAX];  // (W_dt[d][k], W_dt[d+1][k])
+  const bool dok = d < p.D;  // D % 64 == 0: the last block may be half used
+  if (!dok) {
+#pragma unroll
+    for (int k = 0; k < RMAX; ++k) wp[k] = make_float2(0.f, 0.f);
+  } else {
+    const float4* w0 = reinterpret_cast<const float4*>(p.w_dt + (size_t)d * p.R);
+    const float4* w1 = reinterpret_cast<const float4*>(p.w_dt + (size_t)(d + 1) * p.R);
+#pragma unroll
+    for (int q = 0; q < RMAX / 4; ++q) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+      if (q < R4) {
+        a = __ldg(w0 + q);
+        c = __ldg(w1 + q);
+      }
+      wp[4 * q + 0] = make_float2(a.x, c.x);
+      wp[4 * q + 1] = make_float2(a.y, c.y);
+      wp[4 * q + 2] = make_float2(a.z, c.z);
+      wp[4 * q + 3] = make_float2(a.w, c.w);
     }
   }
+  const float2 bias = dok ? make_float2(p.b_dt[d], p.b_dt[d + 1]) : make_float2(0.f, 0.f);
   __syncthreads();
-  float2 wdt[RMAX / 2];
-#pragma unroll
-  for (int r = 0; r < RMAX / 2; ++r)
-    wdt[r] = 2 * r < p.R ? make_float2(s_w[threadIdx.x * p.R + 2 * r], s_w[threadIdx.x * p.R + 2 * r + 1])
-                         : make_float2(0.f, 0.f);
-  const float bdt = p.b_dt[d];
-  for (int j = 0; j < nr; ++j) {
-    const float4* d4 = reinterpret_cast<const float4*>(s_d + j * RMAX);
-    float2 acc = make_float2(bdt, 0.f);
-#pragma unroll
-    for (int r = 0; r < RMAX; r += 4)
-      if (r < p.R) {
-        const float4 q = d4[r / 4];
-        acc = __ffma2_rn(make_float2(q.x, q.y), wdt[r / 2], acc);
-        acc = __ffma2_rn(make_float2(q.z, q.w), wdt[r / 2 + 1], acc);
-      }
-    const float x = acc.x + acc.y;
-    // softplus: log(1 + e^x); for x < -5 the series u - u^2/2 (u = e^x < 7e-3) avoids the rounding of 1 + u
+  if (!dok) return;
+  auto softplus = [](float x) {
+    // log(1 + e^x); for x < -5 the series u - u^2/2 (u = e^x < 7e-3) avoids the rounding of 1 + u
     const float u = __expf(x);
-    p.delta[(r0 + j) * p.D + d] = x > 20.f ? x : (x < -5.f ? u * (1.f - 0.5f * u) : __logf(1.f + u));
+    const float sp = x < -5.f ? u * (1.f - 0.5f * u) : __logf(1.f + u);
+    return x > 20.f ? x : sp;
+  };
+  auto store = [&](int j, float2 x) {
+    *reinterpret_cast<float2*>(p.delta + (r0 + j) * p.D + d) = make_float2(softplus(x.x), softplus(x.y));
+  };
+  int j = 0;
+  for (; j + 4 <= nr; j += 4) {
+    float2 acc[4] = {bias, bias, bias, bias};
+#pragma unroll
+    for (int q = 0; q < RMAX / 4; ++q)
+      if (q < R4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = s_d4[(j + i) * (RMAX / 4) + q];
+          acc[i] = __ffma2_rn(f2(x.x), wp[4 * q + 0], acc[i]);
+          acc[i] = __ffma2_rn(f2(x.y), wp[4 * q + 1], acc[i]);
+          acc[i] = __ffma2_rn(f2(x.z), wp[4 * q + 2], acc[i]);
+          acc[i] = __ffma2_rn(f2(x.w), wp[4 * q + 3], acc[i]);
+        }
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) store(j + i, acc[i]);
+  }
+  for (; j < nr; ++j) {
+    float2 acc = bias;
+#pragma unroll
+    for (int q = 0; q < RMAX / 4; ++q)
+      if (q < R4) {
+        const float4 x = s_d4[j * (RMAX / 4) + q];
+        acc = __ffma2_rn(f2(x.x), wp[4 * q + 0], acc);
+        acc = __ffma2_rn(f2(x.y), wp[4 * q + 1], acc);
+        acc = __ffma2_rn(f2(x.z), wp[4 * q + 2], acc);
+        acc = __ffma2_rn(f2(x.w), wp[4 * q + 3], acc);
+      }
+    store(j, acc);
   }
 }
 
 // ------------------------------------------------------------------------------------------------- pass 1
-template <int N, int DPB>
-__global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
-  using St = StageLayout<DPB, false>;
+// NS threads per channel, each owning NH = N / NS of its states (NS = 2 halves the registers per thread, which
+// doubles the resident warps that hide the MUFU / FMA latencies).
+template <int N, int DPB, int NS>
+__global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
+  constexpr int NT = DPB * NS, NH = N / NS;
+  using St = StageLayout<DPB, NT, false>;
   extern __shared__ __align__(128) uint8_t s_raw[];
   const int W = p.R + 2 * N;
   const size_t SB = St::bytes(W);
+  const int c = threadIdx.x / NS, sub = threadIdx.x % NS;
   const int d0 = blockIdx.x * DPB;
-  const int d = d0 + threadIdx.x;
+  const int d = d0 + c;
+  const int n0 = sub * NH;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
   const long long rbase = (long long)b * (p.L + p.P);
-  float2 A2[N / 2], h[N / 2];
+  float2 A2[NH / 2], h[NH / 2];
 #pragma unroll
-  for (int k = 0; k < N / 2; ++k) {
-    A2[k] = make_float2(-__expf(p.a_log[d * N + 2 * k]) * kLog2e, -__expf(p.a_log[d * N + 2 * k + 1]) * kLog2e);
+  for (int k = 0; k < NH / 2; ++k) {
+    A2[k] = make_float2(-__expf(p.a_log[d * N + n0 + 2 * k]) * kLog2e, -__expf(p.a_log[d * N + n0 + 2 * k + 1]) * kLog2e);
     h[k] = make_float2(0.f, 0.f);
   }
   const bool zoh = p.bbar == 0;
@@ -298,13 +352,13 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     const float* sdelta = reinterpret_cast<const float*>(buf + St::off_dt(W));
     for (int j = 0; j < nt; ++j) {
-      const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
-      const float dt = sdelta[j * DPB + threadIdx.x];
+      const float v = __bfloat162float(sv[j * DPB + c]);
+      const float dt = sdelta[j * DPB + c];
       sdt += dt;
-      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R);  // two state pairs per 16-byte load
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);  // two state pairs per load
       const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
-      for (int k = 0; k < N / 2; ++k) {
+      for (int k = 0; k < NH / 2; ++k) {
         const float4 bq = b4[k / 2];
         const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
@@ -321,24 +375,38 @@ __global__ void __launch_bounds__(DPB) scan_pass1_kernel(ScanParams p) {
     }
     __syncthreads();
   }
-  p.sumdt[((long long)b * p.n_chunks + chunk) * p.D + d] = sdt;
-  float4* dst = reinterpret_cast<float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
+  if (sub == 0) p.sumdt[((long long)b * p.n_chunks + chunk) * p.D + d] = sdt;
+  float4* dst = reinterpret_cast<float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N + n0);
 #pragma unroll
-  for (int k = 0; k < N / 2; k += 2) dst[k / 2] = make_float4(h[k].x, h[k].y, h[k + 1].x, h[k + 1].y);
+  for (int k = 0; k < NH / 2; k += 2) dst[k / 2] = make_float4(h[k].x, h[k].y, h[k + 1].x, h[k + 1].y);
 }
 
 // ------------------------------------------------------------------------------------------------- carry
 // One warp per (image, channel); lane owns states n = lane + 32 j (scaled states h~ = A h throughout).
 // Produces the prefix outputs and every chunk's entry state (overwriting the pass-1 chunk-end states).
+// The warp's chunk summaries (sum of Delta, chunk-end states) are copied to shared memory asynchronously up front,
+// so the two sequential folds over the chunks run from shared memory instead of one global round trip per batch.
 template <int N>
 __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   constexpr int NPL = (N + 31) / 32;
+  extern __shared__ __align__(16) float s_carry[];
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp_global >= p.B * p.D) return;
   const int b = warp_global / p.D;
   const int d = warp_global - b * p.D;
   const int W = p.R + 2 * N;
+  const int nch = p.n_chunks;
+  float* s_sd = s_carry + (threadIdx.x >> 5) * nch * (N + 1);  // [nch] sum of Delta per chunk
+  float* s_hs = s_sd + nch;                                    // [nch][N] chunk-end states from zero
+  const float* sd = p.sumdt + (long long)b * nch * p.D + d;
+  float* hs = p.hs + ((long long)b * nch * p.D + d) * N;
+  for (int c = lane; c < nch; c += 32) cp_async4(s_sd + c, sd + (long long)c * p.D);
+  for (int c = 0; c < nch; ++c)
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (lane + 32 * j < N) cp_async4(s_hs + c * N + lane + 32 * j, hs + (long long)c * p.D * N + lane + 32 * j);
+  cp_async_commit();
   const long long rbase = (long long)b * (p.L + p.P);
   const bool zoh = p.bbar == 0;
   float A2[NPL], invA[NPL];
@@ -363,6 +431,7 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
       h[j] = zoh ? fmaf(dA, h[j] + w, -w) : fmaf(dA, h[j], x * 0.69314718055994531f * w);
     }
   };
+  // copy prefixes (P tokens): beta1 = copy 1 from zero, beta2 = copies 2/3 from zero, alpha2 = their decay
   float beta1[NPL], beta2[NPL], alpha2[NPL];
 #pragma unroll
   for (int j = 0; j < NPL; ++j) beta1[j] = beta2[j] = 0.f;
@@ -374,29 +443,18 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   }
 #pragma unroll
   for (int j = 0; j < NPL; ++j) alpha2[j] = ex2_approx(sdt2 * A2[j]);
-  const float* sd = p.sumdt + (long long)b * p.n_chunks * p.D + d;
-  float* hs = p.hs + ((long long)b * p.n_chunks * p.D + d) * N;
+  cp_async_wait<0>();
+  __syncwarp();
+  // body from zero (input x1): Bb = fold of (exp(A sum Delta_c), b_c) over the chunks
   float Bb[NPL], sall = 0.f;
 #pragma unroll
   for (int j = 0; j < NPL; ++j) Bb[j] = 0.f;
-  constexpr int CB = 8;  // chunk summaries loaded in batches (independent loads, one round trip per batch)
-  for (int c0 = 0; c0 < p.n_chunks; c0 += CB) {
-    float sb[CB], hb[CB][NPL];
+  for (int c = 0; c < nch; ++c) {
+    const float sc = s_sd[c];
+    sall += sc;
 #pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      const int c = c0 + i < p.n_chunks ? c0 + i : p.n_chunks - 1;
-      sb[i] = sd[(long long)c * p.D];
-#pragma unroll
-      for (int j = 0; j < NPL; ++j) hb[i][j] = act[j] ? hs[(long long)c * p.D * N + lane + 32 * j] : 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      if (c0 + i >= p.n_chunks) break;
-      sall += sb[i];
-#pragma unroll
-      for (int j = 0; j < NPL; ++j)
-        if (act[j]) Bb[j] = fmaf(ex2_approx(sb[i] * A2[j]), Bb[j], hb[i][j]);
-    }
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) Bb[j] = fmaf(ex2_approx(sc * A2[j]), Bb[j], s_hs[c * N + lane + 32 * j]);
   }
   float c2[NPL], c3[NPL], H[NPL];
 #pragma unroll
@@ -434,60 +492,52 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
       if (lane == 0) {
         y += Ds * (__bfloat162float(p.v[r1 * p.D + d]) + 2.f * __bfloat162float(p.v[r2 * p.D + d]));
         const long long tok = (long long)b * p.L + t;
-        const float g = p.z ? __bfloat162float(p.gz[tok * p.D + d]) : 1.f;
+        const float g = p.gz ? __bfloat162float(p.gz[tok * p.ld_gz + d]) : 1.f;
         p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
       }
     }
   }
   // chunk entry states of the summed recurrence (input x3): H_in(0) = H_{P-1}; H_in(c+1) = a_c H_in(c) + 3 b_c
-  for (int c0 = 0; c0 < p.n_chunks; c0 += CB) {
-    float sb[CB], hb[CB][NPL];
+  for (int c = 0; c < nch; ++c) {
+    const float sc = s_sd[c];
 #pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      const int c = c0 + i < p.n_chunks ? c0 + i : p.n_chunks - 1;
-      sb[i] = sd[(long long)c * p.D];
-#pragma unroll
-      for (int j = 0; j < NPL; ++j) hb[i][j] = act[j] ? hs[(long long)c * p.D * N + lane + 32 * j] : 0.f;
-    }
-#pragma unroll
-    for (int i = 0; i < CB; ++i) {
-      if (c0 + i >= p.n_chunks) break;
-#pragma unroll
-      for (int j = 0; j < NPL; ++j)
-        if (act[j]) {
-          hs[(long long)(c0 + i) * p.D * N + lane + 32 * j] = H[j];
-          H[j] = fmaf(ex2_approx(sb[i] * A2[j]), H[j], 3.f * hb[i][j]);
-        }
-    }
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) {
+        hs[(long long)c * p.D * N + lane + 32 * j] = H[j];
+        H[j] = fmaf(ex2_approx(sc * A2[j]), H[j], 3.f * s_hs[c * N + lane + 32 * j]);
+      }
   }
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
-template <int N, int DPB>
-__global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
-  using St = StageLayout<DPB, true>;
+template <int N, int DPB, int NS>
+__global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
+  constexpr int NT = DPB * NS, NH = N / NS;
+  using St = StageLayout<DPB, NT, true>;
   extern __shared__ __align__(128) uint8_t s_raw[];
   const int W = p.R + 2 * N;
   const size_t SB = St::bytes(W);
+  const int c = threadIdx.x / NS, sub = threadIdx.x % NS;
   const int d0 = blockIdx.x * DPB;
-  const int d = d0 + threadIdx.x;
+  const int d = d0 + c;
+  const int n0 = sub * NH;
   const int chunk = blockIdx.y;
   const int b = blockIdx.z;
   const long long rbase = (long long)b * (p.L + p.P);
   const long long tok0 = (long long)b * p.L;
-  float2 A2[N / 2], invA[N / 2], h[N / 2];
-  const float4* src = reinterpret_cast<const float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N);
+  float2 A2[NH / 2], invA[NH / 2], h[NH / 2];
+  const float4* src = reinterpret_cast<const float4*>(p.hs + (((long long)b * p.n_chunks + chunk) * p.D + d) * N + n0);
 #pragma unroll
-  for (int k = 0; k < N / 2; k += 2) {
+  for (int k = 0; k < NH / 2; k += 2) {
     const float4 q = src[k / 2];
     h[k] = make_float2(q.x, q.y);
     h[k + 1] = make_float2(q.z, q.w);
   }
 #pragma unroll
-  for (int k = 0; k < N / 2; ++k) {
-    const float a0 = -__expf(p.a_log[d * N + 2 * k]), a1 = -__expf(p.a_log[d * N + 2 * k + 1]);
+  for (int k = 0; k < NH / 2; ++k) {
+    const float a0 = -__expf(p.a_log[d * N + n0 + 2 * k]), a1 = -__expf(p.a_log[d * N + n0 + 2 * k + 1]);
     A2[k] = make_float2(a0 * kLog2e, a1 * kLog2e);
-    invA[k] = make_float2(1.f / a0, 1.f / a1);
+    invA[k] = make_float2(__frcp_rn(a0), __frcp_rn(a1));
   }
   const float D3 = 3.f * p.d_skip[d];
   const bool zoh = p.bbar == 0;
@@ -517,14 +567,15 @@ __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
     const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
     const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
     for (int j = 0; j < nt; ++j) {
-      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R);  // B pairs, then C pairs
-      const float v = __bfloat162float(sv[j * DPB + threadIdx.x]);
-      const float dt = sdt[j * DPB + threadIdx.x];
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);      // B pairs
+      const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + N + n0);  // C pairs
+      const float v = __bfloat162float(sv[j * DPB + c]);
+      const float dt = sdt[j * DPB + c];
       const float2 dt2 = f2(dt), nv3 = f2(-3.f * v);
-      float2 y2 = make_float2(0.f, 0.f);
+      float2 y2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // two chains: shorter FFMA2 dependency
 #pragma unroll
-      for (int k = 0; k < N / 2; ++k) {
-        const float4 bq = b4[k / 2], cq = b4[N / 4 + k / 2];
+      for (int k = 0; k < NH / 2; ++k) {
+        const float4 bq = b4[k / 2], cq = c4[k / 2];
         const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         const float2 ck = (k & 1) ? make_float2(cq.z, cq.w) : make_float2(cq.x, cq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
@@ -537,11 +588,16 @@ __global__ void __launch_bounds__(DPB) scan_pass2_kernel(ScanParams p) {
           const float2 u = __fmul2_rn(__fmul2_rn(x, f2(0.69314718055994531f)), wn);
           h[k] = __ffma2_rn(dA, h[k], __fmul2_rn(u, m1));
         }
-        y2 = __ffma2_rn(__fmul2_rn(ck, invA[k]), h[k], y2);     // C . h = C . (h~ / A)
+        y2[k & 1] = __ffma2_rn(__fmul2_rn(ck, invA[k]), h[k], y2[k & 1]);  // C . h = C . (h~ / A)
       }
-      const float y = fmaf(D3, v, y2.x + y2.y);
-      const float g = p.z ? __bfloat162float(sz[j * DPB + threadIdx.x]) : 1.f;
-      p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
+      float y = (y2[0].x + y2[1].x) + (y2[0].y + y2[1].y);
+#pragma unroll
+      for (int o = 1; o < NS; o <<= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (sub == 0) {
+        y = fmaf(D3, v, y);
+        const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
+        p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
+      }
     }
     __syncthreads();
   }
@@ -555,27 +611,60 @@ struct ScanPlan {
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-static int choose_chunk(int B, int L, int D) {
-  // aim for ~`waves` x 148 CTAs of 128 channels (several resident per SM); chunk length a multiple of TS.
-  // PSCWIN_SCAN_WAVES overrides the target (tuning knob; the result is identical for any chunking).
+// channels per CTA of the passes and threads per channel (the chunk plan depends on them)
+constexpr int PASS_DPB = 64;
+constexpr int PASS_NS = 2;
+
+// Pass-2 CTAs resident per SM (occupancy query; a fixed fallback without a device).
+static int pass2_slots(int N, int W) {
+  int n = 0;
+  cudaError_t e = cudaErrorInvalidValue;
+  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * PASS_NS, true>::bytes(W);
+  if (N == 16)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<16, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
+  else if (N == 32)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<32, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
+  else if (N == 64)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<64, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
+  if (e != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = 4;
+  }
+  return n;
+}
+
+// Chunk length: the (chunk, channel block) CTAs of a pass fill every SM's resident slots exactly `waves` times
+// (one wave by default: all CTAs run concurrently and finish together). PSCWIN_SCAN_WAVES overrides the target
+// (tuning knob; the result does not depend on the chunking beyond fp32 rounding order).
+static int choose_chunk(int B, int L, int D, int N, int W) {
   static int waves = 0;
   if (!waves) {
     const char* e = getenv("PSCWIN_SCAN_WAVES");
-    waves = e ? atoi(e) : 4;
-    if (waves <= 0) waves = 4;
+    waves = e ? atoi(e) : 1;
+    if (waves <= 0) waves = 1;
   }
-  const long long ctas_per_chunk = (long long)B * (D / 128 > 0 ? D / 128 : 1);
-  long long target_chunks = ((long long)waves * 148 + ctas_per_chunk - 1) / ctas_per_chunk;
+  int sms = 148;
+  {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      sms = v;
+    else
+      cudaGetLastError();
+  }
+  const long long cblocks = (long long)B * (D / PASS_DPB);
+  long long target_chunks = (long long)waves * sms * pass2_slots(N, W) / cblocks;
+  if (target_chunks < 1) target_chunks = 1;
+  const long long max_chunks = (48 * 1024) / ((long long)(N + 1) * 4);  // the carry stages one warp's summaries
+  if (target_chunks > max_chunks) target_chunks = max_chunks;
   long long lc = (L + target_chunks - 1) / target_chunks;
-  lc = ((lc + TS - 1) / TS) * TS;
-  if (lc < TS) lc = TS;
+  if (lc < TSUB) lc = TSUB;
   return (int)lc;
 }
 
 static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
   ScanPlan s;
   s.P = k - 1;
-  s.Lc = choose_chunk(B, L, D);
+  s.Lc = choose_chunk(B, L, D, N, R + 2 * N);
   s.n_chunks = (L + s.Lc - 1) / s.Lc;
   s.W = R + 2 * N;
   const size_t rows = (size_t)B * (L + s.P);
@@ -592,13 +681,13 @@ static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
   off += al256((size_t)B * s.n_chunks * D * N * 4);
   s.gz = off;
   off += al256((size_t)B * L * D * 2);
-  // x_proj split-K: enough K splits for the (few) M tiles to cover the SMs, at least 4 k-blocks per split
+  // x_proj split-K (measured: the partial round trip costs more than the idle SMs it fills, so off by default)
   const int m_tiles = (int)((rows + 127) / 128);
-  const int kblocks = (D + 63) / 64;
-  int sp = 148 / (m_tiles > 0 ? m_tiles : 1);
-  if (sp > 8) sp = 8;
-  if (sp > kblocks / 4) sp = kblocks / 4;
-  s.xsplits = sp > 1 ? sp : 1;
+  s.xsplits = 1;
+  if (const char* e = getenv("PSCWIN_XPROJ_SPLITS")) {  // tuning knob (1..8)
+    const int v = atoi(e);
+    if (v >= 1 && v <= 8) s.xsplits = v;
+  }
   s.partial = off;
   off += s.xsplits > 1 ? al256((size_t)s.xsplits * rows * s.W * 4) : 0;
   s.sem = off;
@@ -612,55 +701,55 @@ static int check_scan(int B, int L, int D, int N, int R, int k) {
   if (L < k - 1) return PSCWIN_ERR_CONTRACT;  // copies 2 and 3 must see a full history
   if (!(N == 16 || N == 32 || N == 64)) return PSCWIN_ERR_UNSUPPORTED;
   if (R > 64 || R % 4 || k > 4) return PSCWIN_ERR_UNSUPPORTED;  // float4 smem rows, register conv window
-  if (D % 128 && D % 32) return PSCWIN_ERR_UNSUPPORTED;
   if (D % 64) return PSCWIN_ERR_UNSUPPORTED;  // x_proj GEMM K tiles
   return PSCWIN_OK;
 }
 
-template <int N, int DPB>
+template <int N, int DPB, int NS>
 static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
   dim3 grid(p.D / DPB, p.n_chunks, p.B);
   const int W = p.R + 2 * N;
-  const size_t smem1 = 2 * StageLayout<DPB, false>::bytes(W);
-  const size_t smem2 = 2 * StageLayout<DPB, true>::bytes(W);
+  const size_t smem1 = 2 * StageLayout<DPB, DPB * NS, false>::bytes(W);
+  const size_t smem2 = 2 * StageLayout<DPB, DPB * NS, true>::bytes(W);
   {
     PSCWIN_PROF("scan_dt", s);
     const long long rows = (long long)p.B * (p.L + p.P);
-    dim3 gdt(p.D / DPB, (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
-    const int rmax = p.R <= 16 ? 16 : (p.R <= 48 ? 48 : 64);
-    const size_t smem_dt = ((size_t)DPB * rmax + (size_t)DT_ROWS * rmax) * 4;  // s_w [DPB][<=RMAX], s_d [rows][RMAX]
+    dim3 gdt((p.D + 2 * DT_THREADS - 1) / (2 * DT_THREADS), (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
     if (p.R <= 16)
-      scan_dt_kernel<16><<<gdt, DPB, smem_dt, s>>>(p);
+      scan_dt_kernel<16><<<gdt, DT_THREADS, 0, s>>>(p);
     else if (p.R <= 48)
-      scan_dt_kernel<48><<<gdt, DPB, smem_dt, s>>>(p);
+      scan_dt_kernel<48><<<gdt, DT_THREADS, 0, s>>>(p);
     else
-      scan_dt_kernel<64><<<gdt, DPB, smem_dt, s>>>(p);
+      scan_dt_kernel<64><<<gdt, DT_THREADS, 0, s>>>(p);
   }
   {
     PSCWIN_PROF("scan_pass1", s);
-    scan_pass1_kernel<N, DPB><<<grid, DPB, smem1, s>>>(p);
+    scan_pass1_kernel<N, DPB, NS><<<grid, DPB * NS, smem1, s>>>(p);
   }
   {
     PSCWIN_PROF("scan_carry", s);
     const int warps = p.B * p.D;
-    scan_carry_kernel<N><<<(warps + 7) / 8, 256, 0, s>>>(p);
+    const size_t per_warp = (size_t)p.n_chunks * (N + 1) * 4;
+    int wpb = (int)((48 * 1024) / per_warp);  // warps per block within the default shared-memory window
+    wpb = wpb > 8 ? 8 : (wpb < 1 ? 1 : wpb);
+    scan_carry_kernel<N><<<(warps + wpb - 1) / wpb, 32 * wpb, wpb * per_warp, s>>>(p);
   }
   {
     PSCWIN_PROF("scan_pass2", s);
-    scan_pass2_kernel<N, DPB><<<grid, DPB, smem2, s>>>(p);
+    scan_pass2_kernel<N, DPB, NS><<<grid, DPB * NS, smem2, s>>>(p);
   }
   return (int)cudaGetLastError();
 }
 
 template <int N>
 static int launch_passes(ScanParams& p, cudaStream_t s) {
-  if (p.D % 128 == 0) return launch_passes_dpb<N, 128>(p, s);
-  return launch_passes_dpb<N, 64>(p, s);
+  return launch_passes_dpb<N, PASS_DPB, PASS_NS>(p, s);
 }
 
-// Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out).
+// Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out). z_gated: z already
+// holds SiLU(z) (module path: applied by the in_proj epilogue); otherwise the gate is computed into the workspace.
 static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, const __nv_bfloat16* xin,
-                          long long ld_x, const __nv_bfloat16* z, long long ld_z, const float* conv_w,
+                          long long ld_x, const __nv_bfloat16* z, long long ld_z, bool z_gated, const float* conv_w,
                           const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
                           const float* a_log, const float* d_skip, __nv_bfloat16* out, long long ld_out, void* ws,
                           size_t ws_bytes, cudaStream_t s) {
@@ -680,8 +769,8 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.bbar = bbar;
   p.xin = xin;
   p.ld_x = ld_x;
-  p.z = z;
-  p.ld_z = ld_z;
+  p.gz = z;
+  p.ld_gz = ld_z;
   p.conv_w = conv_w;
   p.conv_b = conv_b;
   p.w_dt = w_dt;
@@ -693,13 +782,20 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.delta = reinterpret_cast<float*>(base + pl.delta);
   p.sumdt = reinterpret_cast<float*>(base + pl.sumdt);
   p.hs = reinterpret_cast<float*>(base + pl.hs);
-  p.gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
   p.out = out;
   p.ld_out = ld_out;
   const long long rows = (long long)B * (L + pl.P);
-  const long long nthreads = (long long)B * ((L + pl.P + CONV_T - 1) / CONV_T) * (D / 8);
+  if (z && !z_gated) {
+    PSCWIN_PROF("silu_gate", s);
+    __nv_bfloat16* gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
+    const long long n = (long long)B * L * (D / 8);
+    silu_gate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(z, ld_z, (long long)B * L, D, gz);
+    p.gz = gz;
+    p.ld_gz = D;
+  }
   {
     PSCWIN_PROF("conv_silu", s);
+    const long long nthreads = (long long)B * ((L + pl.P + CONV_T - 1) / CONV_T) * (D / 8);
     conv_silu_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p);
   }
   GemmArgs g;
@@ -760,10 +856,11 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   a.out = xz;
   a.ldo = 2 * D;
   a.epi = EPI_STORE_BF16;
+  a.silu_col = D;  // the z half leaves the epilogue as the output gate SiLU(z)
   rc = launch_gemm_bf16(u, w->w_in, a, s);
   if (rc) return PSCWIN_ERR_CUDA;
   // a2: cycle scan -> g = sum over copies of y * SiLU(z)
-  rc = run_cycle_scan(d->B, L, D, N, R, d->ssm_conv, d->bbar_mode, xz, 2 * D, xz + D, 2 * D,
+  rc = run_cycle_scan(d->B, L, D, N, R, d->ssm_conv, d->bbar_mode, xz, 2 * D, xz + D, 2 * D, true,
                       (const float*)w->conv_w, (const float*)w->conv_b, w->w_x, (const float*)w->w_dt,
                       (const float*)w->b_dt, w->a_log, w->d_skip, g, D, base + off_scan, scan_bytes, s);
   if (rc) return rc;
@@ -808,6 +905,6 @@ extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, con
   if (rc) return rc;
   if (((uintptr_t)xin | (uintptr_t)z | (uintptr_t)out | (uintptr_t)ws | (uintptr_t)w_x) & 15) return PSCWIN_ERR_ALIGN;
   return run_cycle_scan(d->B, L, d->D, d->N, d->R, d->conv_k, d->bbar_mode, (const __nv_bfloat16*)xin, d->D,
-                        (const __nv_bfloat16*)z, d->D, conv_w, conv_b, w_x, w_dt, b_dt, a_log, d_skip,
+                        (const __nv_bfloat16*)z, d->D, false, conv_w, conv_b, w_x, w_dt, b_dt, a_log, d_skip,
                         (__nv_bfloat16*)out, d->D, ws, ws_bytes, (cudaStream_t)stream);
 }

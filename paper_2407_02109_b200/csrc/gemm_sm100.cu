@@ -250,6 +250,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
         }
+        if (p.silu_col > 0 && col0 >= p.silu_col) {  // gate columns: SiLU(x) = x / (1 + e^-x)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
+        }
         if (resid_tma) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -366,6 +370,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
     }
   }
   if (resid && p.BN > 128) return -2;
+  if (p.silu_col && (p.silu_col % 32 || p.epi == EPI_STORE_F32)) return -2;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
   CUtensorMap tmA, tmB, tmOut, tmRes;

@@ -29,6 +29,8 @@ struct GemmArgs {
   int splits;
   float* partial;
   int* sem;
+  // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
+  int silu_col;
 };
 
 // host helpers (abi.cu)

@@ -1,0 +1,51 @@
+"""Time the library GEMM (pscwin_linear) with CUDA graphs (no host launch gaps): python tools/gemm_probe.py"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2407_02109_b200 as pl  # noqa: E402
+
+REPS = 20
+
+
+def graph_time(fn):
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(REPS):
+                fn()
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        best = min(best, a.elapsed_time(b) * 1000 / REPS)
+    return best
+
+
+shapes = [("qkv", 4096, 768, 2304, False), ("out", 4096, 768, 768, False), ("in_proj", 4096, 768, 3072, False),
+          ("out_scan", 4096, 1536, 768, False), ("x_proj", 4099, 1536, 112, True),
+          ("xp_N16", 4096, 1536, 16, True), ("xp_N64", 4096, 1536, 64, True), ("xp_N256", 4096, 1536, 256, True),
+          ("xp_K384", 4096, 384, 112, True), ("xp_K768", 4096, 768, 112, True), ("xp_K3072", 4096, 3072, 112, True),
+          ("m1tile_K1536", 128, 1536, 128, False), ("m1tile_K6144", 128, 6144, 128, False),
+          ("m148_K1536", 128 * 148, 1536, 128, False),
+          ("big", 8192, 4096, 4096, False)]
+for name, M, K, N, f32 in shapes:
+    A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    us = graph_time(lambda: pl.linear(A, W, out_f32=f32))
+    tf = 2 * M * N * K / us / 1e6
+    kb = (K + 63) // 64
+    print(f"{name:14s} M={M:6d} K={K:5d} N={N:5d} {us:8.2f} us  {tf:7.1f} TF/s  {us / kb:6.3f} us/kblock(if 1 tile/CTA)",
+          flush=True)
