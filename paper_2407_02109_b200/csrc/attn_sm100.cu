@@ -39,6 +39,8 @@ struct AttnKArgs {
 template <int D>
 __global__ void __launch_bounds__(ATT_THREADS, 2)
     window_attn_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnKArgs p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int ROWB = D * 2;                 // bytes per row of Q/K/V/O (64 or 128)
   constexpr int TILE_BYTES = 128 * ROWB;      // smem rows allocated per operand
   constexpr uint32_t LAYOUT = ROWB == 128 ? kLayoutSW128 : kLayoutSW64;
@@ -266,6 +268,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
 // rot_Y(k_p[h][d/2:d]), vp[h][:] = v_p[h][:]  (bf16; rotation in f32 from the f32 projection of p).
 __global__ void pad_tables_kernel(const float* __restrict__ qkv_pad, int C, int heads, int d, int Wp, int Hp, int pl,
                                   int pt, int rope, __nv_bfloat16* kx, __nv_bfloat16* ky, __nv_bfloat16* vp) {
+  pdl_trigger();
+  pdl_wait();
   const int half = d / 2;
   const int nx = Wp * heads * half, ny = Hp * heads * half, nv = heads * d;
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -338,7 +342,7 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
     p.vp = vp;
     int n = (p.Wp + p.Hp) * a.C / 2 + a.C;
     PSCWIN_PROF("pad_tables", stream);
-    pad_tables_kernel<<<(n + 255) / 256, 256, 0, stream>>>(a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
+    launch_k(pad_tables_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
                                                            kx, ky, vp);
   }
   // windows of <= 256 slots: persistent warp-specialised kernel (attn_sm100_ws.cu); PSCWIN_ATTN_V1=1 forces this
@@ -364,14 +368,14 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
       cudaFuncSetAttribute(window_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       set = true;
     }
-    window_attn_kernel<64><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, p);
+    launch_k(window_attn_kernel<64>, dim3(grid), dim3(ATT_THREADS), smem, stream, tmQKV, p);
   } else {
     static bool set = false;
     if (!set) {
       cudaFuncSetAttribute(window_attn_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       set = true;
     }
-    window_attn_kernel<32><<<grid, ATT_THREADS, smem, stream>>>(tmQKV, p);
+    launch_k(window_attn_kernel<32>, dim3(grid), dim3(ATT_THREADS), smem, stream, tmQKV, p);
   }
   return (int)cudaGetLastError();
 }

@@ -47,6 +47,7 @@ struct AttnWsArgs {
 template <int D, bool MASKED>
 __global__ void __launch_bounds__(WS_THREADS, 1)
     window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnWsArgs p) {
+  pdl_trigger();
   constexpr int ROWB = D * 2;
   constexpr int TILE = 128 * ROWB;           // smem bytes reserved per 128-slot tile
   constexpr int STAGE = 6 * TILE;            // Q0 Q1 K0 K1 V0 V1
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
+  pdl_wait();  // barrier init / TMEM allocation overlap the previous kernel; global accesses start here
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -435,7 +437,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   PSCWIN_PROF("window_attention", stream);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, WS_THREADS, smem, stream>>>(tmQKV, p);
+    launch_k(kern, dim3(grid), dim3(WS_THREADS), smem, stream, tmQKV, p);
   };
   const bool masked = p.pad_mode == 1;
   if (d == 64)

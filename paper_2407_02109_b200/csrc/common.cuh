@@ -12,6 +12,12 @@ namespace pscwin {
 
 PSCWIN_DEVICE uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
+// Programmatic dependent launch (kernels are launched with programmatic stream serialization, see launch.h):
+// pdl_trigger lets the next kernel in the stream be scheduled once every CTA of this grid has started;
+// pdl_wait blocks until the previous kernel has completed and its memory is visible. Every kernel calls
+// pdl_wait before its first global access (read or write), so ordering is exactly that of plain stream order.
+PSCWIN_DEVICE void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+PSCWIN_DEVICE void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 PSCWIN_DEVICE uint32_t lane_id() { return threadIdx.x & 31u; }
 
 PSCWIN_DEVICE uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }

@@ -58,6 +58,8 @@ __device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log
 constexpr int KMAX = 4;  // conv width supported (Mamba default 4)
 constexpr int CONV_T = 8;
 __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
+  pdl_trigger();
+  pdl_wait();
   const int dv = p.D / 8;
   const int rows_img = p.L + p.P;
   const int groups_img = (rows_img + CONV_T - 1) / CONV_T;
@@ -151,6 +153,8 @@ __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
 // straight from the in_proj GEMM epilogue instead.
 __global__ void __launch_bounds__(256) silu_gate_kernel(const __nv_bfloat16* z, long long ld_z, long long T, int D,
                                                         __nv_bfloat16* gz) {
+  pdl_trigger();
+  pdl_wait();
   const int dv = D / 8;
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= T * dv) return;
@@ -225,6 +229,8 @@ constexpr int DT_ROWS = 64;
 constexpr int DT_THREADS = 64;
 template <int RMAX>
 __global__ void __launch_bounds__(DT_THREADS) scan_dt_kernel(ScanParams p) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float4 s_d4[DT_ROWS * (RMAX / 4)];
   const int W = p.R + 2 * p.N;
   const int d = blockIdx.x * (2 * DT_THREADS) + 2 * threadIdx.x;
@@ -305,8 +311,10 @@ __global__ void __launch_bounds__(DT_THREADS) scan_dt_kernel(ScanParams p) {
 // ------------------------------------------------------------------------------------------------- pass 1
 // NS threads per channel, each owning NH = N / NS of its states (NS = 2 halves the registers per thread, which
 // doubles the resident warps that hide the MUFU / FMA latencies).
-template <int N, int DPB, int NS>
+template <int N, int DPB, int NS, bool ZOH>
 __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int NT = DPB * NS, NH = N / NS;
   using St = StageLayout<DPB, NT, false>;
   extern __shared__ __align__(128) uint8_t s_raw[];
@@ -325,7 +333,6 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
     A2[k] = make_float2(-__expf(p.a_log[d * N + n0 + 2 * k]) * kLog2e, -__expf(p.a_log[d * N + n0 + 2 * k + 1]) * kLog2e);
     h[k] = make_float2(0.f, 0.f);
   }
-  const bool zoh = p.bbar == 0;
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
   const int tb = max(t0, p.P);
@@ -351,7 +358,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
     const float* sdbc = reinterpret_cast<const float*>(buf);
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     const float* sdelta = reinterpret_cast<const float*>(buf + St::off_dt(W));
-    for (int j = 0; j < nt; ++j) {
+    auto tstep = [&](int j) {
       const float v = __bfloat162float(sv[j * DPB + c]);
       const float dt = sdelta[j * DPB + c];
       sdt += dt;
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
         const float2 x = __fmul2_rn(dt2, A2[k]);
         const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
         const float2 wn = __fmul2_rn(bk, nv2);                    // -w = -B v
-        if (zoh) {
+        if (ZOH) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);               // h~ + w
           h[k] = __ffma2_rn(dA, t, wn);                            // dA (h~ + w) - w
         } else {
@@ -372,6 +379,12 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
           h[k] = __ffma2_rn(dA, h[k], __fmul2_rn(u, m1));
         }
       }
+    };
+    if (nt == TSUB) {  // full sub-chunk: unrolled (constant smem offsets, no per-step index math)
+#pragma unroll
+      for (int j = 0; j < TSUB; ++j) tstep(j);
+    } else {
+      for (int j = 0; j < nt; ++j) tstep(j);
     }
     __syncthreads();
   }
@@ -388,6 +401,8 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
 // so the two sequential folds over the chunks run from shared memory instead of one global round trip per batch.
 template <int N>
 __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int NPL = (N + 31) / 32;
   extern __shared__ __align__(16) float s_carry[];
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -510,8 +525,10 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
-template <int N, int DPB, int NS>
+template <int N, int DPB, int NS, bool ZOH>
 __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int NT = DPB * NS, NH = N / NS;
   using St = StageLayout<DPB, NT, true>;
   extern __shared__ __align__(128) uint8_t s_raw[];
@@ -540,7 +557,6 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     invA[k] = make_float2(__frcp_rn(a0), __frcp_rn(a1));
   }
   const float D3 = 3.f * p.d_skip[d];
-  const bool zoh = p.bbar == 0;
   const int t0 = chunk * p.Lc;
   const int t1 = min(p.L, t0 + p.Lc);
   const int tb = max(t0, p.P);
@@ -566,7 +582,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
     const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
-    for (int j = 0; j < nt; ++j) {
+    auto tstep = [&](int j) {
       const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);      // B pairs
       const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + N + n0);  // C pairs
       const float v = __bfloat162float(sv[j * DPB + c]);
@@ -581,7 +597,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
         const float2 x = __fmul2_rn(dt2, A2[k]);
         const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
         const float2 wn = __fmul2_rn(bk, nv3);                    // -3 B v
-        if (zoh) {
+        if (ZOH) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);
           h[k] = __ffma2_rn(dA, t, wn);
         } else {
@@ -598,6 +614,12 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
         const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
         p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
       }
+    };
+    if (nt == TSUB) {  // full sub-chunk: partially unrolled
+#pragma unroll 4
+      for (int j = 0; j < TSUB; ++j) tstep(j);
+    } else {
+      for (int j = 0; j < nt; ++j) tstep(j);
     }
     __syncthreads();
   }
@@ -613,24 +635,45 @@ static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // channels per CTA of the passes and threads per channel (the chunk plan depends on them)
 constexpr int PASS_DPB = 64;
-constexpr int PASS_NS = 2;
+// threads per channel of the passes (each owns N / NS states). Measured at ViT-B 1024^2: pass 1 is fastest with
+// NS = 4 (more warps, MUFU-bound), pass 2 with NS = 1 (its per-token work -- output reduction, gate, store -- is
+// amortised over all N states). PSCWIN_SCAN_NS1 / PSCWIN_SCAN_NS2 = 1, 2 or 4 override (tuning knobs).
+static int ns_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  return (v == 1 || v == 2 || v == 4) ? v : dflt;
+}
+static int pass1_ns() {
+  static int ns = 0;
+  if (!ns) ns = ns_env("PSCWIN_SCAN_NS1", 4);
+  return ns;
+}
+static int pass_ns() {
+  static int ns = 0;
+  if (!ns) ns = ns_env("PSCWIN_SCAN_NS2", 1);
+  return ns;
+}
 
-// Pass-2 CTAs resident per SM (occupancy query; a fixed fallback without a device).
-static int pass2_slots(int N, int W) {
+template <int N, int NS>
+static int pass2_slots_t(int W) {
   int n = 0;
-  cudaError_t e = cudaErrorInvalidValue;
-  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * PASS_NS, true>::bytes(W);
-  if (N == 16)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<16, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
-  else if (N == 32)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<32, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
-  else if (N == 64)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<64, PASS_DPB, PASS_NS>, PASS_DPB * PASS_NS, smem);
+  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(W);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<N, PASS_DPB, NS, true>,
+                                                                PASS_DPB * NS, smem);
   if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = 4;
   }
   return n;
+}
+template <int N>
+static int pass2_slots_n(int W) {
+  const int ns = pass_ns();
+  return ns == 1 ? pass2_slots_t<N, 1>(W) : (ns == 4 ? pass2_slots_t<N, 4>(W) : pass2_slots_t<N, 2>(W));
+}
+// Pass-2 CTAs resident per SM (occupancy query; a fixed fallback without a device).
+static int pass2_slots(int N, int W) {
+  return N == 16 ? pass2_slots_n<16>(W) : (N == 32 ? pass2_slots_n<32>(W) : pass2_slots_n<64>(W));
 }
 
 // Chunk length: the (chunk, channel block) CTAs of a pass fill every SM's resident slots exactly `waves` times
@@ -705,26 +748,45 @@ static int check_scan(int B, int L, int D, int N, int R, int k) {
   return PSCWIN_OK;
 }
 
-template <int N, int DPB, int NS>
-static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
-  dim3 grid(p.D / DPB, p.n_chunks, p.B);
-  const int W = p.R + 2 * N;
-  const size_t smem1 = 2 * StageLayout<DPB, DPB * NS, false>::bytes(W);
-  const size_t smem2 = 2 * StageLayout<DPB, DPB * NS, true>::bytes(W);
+template <int N, int NS>
+static void launch_pass1(ScanParams& p, cudaStream_t s) {
+  const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
+  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false>::bytes(p.R + 2 * N);
+  if (p.bbar == 0)
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, false>, grid, dim3(PASS_DPB * NS), smem, s, p);
+}
+
+template <int N, int NS>
+static void launch_pass2(ScanParams& p, cudaStream_t s) {
+  const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
+  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(p.R + 2 * N);
+  if (p.bbar == 0)
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, false>, grid, dim3(PASS_DPB * NS), smem, s, p);
+}
+
+template <int N>
+static int launch_passes(ScanParams& p, cudaStream_t s) {
   {
     PSCWIN_PROF("scan_dt", s);
     const long long rows = (long long)p.B * (p.L + p.P);
     dim3 gdt((p.D + 2 * DT_THREADS - 1) / (2 * DT_THREADS), (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
     if (p.R <= 16)
-      scan_dt_kernel<16><<<gdt, DT_THREADS, 0, s>>>(p);
+      launch_k(scan_dt_kernel<16>, gdt, dim3(DT_THREADS), 0, s, p);
     else if (p.R <= 48)
-      scan_dt_kernel<48><<<gdt, DT_THREADS, 0, s>>>(p);
+      launch_k(scan_dt_kernel<48>, gdt, dim3(DT_THREADS), 0, s, p);
     else
-      scan_dt_kernel<64><<<gdt, DT_THREADS, 0, s>>>(p);
+      launch_k(scan_dt_kernel<64>, gdt, dim3(DT_THREADS), 0, s, p);
   }
   {
     PSCWIN_PROF("scan_pass1", s);
-    scan_pass1_kernel<N, DPB, NS><<<grid, DPB * NS, smem1, s>>>(p);
+    const int ns = pass1_ns();
+    if (ns == 1) launch_pass1<N, 1>(p, s);
+    else if (ns == 2) launch_pass1<N, 2>(p, s);
+    else launch_pass1<N, 4>(p, s);
   }
   {
     PSCWIN_PROF("scan_carry", s);
@@ -732,18 +794,16 @@ static int launch_passes_dpb(ScanParams& p, cudaStream_t s) {
     const size_t per_warp = (size_t)p.n_chunks * (N + 1) * 4;
     int wpb = (int)((48 * 1024) / per_warp);  // warps per block within the default shared-memory window
     wpb = wpb > 8 ? 8 : (wpb < 1 ? 1 : wpb);
-    scan_carry_kernel<N><<<(warps + wpb - 1) / wpb, 32 * wpb, wpb * per_warp, s>>>(p);
+    launch_k(scan_carry_kernel<N>, dim3((warps + wpb - 1) / wpb), dim3(32 * wpb), wpb * per_warp, s, p);
   }
   {
     PSCWIN_PROF("scan_pass2", s);
-    scan_pass2_kernel<N, DPB, NS><<<grid, DPB * NS, smem2, s>>>(p);
+    const int ns = pass_ns();
+    if (ns == 1) launch_pass2<N, 1>(p, s);
+    else if (ns == 2) launch_pass2<N, 2>(p, s);
+    else launch_pass2<N, 4>(p, s);
   }
   return (int)cudaGetLastError();
-}
-
-template <int N>
-static int launch_passes(ScanParams& p, cudaStream_t s) {
-  return launch_passes_dpb<N, PASS_DPB, PASS_NS>(p, s);
 }
 
 // Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out). z_gated: z already
@@ -789,14 +849,14 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
     PSCWIN_PROF("silu_gate", s);
     __nv_bfloat16* gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
     const long long n = (long long)B * L * (D / 8);
-    silu_gate_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(z, ld_z, (long long)B * L, D, gz);
+    launch_k(silu_gate_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, z, ld_z, (long long)B * L, D, gz);
     p.gz = gz;
     p.ld_gz = D;
   }
   {
     PSCWIN_PROF("conv_silu", s);
     const long long nthreads = (long long)B * ((L + pl.P + CONV_T - 1) / CONV_T) * (D / 8);
-    conv_silu_kernel<<<(unsigned)((nthreads + 255) / 256), 256, 0, s>>>(p);
+    launch_k(conv_silu_kernel, dim3((unsigned)((nthreads + 255) / 256)), dim3(256), 0, s, p);
   }
   GemmArgs g;
   memset(&g, 0, sizeof(g));

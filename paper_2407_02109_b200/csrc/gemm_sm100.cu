@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      GemmArgs p) {
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   const int BN = p.BN;
   const int B_STAGE_BYTES = BN * BK * 2;
@@ -99,6 +100,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait();  // barrier init / TMEM allocation / descriptor prefetch overlap the previous kernel
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
@@ -404,7 +406,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   const long long tiles = (long long)((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   const int grid = tiles < num_sms() ? (int)tiles : num_sms();
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
-  gemm_bf16_kernel<<<grid, GEMM_THREADS, smem, stream>>>(tmA, tmB, tmOut, tmRes, p);
+  launch_k(gemm_bf16_kernel, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
   return (int)cudaGetLastError();
 }
 

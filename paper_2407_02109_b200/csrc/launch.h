@@ -1,0 +1,53 @@
+// Kernel launch helper: every library kernel is launched with programmatic stream serialization (PDL), so its
+// CTAs can be scheduled (and run their prologue: barrier init, TMEM allocation, descriptor prefetch) while the
+// previous kernel drains; the kernel body starts at pdl_wait() (common.cuh), which restores stream order.
+// Measured on the graph-captured step: no gain (1% slower), so the attribute is off unless PSCWIN_PDL=1.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdlib.h>
+
+#include <utility>
+
+namespace pscwin {
+
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PSCWIN_PDL");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && pdl_enabled()) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// PDL launch (the default for library kernels)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  return launch_kernel(true, kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
+
+// Plain stream-ordered launch: for single-wave kernels whose CTAs must spread evenly over the SMs (an early
+// PDL launch would place them on whichever SMs the previous kernel leaves free first)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k_even(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                 Args&&... args) {
+  const char* e = getenv("PSCWIN_PDL_EVEN");  // tuning knob: 1 = PDL for these launches too
+  return launch_kernel(e && e[0] == '1', kern, grid, block, smem, s, std::forward<Args>(args)...);
+}
+
+}  // namespace pscwin

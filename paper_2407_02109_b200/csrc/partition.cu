@@ -19,6 +19,8 @@ struct Geometry {
 template <typename VecT>
 __global__ void partition_kernel(const VecT* __restrict__ x, const VecT* __restrict__ pad_row, VecT* __restrict__ out,
                                  Geometry g, int vecs_per_row, long long n_rows) {
+  pdl_trigger();
+  pdl_wait();
   long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n_rows) return;
   int lane = threadIdx.x & 31;
@@ -41,6 +43,8 @@ __global__ void partition_kernel(const VecT* __restrict__ x, const VecT* __restr
 template <typename T>
 __global__ void merge_kernel(const T* __restrict__ win, const T* __restrict__ residual, T* __restrict__ out, Geometry g,
                              int Cx, long long n_rows) {
+  pdl_trigger();
+  pdl_wait();
   long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n_rows) return;
   int lane = threadIdx.x & 31;
@@ -113,13 +117,13 @@ int launch_partition(const void* x, const void* pad_row, int B, int H, int W, in
                (pad_row == nullptr || (uintptr_t)pad_row % 16 == 0);
   PSCWIN_PROF("partition", stream);
   if (vec16) {
-    partition_kernel<uint4><<<grid, 256, 0, stream>>>((const uint4*)x, (const uint4*)pad_row, (uint4*)out, g,
+    launch_k(partition_kernel<uint4>, dim3(grid), dim3(256), 0, stream, (const uint4*)x, (const uint4*)pad_row, (uint4*)out, g,
                                                       (int)(row_bytes / 16), n_rows);
   } else if (row_bytes % 4 == 0) {
-    partition_kernel<uint32_t><<<grid, 256, 0, stream>>>((const uint32_t*)x, (const uint32_t*)pad_row,
+    launch_k(partition_kernel<uint32_t>, dim3(grid), dim3(256), 0, stream, (const uint32_t*)x, (const uint32_t*)pad_row,
                                                          (uint32_t*)out, g, (int)(row_bytes / 4), n_rows);
   } else {
-    partition_kernel<uint16_t><<<grid, 256, 0, stream>>>((const uint16_t*)x, (const uint16_t*)pad_row,
+    launch_k(partition_kernel<uint16_t>, dim3(grid), dim3(256), 0, stream, (const uint16_t*)x, (const uint16_t*)pad_row,
                                                          (uint16_t*)out, g, (int)(row_bytes / 2), n_rows);
   }
   return (int)cudaGetLastError();
@@ -133,10 +137,10 @@ int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, in
   unsigned grid = (unsigned)((n_rows + 7) / 8);
   PSCWIN_PROF("merge", stream);
   if (is_f32) {
-    merge_kernel<float><<<grid, 256, 0, stream>>>((const float*)win, (const float*)residual, (float*)out, g, Cx,
+    launch_k(merge_kernel<float>, dim3(grid), dim3(256), 0, stream, (const float*)win, (const float*)residual, (float*)out, g, Cx,
                                                   n_rows);
   } else {
-    merge_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)win,
+    launch_k(merge_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream, (const __nv_bfloat16*)win,
                                                           (const __nv_bfloat16*)residual, (__nv_bfloat16*)out, g,
                                                           Cx, n_rows);
   }

@@ -5,6 +5,7 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "launch.h"
 #include "prof.h"
 
 namespace pscwin {

@@ -10,6 +10,8 @@ namespace pscwin {
 template <typename T>
 __global__ void layer_norm_kernel(const T* __restrict__ x, long long rows, int C, const float* __restrict__ g,
                                   const float* __restrict__ b, float eps, T* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte vector
   long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -87,10 +89,10 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
   PSCWIN_PROF("layer_norm", stream);
   if (is_f32) {
     if (C % 4 || C > 1024) return -1;
-    layer_norm_kernel<float><<<grid, 256, 0, stream>>>((const float*)x, rows, C, g, b, eps, (float*)out);
+    launch_k(layer_norm_kernel<float>, dim3(grid), dim3(256), 0, stream, (const float*)x, rows, C, g, b, eps, (float*)out);
   } else {
     if (C % 8 || C > 2048) return -1;
-    layer_norm_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)x, rows, C, g, b, eps,
+    launch_k(layer_norm_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, g, b, eps,
                                                                (__nv_bfloat16*)out);
   }
   return (int)cudaGetLastError();
@@ -100,6 +102,8 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
 template <typename T>
 __global__ void pad_qkv_kernel(const T* __restrict__ pad, const T* __restrict__ w, const float* __restrict__ bias,
                                int C, float* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (j >= 3 * C) return;
   int lane = threadIdx.x & 31;
@@ -125,9 +129,9 @@ int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C
   unsigned grid = (unsigned)((3 * C + 7) / 8);
   PSCWIN_PROF("pad_qkv", stream);
   if (is_f32)
-    pad_qkv_kernel<float><<<grid, 256, 0, stream>>>((const float*)pad, (const float*)w_qkv, b_qkv, C, out);
+    launch_k(pad_qkv_kernel<float>, dim3(grid), dim3(256), 0, stream, (const float*)pad, (const float*)w_qkv, b_qkv, C, out);
   else
-    pad_qkv_kernel<__nv_bfloat16><<<grid, 256, 0, stream>>>((const __nv_bfloat16*)pad,
+    launch_k(pad_qkv_kernel<__nv_bfloat16>, dim3(grid), dim3(256), 0, stream, (const __nv_bfloat16*)pad,
                                                             (const __nv_bfloat16*)w_qkv, b_qkv, C, out);
   return (int)cudaGetLastError();
 }

@@ -14,9 +14,35 @@ import subprocess
 import sys
 
 LABELS = {  # ncu kernel name prefix -> library profiling label
-    "window_attn_kernel": "window_attention", "scan_pass1_kernel": "scan_pass1", "scan_pass2_kernel": "scan_pass2",
+    "window_attn_kernel": "window_attention", "window_attn_ws_kernel": "window_attention",
+    "scan_pass1_kernel": "scan_pass1", "scan_pass2_kernel": "scan_pass2", "scan_dt_kernel": "scan_dt",
     "scan_carry_kernel": "scan_carry", "conv_silu_kernel": "conv_silu", "layer_norm_kernel": "layer_norm",
+    "pad_qkv_kernel": "pad_qkv", "pad_tables_kernel": "pad_tables",
 }
+
+
+def gemm_labels(names):
+    """Library label of each GEMM launch from its neighbours in the step's launch order (layer structure:
+    LN -> QKV -> [pad] -> attention -> out-proj; LN_s -> in_proj -> conv -> x_proj -> dt/pass1/carry/pass2 ->
+    out_proj_scan)."""
+    out = []
+    for i, n in enumerate(names):
+        if n != "gemm_bf16_kernel":
+            out.append(LABELS.get(n, n))
+            continue
+        prev = names[i - 1] if i > 0 else ""
+        nxt = names[i + 1] if i + 1 < len(names) else ""
+        if prev == "conv_silu_kernel":
+            out.append("gemm_x_proj")
+        elif prev == "scan_pass2_kernel":
+            out.append("gemm_out_proj_scan")
+        elif prev.startswith("window_attn"):
+            out.append("gemm_out_proj")
+        elif nxt == "conv_silu_kernel":
+            out.append("gemm_in_proj")
+        else:
+            out.append("gemm_qkv_rope")
+    return out
 
 
 def short(name):
@@ -66,7 +92,8 @@ def full(path, traffic_out=None):
     print("| kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls (warps per issue) |")
     print("|---" * (len(METRICS) + 2) + "|")
     traffic = {}
-    for r in rows[2:]:
+    labels = gemm_labels([short(r[ki]) for r in rows[2:]])
+    for r, lab in zip(rows[2:], labels):
         vals = []
         for key, _, scale in METRICS:
             try:
@@ -77,12 +104,11 @@ def full(path, traffic_out=None):
                 vals.append("?")
         st = sorted(((float(r[i] or 0), hdr[i][len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")])
                      for i in stall_cols), reverse=True)[:3]
-        print(f"| {short(r[ki])} | " + " | ".join(vals) + " | " + ", ".join(f"{n} {v:.2f}" for v, n in st) + " |")
+        print(f"| {lab} | " + " | ".join(vals) + " | " + ", ".join(f"{n} {v:.2f}" for v, n in st) + " |")
         try:
             ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             b = 1e6 * (float(r[ir].replace(",", "")) * UNIT.get(units[ir], 1e-6) +
                        float(r[iw].replace(",", "")) * UNIT.get(units[iw], 1e-6))
-            lab = LABELS.get(short(r[ki]), short(r[ki]))
             traffic.setdefault(lab, b)
         except (ValueError, IndexError):
             pass
