@@ -9,6 +9,7 @@
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256, K=16 per instruction)
 //   warps 2-9: epilogue (tcgen05.ld 32x32b -> registers -> fused op -> swizzled smem -> TMA tensor store),
 //   double-buffered TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -17,18 +18,24 @@
 namespace pscwin {
 
 namespace {
-constexpr int BM = 128;
+constexpr int BM = 128;                          // accumulator rows per CTA (TMEM lanes)
 constexpr int BK = 64;
-constexpr int STAGES = 4;
+constexpr int MAX_STAGES = 8;
 constexpr int A_STAGE_BYTES = BM * BK * 2;       // 16 KB
 constexpr int STAGE_OUT_BYTES = BM * 64 * 2;     // one 128x64 bf16 output / residual chunk (16 KB)
 constexpr int GEMM_THREADS = 64 + 256;           // TMA warp, MMA warp, 8 epilogue warps
-constexpr size_t GEMM_SMEM_MAX = 230656;         // 1024 + 4 x 48 KB + 32 KB + 256 (also = BN 128 + residual)
-// shared memory layout for a tile width BN (B stage = BN x 64 bf16; residual tiles double-buffered)
-__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid) {
+constexpr size_t GEMM_SMEM_MAX = 232448;         // 227 KB opt-in limit per CTA
+// shared memory layout: [1 KB align slack][stages x (A 128x64 | B rows x 64)][2 x 16 KB output staging]
+// [residual tiles 2 x nch x 16 KB][barriers]; B rows per CTA = BN (single CTA) or BN / 2 (CTA pair)
+__host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid) {
   const size_t nch = (size_t)(BN + 63) / 64;
-  return 1024 + (size_t)STAGES * (A_STAGE_BYTES + (size_t)BN * BK * 2) + 2 * STAGE_OUT_BYTES +
-         (resid ? 2 * nch * STAGE_OUT_BYTES : 0) + 256;
+  return 1024 + 2 * STAGE_OUT_BYTES + (resid ? 2 * nch * STAGE_OUT_BYTES : 0) + 2 * 256 * 4 + 256;
+}
+__host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
+  return A_STAGE_BYTES + (size_t)(pair ? BN / 2 : BN) * BK * 2;
+}
+__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid, bool pair, int stages) {
+  return gemm_fixed_bytes(BN, resid) + (size_t)stages * gemm_stage_bytes(BN, pair);
 }
 }  // namespace
 
@@ -39,6 +46,11 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
   b = x1;
 }
 
+// PAIR: a 2-CTA cluster shares each 256-row tile: tcgen05.mma.cta_group::2 (M = 256) issued by the leader CTA
+// reads A rows [0,128) / [128,256) and B rows [0,BN/2) / [BN/2,BN) from the two CTAs' shared memory; each CTA's
+// TMEM holds its 128 accumulator rows x BN columns and its own epilogue stores them. Per SM this halves the B
+// bytes per MAC (the L2 -> SM traffic that bounds 1-CTA 128-row tiles).
+template <bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
@@ -46,7 +58,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   const int BN = p.BN;
-  const int B_STAGE_BYTES = BN * BK * 2;
+  const int STAGES = p.stages;
+  const int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
   const bool resid_tma = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
   const int nch = (BN + 63) / 64;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -54,7 +68,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
   uint8_t* s_res = s_stage + 2 * STAGE_OUT_BYTES;   // 2 x nch x 16 KB residual tiles (TMA-loaded)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : 0));
+  float* s_bias = reinterpret_cast<float*>(s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : 0));  // [2][256]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 2 * 256);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -65,15 +80,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   int* s_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = warp_id();
+  constexpr int TM = PAIR ? 2 * BM : BM;          // tile rows (the pair's 256 or one CTA's 128)
   const int n_tiles_n = (p.N + BN - 1) / BN;
-  const int S = p.splits > 1 ? p.splits : 1;  // split-K factor (f32 outputs only)
-  const int n_tiles = ((p.M + BM - 1) / BM) * n_tiles_n * S;
+  const int S = p.splits > 1 ? p.splits : 1;  // split-K factor (f32 outputs only; single-CTA tiles)
+  const int n_tiles = ((p.M + TM - 1) / TM) * n_tiles_n * S;
+  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // this CTA's (pair's) first tile
+  const int tstride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nk = (p.K + BK - 1) / BK;
   // work tile -> output tile (m0, n0), k-block range [kb0, kb1) and split index
   auto coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1, int& s) {
     const int mn = tile / S;
     s = tile - mn * S;
-    m0 = (mn / n_tiles_n) * BM;
+    m0 = (mn / n_tiles_n) * TM;
     n0 = (mn % n_tiles_n) * BN;
     kb0 = (int)((long long)nk * s / S);
     kb1 = (int)((long long)nk * (s + 1) / S);
@@ -89,89 +107,140 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 256);
+      mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs of a pair)
       mbar_init(&rfull[i], 1);
       mbar_init(&rempty[i], 256);
     }
     if (resid_tma) tma_prefetch_desc(&tmRes);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if (PAIR)
+      tmem_alloc_pair(tmem_slot, 512);
+    else
+      tmem_alloc(tmem_slot, 512);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer's barriers are initialised before any cross-CTA signal
   tc_fence_after();
   pdl_wait();  // barrier init / TMEM allocation / descriptor prefetch overlap the previous kernel
   const uint32_t tmem_base = *tmem_slot;
+  // rows of the tile that this CTA loads / stores: [m0 + mrow, m0 + mrow + 128)
+  const int mrow = PAIR ? (int)rank * BM : 0;
 
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = policy_evict_last();
+      // CTA pair: both CTAs' loads complete on the leader's full barrier (it issues the MMAs)
+      const uint32_t full0 = PAIR ? smem_in_cta(&full[0], 0) : 0u;
       int stage = 0;
       uint32_t phase = 0;
       int rbuf = 0;
       uint32_t rphase = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < n_tiles; tile += tstride) {
         int m0, n0, kb0, kb1, s;
         coords(tile, m0, n0, kb0, kb1, s);
         if (resid_tma) {
-          // residual tile of this output tile (double-buffered, consumed by the epilogue), issued ahead of the k-loop
+          // residual tile of this CTA's rows (double-buffered, consumed by the epilogue), issued ahead of the k-loop
           mbar_wait(&rempty[rbuf], rphase ^ 1);
-          mbar_arrive_expect_tx(&rfull[rbuf], nch * STAGE_OUT_BYTES);
-          for (int c = 0; c < nch; ++c)
-            tma_load_2d(s_res + (rbuf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[rbuf], n0 + c * 64, m0, pol_a);
+          if (m0 + mrow < p.M) {
+            mbar_arrive_expect_tx(&rfull[rbuf], nch * STAGE_OUT_BYTES);
+            for (int c = 0; c < nch; ++c)
+              tma_load_2d(s_res + (rbuf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[rbuf], n0 + c * 64, m0 + mrow,
+                          pol_a);
+          } else {
+            mbar_arrive(&rfull[rbuf]);  // no rows of this CTA in the tile: nothing to load
+          }
           if (++rbuf == 2) {
             rbuf = 0;
             rphase ^= 1;
           }
         }
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + BN * BK * 2);
-          tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m0, pol_a);
-          tma_load_2d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BK, n0, pol_b);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
+        if (PAIR) {
+          // boxes entirely outside A (rows >= M) or B (rows >= N) are not loaded; their bytes are not expected
+          const bool a0_in = m0 < p.M, a1_in = m0 + BM < p.M;
+          const bool b0_in = n0 < p.N, b1_in = n0 + BN / 2 < p.N;
+          const uint32_t bytes = ((int)a0_in + (int)a1_in) * A_STAGE_BYTES + ((int)b0_in + (int)b1_in) * B_STAGE_BYTES;
+          const bool a_mine = rank ? a1_in : a0_in, b_mine = rank ? b1_in : b0_in;
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+            const uint32_t fb = full0 + stage * 8;
+            if (a_mine) tma_load_2d_pair(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, m0 + mrow, pol_a);
+            if (b_mine)
+              tma_load_2d_pair(sB + stage * B_STAGE_BYTES, &tmB, fb, kb * BK, n0 + (int)rank * (BN / 2), pol_b);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        } else {
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
+            tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m0, pol_a);
+            tma_load_2d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BK, n0, pol_b);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    const uint32_t idesc = make_idesc_bf16(BM, BN, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      int m0, n0, kb0, kb1, s;
-      coords(tile, m0, n0, kb0, kb1, s);
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * 256;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    if (!PAIR || rank == 0) {
+      const uint32_t idesc = make_idesc_bf16(TM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = tile0; tile < n_tiles; tile += tstride) {
+        int m0, n0, kb0, kb1, s;
+        coords(tile, m0, n0, kb0, kb1, s);
+        if (PAIR)
+          mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        else
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t a0 = smem_u32(sA + stage * A_STAGE_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * B_STAGE_BYTES);
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (PAIR)
+            mbar_wait_cluster(&full[stage], phase);
+          else
+            mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a0 = smem_u32(sA + stage * A_STAGE_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * B_STAGE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, kLayoutSW128);
-            uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, kLayoutSW128);
-            umma_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, kLayoutSW128);
+              uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, kLayoutSW128);
+              if (PAIR)
+                umma_ss_pair(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              else
+                umma_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
+            if (PAIR) {
+              umma_commit_pair_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
+              if (kb == kb1 - 1) umma_commit_pair_mc(&tfull[acc], 0x3);
+            } else {
+              umma_commit(&empty[stage]);
+              if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+            }
           }
-          umma_commit(&empty[stage]);
-          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        __syncwarp();
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
   } else {
     // ------------------------------------------------------------------ epilogue warps 2..9
@@ -190,10 +259,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int gseq = 0;
     int rbuf = 0;
     uint32_t rphase = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint32_t tempty0 = PAIR ? smem_in_cta(&tempty[0], 0) : 0u;  // the leader's accumulator-free barriers
+    for (int tile = tile0; tile < n_tiles; tile += tstride) {
       int m0, n0, kb0, kb1, split;
       coords(tile, m0, n0, kb0, kb1, split);
-      const int row = m0 + row_local;
+      const int mb = m0 + mrow;                          // first row of this CTA's 128
+      const int row = mb + row_local;
       const bool row_ok = row < p.M;
       // RoPE of this row (QKV epilogue): this thread's 32 columns of every 64-column chunk are one half of a head
       // (d = 64: axis = half, pair jj -> frequency jj) or one whole head (d = 32: pairs 0-7 x, 8-15 y).
@@ -208,7 +279,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           rope_cs(axis ? py : px, fj, p.d_head, rc[jj], rs[jj]);
         }
       }
-      mbar_wait(&tfull[acc], acc_phase);
+      // bias of the tile's columns staged once in shared memory (read back as broadcasts), double-buffered by
+      // accumulator so the next tile's staging never races this tile's readers
+      float* sb = s_bias + acc * 256;
+      if (p.bias) {
+        if (etid < BN / 4) {
+          const int c = n0 + 4 * etid;
+          float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (c + 4 <= p.N) {
+            b4 = __ldg(reinterpret_cast<const float4*>(p.bias + c));
+          } else {
+            float* bp = reinterpret_cast<float*>(&b4);
+            for (int e = 0; e < 4 && c + e < p.N; ++e) bp[e] = __ldg(p.bias + c + e);
+          }
+          reinterpret_cast<float4*>(sb)[etid] = b4;
+        }
+        if (!tma_out) named_bar_sync(1, 256);  // (the bf16 path's first chunk barrier orders it otherwise)
+      }
+      if (PAIR)
+        mbar_wait_cluster(&tfull[acc], acc_phase);
+      else
+        mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (resid_tma) mbar_wait(&rfull[rbuf], rphase);
       const uint32_t t_row = tmem_base + acc * 256 + ((uint32_t)(quarter * 32) << 16);
@@ -238,15 +329,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.bias) {  // 16-byte broadcast loads (every lane of the warp reads the same columns)
+        if (p.bias && cl < BN) {  // shared-memory broadcast reads (zero past N)
 #pragma unroll
-          for (int j = 0; j < 32; j += 4)
-            if (col0 + j + 4 <= p.N) {
-              const float4 b4 = __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j));
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            } else {
-              for (int e = 0; e < 4 && col0 + j + e < p.N; ++e) v[j + e] += __ldg(p.bias + col0 + j + e);
-            }
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+            v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+          }
         }
         if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
 #pragma unroll
@@ -280,7 +368,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           fence_proxy_async_smem();
           named_bar_sync(1, 256);
           if (issuer) {
-            tma_store_2d(&tmOut, stg, n0 + cc * 64, m0);
+            if (mb < p.M) tma_store_2d(&tmOut, stg, n0 + cc * 64, mb);
             bulk_commit();
           }
         } else if (row_ok && cl < BN) {
@@ -300,7 +388,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {  // one arrival per warp
+        if (PAIR)
+          mbar_arrive_remote(tempty0 + acc * 8);
+        else
+          mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
       if (resid_tma) {
@@ -349,10 +443,49 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (issuer && tma_out) bulk_wait0();
   }
   __syncthreads();
+  if (PAIR) cluster_sync();  // the peer may still read this CTA's shared memory / signal its barriers until here
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    if (PAIR)
+      tmem_dealloc_pair(tmem_base, 512);
+    else
+      tmem_dealloc(tmem_base, 512);
   }
+}
+
+static bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("PSCWIN_GEMM_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// co-resident 2-CTA clusters of the pair kernel (an SM left alone in a GPC cannot host half a cluster)
+static int pair_clusters(size_t smem) {
+  static int cached = 0;
+  static size_t cached_smem = 0;
+  if (cached && cached_smem == smem) return cached;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (num_sms() / 2));
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true>, &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = num_sms() / 2;
+  }
+  cached = n;
+  cached_smem = smem;
+  return n;
 }
 
 int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cudaStream_t stream) {
@@ -361,26 +494,51 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (p.K % 8 != 0) return -1;
   if (p.epi == EPI_QKV_ROPE && p.rope && !(p.d_head == 32 || p.d_head == 64)) return -2;
   const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
-  // tile N: a single tile when N <= 256; else 256, or 128 when 256-wide tiles would leave SMs idle. Residual
-  // epilogues stage the residual tile in shared memory, which fits next to the 4-stage ring only for BN <= 128.
-  if (p.BN <= 0) {
-    if (p.N <= (resid ? 128 : 256)) {
-      p.BN = ((p.N + 15) / 16) * 16;
-    } else {
-      const long long t256 = (long long)((p.M + BM - 1) / BM) * ((p.N + 255) / 256);
-      p.BN = (!resid && t256 >= 2LL * num_sms()) ? 256 : 128;
-    }
-  }
-  if (resid && p.BN > 128) return -2;
   if (p.silu_col && (p.silu_col % 32 || p.epi == EPI_STORE_F32)) return -2;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
+  // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K
+  const bool pair = pair_enabled() && p.splits <= 1 && p.M > BM;
+  const int TMr = pair ? 2 * BM : BM;
+  const int m_tiles = (p.M + TMr - 1) / TMr;
+  const int slots = pair ? num_sms() / 2 : num_sms();
+  // tile N: one tile when N <= 256 (<= 128 with a residual, whose tiles are staged in shared memory); else the
+  // width (256 or 128) with the fewest scheduling rounds, weighting a round by its tile width
+  if (p.BN <= 0) {
+    const int cap = resid ? 128 : 256;
+    if (p.N <= cap) {
+      p.BN = ((p.N + 15) / 16) * 16;
+    } else if (resid) {
+      p.BN = 128;
+    } else {
+      auto cost = [&](int bn) {
+        const long long tiles = (long long)m_tiles * ((p.N + bn - 1) / bn);
+        return ((tiles + slots - 1) / slots) * (bn + 32);
+      };
+      p.BN = cost(256) <= cost(128) ? 256 : 128;
+      if (const char* e = getenv("PSCWIN_GEMM_BN")) {  // tuning knob for the multi-tile case: 128 or 256
+        const int v = atoi(e);
+        if (v == 128 || v == 256) p.BN = v;
+      }
+    }
+  }
+  if (resid && p.BN > 128) return -2;
+  if (pair && (p.BN % 16)) return -2;
+  // ring depth: as many stages as fit next to the staging / residual buffers
+  {
+    const size_t fixed = gemm_fixed_bytes(p.BN, resid), st = gemm_stage_bytes(p.BN, pair);
+    int stages = (int)((GEMM_SMEM_MAX - fixed) / st);
+    if (stages > MAX_STAGES) stages = MAX_STAGES;
+    if (stages < 2) return -2;
+    p.stages = stages;
+  }
+  p.pair = pair ? 1 : 0;
   CUtensorMap tmA, tmB, tmOut, tmRes;
   int rc = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.M, (uint64_t)p.lda * 2, BK, BM,
                         CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_tmap_2d(&tmB, Bw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.N, (uint64_t)p.ldb * 2, BK, p.BN,
-                    CU_TENSOR_MAP_SWIZZLE_128B);
+  rc = make_tmap_2d(&tmB, Bw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.N, (uint64_t)p.ldb * 2, BK,
+                    pair ? p.BN / 2 : p.BN, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   memset(&tmOut, 0, sizeof(tmOut));
   if (p.epi != EPI_STORE_F32) {
@@ -398,15 +556,36 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
+    cudaFuncSetAttribute(gemm_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
+    cudaFuncSetAttribute(gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
     attr_set = true;
   }
-  const size_t smem = gemm_smem_bytes(p.BN, resid);
+  const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages);
   if (smem > GEMM_SMEM_MAX) return -2;
-  const long long tiles = (long long)((p.M + BM - 1) / BM) * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
-  const int grid = tiles < num_sms() ? (int)tiles : num_sms();
+  const long long tiles = (long long)m_tiles * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
-  launch_k(gemm_bf16_kernel, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+  if (!pair) {
+    const int grid = tiles < num_sms() ? (int)tiles : num_sms();
+    launch_k(gemm_bf16_kernel<false>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+    return (int)cudaGetLastError();
+  }
+  const int clusters_max = pair_clusters(smem);
+  const int clusters = tiles < clusters_max ? (int)tiles : clusters_max;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true>, tmA, tmB, tmOut, tmRes, p);
   return (int)cudaGetLastError();
 }
 

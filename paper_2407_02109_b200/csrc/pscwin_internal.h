@@ -32,6 +32,8 @@ struct GemmArgs {
   int* sem;
   // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
   int silu_col;
+  int stages;  // smem ring depth (set by the launcher)
+  int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
 };
 
 // host helpers (abi.cu)

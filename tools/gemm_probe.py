@@ -41,10 +41,19 @@ shapes = [("qkv", 4096, 768, 2304, False), ("out", 4096, 768, 768, False), ("in_
           ("m1tile_K1536", 128, 1536, 128, False), ("m1tile_K6144", 128, 6144, 128, False),
           ("m148_K1536", 128 * 148, 1536, 128, False),
           ("big", 8192, 4096, 4096, False)]
+only = sys.argv[1:]  # optional subset of shape names
+shapes += [("out+bias+res", 4096, 768, 768, "br"), ("qkv+bias", 4096, 768, 2304, "b"), ("in_proj+bias", 4096, 768, 3072, "b")]
 for name, M, K, N, f32 in shapes:
+    if only and name not in only:
+        continue
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
-    us = graph_time(lambda: pl.linear(A, W, out_f32=f32))
+    if isinstance(f32, str):
+        bias = torch.randn(N, device="cuda")
+        res = torch.randn(M, N, device="cuda").to(torch.bfloat16) if "r" in f32 else None
+        us = graph_time(lambda: pl.linear(A, W, bias=bias, residual=res))
+    else:
+        us = graph_time(lambda: pl.linear(A, W, out_f32=f32))
     tf = 2 * M * N * K / us / 1e6
     kb = (K + 63) // 64
     print(f"{name:14s} M={M:6d} K={K:5d} N={N:5d} {us:8.2f} us  {tf:7.1f} TF/s  {us / kb:6.3f} us/kblock(if 1 tile/CTA)",
