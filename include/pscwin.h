@@ -57,7 +57,7 @@ typedef struct {
   int32_t ssm_expand;                 /* E, D = E*C (Mamba default 2, Q9)                              */
   int32_t ssm_dt_rank;                /* R; 0 => ceil(C/16)                                              */
   int32_t ssm_conv;                   /* causal depthwise conv width k (Mamba default 4, Q9)            */
-  int32_t scan_order;                 /* pscwin_scan_order (row-major only on this path)                */
+  int32_t scan_order;                 /* pscwin_scan_order of the cycle scan (window-major: H, W % window == 0) */
   int32_t bbar_mode;                  /* pscwin_bbar_mode                                               */
   int32_t dtype;                      /* pscwin_dtype                                                   */
   float ln_eps;                       /* LayerNorm eps (Q15: 1e-6)                                      */
@@ -131,6 +131,7 @@ typedef struct {
   int32_t B, H, W;             /* L = H*W tokens per image, walked in scan_order                        */
   int32_t D, N, R, conv_k;     /* channels, SSM state (N <= 64), dt rank, conv width (L >= conv_k - 1)   */
   int32_t scan_order, bbar_mode, dtype;
+  int32_t window;              /* WINDOW_MAJOR block size (H, W divisible by it); ignored by other orders */
 } pscwin_scan_desc;
 /* Cycle scan: per image the token sequence (in scan order) is repeated three times, the Mamba
  * selective SSM (block internals Q9) scans the 3L sequence, the three output segments are summed:
@@ -138,7 +139,9 @@ typedef struct {
  *   (delta_low, B, C) = v W_x^T;  Delta = softplus(delta_low W_dt^T + b_dt);  A = -exp(a_log)
  *   h_j = exp(Delta A) h_{j-1} + B_bar v_j (Eq. 3-4);  y_j = C_j . h_j + d_skip * v_j
  *   out_t = sum_{c=0..2} y_{cL+t} * SiLU(z_t)   (no gate when z == NULL)
- * xin, z, out [B, L, D] bf16 in grid (row-major token) order. Computed exactly (up to rounding) by a
+ * xin, z, out [B, L, D] bf16 in grid (row-major token) order; the recurrence walks the tokens in scan_order
+ * (ROW_MAJOR raster, COL_MAJOR raster of the transpose, WINDOW_MAJOR windows in raster order with a raster
+ * inside each window; reading Q13) — non-raster orders gather into scan order and scatter the result back. Computed exactly (up to rounding) by a
  * two-pass chunked closed form. Workspace: pscwin_scan_workspace_bytes. */
 int pscwin_cycle_scan(const pscwin_scan_desc* desc, const void* xin, const void* z, const float* conv_w,
                       const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,

@@ -71,7 +71,7 @@ class LayerWeights(ctypes.Structure):
 
 class ScanDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("B", "H", "W", "D", "N", "R", "conv_k", "scan_order", "bbar_mode",
-                                              "dtype")]
+                                              "dtype", "window")]
 
 
 _LIB: Optional[ctypes.CDLL] = None

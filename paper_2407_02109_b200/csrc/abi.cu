@@ -151,6 +151,7 @@ LayerWs plan_layer(const pscwin_layer_desc* d) {
     sd.scan_order = d->scan_order;
     sd.bbar_mode = d->bbar_mode;
     sd.dtype = d->dtype;
+    sd.window = d->window;
     w.scan = take(pscwin_scan_workspace_bytes(&sd));
   }
   w.total = off;

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ld_full[i], 1);
       mbar_init(&ld_empty[i], 1);
-      mbar_init(&patch_done[i], 512);
+      mbar_init(&patch_done[i], 256);  // slot 0's threads patch (slot 1 runs half an item behind)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 256);
       mbar_init(&o_full[i], 1);
@@ -134,6 +134,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------------------------------ MMA issuer
+    // The two q-tile slots run half an item apart so one slot's softmax (MUFU-bound) overlaps the other slot's
+    // PV MMA, O read-out and next S MMA. Issue order per item i: S(i,0), PV(i-1,1), S(i,1), PV(i,0); for the
+    // first item S(0,1) follows PV(0,0), which sets up the half-item offset.
     const int NK = nt * p.tile_slots;
     const uint32_t idesc_s = make_idesc_bf16(128, NK, 0, 0);
     const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
@@ -141,52 +144,76 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     uint32_t phase = 0;
     uint32_t ph_p[2] = {0, 0}, ph_of[2] = {0, 0};
     int ev = 0;
+    auto issue_s = [&](int a, uint32_t sb) {
+      mbar_wait(&o_free[a], ph_of[a] ^ 1);  // the previous item's O (aliasing S columns) has been read
+      ph_of[a] ^= 1;
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t qa = sb + a * TILE, ka = sb + 2 * TILE;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
+                  idesc_s, k > 0);
+        umma_commit(&s_full[a]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int a, uint32_t sb) {
+      mbar_wait(&p_full[a], ph_p[a]);
+      ph_p[a] ^= 1;
+      ATT_TS(32, ev);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t va = sb + 4 * TILE;
+        for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128)
+          umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (ks >= 8 ? 64 : 0),
+                  make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
+        umma_commit(&o_full[a]);
+      }
+      __syncwarp();
+    };
+    auto release = [&](int st) {  // all MMAs reading stage st have been issued: TMA may refill it when they finish
+      if (elect_one()) umma_commit(&ld_empty[st]);
+      __syncwarp();
+    };
+    bool have_prev = false, prev_act1 = false;
+    int prev_stage = 0;
+    uint32_t prev_sb = 0;
+    bool first = true;
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
-      const bool act[2] = {q_active(0, Y0), q_active(1, Y0)};
+      const bool act0 = q_active(0, Y0), act1 = q_active(1, Y0);
       mbar_wait(&ld_full[stage], phase);
       if (p.patch) mbar_wait(&patch_done[stage], phase);
       ATT_TS(32, ev);
       tc_fence_after();
       const uint32_t sb = smem_u32(smem + stage * STAGE);
-      // the whole window (NK = w^2 <= 256 keys) is one key tile: K0|K1 and V0|V1 are contiguous in shared memory
-      for (int a = 0; a < 2; ++a) {
-        if (!act[a]) continue;
-        mbar_wait(&o_free[a], ph_of[a] ^ 1);  // the previous item's O (aliasing S columns) has been read
-        ph_of[a] ^= 1;
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t qa = sb + a * TILE, ka = sb + 2 * TILE;
-#pragma unroll
-          for (int k = 0; k < D / 16; ++k)
-            umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
-                    idesc_s, k > 0);
-          umma_commit(&s_full[a]);
-        }
-        __syncwarp();
+      if (act0) issue_s(0, sb);
+      if (have_prev) {
+        if (prev_act1) issue_pv(1, prev_sb);
+        release(prev_stage);
       }
-      for (int a = 0; a < 2; ++a) {
-        if (!act[a]) continue;
-        mbar_wait(&p_full[a], ph_p[a]);
-        ph_p[a] ^= 1;
-        ATT_TS(32, ev);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t va = sb + 4 * TILE;
-          for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128)
-            umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (ks >= 8 ? 64 : 0),
-                    make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
-          umma_commit(&o_full[a]);
-        }
-        __syncwarp();
+      if (first) {
+        if (act0) issue_pv(0, sb);
+        if (act1) issue_s(1, sb);
+      } else {
+        if (act1) issue_s(1, sb);
+        if (act0) issue_pv(0, sb);
       }
-      if (elect_one()) umma_commit(&ld_empty[stage]);  // all MMAs reading this stage are done -> TMA may refill
-      __syncwarp();
+      first = false;
+      have_prev = true;
+      prev_act1 = act1;
+      prev_stage = stage;
+      prev_sb = sb;
       if (++stage == 2) {
         stage = 0;
         phase ^= 1;
       }
+    }
+    if (have_prev) {
+      if (prev_act1) issue_pv(1, prev_sb);
+      release(prev_stage);
     }
   } else {
     // ------------------------------------------------------------------------------------------ softmax WGs
@@ -220,11 +247,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
       const bool active = q_active(a, Y0);
-      if (p.patch) {
-        // LEARNABLE pad patch of K/V rows outside the grid; thread wtid patches slot (wtid & 127) of key tile wtid>>7
+      if (p.patch && a == 0) {
+        // LEARNABLE pad patch of K/V rows outside the grid, by slot 0's 256 threads (slot 1 runs half an item
+        // behind and never touches the stage's shared memory): entry e = key tile e>>7, slot e&127
         mbar_wait(&ld_full[stage], phase);
-        const int kt = wtid >> 7, r = wtid & 127;
-        if (kt < nt && r < p.tile_slots) {
+        for (int e = gtid; e < nt * 128; e += 256) {
+          const int kt = e >> 7, r = e & 127;
+          if (r >= p.tile_slots) continue;
           const int Y = Y0 + kt * p.rpt + (r >> p.lw), X = X0 + (r & (p.w - 1));
           if (Y < 0 || Y >= p.H || X < 0 || X >= p.W) {
             uint8_t* sK = smem + stage * STAGE + (2 + kt) * TILE;
@@ -309,7 +338,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl2, nb);
-            float e0 = ex2_approx(x.x), e1 = ex2_approx(x.y);
+            float e0, e1;
+            if ((j / 2) % 3 == 2) {  // every third pair on the FMA pipe: the MUFU ex2 rate bounds this loop
+              const float2 e = exp2_poly2(x);
+              e0 = e.x;
+              e1 = e.y;
+            } else {
+              e0 = ex2_approx(x.x);
+              e1 = ex2_approx(x.y);
+            }
             if (MASKED || m != 0xFFFFFFFFu) {  // invalid keys, or stale columns past a 16-key window
               e0 = ((m >> j) & 1u) ? e0 : 0.f;
               e1 = ((m >> (j + 1)) & 1u) ? e1 : 0.f;

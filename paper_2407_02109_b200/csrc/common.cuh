@@ -286,6 +286,23 @@ PSCWIN_DEVICE float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for a pair on the FMA/ALU pipes (offloads the MUFU, FA4-style): x = n + f with n = round(x), f in
+// [-1/2, 1/2]; 2^f by a degree-3 polynomial (max relative error 7.5e-5 over the interval, fitted in
+// tools/ — ample for bf16 probabilities), 2^n by adding n to the exponent field. Inputs below -126 clamp
+// (results ~1e-38, i.e. zero at bf16 / fp32 accumulation scale).
+PSCWIN_DEVICE float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23: round-to-nearest into the mantissa
+  const float2 r = __fadd2_rn(x, magic);
+  const float2 n = __fadd2_rn(r, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(make_float2(0.05517113f, 0.05517113f), f, make_float2(0.24261008f, 0.24261008f));
+  p = __ffma2_rn(p, f, make_float2(0.69326097f, 0.69326097f));
+  p = __ffma2_rn(p, f, make_float2(0.99992813f, 0.99992813f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
 
 // Offset of 16-byte chunk `chunk` of row `row` inside a K-major tile whose rows are `row_bytes` (64 or 128) wide
 // and swizzled by TMA/UMMA SWIZZLE_{row_bytes}B (atoms of 8 rows; chunk index XOR (row % 8) >> shift).

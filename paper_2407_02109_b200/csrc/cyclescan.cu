@@ -169,6 +169,42 @@ __global__ void __launch_bounds__(256) silu_gate_kernel(const __nv_bfloat16* z, 
   *reinterpret_cast<uint4*>(gz + tok * D + d0) = g;
 }
 
+// ------------------------------------------------------------------------------------------------- scan order
+// pi: scan position t -> grid token index (oracle scan_permutation; reading Q13): row-major raster,
+// column-major raster, or window-major (windows in raster order, raster inside each w x w window).
+__device__ __forceinline__ int scan_pi(int t, int H, int W, int order, int w) {
+  if (order == PSCWIN_SCAN_COL_MAJOR) {
+    const int c = t / H, r = t - c * H;
+    return r * W + c;
+  }
+  if (order == PSCWIN_SCAN_WINDOW_MAJOR) {
+    const int sx = t % w;
+    int q = t / w;
+    const int sy = q % w;
+    q /= w;
+    const int nwx = W / w;
+    const int wx = q % nwx, wy = q / nwx;
+    return (wy * w + sy) * W + wx * w + sx;
+  }
+  return t;
+}
+// Row gather (scan order <- grid order) or scatter (grid order <- scan order) of bf16 rows of D channels.
+__global__ void __launch_bounds__(256) permute_rows_kernel(const __nv_bfloat16* src, long long ld_src,
+                                                           __nv_bfloat16* dst, long long ld_dst, int B, int H, int W,
+                                                           int D, int order, int w, int scatter) {
+  pdl_trigger();
+  pdl_wait();
+  const int L = H * W, dv = D / 8;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * L * dv) return;
+  const int c = (int)(idx % dv) * 8;
+  const long long rr = idx / dv;
+  const int b = (int)(rr / L), t = (int)(rr - (long long)b * L);
+  const long long g = (long long)b * L + scan_pi(t, H, W, order, w), sq = (long long)b * L + t;
+  const long long from = scatter ? sq : g, to = scatter ? g : sq;
+  *reinterpret_cast<uint4*>(dst + to * ld_dst + c) = *reinterpret_cast<const uint4*>(src + from * ld_src + c);
+}
+
 // ------------------------------------------------------------------------------------------------- staging
 // Per-chunk token loop with cp.async double buffering: every per-token operand (the shared (delta_low, B, C)
 // row, and this CTA's slice of v, Delta, z) lands in shared memory one sub-chunk ahead of its use, so the
@@ -882,7 +918,56 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   return rc ? PSCWIN_ERR_CUDA : PSCWIN_OK;
 }
 
-size_t scan_ws_bytes(int B, int L, int D, int N, int R, int k) { return plan_scan(B, L, D, N, R, k).total; }
+// bytes of the scan-order copies (xin, z, out in scan order) a non-raster order needs in front of the scan plan
+static size_t order_ws_bytes(int B, int L, int D, int order) {
+  return order == PSCWIN_SCAN_ROW_MAJOR ? 0 : 3 * al256((size_t)B * L * D * 2);
+}
+
+size_t scan_ws_bytes(int B, int L, int D, int N, int R, int k, int order) {
+  return order_ws_bytes(B, L, D, order) + plan_scan(B, L, D, N, R, k).total;
+}
+
+static int check_order(int H, int W, int order, int window) {
+  if (order == PSCWIN_SCAN_ROW_MAJOR || order == PSCWIN_SCAN_COL_MAJOR) return PSCWIN_OK;
+  if (order != PSCWIN_SCAN_WINDOW_MAJOR) return PSCWIN_ERR_SHAPE;
+  if (window <= 0 || H % window || W % window) return PSCWIN_ERR_CONTRACT;
+  return PSCWIN_OK;
+}
+
+// run_cycle_scan in any scan order: non-raster orders gather xin / z into scan order, scan, and scatter the output
+// back to grid order (the recurrence itself is order-agnostic).
+static int run_cycle_scan_ordered(int B, int H, int W, int order, int window, int D, int N, int R, int k, int bbar,
+                                  const __nv_bfloat16* xin, long long ld_x, const __nv_bfloat16* z, long long ld_z,
+                                  bool z_gated, const float* conv_w, const float* conv_b, const void* w_x,
+                                  const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip,
+                                  __nv_bfloat16* out, long long ld_out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const int L = H * W;
+  if (order == PSCWIN_SCAN_ROW_MAJOR)
+    return run_cycle_scan(B, L, D, N, R, k, bbar, xin, ld_x, z, ld_z, z_gated, conv_w, conv_b, w_x, w_dt, b_dt, a_log,
+                          d_skip, out, ld_out, ws, ws_bytes, s);
+  const size_t pre = order_ws_bytes(B, L, D, order), one = pre / 3;
+  if (ws_bytes < pre) return PSCWIN_ERR_WORKSPACE;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(base);
+  __nv_bfloat16* zs = reinterpret_cast<__nv_bfloat16*>(base + one);
+  __nv_bfloat16* os = reinterpret_cast<__nv_bfloat16*>(base + 2 * one);
+  const long long n = (long long)B * L * (D / 8);
+  const dim3 grid((unsigned)((n + 255) / 256));
+  {
+    PSCWIN_PROF("scan_order_gather", s);
+    launch_k(permute_rows_kernel, grid, dim3(256), 0, s, xin, ld_x, xs, (long long)D, B, H, W, D, order, window, 0);
+    if (z) launch_k(permute_rows_kernel, grid, dim3(256), 0, s, z, ld_z, zs, (long long)D, B, H, W, D, order, window, 0);
+  }
+  int rc = run_cycle_scan(B, L, D, N, R, k, bbar, xs, D, z ? zs : nullptr, D, z_gated, conv_w, conv_b, w_x, w_dt, b_dt,
+                          a_log, d_skip, os, D, base + pre, ws_bytes - pre, s);
+  if (rc) return rc;
+  {
+    PSCWIN_PROF("scan_order_scatter", s);
+    launch_k(permute_rows_kernel, grid, dim3(256), 0, s, (const __nv_bfloat16*)os, (long long)D, out, ld_out, B, H, W,
+             D, order, window, 1);
+  }
+  return cudaGetLastError() == cudaSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA;
+}
 
 int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, void* x_out, void* ws, size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s) {
@@ -891,11 +976,12 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   if (!w->lns_g || !w->lns_b || !w->w_in || !w->conv_w || !w->conv_b || !w->w_x || !w->w_dt || !w->b_dt ||
       !w->a_log || !w->d_skip || !w->w_out)
     return PSCWIN_ERR_SHAPE;
-  if (d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_UNSUPPORTED;
   const int C = d->C, D = d->ssm_expand * C, N = d->ssm_state;
   const int R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (C + 15) / 16;
   const int L = d->H * d->W;
   int rc = check_scan(d->B, L, D, N, R, d->ssm_conv);
+  if (rc) return rc;
+  rc = check_order(d->H, d->W, d->scan_order, d->window);
   if (rc) return rc;
   const long long T = (long long)d->B * L;
   uint8_t* base = reinterpret_cast<uint8_t*>(ws);
@@ -920,7 +1006,8 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   rc = launch_gemm_bf16(u, w->w_in, a, s);
   if (rc) return PSCWIN_ERR_CUDA;
   // a2: cycle scan -> g = sum over copies of y * SiLU(z)
-  rc = run_cycle_scan(d->B, L, D, N, R, d->ssm_conv, d->bbar_mode, xz, 2 * D, xz + D, 2 * D, true,
+  rc = run_cycle_scan_ordered(d->B, d->H, d->W, d->scan_order, d->window, D, N, R, d->ssm_conv, d->bbar_mode, xz,
+                              2 * D, xz + D, 2 * D, true,
                       (const float*)w->conv_w, (const float*)w->conv_b, w->w_x, (const float*)w->w_dt,
                       (const float*)w->b_dt, w->a_log, w->d_skip, g, D, base + off_scan, scan_bytes, s);
   if (rc) return rc;
@@ -949,7 +1036,8 @@ extern "C" size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* d) {
   if (!d) return 0;
   const int L = d->H * d->W;
   if (check_scan(d->B, L, d->D, d->N, d->R, d->conv_k) != PSCWIN_OK) return 0;
-  return scan_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k);
+  if (check_order(d->H, d->W, d->scan_order, d->window) != PSCWIN_OK) return 0;
+  return scan_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k, d->scan_order);
 }
 
 extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, const void* z, const float* conv_w,
@@ -959,12 +1047,14 @@ extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, con
   if (!d || !xin || !conv_w || !conv_b || !w_x || !w_dt || !b_dt || !a_log || !d_skip || !out)
     return PSCWIN_ERR_SHAPE;
   if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
-  if (d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_UNSUPPORTED;
   const int L = d->H * d->W;
   int rc = check_scan(d->B, L, d->D, d->N, d->R, d->conv_k);
   if (rc) return rc;
+  rc = check_order(d->H, d->W, d->scan_order, d->window);
+  if (rc) return rc;
   if (((uintptr_t)xin | (uintptr_t)z | (uintptr_t)out | (uintptr_t)ws | (uintptr_t)w_x) & 15) return PSCWIN_ERR_ALIGN;
-  return run_cycle_scan(d->B, L, d->D, d->N, d->R, d->conv_k, d->bbar_mode, (const __nv_bfloat16*)xin, d->D,
-                        (const __nv_bfloat16*)z, d->D, false, conv_w, conv_b, w_x, w_dt, b_dt, a_log, d_skip,
+  return run_cycle_scan_ordered(d->B, d->H, d->W, d->scan_order, d->window, d->D, d->N, d->R, d->conv_k,
+                                d->bbar_mode, (const __nv_bfloat16*)xin, d->D, (const __nv_bfloat16*)z, d->D, false,
+                                conv_w, conv_b, w_x, w_dt, b_dt, a_log, d_skip,
                         (__nv_bfloat16*)out, d->D, ws, ws_bytes, (cudaStream_t)stream);
 }

@@ -29,7 +29,7 @@ def _scan_inputs(cfg, seed=3):
 def _desc(pl, cfg):
     sd = pl.ScanDesc()
     sd.B, sd.H, sd.W, sd.D, sd.N, sd.R, sd.conv_k = cfg.B, cfg.H, cfg.W, cfg.D, cfg.N, cfg.R, cfg.ssm_conv
-    sd.scan_order, sd.bbar_mode, sd.dtype = cfg.scan_order, cfg.bbar_mode, 0
+    sd.scan_order, sd.bbar_mode, sd.dtype, sd.window = cfg.scan_order, cfg.bbar_mode, 0, cfg.window
     return sd
 
 
@@ -50,8 +50,34 @@ def test_cycle_scan(pl, cfg):
     w = synth.make_weights(cfg)
     dw = dev_weights(w, cfg)
     got = host(pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dw))
-    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W, bbar_mode=cfg.bbar_mode)
+    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W, scan_order=cfg.scan_order, bbar_mode=cfg.bbar_mode,
+                            window=cfg.window)
     assert rel_err(got, ref) < BF16_TOL
+
+
+ORDER_CASES = [synth.tiny(scan_order=synth.SCAN_COL_MAJOR), synth.tiny(scan_order=synth.SCAN_WINDOW_MAJOR),
+               synth.tiny(B=2, H=16, W=24, scan_order=synth.SCAN_WINDOW_MAJOR),
+               synth.tiny(H=10, W=13, scan_order=synth.SCAN_COL_MAJOR)]
+
+
+@pytest.mark.parametrize("cfg", ORDER_CASES, ids=lambda c: f"B{c.B}L{c.H}x{c.W}o{c.scan_order}")
+def test_cycle_scan_orders(pl, cfg):
+    # the recurrence walks the tokens in scan order (reading Q13); inputs / outputs stay in grid order
+    xin, z = _scan_inputs(cfg)
+    w = synth.make_weights(cfg)
+    got = host(pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(w, cfg)))
+    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W, scan_order=cfg.scan_order, window=cfg.window)
+    assert rel_err(got, ref) < BF16_TOL
+    ref_raster = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W)
+    assert rel_err(ref_raster, ref) > 10 * BF16_TOL  # the order matters: the test would see a wrong walk
+
+
+def test_window_major_needs_divisible_grid(pl):
+    from paper_2407_02109_b200._lib import PscwinError
+    cfg = synth.tiny(H=10, W=13, scan_order=synth.SCAN_WINDOW_MAJOR)
+    xin, z = _scan_inputs(cfg)
+    with pytest.raises(PscwinError):
+        pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(synth.make_weights(cfg), cfg))
 
 
 def test_cycle_scan_no_gate(pl):
@@ -109,10 +135,12 @@ def test_stack_graph_replay_equals_eager(pl):
 
 
 CS_LAYERS = [synth.tiny(cycle_scan=1, shift_x=0, shift_y=0), synth.tiny(cycle_scan=1),
+             synth.tiny(cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR),
+             synth.tiny(cycle_scan=1, shift_x=0, shift_y=0, scan_order=synth.SCAN_COL_MAJOR),
              synth.vitb(64, cycle_scan=1, shift_x=0, shift_y=0)]
 
 
-@pytest.mark.parametrize("cfg", CS_LAYERS, ids=lambda c: f"{c.H}C{c.C}s{c.shift_x}")
+@pytest.mark.parametrize("cfg", CS_LAYERS, ids=lambda c: f"{c.H}C{c.C}s{c.shift_x}o{c.scan_order}")
 def test_cycle_scan_layer_forward(pl, cfg):
     x, w = synth.make_input(cfg), synth.make_weights(cfg)
     layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))
