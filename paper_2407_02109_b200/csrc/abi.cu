@@ -107,8 +107,9 @@ int check_layer(const pscwin_layer_desc* d) {
   if (rc) return rc;
   const int dh = d->C / d->heads;
   if (d->rope && dh % 4) return PSCWIN_ERR_CONTRACT;
-  if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->dtype != PSCWIN_BF16 && d->dtype != PSCWIN_F32) return PSCWIN_ERR_UNSUPPORTED;
   if (!(dh == 32 || dh == 64)) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->dtype == PSCWIN_F32 && d->window > 16) return PSCWIN_ERR_UNSUPPORTED;  // f32 window lives in smem
   if (d->window < 4 || d->window > 64 || (d->window & (d->window - 1))) return PSCWIN_ERR_UNSUPPORTED;
   if (d->pad_mode != PSCWIN_PAD_LEARNABLE && d->pad_mode != PSCWIN_PAD_MASKED) return PSCWIN_ERR_CONTRACT;
   if (d->C % 64) return PSCWIN_ERR_UNSUPPORTED;  // GEMM K tiles
@@ -328,6 +329,7 @@ int pscwin_linear(const void* A, int64_t M, int32_t K, const void* Wt, int32_t N
 
 size_t pscwin_workspace_bytes(const pscwin_layer_desc* d) {
   if (check_layer(d) != PSCWIN_OK) return 0;
+  if (d->dtype == PSCWIN_F32) return layer_f32_ws_bytes(d);
   return plan_layer(d).total;
 }
 
@@ -336,6 +338,12 @@ int pscwin_qkv_project(const pscwin_layer_desc* d, const pscwin_layer_weights* w
   int rc = check_layer(d);
   if (rc) return rc;
   if (!wt || !x || !qkv || !wt->w_qkv || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv) return PSCWIN_ERR_SHAPE;
+  if (d->dtype == PSCWIN_F32) {
+    if (!ws || ws_bytes < layer_f32_ws_bytes(d)) return PSCWIN_ERR_WORKSPACE;
+    if (!aligned16(x) || !aligned16(qkv) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+    float* u = reinterpret_cast<float*>(wsp(ws, plan_layer_f32(d).u));
+    return qkv_project_f32(d, wt, (const float*)x, (float*)qkv, qkv_pad, u, (cudaStream_t)stream);
+  }
   LayerWs L = plan_layer(d);
   if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
   if (!aligned16(x) || !aligned16(qkv) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
@@ -349,6 +357,10 @@ int pscwin_window_attention(const pscwin_layer_desc* d, const void* qkv, const f
   if (!qkv || !O) return PSCWIN_ERR_SHAPE;
   const bool shifted = d->shift_x || d->shift_y;
   if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !qkv_pad) return PSCWIN_ERR_CONTRACT;
+  if (d->dtype == PSCWIN_F32) {
+    if (!aligned16(qkv) || !aligned16(O)) return PSCWIN_ERR_ALIGN;
+    return launch_attention_f32(d, (const float*)qkv, qkv_pad, (float*)O, (cudaStream_t)stream);
+  }
   LayerWs L = plan_layer(d);
   if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
   if (!aligned16(qkv) || !aligned16(O) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
@@ -363,6 +375,10 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   const bool shifted = d->shift_x || d->shift_y;
   if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !wt->pad) return PSCWIN_ERR_CONTRACT;
   if (!wt->w_qkv || !wt->w_o || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  if (d->dtype == PSCWIN_F32) {
+    if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+    return forward_f32(d, wt, x_in, x_out, ws, ws_bytes, (cudaStream_t)stream);
+  }
   LayerWs L = plan_layer(d);
   if (!ws || ws_bytes < L.total) return PSCWIN_ERR_WORKSPACE;
   if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;

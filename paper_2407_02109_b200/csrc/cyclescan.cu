@@ -1037,6 +1037,7 @@ extern "C" size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* d) {
   const int L = d->H * d->W;
   if (check_scan(d->B, L, d->D, d->N, d->R, d->conv_k) != PSCWIN_OK) return 0;
   if (check_order(d->H, d->W, d->scan_order, d->window) != PSCWIN_OK) return 0;
+  if (d->dtype == PSCWIN_F32) return scan_f32_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k);
   return scan_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k, d->scan_order);
 }
 
@@ -1046,12 +1047,19 @@ extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, con
                                  void* stream) {
   if (!d || !xin || !conv_w || !conv_b || !w_x || !w_dt || !b_dt || !a_log || !d_skip || !out)
     return PSCWIN_ERR_SHAPE;
-  if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->dtype != PSCWIN_BF16 && d->dtype != PSCWIN_F32) return PSCWIN_ERR_UNSUPPORTED;
   const int L = d->H * d->W;
   int rc = check_scan(d->B, L, d->D, d->N, d->R, d->conv_k);
   if (rc) return rc;
   rc = check_order(d->H, d->W, d->scan_order, d->window);
   if (rc) return rc;
+  if (d->dtype == PSCWIN_F32) {
+    if (((uintptr_t)xin | (uintptr_t)z | (uintptr_t)out | (uintptr_t)ws | (uintptr_t)w_x) & 15) return PSCWIN_ERR_ALIGN;
+    return run_cycle_scan_f32(d->B, d->H, d->W, d->scan_order, d->window, d->D, d->N, d->R, d->conv_k, d->bbar_mode,
+                              (const float*)xin, d->D, (const float*)z, d->D, false, conv_w, conv_b,
+                              (const float*)w_x, w_dt, b_dt, a_log, d_skip, (float*)out, d->D, ws, ws_bytes,
+                              (cudaStream_t)stream);
+  }
   if (((uintptr_t)xin | (uintptr_t)z | (uintptr_t)out | (uintptr_t)ws | (uintptr_t)w_x) & 15) return PSCWIN_ERR_ALIGN;
   return run_cycle_scan_ordered(d->B, d->H, d->W, d->scan_order, d->window, d->D, d->N, d->R, d->conv_k,
                                 d->bbar_mode, (const __nv_bfloat16*)xin, d->D, (const __nv_bfloat16*)z, d->D, false,

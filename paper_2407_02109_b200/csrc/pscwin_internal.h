@@ -5,6 +5,7 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "../../include/pscwin.h"
 #include "launch.h"
 #include "prof.h"
 
@@ -70,6 +71,24 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
 
 
 namespace pscwin {
+// fp32 correctness path (f32path.cu)
+struct LayerWsF32 {
+  size_t u, qkv, qkv_pad, O, xz, g, scan, x1, total;
+};
+LayerWsF32 plan_layer_f32(const pscwin_layer_desc* d);
+size_t layer_f32_ws_bytes(const pscwin_layer_desc* d);
+size_t scan_f32_ws_bytes(int B, int L, int D, int N, int R, int k);
+int forward_f32(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x_in, void* x_out, void* ws,
+                size_t ws_bytes, cudaStream_t s);
+int qkv_project_f32(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const float* x, float* qkv,
+                    float* qkv_pad, float* u, cudaStream_t s);
+int launch_attention_f32(const pscwin_layer_desc* d, const float* qkv, const float* qkv_pad, float* out,
+                         cudaStream_t s);
+int run_cycle_scan_f32(int B, int H, int W, int order, int window, int D, int N, int R, int k, int bbar,
+                       const float* xin, long long ld_x, const float* z, long long ld_z, bool z_gated,
+                       const float* conv_w, const float* conv_b, const float* w_x, const float* w_dt,
+                       const float* b_dt, const float* a_log, const float* d_skip, float* out, long long ld_out,
+                       void* ws, size_t ws_bytes, cudaStream_t s);
 // cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
 int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);

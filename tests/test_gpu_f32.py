@@ -1,0 +1,101 @@
+"""GPU parity of the fp32 correctness path (dtype PSCWIN_F32) against the fp64 oracle at the north star's fp32
+tolerance, max |g - o| / max |o| <= 1e-4. Every step of this path runs in fp32 on the
+GPU (f32path.cu), including a literal 3L recurrence for the cycle scan."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from gpu_util import F32_TOL, dev, dev_weights, host, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2407_02109_b200 as p
+    return p
+
+
+def f32(**kw):
+    return synth.tiny(dtype="f32", **kw)
+
+
+LAYERS = [
+    f32(shift_x=0, shift_y=0),                                     # P
+    f32(),                                                         # S, learnable pad
+    f32(pad_mode=synth.PAD_MASKED),                                # S, masked pad
+    f32(shift_x=3, shift_y=5),                                     # asymmetric shift
+    f32(H=12, W=20, shift_x=2, shift_y=6),                         # ragged grid
+    f32(rope=0),
+    f32(B=2, window=16, shift_x=0, shift_y=0),                     # P1: window = grid (global attention)
+    f32(C=128, heads=2, shift_x=0, shift_y=0),                     # d = 64
+    f32(cycle_scan=1, shift_x=0, shift_y=0),                       # CS + P
+    f32(cycle_scan=1),                                             # CS + S
+    f32(cycle_scan=1, bbar_mode=synth.BBAR_EULER),
+    f32(cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR),
+    f32(cycle_scan=1, scan_order=synth.SCAN_COL_MAJOR, H=12, W=8, shift_x=0, shift_y=0, window=4),
+]
+
+
+@pytest.mark.parametrize("cfg", LAYERS, ids=lambda c: f"B{c.B}{c.H}x{c.W}C{c.C}w{c.window}s{c.shift_x},{c.shift_y}"
+                                                      f"m{c.pad_mode}r{c.rope}cs{c.cycle_scan}o{c.scan_order}b{c.bbar_mode}")
+def test_forward_f32(pl, cfg):
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))
+    got = host(layer(dev(x, "f32")))
+    ref = oracle.pscwin_layer(x, w, cfg)
+    assert rel_err(got, ref) < F32_TOL
+
+
+def test_forward_f32_vitb_mid(pl):
+    # ViT-B widths (C = 768, 12 heads, N = 32, R = 48) on a 16 x 16 grid, shifted + cycle scan
+    cfg = synth.vitb(16, dtype="f32", cycle_scan=1)
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    got = host(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))(dev(x, "f32")))
+    assert rel_err(got, oracle.pscwin_layer(x, w, cfg)) < F32_TOL
+
+
+def test_window_attention_f32_peaky(pl):
+    # near one-hot softmax (W_q scaled by 8, §8(d) "peaky" variant) through the attention entry point alone
+    cfg = f32()
+    w = synth.make_weights(cfg)
+    w = dict(w, w_qkv=np.concatenate([8 * w["w_qkv"][:cfg.C], w["w_qkv"][cfg.C:]]))
+    qkv = oracle.layer_norm(synth.make_input(cfg), w["ln1_g"], w["ln1_b"], cfg.ln_eps) @ w["w_qkv"].T + w["b_qkv"]
+    qkv_r = qkv.copy()
+    X, Y = np.meshgrid(np.arange(cfg.W), np.arange(cfg.H))
+    g = qkv_r.reshape(cfg.B, cfg.H, cfg.W, 3, cfg.heads, cfg.d_head)
+    g[:, :, :, 0] = oracle.rope_2d(g[:, :, :, 0], X[None, :, :, None], Y[None, :, :, None])
+    g[:, :, :, 1] = oracle.rope_2d(g[:, :, :, 1], X[None, :, :, None], Y[None, :, :, None])
+    qkv_p = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
+    import torch
+    d = pl.LayerDesc.from_config(cfg)
+    out = torch.empty(cfg.B, cfg.H, cfg.W, cfg.C, device="cuda")
+    got = host(pl.window_attention(d, dev(qkv_r, "f32"), dev(qkv_p, "f32"), out=out))
+    ref = oracle.attention_core_padded(qkv, qkv_p, cfg.H, cfg.W, cfg.heads, cfg.window, cfg.shift_x, cfg.shift_y,
+                                       cfg.pad_mode, cfg.rope)
+    assert rel_err(got, ref) < F32_TOL
+
+
+def _scan_desc(pl, cfg):
+    sd = pl.ScanDesc()
+    sd.B, sd.H, sd.W, sd.D, sd.N, sd.R, sd.conv_k = cfg.B, cfg.H, cfg.W, cfg.D, cfg.N, cfg.R, cfg.ssm_conv
+    sd.scan_order, sd.bbar_mode, sd.dtype, sd.window = cfg.scan_order, cfg.bbar_mode, 1, cfg.window
+    return sd
+
+
+@pytest.mark.parametrize("cfg", [f32(), f32(H=10, W=13), f32(B=2, H=4, W=6), f32(H=1, W=3),
+                                 f32(C=128, ssm_state=64, ssm_dt_rank=8, H=8, W=8)],
+                         ids=lambda c: f"B{c.B}L{c.H}x{c.W}D{c.D}N{c.N}")
+def test_cycle_scan_f32(pl, cfg):
+    B, L, D = cfg.B, cfg.L, cfg.D
+    xin = 0.6 * synth.normal(synth.stream_seed(3, 1), B * L * D).reshape(B, L, D)
+    z = synth.normal(synth.stream_seed(3, 2), B * L * D).reshape(B, L, D)
+    xin, z = synth.round_f32(xin), synth.round_f32(z)
+    w = synth.make_weights(cfg)
+    got = host(pl.cycle_scan(_scan_desc(pl, cfg), dev(xin, "f32"), dev(z, "f32"), dev_weights(w, cfg)))
+    ref = oracle.cycle_scan(xin, z, w, cfg.H, cfg.W)
+    assert rel_err(got, ref) < F32_TOL
