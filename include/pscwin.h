@@ -157,6 +157,48 @@ size_t pscwin_workspace_bytes(const pscwin_layer_desc* desc);
 int pscwin_forward(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
                    void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------- row bands (multi-GPU, §8(e)) */
+/* Window-row sharding of ONE image (B = 1) over `world` ranks, one band of token rows per rank (SURVEY §8(e),
+ * config 4; cycle-scan carries per SURVEY Appendix A). row_begin / row_end are multiples of the window (the
+ * last band ends at H); rank 0 starts at row 0, rank world-1 ends at H. Token-local steps run on the band.
+ * The caller moves three kinds of bytes between ranks between the phase calls (NCCL over NVLink; every offset
+ * below is relative to the workspace, all buffers device memory):
+ *   conv history (cycle-scan layers, ring): hist_send of rank g -> hist_recv of rank (g+1) mod world;
+ *   scan records (cycle-scan layers): all-gather rec_send of every rank into rec_recv, rank order;
+ *   QKV halo (shifted layers): send_prev of rank g -> recv_next of rank g-1, send_next of g -> recv_prev of g+1
+ *     (pt = (w - shift_y) mod w rows from above, w - pt from below; sizes 0 at the image edges).
+ * Phase order: [cycle-scan layer: scan_begin, ring(hist), scan_mid, allgather(rec), scan_end]
+ *              attn_begin, halo exchange, attn_end.
+ * x_band, x_out [rows, W, C] bf16 (x_out may not alias x_band). Results equal pscwin_forward on the whole
+ * image up to fp32 summation order in the scan (bit-identical elsewhere). bf16 only; scan_order ROW_MAJOR only
+ * (other orders do not give contiguous segments: ERR_CONTRACT). Workspace: pscwin_band_workspace_bytes. */
+typedef struct {
+  int32_t row_begin, row_end;  /* this rank's token rows [row_begin, row_end) */
+  int32_t rank, world;
+} pscwin_band;
+typedef struct {
+  uint64_t hist_send, hist_recv, hist_bytes;      /* conv history (k-1 xin rows of D bf16)                 */
+  uint64_t rec_send, rec_recv, rec_bytes;         /* scan record; rec_recv holds world x rec_bytes           */
+  uint64_t send_prev, send_prev_bytes, send_next, send_next_bytes;  /* QKV halo rows to the neighbours     */
+  uint64_t recv_prev, recv_prev_bytes, recv_next, recv_next_bytes;  /* QKV halo rows from the neighbours   */
+} pscwin_band_io;
+size_t pscwin_band_workspace_bytes(const pscwin_layer_desc* global_desc, const pscwin_band* band);
+int pscwin_band_io_offsets(const pscwin_layer_desc* global_desc, const pscwin_band* band, pscwin_band_io* io);
+int pscwin_band_scan_begin(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                           const pscwin_layer_weights* wts, const void* x_band, void* workspace, size_t ws_bytes,
+                           void* stream);
+int pscwin_band_scan_mid(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                         const pscwin_layer_weights* wts, void* workspace, size_t ws_bytes, void* stream);
+int pscwin_band_scan_end(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                         const pscwin_layer_weights* wts, const void* x_band, void* workspace, size_t ws_bytes,
+                         void* stream);
+int pscwin_band_attn_begin(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                           const pscwin_layer_weights* wts, const void* x_band, void* workspace, size_t ws_bytes,
+                           void* stream);
+int pscwin_band_attn_end(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                         const pscwin_layer_weights* wts, const void* x_band, void* x_out, void* workspace,
+                         size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this library since it was loaded (every launcher counts itself). */
 int64_t pscwin_launch_count(void);

@@ -26,6 +26,8 @@ EXPORTS = [
     "pscwin_layer_norm", "pscwin_linear", "pscwin_qkv_project", "pscwin_window_attention", "pscwin_cycle_scan",
     "pscwin_scan_workspace_bytes", "pscwin_workspace_bytes", "pscwin_forward",
     "pscwin_launch_count", "pscwin_profile_enable", "pscwin_profile_read",
+    "pscwin_band_workspace_bytes", "pscwin_band_io_offsets", "pscwin_band_scan_begin", "pscwin_band_scan_mid",
+    "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
 ]
 
 
@@ -74,6 +76,19 @@ class ScanDesc(ctypes.Structure):
                                               "dtype", "window")]
 
 
+class BandDesc(ctypes.Structure):
+    """pscwin_band: this rank's token rows [row_begin, row_end) of one image split over `world` ranks."""
+    _fields_ = [(n, ctypes.c_int32) for n in ("row_begin", "row_end", "rank", "world")]
+
+
+class BandIO(ctypes.Structure):
+    """pscwin_band_io: workspace byte offsets / sizes of the buffers the ranks exchange."""
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "hist_send", "hist_recv", "hist_bytes", "rec_send", "rec_recv", "rec_bytes",
+        "send_prev", "send_prev_bytes", "send_next", "send_next_bytes",
+        "recv_prev", "recv_prev_bytes", "recv_next", "recv_next_bytes")]
+
+
 _LIB: Optional[ctypes.CDLL] = None
 
 
@@ -105,6 +120,19 @@ def lib() -> ctypes.CDLL:
         "pscwin_workspace_bytes": ([ctypes.POINTER(LayerDesc)], sz),
         "pscwin_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
                            ctypes.c_int),
+        "pscwin_band_workspace_bytes": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc)], sz),
+        "pscwin_band_io_offsets": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(BandIO)],
+                                   ctypes.c_int),
+        "pscwin_band_scan_begin": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                    vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_band_scan_mid": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                  vp, sz, vp], ctypes.c_int),
+        "pscwin_band_scan_end": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                  vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_band_attn_begin": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                    vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_band_attn_end": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                  vp, vp, vp, sz, vp], ctypes.c_int),
         "pscwin_launch_count": ([], ctypes.c_int64),
         "pscwin_profile_enable": ([ctypes.c_int], None),
         "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],

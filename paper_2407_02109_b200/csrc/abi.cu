@@ -209,6 +209,7 @@ int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv
   a.sy = d->shift_y;
   a.pad_mode = d->pad_mode;
   a.rope = d->rope;
+  a.row0 = 0;
   a.qkv = qkv;
   a.qkv_pad = qkv_pad;
   a.out = O;
@@ -414,6 +415,326 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   a.residual = x;
   a.ldr = C;
   return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
+}
+
+}  // extern "C"
+
+// =================================================================================================== row bands
+// Window-row sharding of one image over `world` ranks. Rank g owns token rows
+// [row_begin, row_end) (multiples of the window). Token-local steps run on the band; the shifted windows that
+// straddle a band edge need the neighbours' QKV rows (halo: pt rows above, w - pt below, pt = (w - s_y) mod w);
+// the cycle scan needs the previous rank's last k-1 xin rows (conv history, a ring) and one all-gather of the
+// per-rank segment records. The caller moves those bytes (NCCL) between the
+// phase calls; every byte offset is relative to the workspace and reported by pscwin_band_io_offsets.
+namespace {
+struct BandGeo {
+  int r0, r1, rows, ht, hb, ht_eff, hb_eff, e0, ext_rows, sy_local, P;
+  bool ok;
+};
+
+BandGeo band_geo(const pscwin_layer_desc* d, const pscwin_band* b) {
+  BandGeo g;
+  g.ok = false;
+  const int w = d->window;
+  if (!b || b->world < 1 || b->rank < 0 || b->rank >= b->world) return g;
+  if (d->B != 1) return g;  // one image per band group
+  g.r0 = b->row_begin;
+  g.r1 = b->row_end;
+  if (g.r0 < 0 || g.r1 > d->H || g.r1 <= g.r0 || g.r0 % w || (g.r1 % w && g.r1 != d->H)) return g;
+  if ((b->rank == 0) != (g.r0 == 0) || (b->rank == b->world - 1) != (g.r1 == d->H)) return g;
+  g.rows = g.r1 - g.r0;
+  const int pt = (w - d->shift_y) % w;
+  g.ht = pt;
+  g.hb = pt ? w - pt : 0;
+  g.ht_eff = b->rank > 0 ? g.ht : 0;
+  g.hb_eff = b->rank < b->world - 1 ? g.hb : 0;
+  g.e0 = g.r0 - g.ht_eff;
+  g.ext_rows = g.ht_eff + g.rows + g.hb_eff;
+  // the extended buffer's window grid must coincide with the global one: local pad_top = (pt + e0) mod w
+  const int pt_local = ((pt + g.e0) % w + w) % w;
+  g.sy_local = (w - pt_local) % w;
+  g.P = b->rank == 0 ? d->ssm_conv - 1 : 0;
+  if (g.rows * d->W < d->ssm_conv - 1) return g;
+  g.ok = true;
+  return g;
+}
+
+pscwin_layer_desc sub_desc(const pscwin_layer_desc* d, int rows, int sy) {
+  pscwin_layer_desc s = *d;
+  s.H = rows;
+  s.shift_y = sy;
+  return s;
+}
+
+struct BandWs {
+  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, x1, hist_send, hist_recv, rec_send, rec_recv, scan, total;
+  size_t row_bytes_qkv;
+  int D, N, R;
+};
+
+BandWs plan_band(const pscwin_layer_desc* d, const pscwin_band* b, const BandGeo& g) {
+  BandWs w;
+  memset(&w, 0, sizeof(w));
+  const size_t Wd = d->W, C = d->C;
+  const size_t T = (size_t)g.rows * Wd, Te = (size_t)g.ext_rows * Wd;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.row_bytes_qkv = Wd * 3 * C * 2;
+  w.u = take(T * C * 2);
+  w.qkv = take(Te * 3 * C * 2);
+  w.qkv_pad = take(3 * C * 4);
+  w.O = take(Te * C * 2);
+  w.pad_tab = take(attn_pad_table_bytes(g.ext_rows, d->W, d->C, d->window));
+  if (d->cycle_scan) {
+    w.D = d->ssm_expand * d->C;
+    w.N = d->ssm_state;
+    w.R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (d->C + 15) / 16;
+    const int k = d->ssm_conv;
+    w.xz = take(T * 2 * w.D * 2);
+    w.g = take(T * w.D * 2);
+    w.x1 = take(T * C * 2);
+    w.hist_send = take((size_t)(k - 1) * w.D * 2);
+    w.hist_recv = take((size_t)(k - 1) * w.D * 2);
+    w.rec_send = take(band_scan_record_bytes(w.D, w.N));
+    w.rec_recv = take((size_t)b->world * band_scan_record_bytes(w.D, w.N));
+    w.scan = take(band_scan_ws_bytes((int)T, w.D, w.N, w.R, k, g.P));
+  }
+  w.total = off;
+  return w;
+}
+
+int band_check(const pscwin_layer_desc* d, const pscwin_band* b, BandGeo* g) {
+  int rc = check_layer(d);
+  if (rc) return rc;
+  if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;  // bands run the bf16 product path
+  if (d->cycle_scan && d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_CONTRACT;  // contiguous segments
+  *g = band_geo(d, b);
+  return g->ok ? PSCWIN_OK : PSCWIN_ERR_CONTRACT;
+}
+}  // namespace
+
+extern "C" {
+
+size_t pscwin_band_workspace_bytes(const pscwin_layer_desc* d, const pscwin_band* b) {
+  BandGeo g;
+  if (band_check(d, b, &g)) return 0;
+  return plan_band(d, b, g).total;
+}
+
+int pscwin_band_io_offsets(const pscwin_layer_desc* d, const pscwin_band* b, pscwin_band_io* io) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!io) return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  memset(io, 0, sizeof(*io));
+  if (d->cycle_scan) {
+    io->hist_send = w.hist_send;
+    io->hist_recv = w.hist_recv;
+    io->hist_bytes = (uint64_t)(d->ssm_conv - 1) * w.D * 2;
+    io->rec_send = w.rec_send;
+    io->rec_recv = w.rec_recv;
+    io->rec_bytes = band_scan_record_bytes(w.D, w.N);
+  }
+  const uint64_t rb = w.row_bytes_qkv;
+  io->send_prev = w.qkv + (uint64_t)g.ht_eff * rb;                          // own first hb rows
+  io->send_prev_bytes = b->rank > 0 ? (uint64_t)g.hb * rb : 0;
+  io->send_next = w.qkv + (uint64_t)(g.ht_eff + g.rows - g.ht) * rb;        // own last ht rows
+  io->send_next_bytes = b->rank < b->world - 1 ? (uint64_t)g.ht * rb : 0;
+  io->recv_prev = w.qkv;                                                     // top halo
+  io->recv_prev_bytes = (uint64_t)g.ht_eff * rb;
+  io->recv_next = w.qkv + (uint64_t)(g.ht_eff + g.rows) * rb;               // bottom halo
+  io->recv_next_bytes = (uint64_t)g.hb_eff * rb;
+  return PSCWIN_OK;
+}
+
+int pscwin_band_scan_begin(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                           const void* x_band, void* ws, size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!d->cycle_scan || !wt || !x_band || !wt->lns_g || !wt->lns_b || !wt->w_in) return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_band) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)g.rows * d->W;
+  const int C = d->C, D = w.D, k = d->ssm_conv;
+  void* u = wsp(ws, w.u);
+  __nv_bfloat16* xz = reinterpret_cast<__nv_bfloat16*>(wsp(ws, w.xz));
+  rc = launch_layer_norm(x_band, T, C, (const float*)wt->lns_g, (const float*)wt->lns_b, d->ln_eps, 0, u, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_in_proj";
+  a.M = (int)T;
+  a.N = 2 * D;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = xz;
+  a.ldo = 2 * D;
+  a.epi = EPI_STORE_BF16;
+  a.silu_col = D;
+  if (launch_gemm_bf16(u, wt->w_in, a, s)) return PSCWIN_ERR_CUDA;
+  // conv history for the next rank: this band's last k-1 xin rows
+  if (k > 1 && cudaMemcpy2DAsync(wsp(ws, w.hist_send), (size_t)D * 2, xz + (T - (k - 1)) * 2 * D, (size_t)2 * D * 2,
+                                 (size_t)D * 2, k - 1, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return PSCWIN_ERR_CUDA;
+  return PSCWIN_OK;
+}
+
+int pscwin_band_scan_mid(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt, void* ws,
+                         size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!d->cycle_scan || !wt || !wt->conv_w || !wt->conv_b || !wt->w_x || !wt->w_dt || !wt->b_dt || !wt->a_log)
+    return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  const long long T = (long long)g.rows * d->W;
+  const __nv_bfloat16* xz = reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.xz));
+  return band_scan_mid((int)T, w.D, w.N, w.R, d->ssm_conv, g.P, d->bbar_mode, xz, 2 * w.D,
+                       reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.hist_recv)), (const float*)wt->conv_w,
+                       (const float*)wt->conv_b, wt->w_x, (const float*)wt->w_dt, (const float*)wt->b_dt, wt->a_log,
+                       wt->d_skip, reinterpret_cast<float*>(wsp(ws, w.rec_send)), wsp(ws, w.scan), w.total - w.scan,
+                       (cudaStream_t)stream);
+}
+
+int pscwin_band_scan_end(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                         const void* x_band, void* ws, size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!d->cycle_scan || !wt || !x_band || !wt->d_skip || !wt->w_out) return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)g.rows * d->W;
+  const int C = d->C, D = w.D;
+  const __nv_bfloat16* xz = reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.xz));
+  __nv_bfloat16* gb = reinterpret_cast<__nv_bfloat16*>(wsp(ws, w.g));
+  rc = band_scan_end((int)T, D, w.N, w.R, d->ssm_conv, g.P, d->bbar_mode, xz, 2 * D, xz + D, 2 * D,
+                     (const float*)wt->conv_w, (const float*)wt->conv_b, (const float*)wt->w_dt,
+                     (const float*)wt->b_dt, wt->a_log, wt->d_skip, reinterpret_cast<const float*>(wsp(ws, w.rec_recv)),
+                     b->rank, b->world, gb, D, wsp(ws, w.scan), w.total - w.scan, s);
+  if (rc) return rc;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_out_proj_scan";
+  a.M = (int)T;
+  a.N = C;
+  a.K = D;
+  a.lda = D;
+  a.ldb = D;
+  a.out = wsp(ws, w.x1);
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.residual = x_band;
+  a.ldr = C;
+  return launch_gemm_bf16(gb, wt->w_out, a, s) ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
+int pscwin_band_attn_begin(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                           const void* x_band, void* ws, size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!wt || !x_band || !wt->w_qkv || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv) return PSCWIN_ERR_SHAPE;
+  const bool shifted = d->shift_x || d->shift_y;
+  if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !wt->pad) return PSCWIN_ERR_CONTRACT;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_band) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)g.rows * d->W;
+  const int C = d->C;
+  const void* x = d->cycle_scan ? wsp(ws, w.x1) : x_band;
+  void* u = wsp(ws, w.u);
+  rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, 0, u, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)T;
+  a.N = 3 * C;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = wsp(ws, w.qkv + (size_t)g.ht_eff * w.row_bytes_qkv);  // own rows of the extended buffer
+  a.ldo = 3 * C;
+  a.epi = EPI_QKV_ROPE;
+  a.prof_name = "gemm_qkv_rope";
+  a.bias = (const float*)wt->b_qkv;
+  a.rope = d->rope;
+  a.HW = d->H * d->W;
+  a.Wgrid = d->W;
+  a.C = C;
+  a.d_head = C / d->heads;
+  a.tok0 = g.r0 * d->W;  // RoPE at global grid rows
+  if (launch_gemm_bf16(u, wt->w_qkv, a, s)) return PSCWIN_ERR_CUDA;
+  if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE) {
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, reinterpret_cast<float*>(wsp(ws, w.qkv_pad)),
+                        s);
+    if (rc) return PSCWIN_ERR_CUDA;
+  }
+  return PSCWIN_OK;
+}
+
+int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                         const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!wt || !x_band || !x_out || !wt->w_o || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_out)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)g.rows * d->W;
+  const int C = d->C;
+  // the extended buffer is an image of ext_rows rows whose window grid matches the global one (band_geo)
+  const pscwin_layer_desc e = sub_desc(d, g.ext_rows, g.sy_local);
+  AttnArgs a;
+  a.B = 1;
+  a.H = g.ext_rows;
+  a.W = d->W;
+  a.C = C;
+  a.heads = d->heads;
+  a.d = C / d->heads;
+  a.w = d->window;
+  a.sx = e.shift_x;
+  a.sy = e.shift_y;
+  a.pad_mode = d->pad_mode;
+  a.rope = d->rope;
+  a.row0 = g.e0;
+  a.qkv = wsp(ws, w.qkv);
+  a.qkv_pad = reinterpret_cast<const float*>(wsp(ws, w.qkv_pad));
+  a.out = wsp(ws, w.O);
+  a.pad_tab = wsp(ws, w.pad_tab);
+  rc = launch_window_attention(a, s);
+  if (rc) return status_from(rc);
+  const void* x = d->cycle_scan ? wsp(ws, w.x1) : x_band;
+  GemmArgs o;
+  memset(&o, 0, sizeof(o));
+  o.M = (int)T;
+  o.N = C;
+  o.K = C;
+  o.lda = C;
+  o.ldb = C;
+  o.out = x_out;
+  o.ldo = C;
+  o.epi = EPI_RESID_BF16;
+  o.prof_name = "gemm_out_proj";
+  o.bias = (const float*)wt->b_o;
+  o.residual = x;
+  o.ldr = C;
+  const void* Ob = wsp(ws, w.O + (size_t)g.ht_eff * d->W * C * 2);
+  return status_from(launch_gemm_bf16(Ob, wt->w_o, o, s));
 }
 
 }  // extern "C"

@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
 // Pad tables for the LEARNABLE patch: kx[X+pl][h][0:d/2] = rot_X(k_p[h][0:d/2]), ky[Y+pt][h][0:d/2] =
 // rot_Y(k_p[h][d/2:d]), vp[h][:] = v_p[h][:]  (bf16; rotation in f32 from the f32 projection of p).
 __global__ void pad_tables_kernel(const float* __restrict__ qkv_pad, int C, int heads, int d, int Wp, int Hp, int pl,
-                                  int pt, int rope, __nv_bfloat16* kx, __nv_bfloat16* ky, __nv_bfloat16* vp) {
+                                  int pt, int rope, int row0, __nv_bfloat16* kx, __nv_bfloat16* ky,
+                                  __nv_bfloat16* vp) {
   pdl_trigger();
   pdl_wait();
   const int half = d / 2;
@@ -279,7 +280,7 @@ __global__ void pad_tables_kernel(const float* __restrict__ qkv_pad, int C, int 
     const int pos_idx = k / (heads * half);
     const int hh = (k / half) % heads;
     const int e = k % half;  // element within the half
-    const int pos = pos_idx - (isy ? pt : pl);
+    const int pos = pos_idx - (isy ? pt - row0 : pl);
     const float* kp = qkv_pad + C + hh * d + (isy ? half : 0);
     float val;
     if (rope) {
@@ -343,7 +344,7 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
     int n = (p.Wp + p.Hp) * a.C / 2 + a.C;
     PSCWIN_PROF("pad_tables", stream);
     launch_k(pad_tables_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
-                                                           kx, ky, vp);
+             a.row0, kx, ky, vp);
   }
   // windows of <= 256 slots: persistent warp-specialised kernel (attn_sm100_ws.cu); PSCWIN_ATTN_V1=1 forces this
   // file's one-CTA-per-(q tile, head, window) kernel, which also serves larger windows.

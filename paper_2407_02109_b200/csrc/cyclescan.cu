@@ -45,6 +45,9 @@ struct ScanParams {
   float* hs;         // [B, n_chunks, D, N]
   __nv_bfloat16* out;
   long long ld_out;
+  // band mode (window-row sharding): the k-1 xin rows preceding this segment in the cycled sequence
+  // (the previous rank's tail; rank 0: the global sequence tail) replace the local wrap-around; null = one segment
+  const __nv_bfloat16* hist;
 };
 
 __device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
@@ -71,7 +74,14 @@ __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
   const int r0 = (int)(grp - (long long)b * groups_img) * CONV_T;
   const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
   __nv_bfloat16* vb = p.v + (long long)b * rows_img * p.D + d0;
-  auto load_tok = [&](int tt) { return *reinterpret_cast<const uint4*>(xb + (long long)tt * p.ld_x); };
+  // token tt of the copy-2/3 stream; tt < 0 is the history before this segment (wrap-around or the band's hist)
+  auto load_tok = [&](int tt) {
+    if (tt < 0) {
+      if (p.hist) return *reinterpret_cast<const uint4*>(p.hist + ((long long)b * (p.k - 1) + tt + p.k - 1) * p.D + d0);
+      tt += p.L;
+    }
+    return *reinterpret_cast<const uint4*>(xb + (long long)tt * p.ld_x);
+  };
   float wk[8][KMAX], bias[8];
   {
     const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.conv_b + d0));
@@ -100,8 +110,7 @@ __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
     uint4 xs[CONV_T + KMAX - 1];
 #pragma unroll
     for (int m = 0; m < CONV_T + KMAX - 1; ++m) {
-      int tt = r0 - (p.k - 1) + m;
-      if (tt < 0) tt += p.L;
+      const int tt = r0 - (p.k - 1) + m;
       xs[m] = (m < CONV_T + p.k - 1) ? load_tok(tt) : make_uint4(0u, 0u, 0u, 0u);
     }
     if (p.k == 4) {
@@ -139,9 +148,8 @@ __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
       for (int i = 0; i < KMAX; ++i) {
         xw[i] = make_uint4(0u, 0u, 0u, 0u);
         if (i < p.k) {
-          int tt = t - (p.k - 1) + i;
-          if (tt < 0 && !copy1) tt += p.L;
-          if (tt >= 0) xw[i] = load_tok(tt);
+          const int tt = t - (p.k - 1) + i;
+          if (tt >= 0 || !copy1) xw[i] = load_tok(tt);
         }
       }
       emit(r, xw);
@@ -560,6 +568,202 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
   }
 }
 
+// ------------------------------------------------------------------------------------------------- band mode
+// Window-row sharding of one image: rank g owns the contiguous scan segment of its
+// token rows. After pass 1 each rank reduces its chunks to a segment record; the records of all ranks are
+// all-gathered (NCCL); every rank then folds them locally to its segment's entry state.
+// Record layout (floats): [D] sum of Delta over the segment body | [D][N] segment end state from zero (input x1)
+//                         | [D] sum of Delta over the copy-2/3 prefix | [D][N] beta1 | [D][N] beta2
+// (the last three from rank 0 only — it holds the P = k-1 prefix tokens; other ranks write zeros).
+__host__ __device__ inline size_t band_record_floats(int D, int N) { return (size_t)D * (2 + 3 * (size_t)N); }
+
+template <int N>
+__global__ void __launch_bounds__(256) scan_segment_kernel(ScanParams p, float* rec) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int NPL = (N + 31) / 32;
+  const int d = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (d >= p.D) return;  // B = 1 in band mode
+  const int W = p.R + 2 * N;
+  const bool zoh = p.bbar == 0;
+  float A2[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int n = lane + 32 * j;
+    A2[j] = n < N ? -__expf(p.a_log[d * N + n]) * kLog2e : 0.f;
+  }
+  float* r_sdt = rec;
+  float* r_b = rec + p.D;
+  float* r_sdt2 = r_b + (size_t)p.D * N;
+  float* r_b1 = r_sdt2 + p.D;
+  float* r_b2 = r_b1 + (size_t)p.D * N;
+  // segment end state from zero and sum of Delta: fold of the chunk summaries
+  float Bb[NPL], sall = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) Bb[j] = 0.f;
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const float sc = p.sumdt[(long long)c * p.D + d];
+    sall += sc;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int n = lane + 32 * j;
+      if (n < N) Bb[j] = fmaf(ex2_approx(sc * A2[j]), Bb[j], p.hs[((long long)c * p.D + d) * N + n]);
+    }
+  }
+  if (lane == 0) r_sdt[d] = sall;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j)
+    if (lane + 32 * j < N) r_b[(size_t)d * N + lane + 32 * j] = Bb[j];
+  // copy prefixes (rank 0): beta1 = copy 1 from zero over rows [L, L+P), beta2 = copies 2/3 over rows [0, P)
+  float b1[NPL], b2[NPL], sdt2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) b1[j] = b2[j] = 0.f;
+  auto step = [&](float (&h)[NPL], long long row) {
+    const float dt = p.delta[row * p.D + d];
+    const float v = __bfloat162float(p.v[row * p.D + d]);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int n = lane + 32 * j;
+      if (n >= N) continue;
+      const float w = p.dbc[row * W + p.R + n] * v;
+      const float x = dt * A2[j];
+      const float dA = ex2_approx(x);
+      h[j] = zoh ? fmaf(dA, h[j] + w, -w) : fmaf(dA, h[j], x * 0.69314718055994531f * w);
+    }
+  };
+  for (int t = 0; t < p.P; ++t) {
+    step(b1, p.L + t);
+    step(b2, t);
+    sdt2 += p.delta[(long long)t * p.D + d];
+  }
+  if (lane == 0) r_sdt2[d] = sdt2;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j)
+    if (lane + 32 * j < N) {
+      r_b1[(size_t)d * N + lane + 32 * j] = b1[j];
+      r_b2[(size_t)d * N + lane + 32 * j] = b2[j];
+    }
+}
+
+// Entry states of this rank's chunks from the all-gathered records (recs [world][record]); rank 0 also writes the
+// prefix outputs. Same algebra as scan_carry_kernel with the fold running over ranks first, then own chunks.
+template <int N>
+__global__ void __launch_bounds__(256) scan_dist_carry_kernel(ScanParams p, const float* recs, int rank, int world) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int NPL = (N + 31) / 32;
+  const int d = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (d >= p.D) return;
+  const int W = p.R + 2 * N;
+  const bool zoh = p.bbar == 0;
+  const size_t RF = band_record_floats(p.D, N);
+  float A2[NPL], invA[NPL];
+  bool act[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const int n = lane + 32 * j;
+    act[j] = n < N;
+    const float A = act[j] ? -__expf(p.a_log[d * N + n]) : -1.f;
+    A2[j] = A * kLog2e;
+    invA[j] = 1.f / A;
+  }
+  auto rec_sdt = [&](int g) { return recs[g * RF + d]; };
+  auto rec_b = [&](int g, int j) { return recs[g * RF + p.D + (size_t)d * N + lane + 32 * j]; };
+  const float* r0 = recs;  // rank 0's prefix parts
+  const float sdt2 = r0[p.D + (size_t)p.D * N + d];
+  float beta1[NPL], beta2[NPL], alpha2[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    beta1[j] = act[j] ? r0[2 * p.D + (size_t)p.D * N + (size_t)d * N + lane + 32 * j] : 0.f;
+    beta2[j] = act[j] ? r0[2 * p.D + 2 * (size_t)p.D * N + (size_t)d * N + lane + 32 * j] : 0.f;
+    alpha2[j] = ex2_approx(sdt2 * A2[j]);
+  }
+  // body from zero (input x1) over all segments in rank order
+  float Bb[NPL], sall = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) Bb[j] = 0.f;
+  for (int g = 0; g < world; ++g) {
+    const float sg = rec_sdt(g);
+    sall += sg;
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) Bb[j] = fmaf(ex2_approx(sg * A2[j]), Bb[j], rec_b(g, j));
+  }
+  float c2[NPL], c3[NPL], H[NPL];
+#pragma unroll
+  for (int j = 0; j < NPL; ++j) {
+    const float Ab = ex2_approx(sall * A2[j]);
+    c2[j] = fmaf(Ab, beta1[j], Bb[j]);
+    const float e2 = fmaf(alpha2[j], c2[j], beta2[j]);
+    c3[j] = fmaf(Ab, e2, Bb[j]);
+    const float e3 = fmaf(alpha2[j], c3[j], beta2[j]);
+    H[j] = beta1[j] + e2 + e3;
+  }
+  auto step = [&](float (&h)[NPL], long long row) {
+    const float dt = p.delta[row * p.D + d];
+    const float v = __bfloat162float(p.v[row * p.D + d]);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      if (!act[j]) continue;
+      const float w = p.dbc[row * W + p.R + lane + 32 * j] * v;
+      const float x = dt * A2[j];
+      const float dA = ex2_approx(x);
+      h[j] = zoh ? fmaf(dA, h[j] + w, -w) : fmaf(dA, h[j], x * 0.69314718055994531f * w);
+    }
+  };
+  if (rank == 0) {  // prefix outputs: out_t = (sum_copies C^(c)_t . h^(c)_t + D (v1_t + 2 v2_t)) * SiLU(z_t)
+    float h1[NPL], h2[NPL], h3[NPL];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      h1[j] = 0.f;
+      h2[j] = c2[j];
+      h3[j] = c3[j];
+    }
+    const float Ds = p.d_skip[d];
+    for (int t = 0; t < p.P; ++t) {
+      const long long r1 = p.L + t, r2 = t;
+      step(h1, r1);
+      step(h2, r2);
+      step(h3, r2);
+      float y = 0.f;
+#pragma unroll
+      for (int j = 0; j < NPL; ++j)
+        if (act[j]) {
+          const int n = lane + 32 * j;
+          y += invA[j] * (p.dbc[r1 * W + p.R + N + n] * h1[j] + p.dbc[r2 * W + p.R + N + n] * (h2[j] + h3[j]));
+        }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+      if (lane == 0) {
+        y += Ds * (__bfloat162float(p.v[r1 * p.D + d]) + 2.f * __bfloat162float(p.v[r2 * p.D + d]));
+        const float g = p.gz ? __bfloat162float(p.gz[(long long)t * p.ld_gz + d]) : 1.f;
+        p.out[(long long)t * p.ld_out + d] = __float2bfloat16_rn(y * g);
+      }
+    }
+  }
+  // entry state of this rank's segment: fold of the earlier segments (input x3)
+  for (int g = 0; g < rank; ++g) {
+    const float sg = rec_sdt(g);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) H[j] = fmaf(ex2_approx(sg * A2[j]), H[j], 3.f * rec_b(g, j));
+  }
+  // and of every own chunk (overwriting the pass-1 chunk-end states with chunk entry states)
+  for (int c = 0; c < p.n_chunks; ++c) {
+    const float sc = p.sumdt[(long long)c * p.D + d];
+#pragma unroll
+    for (int j = 0; j < NPL; ++j)
+      if (act[j]) {
+        const long long idx = ((long long)c * p.D + d) * N + lane + 32 * j;
+        const float hb = p.hs[idx];
+        p.hs[idx] = H[j];
+        H[j] = fmaf(ex2_approx(sc * A2[j]), H[j], 3.f * hb);
+      }
+  }
+}
+
 // ------------------------------------------------------------------------------------------------- pass 2
 template <int N, int DPB, int NS, bool ZOH>
 __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
@@ -740,9 +944,9 @@ static int choose_chunk(int B, int L, int D, int N, int W) {
   return (int)lc;
 }
 
-static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
+static ScanPlan plan_scan_p(int B, int L, int D, int N, int R, int k, int P) {
   ScanPlan s;
-  s.P = k - 1;
+  s.P = P;
   s.Lc = choose_chunk(B, L, D, N, R + 2 * N);
   s.n_chunks = (L + s.Lc - 1) / s.Lc;
   s.W = R + 2 * N;
@@ -774,6 +978,7 @@ static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) {
   s.total = off;
   return s;
 }
+static ScanPlan plan_scan(int B, int L, int D, int N, int R, int k) { return plan_scan_p(B, L, D, N, R, k, k - 1); }
 
 static int check_scan(int B, int L, int D, int N, int R, int k) {
   if (B <= 0 || L <= 0 || D <= 0 || N <= 0 || R <= 0 || k <= 0) return PSCWIN_ERR_SHAPE;
@@ -805,7 +1010,7 @@ static void launch_pass2(ScanParams& p, cudaStream_t s) {
 }
 
 template <int N>
-static int launch_passes(ScanParams& p, cudaStream_t s) {
+static void launch_dt_pass1(ScanParams& p, cudaStream_t s) {
   {
     PSCWIN_PROF("scan_dt", s);
     const long long rows = (long long)p.B * (p.L + p.P);
@@ -824,34 +1029,42 @@ static int launch_passes(ScanParams& p, cudaStream_t s) {
     else if (ns == 2) launch_pass1<N, 2>(p, s);
     else launch_pass1<N, 4>(p, s);
   }
-  {
-    PSCWIN_PROF("scan_carry", s);
-    const int warps = p.B * p.D;
-    const size_t per_warp = (size_t)p.n_chunks * (N + 1) * 4;
-    int wpb = (int)((48 * 1024) / per_warp);  // warps per block within the default shared-memory window
-    wpb = wpb > 8 ? 8 : (wpb < 1 ? 1 : wpb);
-    launch_k(scan_carry_kernel<N>, dim3((warps + wpb - 1) / wpb), dim3(32 * wpb), wpb * per_warp, s, p);
-  }
-  {
-    PSCWIN_PROF("scan_pass2", s);
-    const int ns = pass_ns();
-    if (ns == 1) launch_pass2<N, 1>(p, s);
-    else if (ns == 2) launch_pass2<N, 2>(p, s);
-    else launch_pass2<N, 4>(p, s);
-  }
+}
+
+template <int N>
+static void launch_carry(ScanParams& p, cudaStream_t s) {
+  PSCWIN_PROF("scan_carry", s);
+  const int warps = p.B * p.D;
+  const size_t per_warp = (size_t)p.n_chunks * (N + 1) * 4;
+  int wpb = (int)((48 * 1024) / per_warp);  // warps per block within the default shared-memory window
+  wpb = wpb > 8 ? 8 : (wpb < 1 ? 1 : wpb);
+  launch_k(scan_carry_kernel<N>, dim3((warps + wpb - 1) / wpb), dim3(32 * wpb), wpb * per_warp, s, p);
+}
+
+template <int N>
+static void launch_pass2_ns(ScanParams& p, cudaStream_t s) {
+  PSCWIN_PROF("scan_pass2", s);
+  const int ns = pass_ns();
+  if (ns == 1) launch_pass2<N, 1>(p, s);
+  else if (ns == 2) launch_pass2<N, 2>(p, s);
+  else launch_pass2<N, 4>(p, s);
+}
+
+template <int N>
+static int launch_passes(ScanParams& p, cudaStream_t s) {
+  launch_dt_pass1<N>(p, s);
+  launch_carry<N>(p, s);
+  launch_pass2_ns<N>(p, s);
   return (int)cudaGetLastError();
 }
 
 // Full cycle scan given the in_proj output (xin, z with row strides) -> out (row stride ld_out). z_gated: z already
 // holds SiLU(z) (module path: applied by the in_proj epilogue); otherwise the gate is computed into the workspace.
-static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, const __nv_bfloat16* xin,
-                          long long ld_x, const __nv_bfloat16* z, long long ld_z, bool z_gated, const float* conv_w,
-                          const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
-                          const float* a_log, const float* d_skip, __nv_bfloat16* out, long long ld_out, void* ws,
-                          size_t ws_bytes, cudaStream_t s) {
-  ScanPlan pl = plan_scan(B, L, D, N, R, k);
-  if (ws_bytes < pl.total) return PSCWIN_ERR_WORKSPACE;
-  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+static ScanParams make_scan_params(const ScanPlan& pl, int B, int L, int D, int N, int R, int k, int bbar,
+                                   const __nv_bfloat16* xin, long long ld_x, const __nv_bfloat16* gz, long long ld_gz,
+                                   const float* conv_w, const float* conv_b, const float* w_dt, const float* b_dt,
+                                   const float* a_log, const float* d_skip, __nv_bfloat16* out, long long ld_out,
+                                   uint8_t* base) {
   ScanParams p;
   p.B = B;
   p.L = L;
@@ -865,8 +1078,8 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.bbar = bbar;
   p.xin = xin;
   p.ld_x = ld_x;
-  p.gz = z;
-  p.ld_gz = ld_z;
+  p.gz = gz;
+  p.ld_gz = ld_gz;
   p.conv_w = conv_w;
   p.conv_b = conv_b;
   p.w_dt = w_dt;
@@ -880,18 +1093,16 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   p.hs = reinterpret_cast<float*>(base + pl.hs);
   p.out = out;
   p.ld_out = ld_out;
-  const long long rows = (long long)B * (L + pl.P);
-  if (z && !z_gated) {
-    PSCWIN_PROF("silu_gate", s);
-    __nv_bfloat16* gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
-    const long long n = (long long)B * L * (D / 8);
-    launch_k(silu_gate_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, z, ld_z, (long long)B * L, D, gz);
-    p.gz = gz;
-    p.ld_gz = D;
-  }
+  p.hist = nullptr;
+  return p;
+}
+
+// conv + x_proj (the front of the scan, before dt / pass 1)
+static int scan_front(ScanParams& p, const ScanPlan& pl, const void* w_x, uint8_t* base, cudaStream_t s) {
+  const long long rows = (long long)p.B * (p.L + pl.P);
   {
     PSCWIN_PROF("conv_silu", s);
-    const long long nthreads = (long long)B * ((L + pl.P + CONV_T - 1) / CONV_T) * (D / 8);
+    const long long nthreads = (long long)p.B * ((p.L + pl.P + CONV_T - 1) / CONV_T) * (p.D / 8);
     launch_k(conv_silu_kernel, dim3((unsigned)((nthreads + 255) / 256)), dim3(256), 0, s, p);
   }
   GemmArgs g;
@@ -899,9 +1110,9 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   g.prof_name = "gemm_x_proj";
   g.M = (int)rows;
   g.N = pl.W;
-  g.K = D;
-  g.lda = D;
-  g.ldb = D;
+  g.K = p.D;
+  g.lda = p.D;
+  g.ldb = p.D;
   g.out = p.dbc;
   g.ldo = pl.W;
   g.epi = EPI_STORE_F32;
@@ -910,12 +1121,90 @@ static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, co
   g.partial = reinterpret_cast<float*>(base + pl.partial);
   g.sem = reinterpret_cast<int*>(base + pl.sem);
   if (g.splits > 1) cudaMemsetAsync(g.sem, 0, (size_t)((g.M + 127) / 128) * sizeof(int), s);
-  int rc = launch_gemm_bf16(p.v, w_x, g, s);
-  if (rc) return PSCWIN_ERR_CUDA;
+  return launch_gemm_bf16(p.v, w_x, g, s) ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
+static int run_cycle_scan(int B, int L, int D, int N, int R, int k, int bbar, const __nv_bfloat16* xin,
+                          long long ld_x, const __nv_bfloat16* z, long long ld_z, bool z_gated, const float* conv_w,
+                          const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
+                          const float* a_log, const float* d_skip, __nv_bfloat16* out, long long ld_out, void* ws,
+                          size_t ws_bytes, cudaStream_t s) {
+  ScanPlan pl = plan_scan(B, L, D, N, R, k);
+  if (ws_bytes < pl.total) return PSCWIN_ERR_WORKSPACE;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  ScanParams p = make_scan_params(pl, B, L, D, N, R, k, bbar, xin, ld_x, z, ld_z, conv_w, conv_b, w_dt, b_dt, a_log,
+                                  d_skip, out, ld_out, base);
+  if (z && !z_gated) {
+    PSCWIN_PROF("silu_gate", s);
+    __nv_bfloat16* gz = reinterpret_cast<__nv_bfloat16*>(base + pl.gz);
+    const long long n = (long long)B * L * (D / 8);
+    launch_k(silu_gate_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, z, ld_z, (long long)B * L, D, gz);
+    p.gz = gz;
+    p.ld_gz = D;
+  }
+  int rc = scan_front(p, pl, w_x, base, s);
+  if (rc) return rc;
   if (N == 16) rc = launch_passes<16>(p, s);
   else if (N == 32) rc = launch_passes<32>(p, s);
   else rc = launch_passes<64>(p, s);
   return rc ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
+// ------------------------------------------------------------------------------------------------- band mode (host)
+// One image (B = 1), this rank's contiguous scan segment of L tokens; P = k-1 on rank 0 (it holds the copy-1
+// prefix), 0 elsewhere. The record buffer holds band_record_floats(D, N) floats.
+size_t band_scan_ws_bytes(int L, int D, int N, int R, int k, int P) { return plan_scan_p(1, L, D, N, R, k, P).total; }
+size_t band_scan_record_bytes(int D, int N) { return band_record_floats(D, N) * 4; }
+
+// conv (with the preceding k-1 xin rows `hist`) -> x_proj -> dt -> pass 1 -> this segment's record
+int band_scan_mid(int L, int D, int N, int R, int k, int P, int bbar, const __nv_bfloat16* xin, long long ld_x,
+                  const __nv_bfloat16* hist, const float* conv_w, const float* conv_b, const void* w_x,
+                  const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip, float* rec, void* ws,
+                  size_t ws_bytes, cudaStream_t s) {
+  ScanPlan pl = plan_scan_p(1, L, D, N, R, k, P);
+  if (ws_bytes < pl.total) return PSCWIN_ERR_WORKSPACE;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  ScanParams p = make_scan_params(pl, 1, L, D, N, R, k, bbar, xin, ld_x, nullptr, 0, conv_w, conv_b, w_dt, b_dt,
+                                  a_log, d_skip, nullptr, 0, base);
+  p.hist = hist;
+  int rc = scan_front(p, pl, w_x, base, s);
+  if (rc) return rc;
+  if (N == 16) launch_dt_pass1<16>(p, s);
+  else if (N == 32) launch_dt_pass1<32>(p, s);
+  else launch_dt_pass1<64>(p, s);
+  {
+    PSCWIN_PROF("scan_segment", s);
+    const dim3 grid((unsigned)((D + 7) / 8));
+    if (N == 16) launch_k(scan_segment_kernel<16>, grid, dim3(256), 0, s, p, rec);
+    else if (N == 32) launch_k(scan_segment_kernel<32>, grid, dim3(256), 0, s, p, rec);
+    else launch_k(scan_segment_kernel<64>, grid, dim3(256), 0, s, p, rec);
+  }
+  return cudaGetLastError() == cudaSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA;
+}
+
+// all-gathered records (recs [world][record], rank order) -> chunk entry states (+ prefix outputs on rank 0)
+// -> pass 2 -> out (gated by gz = SiLU(z))
+int band_scan_end(int L, int D, int N, int R, int k, int P, int bbar, const __nv_bfloat16* xin, long long ld_x,
+                  const __nv_bfloat16* gz, long long ld_gz, const float* conv_w, const float* conv_b,
+                  const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip, const float* recs,
+                  int rank, int world, __nv_bfloat16* out, long long ld_out, void* ws, size_t ws_bytes,
+                  cudaStream_t s) {
+  ScanPlan pl = plan_scan_p(1, L, D, N, R, k, P);
+  if (ws_bytes < pl.total) return PSCWIN_ERR_WORKSPACE;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  ScanParams p = make_scan_params(pl, 1, L, D, N, R, k, bbar, xin, ld_x, gz, ld_gz, conv_w, conv_b, w_dt, b_dt,
+                                  a_log, d_skip, out, ld_out, base);
+  {
+    PSCWIN_PROF("scan_dist_carry", s);
+    const dim3 grid((unsigned)((D + 7) / 8));
+    if (N == 16) launch_k(scan_dist_carry_kernel<16>, grid, dim3(256), 0, s, p, recs, rank, world);
+    else if (N == 32) launch_k(scan_dist_carry_kernel<32>, grid, dim3(256), 0, s, p, recs, rank, world);
+    else launch_k(scan_dist_carry_kernel<64>, grid, dim3(256), 0, s, p, recs, rank, world);
+  }
+  if (N == 16) launch_pass2_ns<16>(p, s);
+  else if (N == 32) launch_pass2_ns<32>(p, s);
+  else launch_pass2_ns<64>(p, s);
+  return cudaGetLastError() == cudaSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA;
 }
 
 // bytes of the scan-order copies (xin, z, out in scan order) a non-raster order needs in front of the scan plan

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // (d = 64: axis = half, pair jj -> frequency jj) or one whole head (d = 32: pairs 0-7 x, 8-15 y).
       float rc[16], rs[16];
       if (p.epi == EPI_QKV_ROPE && p.rope) {
-        const int t = row % p.HW;
+        const int t = (row + p.tok0) % p.HW;
         const int py = t / p.Wgrid, px = t - py * p.Wgrid;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {

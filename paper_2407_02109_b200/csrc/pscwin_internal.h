@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 #include <stddef.h>
 #include <stdint.h>
 
@@ -33,6 +34,7 @@ struct GemmArgs {
   int* sem;
   // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
   int silu_col;
+  int tok0;    // RoPE: global token index of GEMM row 0 (a row band of the image; 0 otherwise)
   int stages;  // smem ring depth (set by the launcher)
   int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
 };
@@ -57,6 +59,7 @@ int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C
 
 struct AttnArgs {
   int B, H, W, C, heads, d, w, sx, sy, pad_mode, rope;
+  int row0;              // global grid row of local row 0 (row bands: RoPE of pad keys at global coordinates)
   const void* qkv;       // [B,H,W,3C] bf16 (q,k rotated at their grid coordinates)
   const float* qkv_pad;  // [3C] f32 projection of p (unrotated) or null (plain / masked)
   void* out;             // [B,H,W,C] bf16
@@ -89,6 +92,18 @@ int run_cycle_scan_f32(int B, int H, int W, int order, int window, int D, int N,
                        const float* conv_w, const float* conv_b, const float* w_x, const float* w_dt,
                        const float* b_dt, const float* a_log, const float* d_skip, float* out, long long ld_out,
                        void* ws, size_t ws_bytes, cudaStream_t s);
+// band mode of the cycle scan (cyclescan.cu)
+size_t band_scan_ws_bytes(int L, int D, int N, int R, int k, int P);
+size_t band_scan_record_bytes(int D, int N);
+int band_scan_mid(int L, int D, int N, int R, int k, int P, int bbar, const __nv_bfloat16* xin, long long ld_x,
+                  const __nv_bfloat16* hist, const float* conv_w, const float* conv_b, const void* w_x,
+                  const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip, float* rec, void* ws,
+                  size_t ws_bytes, cudaStream_t s);
+int band_scan_end(int L, int D, int N, int R, int k, int P, int bbar, const __nv_bfloat16* xin, long long ld_x,
+                  const __nv_bfloat16* gz, long long ld_gz, const float* conv_w, const float* conv_b,
+                  const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip, const float* recs,
+                  int rank, int world, __nv_bfloat16* out, long long ld_out, void* ws, size_t ws_bytes,
+                  cudaStream_t s);
 // cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
 int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);

@@ -49,3 +49,65 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+# ------------------------------------------------------------------------------------- window-row bands
+def band_rows(H: int, window: int, world: int):
+    """Split the H token rows of one image into `world` contiguous bands of whole window rows (the last band
+    takes the ragged remainder). Returns [(row_begin, row_end)] in rank order."""
+    nwin = -(-H // window)
+    if world <= 0 or world > nwin:
+        raise ValueError(f"cannot split {nwin} window rows over {world} ranks")
+    out = []
+    for r in range(world):
+        lo, hi = shard_range(nwin, world, r)
+        out.append((lo * window, min(hi * window, H)))
+    return out
+
+
+class TorchDistExchange:
+    """The three inter-rank transfers of the band path (include/pscwin.h "row bands") over torch.distributed:
+    NCCL on the GPU box (device tensors, NVLink), gloo in the CPU tests. Tensors are byte views of the ranks'
+    workspaces; sizes agree pairwise by construction (pscwin_band_io_offsets)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _p2p(self, ops):
+        ops = [op for op in ops if op is not None]
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def ring(self, send, recv):
+        """conv history: rank g's send -> rank (g+1) mod world's recv."""
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        self._p2p([self.dist.P2POp(self.dist.isend, send, nxt, self.group),
+                   self.dist.P2POp(self.dist.irecv, recv, prv, self.group)])
+
+    def allgather(self, send, recv):
+        """scan records: recv = concat over ranks (rank order) of send."""
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        self.dist.all_gather(list(recv.view(self.world, -1).unbind(0)), send, group=self.group)
+
+    def halo(self, send_prev, send_next, recv_prev, recv_next):
+        """QKV halo: send_prev -> rank-1's recv_next, send_next -> rank+1's recv_prev (empty at the edges)."""
+        d, ops = self.dist, []
+        if send_prev.numel():
+            ops.append(d.P2POp(d.isend, send_prev, self.rank - 1, self.group))
+        if send_next.numel():
+            ops.append(d.P2POp(d.isend, send_next, self.rank + 1, self.group))
+        if recv_prev.numel():
+            ops.append(d.P2POp(d.irecv, recv_prev, self.rank - 1, self.group))
+        if recv_next.numel():
+            ops.append(d.P2POp(d.irecv, recv_next, self.rank + 1, self.group))
+        self._p2p(ops)

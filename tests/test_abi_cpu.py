@@ -74,3 +74,37 @@ def test_null_and_alignment_checks_without_gpu(pl):
     assert L.pscwin_shifted_pad_partition(ctypes.c_void_p(16), None, 1, 4, 4, 8, 2, 1, 1, 0, ctypes.c_void_p(16),
                                           None) == ERR_CONTRACT
     assert L.pscwin_window_partition(ctypes.c_void_p(18), 1, 4, 4, 8, 2, 0, ctypes.c_void_p(16), None) == ERR_ALIGN
+
+
+def test_band_plan_and_io_offsets(pl):
+    # window-row bands (include/pscwin.h "row bands"): workspace planning and the exchange sizes are host logic
+    import ctypes
+    import synth
+    from paper_2407_02109_b200._lib import BandDesc, BandIO, LayerDesc
+    L = pl.lib()
+    cfg = synth.vitb(256, cycle_scan=1)  # 4096^2, shifted (s = 8): 8 halo rows each way
+    d = LayerDesc.from_config(cfg)
+    rows = [(32 * g, 32 * g + 32) for g in range(8)]
+    ios = []
+    for g, (r0, r1) in enumerate(rows):
+        b = BandDesc(r0, r1, g, 8)
+        assert L.pscwin_band_workspace_bytes(ctypes.byref(d), ctypes.byref(b)) > 0
+        io = BandIO()
+        assert L.pscwin_band_io_offsets(ctypes.byref(d), ctypes.byref(b), ctypes.byref(io)) == 0
+        ios.append(io)
+    row = 256 * 3 * 768 * 2
+    for g in range(8):
+        assert ios[g].recv_prev_bytes == (8 * row if g > 0 else 0)
+        assert ios[g].recv_next_bytes == (8 * row if g < 7 else 0)
+        if g > 0:
+            assert ios[g].send_prev_bytes == ios[g - 1].recv_next_bytes
+        if g < 7:
+            assert ios[g].send_next_bytes == ios[g + 1].recv_prev_bytes
+        assert ios[g].hist_bytes == 3 * 1536 * 2 and ios[g].rec_bytes == 1536 * (2 + 3 * 32) * 4
+    bad = [BandDesc(8, 40, 1, 8),    # not whole window rows
+           BandDesc(0, 32, 1, 8),    # rank 1 cannot start at row 0
+           BandDesc(224, 256, 6, 8)]  # rank 6 cannot end at H
+    for b in bad:
+        assert L.pscwin_band_workspace_bytes(ctypes.byref(d), ctypes.byref(b)) == 0
+    col = LayerDesc.from_config(cfg.replace(scan_order=synth.SCAN_COL_MAJOR))
+    assert L.pscwin_band_workspace_bytes(ctypes.byref(col), ctypes.byref(BandDesc(0, 32, 0, 8))) == 0

@@ -70,3 +70,52 @@ def test_shard_range_partition(n, world):
 def test_single_process_reduce_is_identity():
     d = _load_dist()
     assert d.max_over_ranks(3.25) == 3.25
+
+
+# ------------------------------------------------------------------ window-row bands (host logic of §8(e))
+def _band_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    d = _load_dist()
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ex = d.TorchDistExchange()
+    # ring: rank g receives rank g-1's bytes (rank 0 the last rank's)
+    send = torch.full((6,), 10 + rank, dtype=torch.uint8)
+    recv = torch.zeros(6, dtype=torch.uint8)
+    ex.ring(send, recv)
+    # all-gather in rank order
+    rec = torch.arange(4, dtype=torch.uint8) + 100 * rank
+    recs = torch.zeros(4 * world, dtype=torch.uint8)
+    ex.allgather(rec, recs)
+    # halo: rank 0 has no previous neighbour, the last rank no next one; sizes agree pairwise (3 down, 5 up)
+    sp = torch.full((3 if rank > 0 else 0,), 30 + rank, dtype=torch.uint8)
+    sn = torch.full((5 if rank < world - 1 else 0,), 50 + rank, dtype=torch.uint8)
+    rp = torch.zeros(5 if rank > 0 else 0, dtype=torch.uint8)
+    rn = torch.zeros(3 if rank < world - 1 else 0, dtype=torch.uint8)
+    ex.halo(sp, sn, rp, rn)
+    out[rank] = (recv.tolist(), recs.tolist(), rp.tolist(), rn.tolist())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_exchange_gloo(world):
+    port = _free_port()
+    out = mp.Manager().dict()
+    mp.spawn(_band_worker, args=(world, port, out), nprocs=world, join=True)
+    for g in range(world):
+        recv, recs, rp, rn = out[g]
+        assert recv == [10 + (g - 1) % world] * 6
+        assert recs == [v + 100 * r for r in range(world) for v in range(4)]
+        assert rp == ([50 + g - 1] * 5 if g > 0 else [])
+        assert rn == ([30 + g + 1] * 3 if g < world - 1 else [])
+
+
+@pytest.mark.parametrize("H,w,world", [(256, 16, 8), (64, 16, 4), (20, 8, 3), (32, 8, 1)])
+def test_band_rows_cover_whole_window_rows(H, w, world):
+    d = _load_dist()
+    rows = d.band_rows(H, w, world)
+    assert rows[0][0] == 0 and rows[-1][1] == H and len(rows) == world
+    for (a, b), (c, _) in zip(rows, rows[1:]):
+        assert b == c and a % w == 0 and b % w == 0 and b > a
+    with pytest.raises(ValueError):
+        d.band_rows(H, w, -(-H // w) + 1)

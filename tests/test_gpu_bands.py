@@ -1,0 +1,61 @@
+"""Window-row sharding on one GPU: every band of the image runs its own phases and the
+bands exchange the conv history, the scan records and the QKV halo rows by device copies (the bytes NCCL moves
+between GPUs). The stitched output must equal pscwin_forward on the whole image — bit-identical for attention
+layers, within fp32 summation-order noise for cycle-scan layers (different chunking) — and the oracle."""
+import pytest
+
+import oracle
+import synth
+from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2407_02109_b200 as p
+    return p
+
+
+CASES = [
+    (synth.tiny(H=32, W=16, shift_x=0, shift_y=0), 2),                    # P
+    (synth.tiny(H=32, W=16), 2),                                           # S, learnable
+    (synth.tiny(H=32, W=16), 4),
+    (synth.tiny(H=40, W=24, shift_x=3, shift_y=5), 3),                     # asymmetric shift: 5 / 3 halo rows
+    (synth.tiny(H=36, W=16, pad_mode=synth.PAD_MASKED), 3),                # ragged last band (4 rows)
+    (synth.tiny(H=32, W=16, cycle_scan=1, shift_x=0, shift_y=0), 2),       # CS + P
+    (synth.tiny(H=32, W=16, cycle_scan=1), 4),                             # CS + S
+    (synth.tiny(H=32, W=16, cycle_scan=1, bbar_mode=synth.BBAR_EULER), 3),
+    (synth.vitb(64, cycle_scan=1), 4),                                     # ViT-B 1024^2 as 4 bands
+]
+
+
+@pytest.mark.parametrize("cfg,world", CASES, ids=lambda c: str(c) if isinstance(c, int) else
+                         f"{c.H}x{c.W}C{c.C}s{c.shift_x},{c.shift_y}m{c.pad_mode}cs{c.cycle_scan}b{c.bbar_mode}")
+def test_bands_equal_whole_image(pl, cfg, world):
+    import torch
+    from paper_2407_02109_b200.bands import LoopbackBands
+    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    dw = dev_weights(w, cfg)
+    desc = pl.LayerDesc.from_config(cfg)
+    xd = dev(x)
+    whole = pl.PSCWinLayer(desc, dw)(xd)
+    banded = LoopbackBands(desc, dw, world)(xd)
+    torch.cuda.synchronize()
+    if cfg.cycle_scan:  # different chunk boundaries: fp32 summation order, then bf16 rounding (2 ulp at max scale)
+        assert rel_err(host(banded), host(whole)) < 8e-3
+    else:
+        assert torch.equal(banded, whole)
+    assert rel_err(host(banded), oracle.pscwin_layer(x, w, cfg)) < BF16_TOL
+
+
+def test_band_contract(pl):
+    from paper_2407_02109_b200.bands import BandLayer
+    cfg = synth.tiny(H=32, W=16)
+    desc = pl.LayerDesc.from_config(cfg)
+    dw = dev_weights(synth.make_weights(cfg), cfg)
+    with pytest.raises(ValueError):
+        BandLayer(desc, dw, 4, 20, 1, 2)  # not whole window rows
