@@ -327,6 +327,100 @@ def time_oracle_layer(cfg, layer_idx):
     return time.perf_counter() - t0
 
 
+def run_rows(args, rank, world, local_rank):
+    """--shard rows: ONE image split by window rows over the ranks (config 4; strong scaling). Each rank runs the
+    band phases of every layer (paper_2407_02109_b200.bands) and exchanges halo rows / conv history / scan
+    records with its neighbours over NCCL (dist.TorchDistExchange). Eager launches (the exchanges sit between
+    phases); time = max over ranks of the device-timed step."""
+    import torch
+    import paper_2407_02109_b200 as pl
+    from paper_2407_02109_b200.bands import BandLayer, band_forward
+    from paper_2407_02109_b200.dist import TorchDistExchange, band_rows
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    label, _, cfgs = workload(args.workload)
+    cfgs = [c.replace(B=1) for c in cfgs]
+    c0 = cfgs[0]
+    r0, r1 = band_rows(c0.H, c0.window, world)[rank]
+    if world == 1:
+        import torch.distributed as tdist
+        if not tdist.is_initialized():
+            tdist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
+    exchange = TorchDistExchange()
+    layers = []
+    for i, cfg in enumerate(cfgs):
+        w = synth.make_weights(cfg, layer=i)
+        dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+              for k, v in w.items()}
+        layers.append(BandLayer(pl.LayerDesc.from_config(cfg), dw, r0, r1, rank, world))
+    x_full = synth.make_input(cfgs[0], layer=0)
+    xb = torch.tensor(x_full[:, r0:r1], dtype=torch.bfloat16, device=dev).contiguous()
+    bufs = [torch.empty_like(xb), torch.empty_like(xb)]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step(x):
+        cur = x
+        for j, layer in enumerate(layers):
+            nxt = bufs[j & 1]
+            band_forward(layer, cur, exchange, out=nxt)
+            cur = nxt
+        return cur
+
+    for _ in range(args.warmup):
+        step(xb)
+    torch.cuda.synchronize()
+    n0 = pl.launch_count()
+    step(xb)
+    torch.cuda.synchronize()
+    launches_per_step = pl.launch_count() - n0
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    exchange.dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step(xb)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    # e2e: pinned host band in, band result out, inside the timed region
+    x_pin = torch.empty(xb.shape, dtype=torch.bfloat16, pin_memory=True)
+    x_pin.copy_(xb.cpu())
+    y_pin = torch.empty_like(x_pin).pin_memory()
+    xin = torch.empty_like(xb)
+    e2e = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    exchange.dist.barrier()
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        flush.zero_()
+        e2e[i][0].record(stream)
+        xin.copy_(x_pin, non_blocking=True)
+        y = step(xin)
+        y_pin.copy_(y, non_blocking=True)
+        e2e[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e)
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms, e2e_ms = float(t[0]), float(t[1])
+    return dict(total_ms=total_ms, e2e_ms=e2e_ms, images=args.steps, launches=launches_per_step * args.steps,
+                clocks=clk.summary(), label=label, cfgs=cfgs, band=(r0, r1), h2d=xb.numel() * 2,
+                d2h=xb.numel() * 2)
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def cpu_baseline(args):
     """The fp64 oracle as it stands, timed on this host: one full step of the workload (one image through
     every layer) when that is affordable, else one layer of each kind (summed per image)."""
@@ -440,6 +534,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="also print the per-kernel table to stderr")
     ap.add_argument("--no-graph", action="store_true", help="launch layer by layer instead of a CUDA graph")
+    ap.add_argument("--shard", default="images", choices=["images", "rows"],
+                    help="images: each rank its own image(s) (weak scaling, default); rows: one image split by "
+                         "window rows over the ranks with halo / scan-carry exchange (config 4, strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -456,6 +553,33 @@ def main():
         import torch
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.shard == "rows":
+        if args.workload == "1024" and "--workload" not in sys.argv:
+            args.workload = "4096"  # config 4 is the row-sharded 4096^2 stack
+        res = run_rows(args, rank, world, local_rank)
+        if rank == 0:
+            c0 = res["cfgs"][0]
+            line = {
+                "metric": METRIC, "value": round(res["total_ms"] / res["images"], 4), "unit": "ms/image",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(res["total_ms"] / args.steps, 4), "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded splitmix64; random-init ViT-B PSCWin weights)",
+                "config": {"workload": res["label"].replace("one image per GPU", f"one image split by window rows "
+                                                             f"over {world} GPU(s)"),
+                           "grid": f"{c0.H}x{c0.W}", "layers": len(res["cfgs"]),
+                           "parallelism": f"window-row bands x{world} (halo + scan-carry exchange)",
+                           "rank0_band_rows": list(res["band"]),
+                           "l2": "flushed before every timed step (256 MiB write)", "launch": "eager"},
+                "e2e": {"value": round(res["e2e_ms"] / res["images"], 4), "unit": "ms/image",
+                        "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
+                "gpu_launches": int(res["launches"]), "clocks": res["clocks"], "roofline": None}
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            import torch
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         rl, rows = roofline(res, args)
@@ -468,7 +592,7 @@ def main():
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded splitmix64; random-init ViT-B PSCWin weights)",
             "config": {"workload": res["label"], "grid": f"{c0.H}x{c0.W}", "images_per_rank": res["B"],
-                       "layers": ["CS+" if c.cycle_scan else "" + ("S" if c.shift_x else "P") for c in res["cfgs"]],
+                       "layers": [("CS+" if c.cycle_scan else "") + ("S" if c.shift_x else "P") for c in res["cfgs"]],
                        "C": c0.C, "heads": c0.heads, "window": c0.window, "shift": 8, "ssm_state": c0.N,
                        "ssm_expand": c0.ssm_expand, "pad_mode": "learnable", "parallelism": f"images x{world}",
                        "l2": "flushed before every timed step (256 MiB write)",
