@@ -434,3 +434,109 @@ def pscwin_layer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg) -> np.ndarray:
     if cfg.cycle_scan:
         x = cycle_scan_module(x, wt, cfg)
     return attention_sublayer(x, wt, cfg)
+
+
+# =============================================================================================
+# §3.4 Multi-scale fusion (HRSAM++): packed multi-scale token sequences
+# =============================================================================================
+# Packing (reading Q20): the token grids of all scales are flattened row-major and concatenated
+# ("patchified and concatenated to form a sequence of image tokens with a length of
+# (HW + H_sW_s)/16^2"). With a batch of B samples the scale is the OUTERMOST axis: scale s occupies
+# packed rows [B*off_s, B*off_{s+1}) as a [B, H_s, W_s, C] block (off_s = sum of the earlier scales'
+# H*W). For B = 1 this is exactly the paper's per-sample concatenation.
+
+CS_NONE = 0
+CS_SINGLE_SCALE = 1
+CS_MULTI_SCALE = 2
+
+
+def ms_offsets(scales) -> np.ndarray:
+    """Per-sample token offsets of each scale segment: [0, L_0, L_0+L_1, ...] (SPEC S:L368 bounds)."""
+    return np.concatenate([[0], np.cumsum([h * w for h, w in scales])]).astype(np.int64)
+
+
+def ms_pack(grids) -> np.ndarray:
+    """[B, H_s, W_s, C] per scale -> packed [B * sum L_s, C] (scale outermost, Q20)."""
+    C = grids[0].shape[-1]
+    if any(g.shape[-1] != C for g in grids):
+        raise ValueError("all scales must share C")
+    return np.concatenate([g.reshape(-1, C) for g in grids], axis=0)
+
+
+def ms_unpack(xp: np.ndarray, B: int, scales):
+    """Inverse of ms_pack: packed [B * sum L_s, C] -> list of [B, H_s, W_s, C]."""
+    off = ms_offsets(scales)
+    C = xp.shape[-1]
+    return [xp[B * off[i]:B * off[i + 1]].reshape(B, h, w, C) for i, (h, w) in enumerate(scales)]
+
+
+def ms_index_map(scales, w: int, sx: int = 0, sy: int = 0) -> np.ndarray:
+    """Multi-scale indexing operator (App. C; "reorganized by indexing to ensure
+    tokens within the same window are sequential and tokens from the same scale remain contiguous"):
+    destination = the windows of scale 0 (row-major, slots row-major) then those of scale 1, ...;
+    value = source position in the packed single-sample sequence, or PAD."""
+    off = ms_offsets(scales)
+    maps = []
+    for i, (h, ww) in enumerate(scales):
+        m = index_map(h, ww, w, sx, sy).astype(np.int64)
+        maps.append(np.where(m == PAD, PAD, m + off[i]))
+    return np.concatenate(maps).astype(np.uint32)
+
+
+def ms_attention_sublayer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales) -> np.ndarray:
+    """Multi-scale attention: "computationally equivalent to performing attention on isolated
+    windows" — every scale's grid gets its own (plain / padded-shift) windows with the layer's window,
+    shift and pad token, RoPE at the scale's own grid coordinates (reading Q20); no window spans two
+    scales (block-diagonal mask). xp packed [B * sum L_s, C]."""
+    B = xp.shape[0] // int(ms_offsets(scales)[-1])
+    outs = []
+    for g, (h, w) in zip(ms_unpack(xp, B, scales), scales):
+        outs.append(attention_sublayer(g, wt, cfg.replace(B=B, H=h, W=w)))
+    return ms_pack(outs)
+
+
+def ms_cycle_scan_module(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, mode: int) -> np.ndarray:
+    """Cycle-scan module over a packed multi-scale sequence:
+    SINGLE-SCALE "first splits the tokens by scale, scan each scale's tokens separately by the SSM, and
+    then concatenates them" -> the single-scale module on every scale grid;
+    MULTI-SCALE "directly performs the SSM across the tokens from all the scales": per sample, the
+    scan-order sequences of all scales are concatenated (scale order) into ONE sequence of sum L_s tokens,
+    which is cycled three times, scanned, split and summed like a single-scale sequence.
+    Pre-LN residual (Q13). xp packed [B * sum L_s, C]."""
+    off = ms_offsets(scales)
+    B = xp.shape[0] // int(off[-1])
+    grids = ms_unpack(xp, B, scales)
+    if mode == CS_SINGLE_SCALE:
+        return ms_pack([cycle_scan_module(g, wt, cfg.replace(B=B, H=h, W=w))
+                        for g, (h, w) in zip(grids, scales)])
+    if mode != CS_MULTI_SCALE:
+        raise ValueError(mode)
+    D, C, Ltot = cfg.D, cfg.C, int(off[-1])
+    outs = [g.reshape(B, -1, C).copy() for g in grids]
+    for b in range(B):
+        seq, pis = [], []
+        for g, (h, w) in zip(grids, scales):
+            pi = scan_permutation(h, w, cfg.scan_order, cfg.window)
+            u0 = layer_norm(g[b].reshape(h * w, C), wt["lns_g"], wt["lns_b"], cfg.ln_eps)
+            seq.append(u0[pi])
+            pis.append(pi)
+        s = np.concatenate(seq)
+        X3 = np.concatenate([s, s, s])
+        xz = X3 @ wt["w_in"].T
+        g3 = cycle_ssm_3L(xz[:, :D], xz[:, D:], wt, cfg.bbar_mode)
+        o3 = g3 @ wt["w_out"].T
+        o = o3[:Ltot] + o3[Ltot:2 * Ltot] + o3[2 * Ltot:]
+        for i, pi in enumerate(pis):
+            outs[i][b][pi] += o[off[i]:off[i + 1]]
+    return ms_pack(outs)
+
+
+def ms_layer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, attention: int = 1,
+             cycle_scan: int = CS_NONE) -> np.ndarray:
+    """One HRSAM++ layer over a packed multi-scale sequence: optional cycle-scan module (single- or
+    multi-scale) followed (attention = 1) by the multi-scale window-attention sub-layer."""
+    if cycle_scan:
+        xp = ms_cycle_scan_module(xp, wt, cfg, scales, cycle_scan)
+    if attention:
+        xp = ms_attention_sublayer(xp, wt, cfg, scales)
+    return xp
