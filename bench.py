@@ -59,36 +59,94 @@ def workload(name: str):
     return label, B, cfgs
 
 
+MS_SCALES = [(64, 64), (128, 128), (256, 256)]   # config 5: 1024^2 + 2048^2 + 4096^2 token grids per sample
+
+
+def ms_workload():
+    """configs[4] (HRSAM++ multi-scale): per sample the 64^2 + 128^2 + 256^2 token grids
+    packed into one sequence of 86016 tokens; the 12-layer global-alternation stack with a single-scale
+    cycle-scan module before layers 2, 5, 8, 11 and a multi-scale cycle-scan module closing each stage
+    (after layers 2, 5, 8, 11; Fig. 4). B = 2 samples per GPU (config 5: batch 16 over 8 GPUs).
+    Returns (label, B, [(cfg, attention, cs_mode, weight_seed)])."""
+    B = 2
+    specs = []
+    for i in range(12):
+        shifted, cs = synth.stack_layer_kind(i)
+        cfg = synth.vitb(64, B=B, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0)
+        specs.append((cfg, 1, 1 if cs else 0, i))
+        if cs:
+            specs.append((synth.vitb(64, B=B, shift_x=0, shift_y=0), 0, 2, 100 + i))
+    label = ("HRSAM++ multi-scale: 64^2+128^2+256^2 token grids packed per sample (86016 tokens), 12-layer stack "
+             "+ 4 single-scale and 4 multi-scale cycle-scan modules; ViT-B bf16")
+    return label, B, specs
+
+
+def layer_metas(args):
+    """Per-layer shapes for the roofline accounting: T tokens, widths, whether attention / cycle scan run."""
+    if args.workload == "ms":
+        _, B, specs = ms_workload()
+        T = B * sum(h * w for h, w in MS_SCALES)
+        return [dict(T=T, C=c.C, D=c.D, N=c.N, R=c.R, attn=a, cs=int(cs > 0)) for c, a, cs, _ in specs]
+    _, _, cfgs = workload(args.workload)
+    return [dict(T=c.B * c.H * c.W, C=c.C, D=c.D, N=c.N, R=c.R, attn=1, cs=int(c.cycle_scan)) for c in cfgs]
+
+
 # ----------------------------------------------------------------------------------------------- roofline
-def kernel_work(label: str, cfgs, launches_per_step: int):
-    """Algorithmic work of ONE launch of a kernel label:
-    returns (bound, amount, unit_scale, unit)."""
-    c = cfgs[0]
-    T = c.B * c.H * c.W
-    C, D, N, R = c.C, c.D, c.N, c.R
-    if label == "window_attention":
-        return "hbm", 8.0 * T * C, 1e9, "GB/s"                    # Q,K,V read + O write, bf16, real tokens
-    if label in ("scan_pass1", "scan_pass2"):
-        return "alu", 1.0 * T * D * N, 1e9, "Gexp/s"              # one ex2 per (token, channel, state)
-    if label == "gemm_qkv_rope":
-        return "tensor", 2.0 * T * C * 3 * C, 1e12, "TFLOP/s"
-    if label == "gemm_out_proj":
-        return "tensor", 2.0 * T * C * C, 1e12, "TFLOP/s"
-    if label == "gemm_in_proj":
-        return "tensor", 2.0 * T * C * 2 * D, 1e12, "TFLOP/s"
-    if label == "gemm_out_proj_scan":
-        return "tensor", 2.0 * T * D * C, 1e12, "TFLOP/s"
-    if label == "gemm_x_proj":
-        return "tensor", 2.0 * (T + 3) * D * (R + 2 * N), 1e12, "TFLOP/s"
-    if label == "layer_norm":
-        return "hbm", 4.0 * T * C, 1e9, "GB/s"
-    if label == "conv_silu":
-        return "hbm", 2.0 * T * 2 * D * 0 + 2.0 * T * D * 2, 1e9, "GB/s"
-    return None
+def kernel_work(label: str, metas):
+    """Algorithmic work of a kernel label over ONE step (DESIGN.md §6 "algorithmic work per unit x units"),
+    summed over the layers that launch it: returns (bound, amount, unit_scale, unit) or None."""
+    tot = 0.0
+    bound = unit = None
+    scale = 1.0
+    for m in metas:
+        T, C, D, N, R = m["T"], m["C"], m["D"], m["N"], m["R"]
+        a, cs = m["attn"], m["cs"]
+        if label == "window_attention":
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += a * 8.0 * T * C                      # Q,K,V read + O write, bf16, real tokens
+        elif label in ("scan_pass1", "scan_pass2"):
+            bound, scale, unit = "alu", 1e9, "Gexp/s"
+            tot += cs * 1.0 * T * D * N                 # one ex2 per (token, channel, state)
+        elif label == "gemm_qkv_rope":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += a * 2.0 * T * C * 3 * C
+        elif label == "gemm_out_proj":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += a * 2.0 * T * C * C
+        elif label == "gemm_in_proj":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += cs * 2.0 * T * C * 2 * D
+        elif label == "gemm_out_proj_scan":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += cs * 2.0 * T * D * C
+        elif label == "gemm_x_proj":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += cs * 2.0 * T * D * (R + 2 * N)
+        elif label == "layer_norm":
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += (a + cs) * 4.0 * T * C               # bf16 row read + write
+        elif label == "conv_silu":
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += cs * 4.0 * T * D                     # xin read + v write, bf16
+        else:
+            return None
+    return (bound, tot, scale, unit) if bound and tot > 0 else None
 
 
 def peaks():
+    # MEASURED_PEAKS.json (driver-written) first; else this round's measured values as recorded in BASELINE.md §2;
+    # else the B200_PROFILING.md fallback
     p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "BASELINE.md")) as f:
+            txt = f.read()
+        import re
+        m = re.search(r"HBM ([0-9.]+) GB/s\.\n- bf16 dense ([0-9.]+) TF/s \(([0-9.]+) sustained\)", txt)
+        if m:
+            p.update(hbm_gbs=float(m.group(1)), bf16_tflops=float(m.group(2)),
+                     bf16_tflops_sustained=float(m.group(3)), src="recorded")
+    except Exception:
+        pass
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)
@@ -163,20 +221,40 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------------------------- ours
+def _kind(layer):
+    d = getattr(layer, "desc")
+    if hasattr(d, "n_scales"):
+        cs = {0: "", 1: "CS+", 2: "MSCS"}[d.cycle_scan]
+        return cs + ("" if not d.attention else ("S" if d.layer.shift_x else "P"))
+    return ("CS+" if d.cycle_scan else "") + ("S" if d.shift_x else "P")
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_2407_02109_b200 as pl
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    label, B, cfgs = workload(args.workload)
     layers = []
-    for i, cfg in enumerate(cfgs):
-        w = synth.make_weights(cfg, layer=i)
-        dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
-              for k, v in w.items()}
-        layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dw))
-    x_host = synth.make_input(cfgs[0], layer=rank)
+    if args.workload == "ms":
+        label, B, specs = ms_workload()
+        cfgs = [c for c, _, _, _ in specs]
+        for cfg, att, cs, seed in specs:
+            w = synth.make_weights(cfg, layer=seed)
+            dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+                  for k, v in w.items()}
+            layers.append(pl.PSCWinMSLayer(pl.MSDesc.make(cfg, MS_SCALES, att, cs), dw))
+        # scale-outermost packing (Q20): [B, H_s, W_s, C] blocks of every scale back to back
+        x_host = np.concatenate([synth.make_input(cfgs[0].replace(H=h, W=w), layer=8 * rank + i).reshape(-1, cfgs[0].C)
+                                 for i, (h, w) in enumerate(MS_SCALES)])
+    else:
+        label, B, cfgs = workload(args.workload)
+        for i, cfg in enumerate(cfgs):
+            w = synth.make_weights(cfg, layer=i)
+            dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+                  for k, v in w.items()}
+            layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dw))
+        x_host = synth.make_input(cfgs[0], layer=rank)
     x0 = torch.tensor(x_host, dtype=torch.bfloat16, device=dev)
     bufs = [torch.empty_like(x0), torch.empty_like(x0)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -271,6 +349,7 @@ def run_ours(args, rank, world, local_rank):
     images = args.steps * B * world
     result = dict(total_ms=total_ms, e2e_ms=e2e_ms, images=images, per_step=per_step, layer_ms=layer_ms,
                   prof=prof, launches=launches, clocks=clk.summary(), label=label, B=B, cfgs=cfgs,
+                  kinds=[_kind(l) for l in layers],
                   h2d=x0.numel() * 2 * B // B, d2h=x0.numel() * 2)
     return result
 
@@ -278,15 +357,16 @@ def run_ours(args, rank, world, local_rank):
 def roofline(res, args):
     pk = peaks()
     steps = args.steps
+    metas = layer_metas(args)
     rows = []
+    total = max(sum(v[0] for v in res["prof"].values()), 1e-12)
     for lab, (ms, cnt) in res["prof"].items():
         per_launch = ms / max(cnt, 1)
-        w = kernel_work(lab, res["cfgs"], cnt // max(steps, 1))
-        share = ms / max(sum(v[0] for v in res["prof"].values()), 1e-12)
-        row = {"kernel": lab, "ms_per_launch": per_launch, "launches": cnt, "share": share}
+        w = kernel_work(lab, metas)
+        row = {"kernel": lab, "ms_per_launch": per_launch, "launches": cnt, "share": ms / total}
         if w:
             bound, amount, scale, unit = w
-            achieved = amount / (per_launch * 1e-3) / scale
+            achieved = amount * steps / (ms * 1e-3) / scale      # work of `steps` steps / time of their launches
             if bound == "hbm":
                 peak = pk["hbm_gbs"]
             elif bound == "tensor":
@@ -301,10 +381,12 @@ def roofline(res, args):
     out = None
     if dom:
         tr = traffic.get(dom["kernel"])
+        src = {"measured": "of measured (MEASURED_PEAKS.json)", "recorded": "of measured (BASELINE.md §2 record)",
+               "fallback": "of fallback (B200_PROFILING.md)"}[pk["src"]]
         out = {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": round(dom["achieved"], 2),
                "peak": round(dom["peak"], 2), "unit": dom["unit"], "frac": round(dom["frac"], 4),
                "traffic": tr, "share_of_step": round(dom["share"], 4),
-               "peak_src": pk["src"] if dom["bound"] != "alu" else "derived: 16 ex2/clk/SM x 148 SMs x max SM clock"}
+               "peak_src": src if dom["bound"] != "alu" else "derived: 16 ex2/clk/SM x 148 SMs x max SM clock"}
     return out, rows
 
 
@@ -422,8 +504,18 @@ def _free_port():
 
 
 def cpu_baseline(args):
-    """The fp64 oracle as it stands, timed on this host: one full step of the workload (one image through
-    every layer) when that is affordable, else one layer of each kind (summed per image)."""
+    """The fp64 oracle as it stands, timed on this host: one image through one layer of each kind (summed per
+    image) — or, for the multi-scale workload, each bounded oracle piece of one sample timed once and scaled."""
+    if args.workload == "ms":
+        items = reference_items(reference_entries(args))
+        tot = 0.0
+        for name, fn, scale in items:
+            t0 = time.perf_counter()
+            fn()
+            tot += (time.perf_counter() - t0) * scale
+        return {"value": round(1e3 * tot, 1), "unit": "ms/image", "cores": oracle_threads(), "kind": "oracle",
+                "sample": f"one sample; {len(items)} bounded oracle pieces (1/16 of the projection rows, one window "
+                          f"row, 1/16 of the 3L scan) timed once each and scaled to the full stack"}
     label, B, cfgs = workload(args.workload)
     one = [c.replace(B=1) for c in cfgs]
     kinds = {}
@@ -438,38 +530,54 @@ def cpu_baseline(args):
             "sample": sample}
 
 
-def reference_items(cfgs):
+def reference_entries(args):
+    """(cfg, attention repeats, cycle-scan repeats) per distinct piece of one image / sample of the workload."""
+    if args.workload == "ms":
+        ents = []
+        for h, w in MS_SCALES:
+            base = synth.vitb(h, B=1, H=h, W=w)
+            ents += [(base.replace(shift_x=0, shift_y=0), 6, 0), (base, 6, 0),
+                     (base.replace(shift_x=0, shift_y=0, cycle_scan=1), 0, 4)]      # single-scale modules
+        Lt = sum(h * w for h, w in MS_SCALES)
+        ents.append((synth.vitb(64, B=1, H=1, W=Lt, shift_x=0, shift_y=0, cycle_scan=1), 0, 4))  # multi-scale
+        return ents
+    _, _, cfgs = workload(args.workload)
+    return [(c.replace(B=1), 1, 1 if c.cycle_scan else 0) for c in cfgs]
+
+
+def reference_items(entries):
     """The reference arm's bounded samples: every layer split into oracle pieces, each timed on a sample of its
     independent units and scaled back up (projections: 1/16 of the token rows; window attention: one window
     row of the padded grid; cycle-scan SSM: the sequential recurrence over the first 1/16 of the 3L tokens,
     all channels — the oracle's cost per token row / window row / scan token is uniform, so each sample times
-    a fixed fraction of the layer's work)."""
+    a fixed fraction of the layer's work). entries: (cfg, attention repeats, cycle-scan repeats)."""
     import oracle
     items = []
-    for j, c in enumerate(cfgs):
+    for j, (c, na, ncs) in enumerate(entries):
         x = synth.make_input(c, layer=0)
         w = synth.make_weights(c, layer=j)
         T = c.H * c.W
-        rows = np.arange(0, T, 16)
-        xr = x.reshape(T, c.C)[rows]
+        if na:
+            rows = np.arange(0, T, 16)
+            xr = x.reshape(T, c.C)[rows]
 
-        def proj(xr=xr, w=w, c=c):
-            u = oracle.layer_norm(xr, w["ln1_g"], w["ln1_b"], c.ln_eps)
+            def proj(xr=xr, w=w, c=c):
+                u = oracle.layer_norm(xr, w["ln1_g"], w["ln1_b"], c.ln_eps)
+                qkv = u @ w["w_qkv"].T + w["b_qkv"]
+                _ = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
+                return qkv[:, :c.C] @ w["w_o"].T + w["b_o"]
+            items.append((f"E{j} ln+qkv+out-proj", proj, na * T / len(rows)))
+            u = oracle.layer_norm(x, w["ln1_g"], w["ln1_b"], c.ln_eps)
             qkv = u @ w["w_qkv"].T + w["b_qkv"]
-            _ = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
-            return qkv[:, :c.C] @ w["w_o"].T + w["b_o"]
-        items.append((f"L{j} ln+qkv+out-proj", proj, T / len(rows)))
-        u = oracle.layer_norm(x, w["ln1_g"], w["ln1_b"], c.ln_eps)
-        qkv = u @ w["w_qkv"].T + w["b_qkv"]
-        qkv_p = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
-        pt, _, pb, _ = oracle.shifted_geometry(c.H, c.W, c.window, c.shift_x, c.shift_y)
-        nwy = (c.H + pt + pb) // c.window
+            qkv_p = w["pad"] @ w["w_qkv"].T + w["b_qkv"]
+            pt, _, pb, _ = oracle.shifted_geometry(c.H, c.W, c.window, c.shift_x, c.shift_y)
+            nwy = (c.H + pt + pb) // c.window
 
-        def attn(qkv=qkv, qkv_p=qkv_p, c=c, nwy=nwy):
-            return oracle.attention_core_padded(qkv, qkv_p, c.H, c.W, c.heads, c.window, c.shift_x, c.shift_y,
-                                                c.pad_mode, c.rope, window_rows=[nwy // 2])
-        items.append((f"L{j} window attention", attn, nwy))
-        if c.cycle_scan:
+            def attn(qkv=qkv, qkv_p=qkv_p, c=c, nwy=nwy):
+                return oracle.attention_core_padded(qkv, qkv_p, c.H, c.W, c.heads, c.window, c.shift_x, c.shift_y,
+                                                    c.pad_mode, c.rope, window_rows=[nwy // 2])
+            items.append((f"E{j} window attention", attn, na * nwy))
+        if ncs:
             L, D = T, c.D
             rows3 = np.arange(0, 3 * L, 16)
 
@@ -478,14 +586,14 @@ def reference_items(cfgs):
                 X3 = np.concatenate([u0, u0, u0])[rows3]
                 xz = X3 @ w["w_in"].T
                 return xz[:, :c.D] @ w["w_out"].T
-            items.append((f"L{j} cycle-scan LN+in/out-proj", cs_proj, 3 * L / len(rows3)))
+            items.append((f"E{j} cycle-scan LN+in/out-proj", cs_proj, ncs * 3 * L / len(rows3)))
             u0 = oracle.layer_norm(x, w["lns_g"], w["lns_b"], c.ln_eps).reshape(L, c.C)
-            xz = np.concatenate([u0, u0, u0]) @ w["w_in"].T
             n3 = 3 * L // 16
+            xz = np.concatenate([u0, u0, u0])[:n3] @ w["w_in"].T
 
-            def cs_ssm(xz=xz, w=w, c=c, n3=n3, D=D):  # the recurrence over the first 1/16 of the 3L tokens
-                return oracle.cycle_ssm_3L(xz[:n3, :D], xz[:n3, D:], w, c.bbar_mode)
-            items.append((f"L{j} cycle-scan SSM", cs_ssm, 3 * L / n3))
+            def cs_ssm(xz=xz, w=w, c=c, D=D):  # the recurrence over the first 1/16 of the 3L tokens
+                return oracle.cycle_ssm_3L(xz[:, :D], xz[:, D:], w, c.bbar_mode)
+            items.append((f"E{j} cycle-scan SSM", cs_ssm, ncs * 3 * L / n3))
     return items
 
 
@@ -493,9 +601,8 @@ def run_reference(args):
     """--impl reference: the fp64 oracle timed as the reference arm, same metric/config. Each step runs one
     bounded sample (reference_items, round-robin) so any --steps K finishes in minutes; value = sum over the
     pieces of (mean sample time x its scale) = oracle ms per image."""
-    label, B, cfgs = workload(args.workload)
-    one = [c.replace(B=1) for c in cfgs]
-    items = reference_items(one)
+    label = ms_workload()[0] if args.workload == "ms" else workload(args.workload)[0]
+    items = reference_items(reference_entries(args))
     for i in range(max(args.warmup, 1)):
         items[i % len(items)][1]()
     times = {}
@@ -516,7 +623,7 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(n_run, 1), 2),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": label, "images_per_rank": 1, "layers": len(one)},
+            "config": {"workload": label, "images_per_rank": 1, "pieces": len(items)},
             "cpu_baseline": {"value": round(ms_img, 2), "unit": "ms/image", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": round(ms_img, 2), "unit": "ms/image", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -529,7 +636,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="1024", choices=["1024", "2048", "4096"])
+    ap.add_argument("--workload", default="1024", choices=["1024", "2048", "4096", "ms"],
+                    help="1024: configs[1] (default); 2048 / 4096: the 12-layer stacks (configs[2], [3]); "
+                         "ms: HRSAM++ multi-scale (configs[4])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="also print the per-kernel table to stderr")
@@ -554,6 +663,8 @@ def main():
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.shard == "rows":
+        if args.workload == "ms":
+            raise SystemExit("--shard rows splits one image (config 4); the multi-scale workload shards by sample")
         if args.workload == "1024" and "--workload" not in sys.argv:
             args.workload = "4096"  # config 4 is the row-sharded 4096^2 stack
         res = run_rows(args, rank, world, local_rank)
@@ -591,8 +702,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": round(res["total_ms"] / args.steps, 4),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded splitmix64; random-init ViT-B PSCWin weights)",
-            "config": {"workload": res["label"], "grid": f"{c0.H}x{c0.W}", "images_per_rank": res["B"],
-                       "layers": [("CS+" if c.cycle_scan else "") + ("S" if c.shift_x else "P") for c in res["cfgs"]],
+            "config": {"workload": res["label"],
+                       "grid": ("+".join(f"{h}x{w}" for h, w in MS_SCALES) if args.workload == "ms"
+                                else f"{c0.H}x{c0.W}"),
+                       "images_per_rank": res["B"], "layers": res["kinds"],
                        "C": c0.C, "heads": c0.heads, "window": c0.window, "shift": 8, "ssm_state": c0.N,
                        "ssm_expand": c0.ssm_expand, "pad_mode": "learnable", "parallelism": f"images x{world}",
                        "l2": "flushed before every timed step (256 MiB write)",

@@ -157,6 +157,41 @@ size_t pscwin_workspace_bytes(const pscwin_layer_desc* desc);
 int pscwin_forward(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
                    void* workspace, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- HRSAM++ multi-scale */
+/* PAPER.md §3.4 "Multi-scale Fusion": the token grids of several input scales are concatenated
+ * into one sequence ("patchified and concatenated ... (HW + H_sW_s)/16^2"). Window attention runs on
+ * every scale's own grid ("tokens from the same scale remain contiguous", block-diagonal over windows; no window
+ * spans two scales); the cycle-scan module runs SINGLE-SCALE ("splits the tokens by scale, scan each scale's
+ * tokens separately") or MULTI-SCALE ("directly performs the SSM across the tokens from all the scales").
+ * Packing (reading Q20): scale outermost — scale s occupies packed rows [B*off_s, B*off_{s+1}) as a
+ * [B, H[s], W[s], C] grid, off_s = sum of the earlier scales' H*W (B = 1: the paper's per-sample concatenation).
+ * The multi-scale SSM scans, per sample, the concatenation of every scale's scan-order sequence (scale order).
+ * RoPE uses each scale's own grid coordinates (Q20). */
+#define PSCWIN_MAX_SCALES 4
+typedef enum { PSCWIN_CS_NONE = 0, PSCWIN_CS_SINGLE_SCALE = 1, PSCWIN_CS_MULTI_SCALE = 2 } pscwin_cs_mode;
+typedef struct {
+  pscwin_layer_desc layer;     /* B, C, heads, window, shifts, pad_mode, rope, ssm_*, scan_order, bbar_mode,
+                                  dtype (BF16 only here), ln_eps; layer.H / layer.W / layer.cycle_scan ignored */
+  int32_t n_scales;            /* 1 .. PSCWIN_MAX_SCALES                                                      */
+  int32_t H[PSCWIN_MAX_SCALES], W[PSCWIN_MAX_SCALES];  /* token grid of each scale, in packing order          */
+  int32_t attention;           /* 1: run the multi-scale window-attention sub-layer; 0: cycle-scan module only */
+  int32_t cycle_scan;          /* pscwin_cs_mode of the cycle-scan module run before attention                 */
+} pscwin_ms_desc;
+/* Windows of all scales (sum of pscwin_window_count over the scales; ERR_CONTRACT as for each scale). */
+int pscwin_ms_window_count(const pscwin_ms_desc* desc, int32_t* n_windows /* host, out */);
+/* Host-side multi-scale indexing operator (App. C): destination = scale 0's windows (row-major,
+ * slots row-major) then scale 1's, ...; value = source position in ONE sample's packed sequence (scale s token
+ * y*W[s]+x at off_s + y*W[s] + x) or 0xFFFFFFFF (PAD). host_map holds n_windows * window^2 entries. */
+int pscwin_ms_index_map(const pscwin_ms_desc* desc, uint32_t* host_map);
+size_t pscwin_ms_workspace_bytes(const pscwin_ms_desc* desc);
+/* One HRSAM++ layer over a packed multi-scale sequence: [cycle-scan module (single- or multi-scale)] then
+ * [x += multi-scale window attention]. x_in, x_out [B * sum_s H[s]*W[s], C] bf16 (x_out may alias x_in).
+ * Errors: ERR_CONTRACT for a scale grid that violates the layer's window contract (plain windows: H, W divisible
+ * by window) or a scan shorter than conv_k - 1 tokens; ERR_UNSUPPORTED for dtype F32.
+ * Workspace: pscwin_ms_workspace_bytes(desc). */
+int pscwin_ms_forward(const pscwin_ms_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
+                      void* workspace, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------- row bands (multi-GPU, §8(e)) */
 /* Window-row sharding of ONE image (B = 1) over `world` ranks, one band of token rows per rank (SURVEY §8(e),
  * config 4; cycle-scan carries per SURVEY Appendix A). row_begin / row_end are multiples of the window (the

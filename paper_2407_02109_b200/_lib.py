@@ -18,6 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libpscwin.so")
 OK, ERR_SHAPE, ERR_CONTRACT, ERR_ALIGN, ERR_WORKSPACE, ERR_CUDA, ERR_UNSUPPORTED = range(7)
 BF16, F32 = 0, 1
 PAD_LEARNABLE, PAD_MASKED = 0, 1
+CS_NONE, CS_SINGLE_SCALE, CS_MULTI_SCALE = 0, 1, 2
+MAX_SCALES = 4
 
 # every symbol include/pscwin.h declares (checked by tests/test_abi_cpu.py)
 EXPORTS = [
@@ -28,6 +30,7 @@ EXPORTS = [
     "pscwin_launch_count", "pscwin_profile_enable", "pscwin_profile_read",
     "pscwin_band_workspace_bytes", "pscwin_band_io_offsets", "pscwin_band_scan_begin", "pscwin_band_scan_mid",
     "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
+    "pscwin_ms_window_count", "pscwin_ms_index_map", "pscwin_ms_workspace_bytes", "pscwin_ms_forward",
 ]
 
 
@@ -69,6 +72,29 @@ class LayerWeights(ctypes.Structure):
             if name in t and t[name] is not None:
                 setattr(w, name, t[name].data_ptr())
         return w
+
+
+class MSDesc(ctypes.Structure):
+    """pscwin_ms_desc: one HRSAM++ layer over a packed multi-scale sequence (scale-outermost packing, Q20)."""
+    _fields_ = [("layer", LayerDesc), ("n_scales", ctypes.c_int32), ("H", ctypes.c_int32 * MAX_SCALES),
+                ("W", ctypes.c_int32 * MAX_SCALES), ("attention", ctypes.c_int32), ("cycle_scan", ctypes.c_int32)]
+
+    @classmethod
+    def make(cls, cfg, scales, attention: int = 1, cycle_scan: int = CS_NONE) -> "MSDesc":
+        if not 1 <= len(scales) <= MAX_SCALES:
+            raise ValueError(f"1..{MAX_SCALES} scales")
+        m = cls()
+        m.layer = LayerDesc.from_config(cfg.replace(H=scales[0][0], W=scales[0][1], cycle_scan=0))
+        m.n_scales = len(scales)
+        for i, (h, w) in enumerate(scales):
+            m.H[i], m.W[i] = h, w
+        m.attention = int(attention)
+        m.cycle_scan = int(cycle_scan)
+        return m
+
+    @property
+    def tokens_per_sample(self) -> int:
+        return sum(self.H[i] * self.W[i] for i in range(self.n_scales))
 
 
 class ScanDesc(ctypes.Structure):
@@ -133,6 +159,11 @@ def lib() -> ctypes.CDLL:
                                     vp, vp, sz, vp], ctypes.c_int),
         "pscwin_band_attn_end": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
                                   vp, vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_ms_window_count": ([ctypes.POINTER(MSDesc), ctypes.POINTER(i32)], ctypes.c_int),
+        "pscwin_ms_index_map": ([ctypes.POINTER(MSDesc), vp], ctypes.c_int),
+        "pscwin_ms_workspace_bytes": ([ctypes.POINTER(MSDesc)], sz),
+        "pscwin_ms_forward": ([ctypes.POINTER(MSDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
+                              ctypes.c_int),
         "pscwin_launch_count": ([], ctypes.c_int64),
         "pscwin_profile_enable": ([ctypes.c_int], None),
         "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],
@@ -181,4 +212,14 @@ def index_map(H: int, W: int, window: int, sx: int = 0, sy: int = 0) -> np.ndarr
     n = window_count(H, W, window, sx, sy)
     out = np.empty(n * window * window, dtype=np.uint32)
     check(lib().pscwin_index_map(H, W, window, sx, sy, out.ctypes.data), "index_map")
+    return out
+
+
+def ms_index_map(desc: "MSDesc") -> np.ndarray:
+    """Multi-scale indexing operator (App. C over a packed multi-scale sequence), host-side."""
+    n = ctypes.c_int32()
+    check(lib().pscwin_ms_window_count(ctypes.byref(desc), ctypes.byref(n)), "ms_window_count")
+    w = desc.layer.window
+    out = np.empty(n.value * w * w, dtype=np.uint32)
+    check(lib().pscwin_ms_index_map(ctypes.byref(desc), out.ctypes.data), "ms_index_map")
     return out

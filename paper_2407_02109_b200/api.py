@@ -11,8 +11,8 @@ from typing import Dict, Optional
 
 import torch
 
-from ._lib import (BF16, F32, LayerDesc, LayerWeights, ScanDesc, check, index_map, lib,  # noqa: F401
-                   window_count)
+from ._lib import (BF16, CS_MULTI_SCALE, CS_NONE, CS_SINGLE_SCALE, F32, LayerDesc, LayerWeights,  # noqa: F401
+                   MSDesc, ScanDesc, check, index_map, lib, ms_index_map, window_count)
 
 
 def _stream() -> int:
@@ -162,6 +162,37 @@ class PSCWinLayer:
 
     def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         return forward(self.desc, self.weights, x, out=out, ws=self.ws, wts=self.wts)
+
+
+def ms_workspace_bytes(desc: MSDesc) -> int:
+    return int(lib().pscwin_ms_workspace_bytes(ctypes.byref(desc)))
+
+
+def ms_forward(desc: MSDesc, weights: Dict[str, torch.Tensor], x: torch.Tensor, out: Optional[torch.Tensor] = None,
+               ws: Optional[Workspace] = None, wts: Optional[LayerWeights] = None) -> torch.Tensor:
+    """pscwin_ms_forward: x, out [B * sum_s H_s W_s, C] bf16, scale-outermost packing (include/pscwin.h)."""
+    ws = ws or Workspace(ms_workspace_bytes(desc), x.device)
+    if out is None:
+        out = torch.empty_like(x)
+    wts = wts or LayerWeights.from_tensors(weights)
+    check(lib().pscwin_ms_forward(ctypes.byref(desc), ctypes.byref(wts), _ptr(x), _ptr(out), ws.ptr, ws.nbytes,
+                                  _stream()), "ms_forward")
+    return out
+
+
+class PSCWinMSLayer:
+    """One HRSAM++ layer (multi-scale attention and / or a single- or multi-scale cycle-scan module) over a packed
+    multi-scale sequence, with device-resident weights and a persistent workspace."""
+
+    def __init__(self, desc: MSDesc, weights: Dict[str, torch.Tensor]):
+        self.desc = desc
+        self.weights = weights
+        self.wts = LayerWeights.from_tensors(weights)
+        dev = next(iter(weights.values())).device
+        self.ws = Workspace(ms_workspace_bytes(desc), dev)
+
+    def __call__(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        return ms_forward(self.desc, self.weights, x, out=out, ws=self.ws, wts=self.wts)
 
 
 class PSCWinStack:

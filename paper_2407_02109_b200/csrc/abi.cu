@@ -417,6 +417,216 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
 }
 
+// ---------------------------------------------------------------------------- HRSAM++ multi-scale layer
+namespace {
+int ms_geo(const pscwin_ms_desc* m, MsGeo* g) {
+  if (!m || m->n_scales < 1 || m->n_scales > PSCWIN_MAX_SCALES) return PSCWIN_ERR_SHAPE;
+  g->n = m->n_scales;
+  g->off[0] = 0;
+  for (int i = 0; i < 4; ++i) {
+    g->H[i] = i < m->n_scales ? m->H[i] : 1;
+    g->W[i] = i < m->n_scales ? m->W[i] : 1;
+  }
+  for (int i = 0; i < m->n_scales; ++i) {
+    if (m->H[i] <= 0 || m->W[i] <= 0) return PSCWIN_ERR_SHAPE;
+    const long long nx = (long long)g->off[i] + (long long)m->H[i] * m->W[i];
+    if (nx > (1ll << 30)) return PSCWIN_ERR_SHAPE;
+    g->off[i + 1] = (int)nx;
+  }
+  for (int i = m->n_scales + 1; i < 5; ++i) g->off[i] = g->off[m->n_scales];
+  return PSCWIN_OK;
+}
+
+pscwin_layer_desc scale_desc(const pscwin_ms_desc* m, int i) {
+  pscwin_layer_desc d = m->layer;
+  d.H = m->H[i];
+  d.W = m->W[i];
+  d.cycle_scan = 0;
+  return d;
+}
+
+int check_ms(const pscwin_ms_desc* m, MsGeo* g) {
+  int rc = ms_geo(m, g);
+  if (rc) return rc;
+  if (m->layer.dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;
+  if (m->cycle_scan < PSCWIN_CS_NONE || m->cycle_scan > PSCWIN_CS_MULTI_SCALE) return PSCWIN_ERR_CONTRACT;
+  if (!m->attention && !m->cycle_scan) return PSCWIN_ERR_CONTRACT;
+  for (int i = 0; i < m->n_scales; ++i) {
+    pscwin_layer_desc d = scale_desc(m, i);
+    if (!m->attention) d.shift_x = d.shift_y = 0, d.H = d.W = d.window;  // only the shared fields matter
+    rc = check_layer(&d);
+    if (rc) return rc;
+  }
+  return PSCWIN_OK;
+}
+
+struct MsWs {
+  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, scan, total;
+};
+
+MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
+  MsWs w;
+  const pscwin_layer_desc& d = m->layer;
+  const size_t T = (size_t)d.B * g.off[g.n], C = d.C;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  w.u = take(T * C * 2);
+  w.qkv = w.qkv_pad = w.O = w.pad_tab = w.xz = w.g = w.scan = 0;
+  if (m->attention) {
+    w.qkv = take(T * 3 * C * 2);
+    w.qkv_pad = take(3 * C * 4);
+    w.O = take(T * C * 2);
+    size_t pt = 0;
+    for (int i = 0; i < g.n; ++i) {
+      const size_t b = attn_pad_table_bytes(g.H[i], g.W[i], d.C, d.window);
+      pt = b > pt ? b : pt;
+    }
+    w.pad_tab = take(pt);
+  }
+  if (m->cycle_scan) {
+    const size_t D = (size_t)d.ssm_expand * C;
+    w.xz = take(T * 2 * D * 2);
+    w.g = take(T * D * 2);
+    const int R = d.ssm_dt_rank > 0 ? d.ssm_dt_rank : (d.C + 15) / 16;
+    w.scan = take(ms_scan_ws_bytes(d.B, g, m->cycle_scan, (int)D, d.ssm_state, R, d.ssm_conv, d.scan_order));
+  }
+  w.total = off;
+  return w;
+}
+}  // namespace
+
+int pscwin_ms_window_count(const pscwin_ms_desc* m, int32_t* n) {
+  MsGeo g;
+  int rc = ms_geo(m, &g);
+  if (rc) return rc;
+  int tot = 0;
+  for (int i = 0; i < m->n_scales; ++i) {
+    Geo q;
+    rc = geometry(m->H[i], m->W[i], m->layer.window, m->layer.shift_x, m->layer.shift_y, &q);
+    if (rc) return rc;
+    tot += q.nw;
+  }
+  if (n) *n = tot;
+  return PSCWIN_OK;
+}
+
+int pscwin_ms_index_map(const pscwin_ms_desc* m, uint32_t* map) {
+  MsGeo g;
+  int rc = ms_geo(m, &g);
+  if (rc) return rc;
+  if (!map) return PSCWIN_ERR_SHAPE;
+  const int w = m->layer.window;
+  for (int i = 0; i < m->n_scales; ++i) {
+    Geo q;
+    rc = pscwin_index_map(m->H[i], m->W[i], w, m->layer.shift_x, m->layer.shift_y, map);
+    if (rc) return rc;
+    geometry(m->H[i], m->W[i], w, m->layer.shift_x, m->layer.shift_y, &q);
+    const size_t n = (size_t)q.nw * w * w;
+    for (size_t j = 0; j < n; ++j)
+      if (map[j] != 0xFFFFFFFFu) map[j] += (uint32_t)g.off[i];
+    map += n;
+  }
+  return PSCWIN_OK;
+}
+
+size_t pscwin_ms_workspace_bytes(const pscwin_ms_desc* m) {
+  MsGeo g;
+  if (check_ms(m, &g) != PSCWIN_OK) return 0;
+  return plan_ms(m, g).total;
+}
+
+int pscwin_ms_forward(const pscwin_ms_desc* m, const pscwin_layer_weights* wt, const void* x_in, void* x_out,
+                      void* ws, size_t ws_bytes, void* stream) {
+  MsGeo g;
+  int rc = check_ms(m, &g);
+  if (rc) return rc;
+  if (!wt || !x_in || !x_out) return PSCWIN_ERR_SHAPE;
+  const pscwin_layer_desc& d = m->layer;
+  const bool shifted = d.shift_x || d.shift_y;
+  const bool learn_pad = m->attention && shifted && d.pad_mode == PSCWIN_PAD_LEARNABLE;
+  if (learn_pad && !wt->pad) return PSCWIN_ERR_CONTRACT;
+  if (m->attention && (!wt->w_qkv || !wt->w_o || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv || !wt->b_o))
+    return PSCWIN_ERR_SHAPE;
+  MsWs P = plan_ms(m, g);
+  if (!ws || ws_bytes < P.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)d.B * g.off[g.n];
+  const int C = d.C;
+  const void* x = x_in;
+  if (m->cycle_scan) {
+    rc = ms_cycle_scan_module(&d, wt, g, m->cycle_scan, x_in, x_out, ws, P.u, P.xz, P.g, P.scan, P.total - P.scan, s);
+    if (rc) return rc;
+    x = x_out;
+  }
+  if (!m->attention) return PSCWIN_OK;
+  // a4 over every packed row: LN1, QKV GEMM with RoPE at each scale's own grid coordinates (segment table)
+  void* u = wsp(ws, P.u);
+  __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(wsp(ws, P.qkv));
+  float* qkv_pad = reinterpret_cast<float*>(wsp(ws, P.qkv_pad));
+  __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(wsp(ws, P.O));
+  rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d.ln_eps, 0, u, s);
+  if (rc) return status_from(rc);
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = (int)T;
+  a.N = 3 * C;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = qkv;
+  a.ldo = 3 * C;
+  a.epi = EPI_QKV_ROPE;
+  a.prof_name = "gemm_qkv_rope";
+  a.bias = (const float*)wt->b_qkv;
+  a.rope = d.rope;
+  a.HW = g.H[0] * g.W[0];
+  a.Wgrid = g.W[0];
+  a.C = C;
+  a.d_head = C / d.heads;
+  a.nseg = g.n;
+  for (int i = 0; i < g.n; ++i) {
+    a.seg_row[i] = d.B * g.off[i];
+    a.seg_HW[i] = g.H[i] * g.W[i];
+    a.seg_W[i] = g.W[i];
+  }
+  rc = launch_gemm_bf16(u, wt->w_qkv, a, s);
+  if (rc) return status_from(rc);
+  if (learn_pad) {
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, s);
+    if (rc) return status_from(rc);
+  }
+  // a5 + a6 per scale (windows never span scales: the block-diagonal structure of P:L185)
+  LayerWs L;
+  memset(&L, 0, sizeof(L));
+  L.pad_tab = P.pad_tab;
+  for (int i = 0; i < g.n; ++i) {
+    pscwin_layer_desc di = scale_desc(m, i);
+    const long long r0 = (long long)d.B * g.off[i];
+    rc = attention_impl(&di, qkv + r0 * 3 * C, learn_pad ? qkv_pad : nullptr, O + r0 * C, ws, L, s);
+    if (rc) return status_from(rc);
+  }
+  // a7 over every packed row: x_out = x + O W_o^T + b_o
+  memset(&a, 0, sizeof(a));
+  a.M = (int)T;
+  a.N = C;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = x_out;
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.prof_name = "gemm_out_proj";
+  a.bias = (const float*)wt->b_o;
+  a.residual = x;
+  a.ldr = C;
+  return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
+}
+
 }  // extern "C"
 
 // =================================================================================================== row bands

@@ -213,6 +213,31 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const __nv_bfloat16* 
   *reinterpret_cast<uint4*>(dst + to * ld_dst + c) = *reinterpret_cast<const uint4*>(src + from * ld_src + c);
 }
 
+// Multi-scale row gather / scatter (HRSAM++ multi-scale cycle scan): sequence row (b, t) of the per-sample
+// concatenation of every scale's scan-order sequence <-> packed row B*off[s] + b*L_s + pi_s(t - off[s]) of the
+// scale-outermost packing (reading Q20). ncols % 8 == 0.
+__global__ void __launch_bounds__(256) ms_permute_rows_kernel(const __nv_bfloat16* src, long long ld_src,
+                                                              __nv_bfloat16* dst, long long ld_dst, int B, MsGeo g,
+                                                              int ncols, int order, int w, int scatter) {
+  pdl_trigger();
+  pdl_wait();
+  const int Lt = g.off[g.n], nv = ncols / 8;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * Lt * nv) return;
+  const int c = (int)(idx % nv) * 8;
+  const long long rr = idx / nv;
+  const int b = (int)(rr / Lt), t = (int)(rr - (long long)b * Lt);
+  int sg = 0;
+#pragma unroll
+  for (int q = 1; q < 4; ++q)
+    if (q < g.n && t >= g.off[q]) sg = q;
+  const int Hs = g.H[sg], Ws = g.W[sg];
+  const long long packed =
+      (long long)B * g.off[sg] + (long long)b * Hs * Ws + scan_pi(t - g.off[sg], Hs, Ws, order, w);
+  const long long from = scatter ? rr : packed, to = scatter ? packed : rr;
+  *reinterpret_cast<uint4*>(dst + to * ld_dst + c) = *reinterpret_cast<const uint4*>(src + from * ld_src + c);
+}
+
 // ------------------------------------------------------------------------------------------------- staging
 // Per-chunk token loop with cp.async double buffering: every per-token operand (the shared (delta_low, B, C)
 // row, and this CTA's slice of v, Delta, z) lands in shared memory one sub-chunk ahead of its use, so the
@@ -1315,6 +1340,119 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   a.ldr = C;
   rc = launch_gemm_bf16(g, w->w_out, a, s);
   return rc ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
+// ------------------------------------------------------------------------------------------------- multi-scale
+static bool ms_needs_perm(int B, int order) { return B > 1 || order != PSCWIN_SCAN_ROW_MAJOR; }
+
+size_t ms_scan_ws_bytes(int B, const MsGeo& g, int mode, int D, int N, int R, int k, int order) {
+  if (mode == 1) {
+    size_t m = 0;
+    for (int i = 0; i < g.n; ++i) {
+      const size_t b = scan_ws_bytes(B, g.H[i] * g.W[i], D, N, R, k, order);
+      m = b > m ? b : m;
+    }
+    return m;
+  }
+  const int Lt = g.off[g.n];
+  size_t pre = ms_needs_perm(B, order) ? al256((size_t)B * Lt * 2 * D * 2) + al256((size_t)B * Lt * D * 2) : 0;
+  return pre + plan_scan(B, Lt, D, N, R, k).total;
+}
+
+int ms_cycle_scan_module(const void* desc_v, const void* wts_v, const MsGeo& g, int mode, const void* x_in,
+                         void* x_out, void* ws, size_t off_u, size_t off_xz, size_t off_g, size_t off_scan,
+                         size_t scan_bytes, cudaStream_t s) {
+  const pscwin_layer_desc* d = reinterpret_cast<const pscwin_layer_desc*>(desc_v);
+  const pscwin_layer_weights* w = reinterpret_cast<const pscwin_layer_weights*>(wts_v);
+  if (!w->lns_g || !w->lns_b || !w->w_in || !w->conv_w || !w->conv_b || !w->w_x || !w->w_dt || !w->b_dt ||
+      !w->a_log || !w->d_skip || !w->w_out)
+    return PSCWIN_ERR_SHAPE;
+  if (mode != 1 && mode != 2) return PSCWIN_ERR_CONTRACT;
+  const int C = d->C, D = d->ssm_expand * C, N = d->ssm_state, B = d->B;
+  const int R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (C + 15) / 16;
+  const int k = d->ssm_conv, order = d->scan_order;
+  const int Lt = g.off[g.n];
+  int rc;
+  for (int i = 0; i < g.n; ++i) {
+    rc = check_order(g.H[i], g.W[i], order, d->window);
+    if (rc) return rc;
+    if (mode == 1 && (rc = check_scan(B, g.H[i] * g.W[i], D, N, R, k))) return rc;
+  }
+  if (mode == 2 && (rc = check_scan(B, Lt, D, N, R, k))) return rc;
+  const long long T = (long long)B * Lt;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(base + off_u);
+  __nv_bfloat16* xz = reinterpret_cast<__nv_bfloat16*>(base + off_xz);
+  __nv_bfloat16* gout = reinterpret_cast<__nv_bfloat16*>(base + off_g);
+  uint8_t* sws = base + off_scan;
+  // a1 over every packed row at once (token-local): u0 = LN_s(x); [xin, SiLU(z)] = u0 W_in^T
+  if (launch_layer_norm(x_in, T, C, (const float*)w->lns_g, (const float*)w->lns_b, d->ln_eps, 0, u, s))
+    return PSCWIN_ERR_CUDA;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_in_proj";
+  a.M = (int)T;
+  a.N = 2 * D;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = xz;
+  a.ldo = 2 * D;
+  a.epi = EPI_STORE_BF16;
+  a.silu_col = D;
+  if (launch_gemm_bf16(u, w->w_in, a, s)) return PSCWIN_ERR_CUDA;
+  const float *cw = (const float*)w->conv_w, *cb = (const float*)w->conv_b, *wdt = (const float*)w->w_dt,
+              *bdt = (const float*)w->b_dt;
+  if (mode == 1) {
+    // single-scale: every scale's [B, H_s, W_s] block is its own batch of cycled sequences
+    for (int i = 0; i < g.n; ++i) {
+      const long long r0 = (long long)B * g.off[i];
+      rc = run_cycle_scan_ordered(B, g.H[i], g.W[i], order, d->window, D, N, R, k, d->bbar_mode, xz + r0 * 2 * D,
+                                  2 * D, xz + r0 * 2 * D + D, 2 * D, true, cw, cb, w->w_x, wdt, bdt, w->a_log,
+                                  w->d_skip, gout + r0 * D, D, sws, scan_bytes, s);
+      if (rc) return rc;
+    }
+  } else if (!ms_needs_perm(B, order)) {
+    // multi-scale, one sample, raster order: the packed rows ARE the concatenated sequence
+    rc = run_cycle_scan(1, Lt, D, N, R, k, d->bbar_mode, xz, 2 * D, xz + D, 2 * D, true, cw, cb, w->w_x, wdt, bdt,
+                        w->a_log, w->d_skip, gout, D, sws, scan_bytes, s);
+    if (rc) return rc;
+  } else {
+    // multi-scale: gather [xin | SiLU(z)] rows into per-sample concatenated scan order, scan, scatter the output
+    const size_t one = al256((size_t)T * 2 * D * 2), two = al256((size_t)T * D * 2);
+    if (scan_bytes < one + two) return PSCWIN_ERR_WORKSPACE;
+    __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sws);
+    __nv_bfloat16* os = reinterpret_cast<__nv_bfloat16*>(sws + one);
+    {
+      PSCWIN_PROF("scan_ms_gather", s);
+      const long long n = T * (2 * D / 8);
+      launch_k(ms_permute_rows_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s,
+               (const __nv_bfloat16*)xz, (long long)2 * D, xs, (long long)2 * D, B, g, 2 * D, order, d->window, 0);
+    }
+    rc = run_cycle_scan(B, Lt, D, N, R, k, d->bbar_mode, xs, 2 * D, xs + D, 2 * D, true, cw, cb, w->w_x, wdt, bdt,
+                        w->a_log, w->d_skip, os, D, sws + one + two, scan_bytes - one - two, s);
+    if (rc) return rc;
+    {
+      PSCWIN_PROF("scan_ms_scatter", s);
+      const long long n = T * (D / 8);
+      launch_k(ms_permute_rows_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s,
+               (const __nv_bfloat16*)os, (long long)D, gout, (long long)D, B, g, D, order, d->window, 1);
+    }
+  }
+  // a3 over every packed row: x_out = x_in + g W_out^T
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_out_proj_scan";
+  a.M = (int)T;
+  a.N = C;
+  a.K = D;
+  a.lda = D;
+  a.ldb = D;
+  a.out = x_out;
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.residual = x_in;
+  a.ldr = C;
+  return launch_gemm_bf16(gout, w->w_out, a, s) ? PSCWIN_ERR_CUDA : PSCWIN_OK;
 }
 
 }  // namespace pscwin

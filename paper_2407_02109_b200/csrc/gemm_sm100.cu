@@ -270,8 +270,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // (d = 64: axis = half, pair jj -> frequency jj) or one whole head (d = 32: pairs 0-7 x, 8-15 y).
       float rc[16], rs[16];
       if (p.epi == EPI_QKV_ROPE && p.rope) {
-        const int t = (row + p.tok0) % p.HW;
-        const int py = t / p.Wgrid, px = t - py * p.Wgrid;
+        int r = row + p.tok0, HW = p.HW, Wg = p.Wgrid;
+        if (p.nseg > 1) {  // packed multi-scale rows: each scale's grid has its own coordinates (reading Q20)
+          int r0 = 0;
+#pragma unroll
+          for (int sg = 0; sg < 4; ++sg)
+            if (sg < p.nseg && r >= p.seg_row[sg]) {
+              r0 = p.seg_row[sg];
+              HW = p.seg_HW[sg];
+              Wg = p.seg_W[sg];
+            }
+          r -= r0;
+        }
+        const int t = r % HW;
+        const int py = t / Wg, px = t - py * Wg;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
           const int axis = p.d_head == 64 ? half : (jj >= 8);

@@ -35,6 +35,10 @@ struct GemmArgs {
   // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
   int silu_col;
   int tok0;    // RoPE: global token index of GEMM row 0 (a row band of the image; 0 otherwise)
+  // RoPE over a packed multi-scale sequence (HRSAM++): rows [seg_row[s], seg_row[s+1]) hold [B, H_s, W_s] grids
+  // (seg_HW[s] = H_s*W_s, seg_W[s] = W_s); nseg <= 1 = one grid described by HW / Wgrid
+  int nseg;
+  int seg_row[4], seg_HW[4], seg_W[4];
   int stages;  // smem ring depth (set by the launcher)
   int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
 };
@@ -104,6 +108,19 @@ int band_scan_end(int L, int D, int N, int R, int k, int P, int bbar, const __nv
                   const float* w_dt, const float* b_dt, const float* a_log, const float* d_skip, const float* recs,
                   int rank, int world, __nv_bfloat16* out, long long ld_out, void* ws, size_t ws_bytes,
                   cudaStream_t s);
+// packed multi-scale sequence (HRSAM++; reading Q20): scale s holds packed rows
+// [B*off[s], B*off[s+1]) as a [B, H[s], W[s]] grid (off = per-sample token offsets)
+struct MsGeo {
+  int n;
+  int off[5];
+  int H[4], W[4];
+};
+size_t ms_scan_ws_bytes(int B, const MsGeo& g, int mode, int D, int N, int R, int k, int order);
+// cycle-scan module over a packed multi-scale sequence: mode 1 = single-scale (each scale its own cycled
+// sequence), 2 = multi-scale (one cycled sequence per sample over all scales)
+int ms_cycle_scan_module(const void* desc, const void* wts, const MsGeo& g, int mode, const void* x_in, void* x_out,
+                         void* ws, size_t off_u, size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes,
+                         cudaStream_t s);
 // cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
 int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);

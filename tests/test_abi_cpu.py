@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
+import synth
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -108,3 +109,20 @@ def test_band_plan_and_io_offsets(pl):
         assert L.pscwin_band_workspace_bytes(ctypes.byref(d), ctypes.byref(b)) == 0
     col = LayerDesc.from_config(cfg.replace(scan_order=synth.SCAN_COL_MAJOR))
     assert L.pscwin_band_workspace_bytes(ctypes.byref(col), ctypes.byref(BandDesc(0, 32, 0, 8))) == 0
+
+
+@pytest.mark.parametrize("scales,w,sx,sy", [([(4, 4), (2, 2)], 2, 0, 0), ([(16, 16), (8, 8), (24, 8)], 8, 4, 4),
+                                            ([(12, 20), (7, 9), (3, 3), (5, 1)], 4, 1, 3)])
+def test_ms_index_map_matches_oracle(pl, scales, w, sx, sy):
+    desc = pl.MSDesc.make(synth.tiny(window=w, shift_x=sx, shift_y=sy), scales)
+    assert np.array_equal(pl.ms_index_map(desc), oracle.ms_index_map(scales, w, sx, sy))
+
+
+def test_ms_workspace_and_contract(pl):
+    cfg = synth.vitb(64)
+    full = pl.MSDesc.make(cfg.replace(B=2), [(64, 64), (128, 128), (256, 256)], 1, 2)
+    assert pl.ms_workspace_bytes(full) > 0
+    bad = pl.MSDesc.make(cfg.replace(shift_x=0, shift_y=0), [(64, 64), (40, 40)], 1, 0)  # 40 % 16 != 0 (plain)
+    assert pl.ms_workspace_bytes(bad) == 0
+    none = pl.MSDesc.make(cfg, [(64, 64)], 0, 0)                                          # nothing to run
+    assert pl.ms_workspace_bytes(none) == 0
