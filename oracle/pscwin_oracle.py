@@ -428,12 +428,29 @@ def cycle_scan_module(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_part
     return out
 
 
+def gelu(x: np.ndarray) -> np.ndarray:
+    """Exact GELU, x * Phi(x) = 0.5 x (1 + erf(x / sqrt 2)) (ViT / MAE FFN activation; reading Q21)."""
+    from scipy.special import erf
+    return 0.5 * x * (1.0 + erf(x / math.sqrt(2.0)))
+
+
+def ffn_sublayer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg) -> np.ndarray:
+    """The ViT block's FFN ("the typical FFN has a hidden layer dimension of 768x4"), pre-LN residual
+    (reading Q21): x + GELU(LN2(x) W_fc1^T + b_fc1) W_fc2^T + b_fc2."""
+    u = layer_norm(x, wt["ln2_g"], wt["ln2_b"], cfg.ln_eps)
+    h = gelu(u @ wt["w_fc1"].T + wt["b_fc1"])
+    return x + h @ wt["w_fc2"].T + wt["b_fc2"]
+
+
 def pscwin_layer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg) -> np.ndarray:
     """One PSCWin layer: optional cycle-scan module ("prior to the final block of each stage")
-    followed by the plain or padded-shift attention sub-layer."""
+    followed by the plain or padded-shift attention sub-layer, then (cfg.mlp_hidden > 0) the FFN sub-layer."""
     if cfg.cycle_scan:
         x = cycle_scan_module(x, wt, cfg)
-    return attention_sublayer(x, wt, cfg)
+    x = attention_sublayer(x, wt, cfg)
+    if getattr(cfg, "mlp_hidden", 0):
+        x = ffn_sublayer(x, wt, cfg)
+    return x
 
 
 # =============================================================================================
@@ -539,4 +556,6 @@ def ms_layer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, attention: 
         xp = ms_cycle_scan_module(xp, wt, cfg, scales, cycle_scan)
     if attention:
         xp = ms_attention_sublayer(xp, wt, cfg, scales)
+        if getattr(cfg, "mlp_hidden", 0):
+            xp = ffn_sublayer(xp, wt, cfg)
     return xp

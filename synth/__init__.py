@@ -123,6 +123,7 @@ class LayerConfig:
     bbar_mode: int = BBAR_ZOH
     dtype: str = "bf16"           # "bf16" or "f32"
     ln_eps: float = 1e-6
+    mlp_hidden: int = 0           # FFN hidden width (768 x 4); 0 = no FFN sub-layer
 
     @property
     def d_head(self) -> int:
@@ -221,6 +222,14 @@ def make_weights(cfg: LayerConfig, layer: int = 0, peaky: bool = False) -> Dict[
     w["a_log"] = _store(np.log(np.tile(np.arange(1, N + 1, dtype=np.float64), (D, 1))), "f32", cfg)
     w["d_skip"] = _store(np.ones(D), "f32", cfg)
     w["w_out"] = _store(0.02 * g(19, C * D).reshape(C, D), "mat", cfg)
+    # FFN sub-layer ("the typical FFN has a hidden layer dimension of 768x4"; reading Q21)
+    Hd = cfg.mlp_hidden if cfg.mlp_hidden > 0 else 4 * C
+    w["ln2_g"] = _store(1.0 + 0.1 * g(21, C), "f32", cfg)
+    w["ln2_b"] = _store(0.02 * g(22, C), "f32", cfg)
+    w["w_fc1"] = _store(0.02 * g(23, Hd * C).reshape(Hd, C), "mat", cfg)
+    w["b_fc1"] = _store(0.02 * g(24, Hd), "f32", cfg)
+    w["w_fc2"] = _store(0.02 * g(25, C * Hd).reshape(C, Hd), "mat", cfg)
+    w["b_fc2"] = _store(0.02 * g(26, C), "f32", cfg)
     return w
 
 

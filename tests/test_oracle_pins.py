@@ -503,3 +503,30 @@ def test_scan_orders_are_permutations(order):
         assert list(pi[:3]) == [0, 12, 24]
     else:
         assert list(pi[:6]) == [0, 1, 2, 3, 12, 13]
+
+
+# ------------------------------------------------------------------------------------------
+# FFN sub-layer (NEXT-2): library routines and GELU closed forms
+# ------------------------------------------------------------------------------------------
+
+def test_gelu_closed_forms():
+    x = np.array([0.0, 1.0, -1.0, 3.0, -7.5, 40.0])
+    g = oracle.gelu(x)
+    assert g[0] == 0.0 and abs(g[-1] - 40.0) < 1e-12           # GELU(0) = 0, GELU(x) -> x
+    assert np.max(np.abs(g - oracle.gelu(-x) - x)) < 1e-15     # x Phi(x) - (-x) Phi(-x) = x
+    assert abs(g[1] - 0.8413447460685429) < 1e-15              # Phi(1) (normal table)
+    ref = F.gelu(torch.from_numpy(x)).numpy()                   # exact (erf) GELU of the library
+    assert np.max(np.abs(g - ref)) < 1e-14
+
+
+def test_ffn_sublayer_vs_torch():
+    cfg = synth.tiny(mlp_hidden=256, dtype="f32")
+    x, wt = synth.make_input(cfg), synth.make_weights(cfg)
+    t = {k: torch.from_numpy(v) for k, v in wt.items()}
+    xt = torch.from_numpy(x)
+    u = F.layer_norm(xt, (cfg.C,), t["ln2_g"], t["ln2_b"], cfg.ln_eps)
+    ref = xt + F.linear(F.gelu(F.linear(u, t["w_fc1"], t["b_fc1"])), t["w_fc2"], t["b_fc2"])
+    assert np.max(np.abs(oracle.ffn_sublayer(x, wt, cfg) - ref.numpy())) < 1e-12
+    # the layer applies it after attention
+    assert np.array_equal(oracle.pscwin_layer(x, wt, cfg),
+                          oracle.ffn_sublayer(oracle.attention_sublayer(x, wt, cfg), wt, cfg))
