@@ -34,8 +34,11 @@ import numpy as np  # noqa: E402
 import synth  # noqa: E402
 
 F32_KEYS = {"ln1_g", "ln1_b", "b_qkv", "b_o", "lns_g", "lns_b", "conv_w", "conv_b", "w_dt", "b_dt", "a_log",
-            "d_skip"}
+            "d_skip", "ln2_g", "ln2_b", "b_fc1", "b_fc2"}
 METRIC = "PSCWin encoder-layer latency ms/image"
+
+
+FFN_HIDDEN = 0   # set by --ffn: 3072 = 768 x 4, the FFN sub-layer after every attention sub-layer
 
 
 def workload(name: str):
@@ -55,7 +58,9 @@ def workload(name: str):
     for i in range(n_layers):
         shifted, cs = synth.stack_layer_kind(i)
         cfgs.append(synth.vitb(side, B=B, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0,
-                               cycle_scan=int(cs)))
+                               cycle_scan=int(cs), mlp_hidden=FFN_HIDDEN))
+    if FFN_HIDDEN:
+        label += f" + FFN {FFN_HIDDEN}"
     return label, B, cfgs
 
 
@@ -72,12 +77,14 @@ def ms_workload():
     specs = []
     for i in range(12):
         shifted, cs = synth.stack_layer_kind(i)
-        cfg = synth.vitb(64, B=B, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0)
+        cfg = synth.vitb(64, B=B, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, mlp_hidden=FFN_HIDDEN)
         specs.append((cfg, 1, 1 if cs else 0, i))
         if cs:
             specs.append((synth.vitb(64, B=B, shift_x=0, shift_y=0), 0, 2, 100 + i))
     label = ("HRSAM++ multi-scale: 64^2+128^2+256^2 token grids packed per sample (86016 tokens), 12-layer stack "
              "+ 4 single-scale and 4 multi-scale cycle-scan modules; ViT-B bf16")
+    if FFN_HIDDEN:
+        label += f" + FFN {FFN_HIDDEN}"
     return label, B, specs
 
 
@@ -86,9 +93,11 @@ def layer_metas(args):
     if args.workload == "ms":
         _, B, specs = ms_workload()
         T = B * sum(h * w for h, w in MS_SCALES)
-        return [dict(T=T, C=c.C, D=c.D, N=c.N, R=c.R, attn=a, cs=int(cs > 0)) for c, a, cs, _ in specs]
+        return [dict(T=T, C=c.C, D=c.D, N=c.N, R=c.R, attn=a, cs=int(cs > 0), Hd=c.mlp_hidden * a)
+                for c, a, cs, _ in specs]
     _, _, cfgs = workload(args.workload)
-    return [dict(T=c.B * c.H * c.W, C=c.C, D=c.D, N=c.N, R=c.R, attn=1, cs=int(c.cycle_scan)) for c in cfgs]
+    return [dict(T=c.B * c.H * c.W, C=c.C, D=c.D, N=c.N, R=c.R, attn=1, cs=int(c.cycle_scan), Hd=c.mlp_hidden)
+            for c in cfgs]
 
 
 # ----------------------------------------------------------------------------------------------- roofline
@@ -100,7 +109,7 @@ def kernel_work(label: str, metas):
     scale = 1.0
     for m in metas:
         T, C, D, N, R = m["T"], m["C"], m["D"], m["N"], m["R"]
-        a, cs = m["attn"], m["cs"]
+        a, cs, Hd = m["attn"], m["cs"], m["Hd"]
         if label == "window_attention":
             bound, scale, unit = "hbm", 1e9, "GB/s"
             tot += a * 8.0 * T * C                      # Q,K,V read + O write, bf16, real tokens
@@ -122,9 +131,15 @@ def kernel_work(label: str, metas):
         elif label == "gemm_x_proj":
             bound, scale, unit = "tensor", 1e12, "TFLOP/s"
             tot += cs * 2.0 * T * D * (R + 2 * N)
+        elif label == "gemm_fc1_gelu":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += 2.0 * T * C * Hd
+        elif label == "gemm_fc2":
+            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
+            tot += 2.0 * T * Hd * C
         elif label == "layer_norm":
             bound, scale, unit = "hbm", 1e9, "GB/s"
-            tot += (a + cs) * 4.0 * T * C               # bf16 row read + write
+            tot += (a + cs + (Hd > 0)) * 4.0 * T * C    # bf16 row read + write
         elif label == "conv_silu":
             bound, scale, unit = "hbm", 1e9, "GB/s"
             tot += cs * 4.0 * T * D                     # xin read + v write, bf16
@@ -535,7 +550,7 @@ def reference_entries(args):
     if args.workload == "ms":
         ents = []
         for h, w in MS_SCALES:
-            base = synth.vitb(h, B=1, H=h, W=w)
+            base = synth.vitb(h, B=1, H=h, W=w, mlp_hidden=FFN_HIDDEN)
             ents += [(base.replace(shift_x=0, shift_y=0), 6, 0), (base, 6, 0),
                      (base.replace(shift_x=0, shift_y=0, cycle_scan=1), 0, 4)]      # single-scale modules
         Lt = sum(h * w for h, w in MS_SCALES)
@@ -577,6 +592,10 @@ def reference_items(entries):
                 return oracle.attention_core_padded(qkv, qkv_p, c.H, c.W, c.heads, c.window, c.shift_x, c.shift_y,
                                                     c.pad_mode, c.rope, window_rows=[nwy // 2])
             items.append((f"E{j} window attention", attn, na * nwy))
+            if c.mlp_hidden:
+                def ffn(xr=xr, w=w, c=c):
+                    return oracle.ffn_sublayer(xr, w, c)
+                items.append((f"E{j} FFN", ffn, na * T / len(rows)))
         if ncs:
             L, D = T, c.D
             rows3 = np.arange(0, 3 * L, 16)
@@ -646,8 +665,12 @@ def main():
     ap.add_argument("--shard", default="images", choices=["images", "rows"],
                     help="images: each rank its own image(s) (weak scaling, default); rows: one image split by "
                          "window rows over the ranks with halo / scan-carry exchange (config 4, strong scaling)")
+    ap.add_argument("--ffn", action="store_true",
+                    help="add the FFN sub-layer (hidden 768 x 4, P:L625; SURVEY NEXT-2) after every attention sub-layer")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global FFN_HIDDEN
+    FFN_HIDDEN = 3072 if args.ffn else 0
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -61,6 +61,8 @@ typedef struct {
   int32_t bbar_mode;                  /* pscwin_bbar_mode                                               */
   int32_t dtype;                      /* pscwin_dtype                                                   */
   float ln_eps;                       /* LayerNorm eps (Q15: 1e-6)                                      */
+  int32_t mlp_hidden;                 /* FFN sub-layer hidden width (768 x 4; reading Q21); 0 = none.
+                                         A multiple of 64. x += GELU(LN2(x) W_fc1^T + b_fc1) W_fc2^T + b_fc2 */
 } pscwin_layer_desc;
 
 /* Weights of one layer. Linear weights are nn.Linear-style [out, in], bf16 (dtype BF16).
@@ -68,11 +70,14 @@ typedef struct {
  * V = [2C,3C), head-contiguous, Q3); pad [C] = learnable pad token p; w_o [C, C]; b_o [C] f32.
  * Cycle scan (a1-a3, Mamba-1 block, Q9): lns_g, lns_b [C] f32; w_in [2D, C] (x-branch rows [0,D), z rows
  * [D,2D)); conv_w [D, k] f32; conv_b [D] f32; w_x [R+2N, D] (delta_low, B, C); w_dt [D, R] f32; b_dt [D] f32;
- * a_log [D, N] f32 (A = -exp(a_log)); d_skip [D] f32; w_out [C, D]. Unused pointers may be NULL. */
+ * a_log [D, N] f32 (A = -exp(a_log)); d_skip [D] f32; w_out [C, D].
+ * FFN (mlp_hidden = Hd > 0): ln2_g, ln2_b [C] f32; w_fc1 [Hd, C]; b_fc1 [Hd] f32; w_fc2 [C, Hd]; b_fc2 [C] f32.
+ * Unused pointers may be NULL. */
 typedef struct {
   const void *ln1_g, *ln1_b, *w_qkv, *b_qkv, *pad, *w_o, *b_o;
   const void *lns_g, *lns_b, *w_in, *conv_w, *conv_b, *w_x, *w_dt, *b_dt, *w_out;
   const float *a_log, *d_skip;
+  const void *ln2_g, *ln2_b, *w_fc1, *b_fc1, *w_fc2, *b_fc2;
 } pscwin_layer_weights;
 
 /* ------------------------------------------------------------------------------------------------ info */
@@ -151,7 +156,8 @@ size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* desc);
 
 /* ----------------------------------------------------------------------------------- the whole layer */
 /* One PSCWin layer: [cycle-scan module: x += (cycle_scan(in_proj(LN_s(x)))) W_out^T] then
- * x_out = x + window_attention(qkv_project(x)) W_o^T + b_o. x_in, x_out [B,H,W,C] bf16; x_out may alias
+ * x_out = x + window_attention(qkv_project(x)) W_o^T + b_o, then [FFN sub-layer when mlp_hidden > 0:
+ * x_out += GELU(LN2(x_out) W_fc1^T + b_fc1) W_fc2^T + b_fc2]. x_in, x_out [B,H,W,C] bf16; x_out may alias
  * x_in. Workspace: pscwin_workspace_bytes(desc). */
 size_t pscwin_workspace_bytes(const pscwin_layer_desc* desc);
 int pscwin_forward(const pscwin_layer_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,

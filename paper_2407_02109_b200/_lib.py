@@ -45,7 +45,7 @@ class LayerDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "B", "H", "W", "C", "heads", "window", "shift_x", "shift_y", "pad_mode", "rope", "cycle_scan",
         "ssm_state", "ssm_expand", "ssm_dt_rank", "ssm_conv", "scan_order", "bbar_mode", "dtype")] + \
-        [("ln_eps", ctypes.c_float)]
+        [("ln_eps", ctypes.c_float), ("mlp_hidden", ctypes.c_int32)]
 
     @classmethod
     def from_config(cls, cfg) -> "LayerDesc":
@@ -55,6 +55,8 @@ class LayerDesc(ctypes.Structure):
                 d.dtype = BF16 if getattr(cfg, "dtype", "bf16") == "bf16" else F32
             elif name == "ssm_dt_rank":
                 d.ssm_dt_rank = getattr(cfg, "R", 0)
+            elif name == "mlp_hidden":
+                d.mlp_hidden = getattr(cfg, "mlp_hidden", 0)
             else:
                 setattr(d, name, getattr(cfg, name))
         return d
@@ -63,7 +65,8 @@ class LayerDesc(ctypes.Structure):
 class LayerWeights(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in (
         "ln1_g", "ln1_b", "w_qkv", "b_qkv", "pad", "w_o", "b_o",
-        "lns_g", "lns_b", "w_in", "conv_w", "conv_b", "w_x", "w_dt", "b_dt", "w_out", "a_log", "d_skip")]
+        "lns_g", "lns_b", "w_in", "conv_w", "conv_b", "w_x", "w_dt", "b_dt", "w_out", "a_log", "d_skip",
+        "ln2_g", "ln2_b", "w_fc1", "b_fc1", "w_fc2", "b_fc2")]
 
     @classmethod
     def from_tensors(cls, t: Dict[str, "torch.Tensor"]) -> "LayerWeights":

@@ -1,6 +1,7 @@
 // C-ABI entry points of libpscwin.so (declared and documented in include/pscwin.h): argument / contract
 // validation, workspace planning, TMA descriptor encoding and the per-layer launch sequence.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "../../include/pscwin.h"
@@ -65,6 +66,41 @@ int make_tmap_5d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const
   return r == CUDA_SUCCESS ? 0 : -11;
 }
 
+int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts_v, void* x, void* u, void* h,
+             cudaStream_t s) {
+  const pscwin_layer_weights* w = reinterpret_cast<const pscwin_layer_weights*>(wts_v);
+  int rc = launch_layer_norm(x, T, C, (const float*)w->ln2_g, (const float*)w->ln2_b, eps, 0, u, s);
+  if (rc) return PSCWIN_ERR_CUDA;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_fc1_gelu";
+  a.M = (int)T;
+  a.N = hidden;
+  a.K = C;
+  a.lda = C;
+  a.ldb = C;
+  a.out = h;
+  a.ldo = hidden;
+  a.epi = EPI_STORE_BF16;
+  a.bias = (const float*)w->b_fc1;
+  a.gelu = 1;
+  if (launch_gemm_bf16(u, w->w_fc1, a, s)) return PSCWIN_ERR_CUDA;
+  memset(&a, 0, sizeof(a));
+  a.prof_name = "gemm_fc2";
+  a.M = (int)T;
+  a.N = C;
+  a.K = hidden;
+  a.lda = hidden;
+  a.ldb = hidden;
+  a.out = x;
+  a.ldo = C;
+  a.epi = EPI_RESID_BF16;
+  a.bias = (const float*)w->b_fc2;
+  a.residual = x;  // in place: every output tile reads its own residual tile before storing it
+  a.ldr = C;
+  return launch_gemm_bf16(h, w->w_fc2, a, s) ? PSCWIN_ERR_CUDA : PSCWIN_OK;
+}
+
 }  // namespace pscwin
 
 using namespace pscwin;
@@ -113,12 +149,17 @@ int check_layer(const pscwin_layer_desc* d) {
   if (d->window < 4 || d->window > 64 || (d->window & (d->window - 1))) return PSCWIN_ERR_UNSUPPORTED;
   if (d->pad_mode != PSCWIN_PAD_LEARNABLE && d->pad_mode != PSCWIN_PAD_MASKED) return PSCWIN_ERR_CONTRACT;
   if (d->C % 64) return PSCWIN_ERR_UNSUPPORTED;  // GEMM K tiles
+  if (d->mlp_hidden < 0 || d->mlp_hidden % 64) return PSCWIN_ERR_CONTRACT;
   return PSCWIN_OK;
+}
+
+bool ffn_weights_ok(const pscwin_layer_weights* w) {
+  return w->ln2_g && w->ln2_b && w->w_fc1 && w->b_fc1 && w->w_fc2 && w->b_fc2;
 }
 
 // Workspace layout shared by qkv_project / window_attention / forward.
 struct LayerWs {
-  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, scan, total;
+  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, h, scan, total;
 };
 
 LayerWs plan_layer(const pscwin_layer_desc* d) {
@@ -136,6 +177,7 @@ LayerWs plan_layer(const pscwin_layer_desc* d) {
   w.qkv_pad = take(3 * C * 4);
   w.O = take(T * C * 2);
   w.pad_tab = take(attn_pad_table_bytes(d->H, d->W, d->C, d->window));
+  w.h = d->mlp_hidden > 0 ? take(T * d->mlp_hidden * 2) : 0;
   w.xz = w.g = w.scan = 0;
   if (d->cycle_scan) {
     const size_t D = (size_t)d->ssm_expand * C;
@@ -195,9 +237,9 @@ int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt,
   return 0;
 }
 
-int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv_pad, void* O, void* ws,
-                   const LayerWs& L, cudaStream_t s) {
+AttnArgs attn_args(const pscwin_layer_desc* d, const void* qkv, const float* qkv_pad, void* O, void* pad_tab) {
   AttnArgs a;
+  memset(&a, 0, sizeof(a));
   a.B = d->B;
   a.H = d->H;
   a.W = d->W;
@@ -213,8 +255,37 @@ int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv
   a.qkv = qkv;
   a.qkv_pad = qkv_pad;
   a.out = O;
-  a.pad_tab = wsp(ws, L.pad_tab);
+  a.pad_tab = pad_tab;
+  return a;
+}
+
+int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv_pad, void* O, void* ws,
+                   const LayerWs& L, cudaStream_t s, int tables_ready = 0) {
+  AttnArgs a = attn_args(d, qkv, qkv_pad, O, wsp(ws, L.pad_tab));
+  a.tables_ready = tables_ready;
   return launch_window_attention(a, s);
+}
+
+// A side stream (one per process, created on first use) for the weight-only pad work of a shifted LEARNABLE layer
+// (qkv_pad = p W_qkv^T + b and its rotated pad-key / value tables): forked from the caller's stream at the start
+// of the attention sub-layer and joined before the attention kernel, so it overlaps LN1 + the QKV GEMM instead of
+// sitting on the critical path. Event fork / join is captured into CUDA graphs as graph edges.
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+};
+Side& side() {
+  static Side sd;
+  if (!sd.ok && !sd.s) {
+    if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) == cudaSuccess)
+      sd.ok = getenv("PSCWIN_NO_SIDE_STREAM") == nullptr;
+    else
+      cudaGetLastError();
+  }
+  return sd;
 }
 
 }  // namespace
@@ -376,6 +447,7 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   const bool shifted = d->shift_x || d->shift_y;
   if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE && !wt->pad) return PSCWIN_ERR_CONTRACT;
   if (!wt->w_qkv || !wt->w_o || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  if (d->mlp_hidden > 0 && !ffn_weights_ok(wt)) return PSCWIN_ERR_SHAPE;
   if (d->dtype == PSCWIN_F32) {
     if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
     return forward_f32(d, wt, x_in, x_out, ws, ws_bytes, (cudaStream_t)stream);
@@ -395,10 +467,23 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   void* qkv = wsp(ws, L.qkv);
   float* qkv_pad = reinterpret_cast<float*>(wsp(ws, L.qkv_pad));
   void* O = wsp(ws, L.O);
-  rc = qkv_project_impl(d, wt, x, qkv, (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE) ? qkv_pad : nullptr, ws, L,
-                        s);
+  const bool learn_pad = shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE;
+  Side& sd = side();
+  const bool fork = learn_pad && sd.ok;
+  if (fork) {  // weight-only pad work overlaps LN1 + the QKV GEMM (see side())
+    if (cudaEventRecord(sd.fork, s) != cudaSuccess || cudaStreamWaitEvent(sd.s, sd.fork, 0) != cudaSuccess)
+      return PSCWIN_ERR_CUDA;
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, sd.s);
+    if (rc) return status_from(rc);
+    AttnArgs pa = attn_args(d, qkv, qkv_pad, O, wsp(ws, L.pad_tab));
+    rc = launch_pad_tables(pa, sd.s);
+    if (rc) return status_from(rc);
+    if (cudaEventRecord(sd.join, sd.s) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  }
+  rc = qkv_project_impl(d, wt, x, qkv, (learn_pad && !fork) ? qkv_pad : nullptr, ws, L, s);
   if (rc) return status_from(rc);
-  rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s);
+  if (fork && cudaStreamWaitEvent(s, sd.join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s, fork ? 1 : 0);
   if (rc) return status_from(rc);
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -414,7 +499,11 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   a.bias = (const float*)wt->b_o;
   a.residual = x;
   a.ldr = C;
-  return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
+  rc = launch_gemm_bf16(O, wt->w_o, a, s);
+  if (rc) return status_from(rc);
+  if (d->mlp_hidden > 0)
+    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, L.u), wsp(ws, L.h), s);
+  return PSCWIN_OK;
 }
 
 // ---------------------------------------------------------------------------- HRSAM++ multi-scale layer
@@ -461,7 +550,7 @@ int check_ms(const pscwin_ms_desc* m, MsGeo* g) {
 }
 
 struct MsWs {
-  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, scan, total;
+  size_t u, qkv, qkv_pad, O, pad_tab, h, xz, g, scan, total;
 };
 
 MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
@@ -475,7 +564,7 @@ MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
     return o;
   };
   w.u = take(T * C * 2);
-  w.qkv = w.qkv_pad = w.O = w.pad_tab = w.xz = w.g = w.scan = 0;
+  w.qkv = w.qkv_pad = w.O = w.pad_tab = w.h = w.xz = w.g = w.scan = 0;
   if (m->attention) {
     w.qkv = take(T * 3 * C * 2);
     w.qkv_pad = take(3 * C * 4);
@@ -486,6 +575,7 @@ MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
       pt = b > pt ? b : pt;
     }
     w.pad_tab = take(pt);
+    if (d.mlp_hidden > 0) w.h = take(T * d.mlp_hidden * 2);
   }
   if (m->cycle_scan) {
     const size_t D = (size_t)d.ssm_expand * C;
@@ -551,6 +641,7 @@ int pscwin_ms_forward(const pscwin_ms_desc* m, const pscwin_layer_weights* wt, c
   if (learn_pad && !wt->pad) return PSCWIN_ERR_CONTRACT;
   if (m->attention && (!wt->w_qkv || !wt->w_o || !wt->ln1_g || !wt->ln1_b || !wt->b_qkv || !wt->b_o))
     return PSCWIN_ERR_SHAPE;
+  if (m->attention && d.mlp_hidden > 0 && !ffn_weights_ok(wt)) return PSCWIN_ERR_SHAPE;
   MsWs P = plan_ms(m, g);
   if (!ws || ws_bytes < P.total) return PSCWIN_ERR_WORKSPACE;
   if (!aligned16(x_in) || !aligned16(x_out) || !aligned16(ws)) return PSCWIN_ERR_ALIGN;
@@ -624,7 +715,10 @@ int pscwin_ms_forward(const pscwin_ms_desc* m, const pscwin_layer_weights* wt, c
   a.bias = (const float*)wt->b_o;
   a.residual = x;
   a.ldr = C;
-  return status_from(launch_gemm_bf16(O, wt->w_o, a, s));
+  rc = launch_gemm_bf16(O, wt->w_o, a, s);
+  if (rc) return status_from(rc);
+  if (d.mlp_hidden > 0) return ffn_bf16(T, C, d.mlp_hidden, d.ln_eps, wt, x_out, u, wsp(ws, P.h), s);
+  return PSCWIN_OK;
 }
 
 }  // extern "C"
@@ -677,7 +771,7 @@ pscwin_layer_desc sub_desc(const pscwin_layer_desc* d, int rows, int sy) {
 }
 
 struct BandWs {
-  size_t u, qkv, qkv_pad, O, pad_tab, xz, g, x1, hist_send, hist_recv, rec_send, rec_recv, scan, total;
+  size_t u, qkv, qkv_pad, O, pad_tab, h, xz, g, x1, hist_send, hist_recv, rec_send, rec_recv, scan, total;
   size_t row_bytes_qkv;
   int D, N, R;
 };
@@ -699,6 +793,7 @@ BandWs plan_band(const pscwin_layer_desc* d, const pscwin_band* b, const BandGeo
   w.qkv_pad = take(3 * C * 4);
   w.O = take(Te * C * 2);
   w.pad_tab = take(attn_pad_table_bytes(g.ext_rows, d->W, d->C, d->window));
+  if (d->mlp_hidden > 0) w.h = take(T * d->mlp_hidden * 2);
   if (d->cycle_scan) {
     w.D = d->ssm_expand * d->C;
     w.N = d->ssm_state;
@@ -926,6 +1021,7 @@ int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const
   a.qkv_pad = reinterpret_cast<const float*>(wsp(ws, w.qkv_pad));
   a.out = wsp(ws, w.O);
   a.pad_tab = wsp(ws, w.pad_tab);
+  a.tables_ready = 0;
   rc = launch_window_attention(a, s);
   if (rc) return status_from(rc);
   const void* x = d->cycle_scan ? wsp(ws, w.x1) : x_band;
@@ -944,7 +1040,13 @@ int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const
   o.residual = x;
   o.ldr = C;
   const void* Ob = wsp(ws, w.O + (size_t)g.ht_eff * d->W * C * 2);
-  return status_from(launch_gemm_bf16(Ob, wt->w_o, o, s));
+  rc = launch_gemm_bf16(Ob, wt->w_o, o, s);
+  if (rc) return status_from(rc);
+  if (d->mlp_hidden > 0) {  // the FFN is token-local: it runs on the band's own rows
+    if (!ffn_weights_ok(wt)) return PSCWIN_ERR_SHAPE;
+    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, w.u), wsp(ws, w.h), s);
+  }
+  return PSCWIN_OK;
 }
 
 }  // extern "C"

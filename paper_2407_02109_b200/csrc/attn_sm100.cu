@@ -305,6 +305,22 @@ size_t attn_pad_table_bytes(int H, int W, int C, int w) {
   return (bytes + 255) & ~size_t(255);
 }
 
+int launch_pad_tables(const AttnArgs& a, cudaStream_t stream) {
+  const int d = a.d, w = a.w;
+  const int pl = (w - a.sx) % w, pt = (w - a.sy) % w;
+  const int Wp = pl + a.W + ((-(pl + a.W)) % w + w) % w;
+  const int Hp = pt + a.H + ((-(pt + a.H)) % w + w) % w;
+  if (!a.qkv_pad || !a.pad_tab) return -3;
+  __nv_bfloat16* kx = reinterpret_cast<__nv_bfloat16*>(a.pad_tab);
+  __nv_bfloat16* ky = kx + (size_t)Wp * a.C / 2;
+  __nv_bfloat16* vp = ky + (size_t)Hp * a.C / 2;
+  const int n = (Wp + Hp) * a.C / 2 + a.C;
+  PSCWIN_PROF("pad_tables", stream);
+  launch_k(pad_tables_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, a.qkv_pad, a.C, a.heads, d, Wp, Hp, pl, pt,
+           a.rope, a.row0, kx, ky, vp);
+  return (int)cudaGetLastError();
+}
+
 int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
   const int d = a.d;
   if (!(d == 32 || d == 64)) return -2;
@@ -341,10 +357,10 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
     p.kx = kx;
     p.ky = ky;
     p.vp = vp;
-    int n = (p.Wp + p.Hp) * a.C / 2 + a.C;
-    PSCWIN_PROF("pad_tables", stream);
-    launch_k(pad_tables_kernel, dim3((n + 255) / 256), dim3(256), 0, stream, a.qkv_pad, a.C, a.heads, d, p.Wp, p.Hp, p.pl, p.pt, a.rope,
-             a.row0, kx, ky, vp);
+    if (!a.tables_ready) {
+      const int rc = launch_pad_tables(a, stream);
+      if (rc) return rc;
+    }
   }
   // windows of <= 256 slots: persistent warp-specialised kernel (attn_sm100_ws.cu); PSCWIN_ATTN_V1=1 forces this
   // file's one-CTA-per-(q tile, head, window) kernel, which also serves larger windows.

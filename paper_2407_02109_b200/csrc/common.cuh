@@ -286,6 +286,29 @@ PSCWIN_DEVICE float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+PSCWIN_DEVICE float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// GELU(x) = x Phi(x) = 0.5 x (1 + erf(x / sqrt 2)) with erf from Abramowitz & Stegun 7.1.26
+// (|error| <= 1.5e-7, far below the bf16 rounding of the stored result): erf(z) = 1 - t (a1 + t (a2 + ...)) e^{-z^2},
+// t = 1 / (1 + p z), z = |x| / sqrt 2. Branch-free: two MUFU ops (rcp, ex2) and ten FP32 ops instead of erff's
+// branchy polynomial; used by the FFN fc1 epilogue (reading Q21).
+PSCWIN_DEVICE float gelu_erf(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = rcp_approx(fmaf(0.3275911f, z, 1.f));
+  float q = fmaf(t, 1.061405429f, -1.453152027f);
+  q = fmaf(t, q, 1.421413741f);
+  q = fmaf(t, q, -0.284496736f);
+  q = fmaf(t, q, 0.254829592f);
+  q *= t;
+  const float e = ex2_approx(-z * z * 1.4426950408889634f);
+  const float erfz = fmaf(-q, e, 1.f);
+  return 0.5f * x * (1.f + copysignf(erfz, x));
+}
 // 2^x for a pair on the FMA/ALU pipes (offloads the MUFU, FA4-style): x = n + f with n = round(x), f in
 // [-1/2, 1/2]; 2^f by a degree-3 polynomial (max relative error 7.5e-5 over the interval, fitted in
 // tools/ — ample for bf16 probabilities), 2^n by adding n to the exponent field. Inputs below -126 clamp

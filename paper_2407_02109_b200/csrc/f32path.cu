@@ -30,6 +30,7 @@ struct SgemmArgs {
   const float* residual;  // [M, ldr] or null
   int ldr;
   int silu_col;           // columns >= silu_col get SiLU (0 = off)
+  int gelu;               // 1: exact GELU on every output (FFN fc1)
   int rope, HW, Wgrid, C, d_head;  // 2-D RoPE on q = cols [0, C) and k = [C, 2C) (QKV projection)
 };
 
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(SgemmArgs p) {
       const int col = c0 + j;
       if (col >= p.N) continue;
       float y = v[j];
+      if (p.gelu) y = 0.5f * y * (1.f + erff(y * 0.70710678118654752f));
       if (p.silu_col > 0 && col >= p.silu_col) y = y / (1.f + expf(-y));
       if (p.residual) y += p.residual[(size_t)row * p.ldr + col];
       p.out[(size_t)row * p.ldo + col] = y;
@@ -482,6 +484,7 @@ LayerWsF32 plan_layer_f32(const pscwin_layer_desc* d) {
   w.qkv = take(T * 3 * C * 4);
   w.qkv_pad = take(3 * C * 4);
   w.O = take(T * C * 4);
+  w.h = d->mlp_hidden > 0 ? take(T * d->mlp_hidden * 4) : 0;
   w.xz = w.g = w.scan = w.x1 = 0;
   if (d->cycle_scan) {
     const size_t D = (size_t)d->ssm_expand * C;
@@ -606,6 +609,39 @@ int forward_f32(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, cons
   a.residual = x;
   a.ldr = C;
   if (launch_sgemm(a, s)) return PSCWIN_ERR_CUDA;
+  if (d->mlp_hidden > 0) {  // FFN sub-layer: x_out += GELU(LN2(x_out) W_fc1^T + b_fc1) W_fc2^T + b_fc2
+    const int Hd = d->mlp_hidden;
+    float* h = reinterpret_cast<float*>(base + L.h);
+    rc = launch_layer_norm(x_out, T, C, (const float*)wt->ln2_g, (const float*)wt->ln2_b, d->ln_eps, 1, u, s);
+    if (rc) return PSCWIN_ERR_CUDA;
+    memset(&a, 0, sizeof(a));
+    a.M = (int)T;
+    a.N = Hd;
+    a.K = C;
+    a.A = u;
+    a.lda = C;
+    a.B = (const float*)wt->w_fc1;
+    a.ldb = C;
+    a.out = h;
+    a.ldo = Hd;
+    a.bias = (const float*)wt->b_fc1;
+    a.gelu = 1;
+    if (launch_sgemm(a, s)) return PSCWIN_ERR_CUDA;
+    memset(&a, 0, sizeof(a));
+    a.M = (int)T;
+    a.N = C;
+    a.K = Hd;
+    a.A = h;
+    a.lda = Hd;
+    a.B = (const float*)wt->w_fc2;
+    a.ldb = Hd;
+    a.out = x_out;
+    a.ldo = C;
+    a.bias = (const float*)wt->b_fc2;
+    a.residual = x_out;  // each element's residual is read by the thread that then writes it
+    a.ldr = C;
+    if (launch_sgemm(a, s)) return PSCWIN_ERR_CUDA;
+  }
   return PSCWIN_OK;
 }
 

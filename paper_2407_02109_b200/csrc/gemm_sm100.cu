@@ -51,7 +51,7 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
 // TMEM holds its 128 accumulator rows x BN columns and its own epilogue stores them. Per SM this halves the B
 // bytes per MAC (the L2 -> SM traffic that bounds 1-CTA 128-row tiles).
 template <bool PAIR>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __maxnreg__(200)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      GemmArgs p) {
@@ -352,6 +352,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
         }
+        if (p.gelu) {  // FFN fc1: GELU (erf form, reading Q21)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+        }
         if (p.silu_col > 0 && col0 >= p.silu_col) {  // gate columns: SiLU(x) = x / (1 + e^-x)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
@@ -507,6 +511,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (p.epi == EPI_QKV_ROPE && p.rope && !(p.d_head == 32 || p.d_head == 64)) return -2;
   const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
   if (p.silu_col && (p.silu_col % 32 || p.epi == EPI_STORE_F32)) return -2;
+  if (p.gelu && p.epi != EPI_STORE_BF16) return -2;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
   // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K

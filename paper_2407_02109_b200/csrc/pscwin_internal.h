@@ -34,6 +34,7 @@ struct GemmArgs {
   int* sem;
   // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
   int silu_col;
+  int gelu;    // 1: exact GELU 0.5 x (1 + erf(x / sqrt 2)) on every output (after bias; FFN fc1, reading Q21)
   int tok0;    // RoPE: global token index of GEMM row 0 (a row band of the image; 0 otherwise)
   // RoPE over a packed multi-scale sequence (HRSAM++): rows [seg_row[s], seg_row[s+1]) hold [B, H_s, W_s] grids
   // (seg_HW[s] = H_s*W_s, seg_W[s] = W_s); nseg <= 1 = one grid described by HW / Wgrid
@@ -68,8 +69,11 @@ struct AttnArgs {
   const float* qkv_pad;  // [3C] f32 projection of p (unrotated) or null (plain / masked)
   void* out;             // [B,H,W,C] bf16
   void* pad_tab;         // workspace for rotated pad K halves + V (bf16)
+  int tables_ready;      // 1: pad_tab was already filled by launch_pad_tables (e.g. on a side stream)
 };
 size_t attn_pad_table_bytes(int H, int W, int C, int w);
+// rotated pad-key / pad-value tables of a shifted LEARNABLE layer (depends only on qkv_pad and the geometry)
+int launch_pad_tables(const AttnArgs& a, cudaStream_t stream);
 int launch_window_attention(const AttnArgs& a, cudaStream_t stream);
 int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky, const void* vp, int patch,
                                cudaStream_t stream);
@@ -80,7 +84,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
 namespace pscwin {
 // fp32 correctness path (f32path.cu)
 struct LayerWsF32 {
-  size_t u, qkv, qkv_pad, O, xz, g, scan, x1, total;
+  size_t u, qkv, qkv_pad, O, h, xz, g, scan, x1, total;
 };
 LayerWsF32 plan_layer_f32(const pscwin_layer_desc* d);
 size_t layer_f32_ws_bytes(const pscwin_layer_desc* d);
@@ -121,6 +125,9 @@ size_t ms_scan_ws_bytes(int B, const MsGeo& g, int mode, int D, int N, int R, in
 int ms_cycle_scan_module(const void* desc, const void* wts, const MsGeo& g, int mode, const void* x_in, void* x_out,
                          void* ws, size_t off_u, size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes,
                          cudaStream_t s);
+// FFN sub-layer (NEXT-2): x += GELU(LN2(x) W_fc1^T + b_fc1) W_fc2^T + b_fc2 over T rows, in place; u [T, C] and
+// h [T, hidden] bf16 scratch
+int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts, void* x, void* u, void* h, cudaStream_t s);
 // cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
 int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);

@@ -3,7 +3,7 @@ ABI expects, and the error metric of DESIGN.md "Tolerances" (reading Q17)."""
 import numpy as np
 
 F32_KEYS = {"ln1_g", "ln1_b", "b_qkv", "b_o", "lns_g", "lns_b", "conv_w", "conv_b", "w_dt", "b_dt", "a_log",
-            "d_skip"}
+            "d_skip", "ln2_g", "ln2_b", "b_fc1", "b_fc2"}
 
 
 def dev(a, dtype="bf16"):

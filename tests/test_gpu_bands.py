@@ -30,11 +30,12 @@ CASES = [
     (synth.tiny(H=32, W=16, cycle_scan=1), 4),                             # CS + S
     (synth.tiny(H=32, W=16, cycle_scan=1, bbar_mode=synth.BBAR_EULER), 3),
     (synth.vitb(64, cycle_scan=1), 4),                                     # ViT-B 1024^2 as 4 bands
+    (synth.tiny(H=32, W=16, cycle_scan=1, mlp_hidden=256), 2),             # CS + S + FFN
 ]
 
 
 @pytest.mark.parametrize("cfg,world", CASES, ids=lambda c: str(c) if isinstance(c, int) else
-                         f"{c.H}x{c.W}C{c.C}s{c.shift_x},{c.shift_y}m{c.pad_mode}cs{c.cycle_scan}b{c.bbar_mode}")
+                         f"{c.H}x{c.W}C{c.C}s{c.shift_x},{c.shift_y}m{c.pad_mode}cs{c.cycle_scan}b{c.bbar_mode}f{c.mlp_hidden}")
 def test_bands_equal_whole_image(pl, cfg, world):
     import torch
     from paper_2407_02109_b200.bands import LoopbackBands

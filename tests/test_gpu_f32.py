@@ -38,11 +38,13 @@ LAYERS = [
     f32(cycle_scan=1, bbar_mode=synth.BBAR_EULER),
     f32(cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR),
     f32(cycle_scan=1, scan_order=synth.SCAN_COL_MAJOR, H=12, W=8, shift_x=0, shift_y=0, window=4),
+    f32(mlp_hidden=256),                                           # + FFN sub-layer (NEXT-2)
+    f32(cycle_scan=1, mlp_hidden=192, H=12, W=20, shift_x=2, shift_y=6),
 ]
 
 
 @pytest.mark.parametrize("cfg", LAYERS, ids=lambda c: f"B{c.B}{c.H}x{c.W}C{c.C}w{c.window}s{c.shift_x},{c.shift_y}"
-                                                      f"m{c.pad_mode}r{c.rope}cs{c.cycle_scan}o{c.scan_order}b{c.bbar_mode}")
+                                                      f"m{c.pad_mode}r{c.rope}cs{c.cycle_scan}o{c.scan_order}b{c.bbar_mode}f{c.mlp_hidden}")
 def test_forward_f32(pl, cfg):
     x, w = synth.make_input(cfg), synth.make_weights(cfg)
     layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))

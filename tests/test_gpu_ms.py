@@ -61,16 +61,21 @@ CASES = [
     (synth.tiny(), [(16, 16), (8, 8)], 2, 0, "ms"),                                # cycle-scan module only
     (synth.tiny(shift_x=0, shift_y=0, scan_order=synth.SCAN_WINDOW_MAJOR), [(16, 16), (8, 8)], 1, 1, "ms"),
     (synth.tiny(shift_x=0, shift_y=0, scan_order=synth.SCAN_COL_MAJOR), [(16, 16), (8, 8)], 2, 0, "ss"),
+    (synth.tiny(mlp_hidden=256), [(16, 16), (8, 8)], 2, 1, "ss"),                  # + FFN sub-layer
 ]
 
 
 @pytest.mark.parametrize("cfg,scales,B,attention,cs", CASES,
-                         ids=lambda v: str(v) if not hasattr(v, "H") else f"s{v.shift_x}m{v.pad_mode}o{v.scan_order}")
+                         ids=lambda v: str(v) if not hasattr(v, "H") else f"s{v.shift_x}m{v.pad_mode}o{v.scan_order}f{v.mlp_hidden}")
 def test_ms_layer(pl, cfg, scales, B, attention, cs):
     xp, got, ref = _run(pl, cfg, scales, B, attention, CS[cs])
     assert rel_err(got, ref) < BF16_TOL
+    # the increment x_out - x, scaled by its own magnitude, plus one bf16 half-ulp (<= 2^-8 relative) per residual
+    # store of x (Q16: cycle-scan module, attention, FFN)
+    n_res = int(cs != "none") + attention + int(attention and cfg.mlp_hidden > 0)
     inc = ref - xp
-    assert float(np.max(np.abs((got - xp) - inc))) < BF16_TOL * np.max(np.abs(inc)) + 2.0 ** -8 * np.max(np.abs(ref))
+    assert float(np.max(np.abs((got - xp) - inc))) < BF16_TOL * np.max(np.abs(inc)) + \
+        n_res * 2.0 ** -8 * np.max(np.abs(ref))
 
 
 def test_ms_single_scale_equals_layer_forward(pl):
