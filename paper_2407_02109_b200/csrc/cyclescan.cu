@@ -1036,9 +1036,28 @@ static void launch_pass2(ScanParams& p, cudaStream_t s) {
 
 template <int N>
 static void launch_dt_pass1(ScanParams& p, cudaStream_t s) {
-  {
+  static const bool dt_ffma = getenv("PSCWIN_DT_FFMA") != nullptr;  // A/B knob: the CUDA-core dt kernel
+  const long long rows = (long long)p.B * (p.L + p.P);
+  if (!dt_ffma && p.R % 4 == 0) {
+    // Delta = softplus(delta_low W_dt^T + b_dt) as a TF32 tensor-core GEMM (M = rows, N = D, K = R) reading
+    // delta_low straight out of the x_proj output (row stride R + 2N) with the softplus in the f32 epilogue
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.prof_name = "scan_dt";
+    g.M = (int)rows;
+    g.N = p.D;
+    g.K = p.R;
+    g.lda = p.R + 2 * N;
+    g.ldb = p.R;
+    g.out = p.delta;
+    g.ldo = p.D;
+    g.epi = EPI_STORE_F32;
+    g.bias = p.b_dt;
+    g.tf32 = 1;
+    g.softplus = 1;
+    launch_gemm_bf16(p.dbc, p.w_dt, g, s);
+  } else {
     PSCWIN_PROF("scan_dt", s);
-    const long long rows = (long long)p.B * (p.L + p.P);
     dim3 gdt((p.D + 2 * DT_THREADS - 1) / (2 * DT_THREADS), (unsigned)((rows + DT_ROWS - 1) / DT_ROWS));
     if (p.R <= 16)
       launch_k(scan_dt_kernel<16>, gdt, dim3(DT_THREADS), 0, s, p);

@@ -50,8 +50,11 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
 // reads A rows [0,128) / [128,256) and B rows [0,BN/2) / [BN/2,BN) from the two CTAs' shared memory; each CTA's
 // TMEM holds its 128 accumulator rows x BN columns and its own epilogue stores them. Per SM this halves the B
 // bytes per MAC (the L2 -> SM traffic that bounds 1-CTA 128-row tiles).
-template <bool PAIR>
-__global__ void __maxnreg__(200)
+// EK: epilogue kind, a compile-time specialisation so each variant's registers are allocated for its own work
+// (EK_ROPE keeps 32 cos / sin values per row live across the tile; EK_GELU inlines 32 GELUs per chunk).
+enum { EK_PLAIN = 0, EK_ROPE = 1, EK_GELU = 2, EK_F32 = 3 };
+template <bool PAIR, int EK>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
                      GemmArgs p) {
@@ -86,7 +89,8 @@ __global__ void __maxnreg__(200)
   const int n_tiles = ((p.M + TM - 1) / TM) * n_tiles_n * S;
   const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // this CTA's (pair's) first tile
   const int tstride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const int nk = (p.K + BK - 1) / BK;
+  const int BKe = p.tf32 ? BK / 2 : BK;  // K elements per 128-byte k-block row (bf16: 64, tf32: 32)
+  const int nk = (p.K + BKe - 1) / BKe;
   // work tile -> output tile (m0, n0), k-block range [kb0, kb1) and split index
   auto coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1, int& s) {
     const int mn = tile / S;
@@ -100,7 +104,7 @@ __global__ void __maxnreg__(200)
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (p.epi != EPI_STORE_F32) tma_prefetch_desc(&tmOut);
+    if (p.epi != EPI_STORE_F32 || p.f32_tma) tma_prefetch_desc(&tmOut);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -168,9 +172,9 @@ __global__ void __maxnreg__(200)
             mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
             const uint32_t fb = full0 + stage * 8;
-            if (a_mine) tma_load_2d_pair(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BK, m0 + mrow, pol_a);
+            if (a_mine) tma_load_2d_pair(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BKe, m0 + mrow, pol_a);
             if (b_mine)
-              tma_load_2d_pair(sB + stage * B_STAGE_BYTES, &tmB, fb, kb * BK, n0 + (int)rank * (BN / 2), pol_b);
+              tma_load_2d_pair(sB + stage * B_STAGE_BYTES, &tmB, fb, kb * BKe, n0 + (int)rank * (BN / 2), pol_b);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -180,8 +184,8 @@ __global__ void __maxnreg__(200)
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
-            tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BK, m0, pol_a);
-            tma_load_2d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BK, n0, pol_b);
+            tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BKe, m0, pol_a);
+            tma_load_2d(sB + stage * B_STAGE_BYTES, &tmB, &full[stage], kb * BKe, n0, pol_b);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -192,7 +196,7 @@ __global__ void __maxnreg__(200)
     }
   } else if (warp == 1) {
     if (!PAIR || rank == 0) {
-      const uint32_t idesc = make_idesc_bf16(TM, BN, 0, 0);
+      const uint32_t idesc = p.tf32 ? make_idesc_tf32(TM, BN) : make_idesc_bf16(TM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -219,10 +223,17 @@ __global__ void __maxnreg__(200)
             for (int k = 0; k < BK / 16; ++k) {
               uint64_t ad = make_sdesc(a0 + k * 32, 16, 1024, kLayoutSW128);
               uint64_t bd = make_sdesc(b0 + k * 32, 16, 1024, kLayoutSW128);
-              if (PAIR)
-                umma_ss_pair(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-              else
-                umma_ss(d_tmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+              if (p.tf32) {
+                if (PAIR)
+                  umma_ss_pair_tf32(d_tmem, ad, bd, idesc, accum);
+                else
+                  umma_ss_tf32(d_tmem, ad, bd, idesc, accum);
+              } else if (PAIR) {
+                umma_ss_pair(d_tmem, ad, bd, idesc, accum);
+              } else {
+                umma_ss(d_tmem, ad, bd, idesc, accum);
+              }
             }
             if (PAIR) {
               umma_commit_pair_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
@@ -252,7 +263,8 @@ __global__ void __maxnreg__(200)
     const int lane = lane_id();
     const int etid = threadIdx.x - 64;                 // 0..255
     const bool issuer = etid == 0;
-    const bool tma_out = p.epi != EPI_STORE_F32;
+    const bool tma_out = EK != EK_F32;
+    const bool f32_tma = EK == EK_F32 && S == 1 && p.f32_tma;  // f32 tiles staged in smem, TMA-stored
     const int row_local = quarter * 32 + lane;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -268,8 +280,8 @@ __global__ void __maxnreg__(200)
       const bool row_ok = row < p.M;
       // RoPE of this row (QKV epilogue): this thread's 32 columns of every 64-column chunk are one half of a head
       // (d = 64: axis = half, pair jj -> frequency jj) or one whole head (d = 32: pairs 0-7 x, 8-15 y).
-      float rc[16], rs[16];
-      if (p.epi == EPI_QKV_ROPE && p.rope) {
+      float rc[EK == EK_ROPE ? 16 : 1], rs[EK == EK_ROPE ? 16 : 1];
+      if (EK == EK_ROPE && p.rope) {
         int r = row + p.tok0, HW = p.HW, Wg = p.Wgrid;
         if (p.nseg > 1) {  // packed multi-scale rows: each scale's grid has its own coordinates (reading Q20)
           int r0 = 0;
@@ -284,11 +296,13 @@ __global__ void __maxnreg__(200)
         }
         const int t = r % HW;
         const int py = t / Wg, px = t - py * Wg;
+        if constexpr (EK == EK_ROPE) {
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int axis = p.d_head == 64 ? half : (jj >= 8);
-          const int fj = p.d_head == 64 ? jj : (jj & 7);
-          rope_cs(axis ? py : px, fj, p.d_head, rc[jj], rs[jj]);
+          for (int jj = 0; jj < 16; ++jj) {
+            const int axis = p.d_head == 64 ? half : (jj >= 8);
+            const int fj = p.d_head == 64 ? jj : (jj & 7);
+            rope_cs(axis ? py : px, fj, p.d_head, rc[jj], rs[jj]);
+          }
         }
       }
       // bias of the tile's columns staged once in shared memory (read back as broadcasts), double-buffered by
@@ -306,7 +320,7 @@ __global__ void __maxnreg__(200)
           }
           reinterpret_cast<float4*>(sb)[etid] = b4;
         }
-        if (!tma_out) named_bar_sync(1, 256);  // (the bf16 path's first chunk barrier orders it otherwise)
+        if (!tma_out && !f32_tma) named_bar_sync(1, 256);  // (the staged paths' chunk barrier orders it otherwise)
       }
       if (PAIR)
         mbar_wait_cluster(&tfull[acc], acc_phase);
@@ -329,6 +343,9 @@ __global__ void __maxnreg__(200)
         if (tma_out) {
           if (issuer && gseq >= 2) bulk_wait_read1();
           named_bar_sync(1, 256);
+        } else if (f32_tma) {  // both staging buffers hold this chunk (two 128 x 32 f32 boxes): the previous
+          if (issuer && gseq >= 1) bulk_wait_read0();  // chunk's stores must have read them out
+          named_bar_sync(1, 256);
         }
         uint32_t r[32];
         if (cl < BN) {
@@ -348,15 +365,21 @@ __global__ void __maxnreg__(200)
             v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
           }
         }
-        if (p.epi == EPI_QKV_ROPE && p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
+        if constexpr (EK == EK_ROPE) {
+          if (p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
+            for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
+          }
         }
-        if (p.gelu) {  // FFN fc1: GELU (erf form, reading Q21)
+        if (EK == EK_F32 && p.softplus) {  // Delta = softplus(delta_low W_dt^T + b_dt) (f32 output path)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = v[j] > 20.f ? v[j] : log1pf(__expf(v[j]));
+        }
+        if (EK == EK_GELU) {  // FFN fc1: GELU (erf form, reading Q21)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
         }
-        if (p.silu_col > 0 && col0 >= p.silu_col) {  // gate columns: SiLU(x) = x / (1 + e^-x)
+        if (EK == EK_PLAIN && p.silu_col > 0 && col0 >= p.silu_col) {  // gate columns: SiLU(x) = x / (1 + e^-x)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
         }
@@ -385,6 +408,23 @@ __global__ void __maxnreg__(200)
           named_bar_sync(1, 256);
           if (issuer) {
             if (mb < p.M) tma_store_2d(&tmOut, stg, n0 + cc * 64, mb);
+            bulk_commit();
+          }
+        } else if (f32_tma) {
+          // f32: this thread's 32 values are one 128-byte row of box `half` (128B-swizzled like the bf16 staging)
+          uint8_t* sh = s_stage + half * STAGE_OUT_BYTES;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(sh + swz_offset(row_local, q, 128)) =
+                make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
+                           __float_as_uint(v[4 * q + 3]));
+          fence_proxy_async_smem();
+          named_bar_sync(1, 256);
+          if (issuer) {
+            if (mb < p.M && n0 + cc * 64 < p.N) {
+              tma_store_2d(&tmOut, s_stage, n0 + cc * 64, mb);
+              if (n0 + cc * 64 + 32 < p.N) tma_store_2d(&tmOut, s_stage + STAGE_OUT_BYTES, n0 + cc * 64 + 32, mb);
+            }
             bulk_commit();
           }
         } else if (row_ok && cl < BN) {
@@ -456,7 +496,7 @@ __global__ void __maxnreg__(200)
         named_bar_sync(1, 256);
       }
     }
-    if (issuer && tma_out) bulk_wait0();
+    if (issuer && (tma_out || f32_tma)) bulk_wait0();
   }
   __syncthreads();
   if (PAIR) cluster_sync();  // the peer may still read this CTA's shared memory / signal its barriers until here
@@ -495,7 +535,7 @@ static int pair_clusters(size_t smem) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true>, &cfg) != cudaSuccess || n <= 0) {
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true, EK_PLAIN>, &cfg) != cudaSuccess || n <= 0) {
     cudaGetLastError();
     n = num_sms() / 2;
   }
@@ -507,11 +547,13 @@ static int pair_clusters(size_t smem) {
 int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cudaStream_t stream) {
   GemmArgs p = args_in;
   if (p.M <= 0 || p.N <= 0) return 0;
-  if (p.K % 8 != 0) return -1;
+  if (p.K % (p.tf32 ? 4 : 8) != 0) return -1;
   if (p.epi == EPI_QKV_ROPE && p.rope && !(p.d_head == 32 || p.d_head == 64)) return -2;
   const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
   if (p.silu_col && (p.silu_col % 32 || p.epi == EPI_STORE_F32)) return -2;
   if (p.gelu && p.epi != EPI_STORE_BF16) return -2;
+  if ((p.tf32 || p.softplus) && (p.epi != EPI_STORE_F32 || p.splits > 1)) return -2;
+  if (p.tf32 && (p.K % 4 || (p.lda * 4) % 16 || (p.ldb * 4) % 16)) return -1;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
   // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K
@@ -551,13 +593,22 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   }
   p.pair = pair ? 1 : 0;
   CUtensorMap tmA, tmB, tmOut, tmRes;
-  int rc = make_tmap_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.M, (uint64_t)p.lda * 2, BK, BM,
-                        CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMapDataType in_t = p.tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const int esz = p.tf32 ? 4 : 2, bke = p.tf32 ? BK / 2 : BK;
+  int rc = make_tmap_2d(&tmA, A, in_t, p.K, p.M, (uint64_t)p.lda * esz, bke, BM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_tmap_2d(&tmB, Bw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.K, p.N, (uint64_t)p.ldb * 2, BK,
-                    pair ? p.BN / 2 : p.BN, CU_TENSOR_MAP_SWIZZLE_128B);
+  rc = make_tmap_2d(&tmB, Bw, in_t, p.K, p.N, (uint64_t)p.ldb * esz, bke, pair ? p.BN / 2 : p.BN,
+                    CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   memset(&tmOut, 0, sizeof(tmOut));
+  // f32 outputs without split-K go through a TMA store when the row stride allows it (16-byte multiple)
+  p.f32_tma = (p.epi == EPI_STORE_F32 && p.splits <= 1 && (p.ldo * 4) % 16 == 0 && !getenv("PSCWIN_GEMM_F32_DIRECT"))
+                  ? 1 : 0;
+  if (p.f32_tma) {
+    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.N, p.M, (uint64_t)p.ldo * 4, 32, BM,
+                      CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
   if (p.epi != EPI_STORE_F32) {
     if ((p.ldo * 2) % 16) return -1;
     rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldo * 2, 64, BM,
@@ -573,17 +624,28 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_bf16_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
-    cudaFuncSetAttribute(gemm_bf16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
+    const void* fns[8] = {(const void*)gemm_bf16_kernel<false, EK_PLAIN>, (const void*)gemm_bf16_kernel<false, EK_ROPE>,
+                          (const void*)gemm_bf16_kernel<false, EK_GELU>, (const void*)gemm_bf16_kernel<false, EK_F32>,
+                          (const void*)gemm_bf16_kernel<true, EK_PLAIN>, (const void*)gemm_bf16_kernel<true, EK_ROPE>,
+                          (const void*)gemm_bf16_kernel<true, EK_GELU>, (const void*)gemm_bf16_kernel<true, EK_F32>};
+    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
     attr_set = true;
   }
+  const int ek = p.epi == EPI_QKV_ROPE ? EK_ROPE : (p.gelu ? EK_GELU : (p.epi == EPI_STORE_F32 ? EK_F32 : EK_PLAIN));
   const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages);
   if (smem > GEMM_SMEM_MAX) return -2;
   const long long tiles = (long long)m_tiles * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
   if (!pair) {
     const int grid = tiles < num_sms() ? (int)tiles : num_sms();
-    launch_k(gemm_bf16_kernel<false>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+    if (ek == EK_ROPE)
+      launch_k(gemm_bf16_kernel<false, EK_ROPE>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+    else if (ek == EK_GELU)
+      launch_k(gemm_bf16_kernel<false, EK_GELU>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+    else if (ek == EK_F32)
+      launch_k(gemm_bf16_kernel<false, EK_F32>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
+    else
+      launch_k(gemm_bf16_kernel<false, EK_PLAIN>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
     return (int)cudaGetLastError();
   }
   const int clusters_max = pair_clusters(smem);
@@ -602,7 +664,14 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true>, tmA, tmB, tmOut, tmRes, p);
+  if (ek == EK_ROPE)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_ROPE>, tmA, tmB, tmOut, tmRes, p);
+  else if (ek == EK_GELU)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_GELU>, tmA, tmB, tmOut, tmRes, p);
+  else if (ek == EK_F32)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_F32>, tmA, tmB, tmOut, tmRes, p);
+  else
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_PLAIN>, tmA, tmB, tmOut, tmRes, p);
   return (int)cudaGetLastError();
 }
 

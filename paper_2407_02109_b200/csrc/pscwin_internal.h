@@ -34,6 +34,9 @@ struct GemmArgs {
   int* sem;
   // bf16 epilogues: columns >= silu_col leave as SiLU(value) (0 = off; must be a multiple of the tile width)
   int silu_col;
+  int tf32;      // 1: A and B are f32 (row strides lda / ldb in f32 elements) multiplied as TF32 (kind::tf32,
+                 //    K-blocks of 32); f32 output only
+  int softplus;  // 1 (f32 output): softplus(value + bias) (the cycle scan's Delta = softplus(delta_low W_dt^T + b_dt))
   int gelu;    // 1: exact GELU 0.5 x (1 + erf(x / sqrt 2)) on every output (after bias; FFN fc1, reading Q21)
   int tok0;    // RoPE: global token index of GEMM row 0 (a row band of the image; 0 otherwise)
   // RoPE over a packed multi-scale sequence (HRSAM++): rows [seg_row[s], seg_row[s+1]) hold [B, H_s, W_s] grids
@@ -41,6 +44,7 @@ struct GemmArgs {
   int nseg;
   int seg_row[4], seg_HW[4], seg_W[4];
   int stages;  // smem ring depth (set by the launcher)
+  int f32_tma;  // f32 output staged in smem and TMA-stored (set by the launcher)
   int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
 };
 

@@ -23,23 +23,30 @@ LABELS = {  # ncu kernel name prefix -> library profiling label
 
 def gemm_labels(names):
     """Library label of each GEMM launch from its neighbours in the step's launch order (layer structure:
-    LN -> QKV -> [pad] -> attention -> out-proj; LN_s -> in_proj -> conv -> x_proj -> dt/pass1/carry/pass2 ->
-    out_proj_scan)."""
+    LN -> QKV -> [pad] -> attention -> out-proj [-> LN2 -> fc1 -> fc2]; LN_s -> in_proj -> conv -> x_proj ->
+    dt (TF32 GEMM) -> pass1 / carry / pass2 -> out_proj_scan)."""
     out = []
     for i, n in enumerate(names):
         if n != "gemm_bf16_kernel":
             out.append(LABELS.get(n, n))
             continue
         prev = names[i - 1] if i > 0 else ""
+        prev_lab = out[-1] if out else ""
         nxt = names[i + 1] if i + 1 < len(names) else ""
         if prev == "conv_silu_kernel":
             out.append("gemm_x_proj")
+        elif prev_lab == "gemm_x_proj":
+            out.append("scan_dt")
         elif prev == "scan_pass2_kernel":
             out.append("gemm_out_proj_scan")
         elif prev.startswith("window_attn"):
             out.append("gemm_out_proj")
         elif nxt == "conv_silu_kernel":
             out.append("gemm_in_proj")
+        elif prev_lab == "gemm_fc1_gelu":
+            out.append("gemm_fc2")
+        elif nxt == "gemm_bf16_kernel":
+            out.append("gemm_fc1_gelu")
         else:
             out.append("gemm_qkv_rope")
     return out
