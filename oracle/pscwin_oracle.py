@@ -264,6 +264,26 @@ def attention_core_padded(qkv: np.ndarray, qkv_p: np.ndarray, H: int, W: int, he
     return out[:, pt:pt + H, pl:pl + W].reshape(B, H, W, C)
 
 
+def global_attention_rows(qkv: np.ndarray, H: int, W: int, heads: int, tokens, rope: int = 1) -> np.ndarray:
+    """Global attention (Eq. 1; the Table 3 "Global" comparator) evaluated for the given
+    query tokens only (y*W + x of image 0): o_t = softmax(q_t K^T / sqrt(d)) V over ALL H*W keys, RoPE at grid
+    coordinates (Q6). Equals window attention with window = H = W. qkv [B,H,W,3C] unrotated. Returns [n, C]."""
+    C = qkv.shape[-1] // 3
+    d = C // heads
+    g = qkv[0].reshape(H * W, 3, heads, d)
+    Y, X = np.divmod(np.arange(H * W), W)
+    q, k, v = g[:, 0], g[:, 1], g[:, 2]
+    if rope:
+        q = rope_2d(q, X[:, None].astype(float), Y[:, None].astype(float))
+        k = rope_2d(k, X[:, None].astype(float), Y[:, None].astype(float))
+    tokens = np.asarray(tokens)
+    out = np.empty((len(tokens), heads, d))
+    for h in range(heads):
+        logits = q[tokens, h] @ k[:, h].T / math.sqrt(d)
+        out[:, h] = stable_softmax(logits, axis=-1) @ v[:, h]
+    return out.reshape(len(tokens), C)
+
+
 def attention_sublayer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False):
     """One PSCWin attention sub-layer (a4-a7), pre-LN residual:
     u = LN1(x); qkv = u W_qkv^T + b_qkv; qkv_p = p W_qkv^T + b_qkv (p not normalised, Q14);
@@ -559,3 +579,61 @@ def ms_layer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, attention: 
         if getattr(cfg, "mlp_hidden", 0):
             xp = ffn_sublayer(xp, wt, cfg)
     return xp
+
+
+# =============================================================================================
+# Encoder ends (reading Q22)
+# =============================================================================================
+
+def patch_embed(img: np.ndarray, w: np.ndarray, b: np.ndarray, p: int = 16) -> np.ndarray:
+    """ViT patch embedding ("image encoder ... ViT"; 1024^2 -> 64 x 64 tokens): a p x p convolution
+    with stride p, written out as its definition. img [B, 3, pH, pW]; w [C, 3, p, p]; b [C]. Returns [B, H, W, C]
+    (no absolute position embedding: positions enter through RoPE, reading Q22)."""
+    B, Ci, Hi, Wi = img.shape
+    H, W = Hi // p, Wi // p
+    patches = img.reshape(B, Ci, H, p, W, p).transpose(0, 2, 4, 1, 3, 5).reshape(B, H, W, Ci * p * p)
+    return patches @ w.reshape(w.shape[0], -1).T + b
+
+
+def conv3x3(x: np.ndarray, w: np.ndarray) -> np.ndarray:
+    """3 x 3 convolution, stride 1, zero padding 1, no bias, channels-last: out[b,y,x,o] =
+    sum_{dy,dx,i} x[b, y+dy-1, x+dx-1, i] w[o, i, dy, dx]. x [B,H,W,Ci]; w [Co, Ci, 3, 3]."""
+    B, H, W, Ci = x.shape
+    xp = np.zeros((B, H + 2, W + 2, Ci))
+    xp[:, 1:H + 1, 1:W + 1] = x
+    out = np.zeros((B, H, W, w.shape[0]))
+    for dy in range(3):
+        for dx in range(3):
+            out += xp[:, dy:dy + H, dx:dx + W] @ w[:, :, dy, dx].T
+    return out
+
+
+def encoder_neck(stage_outs, wt: Dict[str, np.ndarray], eps: float = 1e-6) -> np.ndarray:
+    """HRSAM's output fusion ("fusing outputs from all four stages through summation, followed by a
+    convolutional block"; "the output dimension of each stage is 256"), reading Q22: each stage output is
+    projected to 256 channels (1x1 conv, no bias), the projections are summed, and the sum passes SAM's neck
+    block LN2d -> conv3x3 (no bias) -> LN2d. stage_outs: list of [B,H,W,C]. Returns [B,H,W,256]."""
+    f = sum(s @ wt[f"w_stage{i}"].T for i, s in enumerate(stage_outs))
+    f = layer_norm(f, wt["neck_ln1_g"], wt["neck_ln1_b"], eps)
+    f = conv3x3(f, wt["w_neck_conv"])
+    return layer_norm(f, wt["neck_ln2_g"], wt["neck_ln2_b"], eps)
+
+
+def resize_bilinear(x: np.ndarray, H: int, W: int) -> np.ndarray:
+    """Bilinear resize, align_corners = False (half-pixel centres; reading Q22), channels-last [B,h,w,C] ->
+    [B,H,W,C]: source coordinate s = (d + 0.5) * in / out - 0.5 clamped at 0, linear weights between floor(s)
+    and floor(s) + 1 (clamped to the last row / column). HRSAM++ resizes the overview scale's outputs to the main
+    grid (Fig. 4 caption)."""
+    B, h, w, C = x.shape
+
+    def axis(n_out, n_in):
+        s = np.maximum((np.arange(n_out) + 0.5) * n_in / n_out - 0.5, 0.0)
+        i0 = np.minimum(np.floor(s).astype(int), n_in - 1)
+        i1 = np.minimum(i0 + 1, n_in - 1)
+        return i0, i1, s - i0
+
+    y0, y1, fy = axis(H, h)
+    x0, x1, fx = axis(W, w)
+    top = x[:, y0][:, :, x0] * (1 - fx)[None, None, :, None] + x[:, y0][:, :, x1] * fx[None, None, :, None]
+    bot = x[:, y1][:, :, x0] * (1 - fx)[None, None, :, None] + x[:, y1][:, :, x1] * fx[None, None, :, None]
+    return top * (1 - fy)[None, :, None, None] + bot * fy[None, :, None, None]

@@ -241,3 +241,26 @@ def make_qkv(cfg: LayerConfig, seed: int = 7) -> np.ndarray:
 
 def make_pad_qkv(cfg: LayerConfig, seed: int = 7) -> np.ndarray:
     return _store(0.5 * normal(stream_seed(seed, 2), 3 * cfg.C), "mat", cfg)
+
+
+def make_image(B: int, H: int, W: int, seed: int = 50) -> np.ndarray:
+    """Synthetic input image [B, 3, 16H, 16W] ~ N(0,1) (normalised pixels), stored in bf16."""
+    n = B * 3 * 16 * H * 16 * W
+    return round_bf16(normal(stream_seed(seed, B, H, W), n).reshape(B, 3, 16 * H, 16 * W))
+
+
+def make_ends_weights(C: int = 768, C_out: int = 256, n_stages: int = 4, seed: int = 300) -> Dict[str, np.ndarray]:
+    """Encoder-end weights (reading Q22): patch embedding conv [C, 3, 16, 16] + bias, per-stage 1x1 projections
+    [C_out, C], neck LN2d / conv3x3 [C_out, C_out, 3, 3] / LN2d. Matrices bf16, LN params / bias f32."""
+    g = lambda idx, n: normal(stream_seed(seed, idx), n)
+    w: Dict[str, np.ndarray] = {}
+    w["w_patch"] = round_bf16(0.02 * g(1, C * 768).reshape(C, 3, 16, 16))
+    w["b_patch"] = round_f32(0.02 * g(2, C))
+    for i in range(n_stages):
+        w[f"w_stage{i}"] = round_bf16(0.02 * g(10 + i, C_out * C).reshape(C_out, C))
+    w["neck_ln1_g"] = round_f32(1.0 + 0.1 * g(20, C_out))
+    w["neck_ln1_b"] = round_f32(0.02 * g(21, C_out))
+    w["w_neck_conv"] = round_bf16(0.02 * g(22, C_out * C_out * 9).reshape(C_out, C_out, 3, 3))
+    w["neck_ln2_g"] = round_f32(1.0 + 0.1 * g(23, C_out))
+    w["neck_ln2_b"] = round_f32(0.02 * g(24, C_out))
+    return w

@@ -530,3 +530,21 @@ def test_ffn_sublayer_vs_torch():
     # the layer applies it after attention
     assert np.array_equal(oracle.pscwin_layer(x, wt, cfg),
                           oracle.ffn_sublayer(oracle.attention_sublayer(x, wt, cfg), wt, cfg))
+
+
+def test_global_attention_rows_vs_sdpa():
+    # the Table 3 "Global" comparator: sampled query rows of Eq. 1 over ALL keys equal torch fp64 SDPA
+    # on the RoPE'd sequence (library routine), and the window = grid case of the window oracle
+    cfg = synth.tiny(H=12, W=8, window=4, shift_x=0, shift_y=0, dtype="f32")
+    qkv = synth.make_qkv(cfg)
+    H, W, heads, C = 12, 8, cfg.heads, cfg.C
+    d = C // heads
+    toks = [0, 17, 95]
+    got = oracle.global_attention_rows(qkv, H, W, heads, toks, 1)
+    g = qkv[0].reshape(H * W, 3, heads, d)
+    Y, X = np.divmod(np.arange(H * W), W)
+    q = oracle.rope_2d(g[:, 0], X[:, None].astype(float), Y[:, None].astype(float))
+    k = oracle.rope_2d(g[:, 1], X[:, None].astype(float), Y[:, None].astype(float))
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a.transpose(1, 0, 2)))
+    ref = F.scaled_dot_product_attention(tt(q), tt(k), tt(g[:, 2])).numpy().transpose(1, 0, 2).reshape(H * W, C)
+    assert np.max(np.abs(got - ref[toks])) < 1e-12
