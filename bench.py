@@ -649,6 +649,86 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------------------------- ablation
+# Table 3 (P:L344-383) as a B200 rendition (SURVEY §8(f) NEXT-4): the 12-block ViT-B encoder body (attention +
+# FFN 768x4 per block) with each attention / cycle-scan combination the paper ablates, one image, bf16.
+# Patch embedding and the neck are not part of the timed body. The paper's latencies (unstated GPU) are context.
+PAPER_TABLE3 = {  # variant -> (1024^2 ms, 2048^2 ms), P:L363-376
+    "Global": (104, 1338), "Global+PlainWin": (61, 528), "PlainWin+VanSwin": (37, 122),
+    "PlainWin+PadSwin": (44, 136), "PlainWin+VanSwin+SSCScan": (52, 178),
+    "PlainWin+PadSwin+SSCScan (HRSAM)": (58, 192), "PlainWin+PadSwin+SSCScan+MSCScan (HRSAM++)": (98, 277)}
+
+
+def ablation_specs(side: int, variant: str):
+    """[(kind, cfg, attention, cs_mode)] for one encoder variant on a side x side token grid."""
+    out = []
+    for i in range(12):
+        shifted, cs = synth.stack_layer_kind(i)
+        base = synth.vitb(side, mlp_hidden=3072)
+        if variant == "Global":
+            cfg, csm = base.replace(window=side, shift_x=0, shift_y=0), 0
+        elif variant == "Global+PlainWin":  # SAM-style: global attention in blocks 2, 5, 8, 11
+            cfg = base.replace(window=side, shift_x=0, shift_y=0) if cs else base.replace(shift_x=0, shift_y=0)
+            csm = 0
+        else:
+            pad = synth.PAD_MASKED if "VanSwin" in variant else synth.PAD_LEARNABLE
+            cfg = base.replace(shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, pad_mode=pad)
+            csm = 1 if (cs and "SSCScan" in variant) else 0
+        out.append(("ms" if "MSCScan" in variant else "layer", cfg, 1, csm))
+        if cs and "MSCScan" in variant:
+            out.append(("ms", base.replace(shift_x=0, shift_y=0), 0, 2))
+    return out
+
+
+def run_ablation(args):
+    import torch
+    import paper_2407_02109_b200 as pl
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    rows = []
+    for side in (64, 128):
+        for variant, paper in PAPER_TABLE3.items():
+            specs = ablation_specs(side, variant)
+            scales = [(side, side), (32, 32)]   # HRSAM++: the 512^2 overview image -> 32 x 32 tokens (P:L181)
+            layers = []
+            for j, (kind, cfg, att, csm) in enumerate(specs):
+                w = synth.make_weights(cfg, layer=j)
+                dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+                      for k, v in w.items()}
+                if kind == "ms":
+                    layers.append(pl.PSCWinMSLayer(pl.MSDesc.make(cfg, scales, att, csm), dw))
+                else:
+                    layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg.replace(cycle_scan=csm)), dw))
+            T = side * side + (32 * 32 if "MSCScan" in variant else 0)
+            shape = (T, 768) if "MSCScan" in variant else (1, side, side, 768)
+            stack = pl.PSCWinStack(layers, shape, device=dev, graph=True)
+            stack.x_in.copy_(torch.randn(shape, device=dev).to(torch.bfloat16))
+            for _ in range(3):
+                stack.replay()
+            ts = []
+            for _ in range(max(3, min(args.steps, 20))):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                stack.replay()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ms = float(np.median(ts))
+            res = {"metric": "encoder body latency ms/image (Table 3 rendition)", "variant": variant,
+                   "input": f"{16 * side}^2", "value": round(ms, 4), "unit": "ms/image",
+                   "paper_ms_context": paper[0 if side == 64 else 1], "dtype": "bf16", "data": "synthetic",
+                   "config": {"blocks": 12, "ffn": 3072, "launches_per_step": stack.launches_per_step}}
+            print(json.dumps(res), flush=True)
+            rows.append(res)
+            del stack, layers
+            torch.cuda.empty_cache()
+    print("| variant | input | B200 ms | paper ms (GPU unstated) |\n|---|---|---|---|", file=sys.stderr)
+    for r in rows:
+        print(f"| {r['variant']} | {r['input']} | {r['value']:.3f} | {r['paper_ms_context']} |", file=sys.stderr)
+
+
 # ----------------------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -665,6 +745,9 @@ def main():
     ap.add_argument("--shard", default="images", choices=["images", "rows"],
                     help="images: each rank its own image(s) (weak scaling, default); rows: one image split by "
                          "window rows over the ranks with halo / scan-carry exchange (config 4, strong scaling)")
+    ap.add_argument("--ablation", action="store_true",
+                    help="Table 3 rendition: the 12-block encoder body per attention / cycle-scan variant at 1024^2 and "
+                         "2048^2 (one JSON line per variant; SURVEY NEXT-4)")
     ap.add_argument("--ffn", action="store_true",
                     help="add the FFN sub-layer (hidden 768 x 4, P:L625; SURVEY NEXT-2) after every attention sub-layer")
     args = ap.parse_args()
@@ -679,6 +762,10 @@ def main():
     if args.impl == "reference":
         if rank == 0:
             run_reference(args)
+        return
+    if args.ablation:
+        if rank == 0:
+            run_ablation(args)
         return
 
     if world > 1:

@@ -48,7 +48,7 @@ typedef enum { PSCWIN_BBAR_ZOH = 0, PSCWIN_BBAR_EULER = 1 } pscwin_bbar_mode;
 /* One PSCWin layer. Token grid H x W = image / 16. */
 typedef struct {
   int32_t B, H, W, C, heads;          /* d_head = C / heads; d_head in {32, 64} on this path          */
-  int32_t window;                     /* w; power of two in [4, 64]                            */
+  int32_t window;                     /* w; power of two in [4, 128] (w = H = W: global attention) */
   int32_t shift_x, shift_y;           /* in [0, w); (0,0) = plain window attention (Q7)          */
   int32_t pad_mode;                   /* pscwin_pad_mode                                                */
   int32_t rope;                       /* 0 off, 1 axial 2-D RoPE base 10000 on q,k (Q6)         */

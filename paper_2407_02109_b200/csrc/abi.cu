@@ -146,7 +146,7 @@ int check_layer(const pscwin_layer_desc* d) {
   if (d->dtype != PSCWIN_BF16 && d->dtype != PSCWIN_F32) return PSCWIN_ERR_UNSUPPORTED;
   if (!(dh == 32 || dh == 64)) return PSCWIN_ERR_UNSUPPORTED;
   if (d->dtype == PSCWIN_F32 && d->window > 16) return PSCWIN_ERR_UNSUPPORTED;  // f32 window lives in smem
-  if (d->window < 4 || d->window > 64 || (d->window & (d->window - 1))) return PSCWIN_ERR_UNSUPPORTED;
+  if (d->window < 4 || d->window > 128 || (d->window & (d->window - 1))) return PSCWIN_ERR_UNSUPPORTED;
   if (d->pad_mode != PSCWIN_PAD_LEARNABLE && d->pad_mode != PSCWIN_PAD_MASKED) return PSCWIN_ERR_CONTRACT;
   if (d->C % 64) return PSCWIN_ERR_UNSUPPORTED;  // GEMM K tiles
   if (d->mlp_hidden < 0 || d->mlp_hidden % 64) return PSCWIN_ERR_CONTRACT;

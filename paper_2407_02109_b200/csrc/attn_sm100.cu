@@ -325,7 +325,7 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
   const int d = a.d;
   if (!(d == 32 || d == 64)) return -2;
   const int w = a.w;
-  if (w < 4 || w > 64 || (w & (w - 1))) return -2;
+  if (w < 4 || w > 128 || (w & (w - 1))) return -2;
   AttnKArgs p;
   p.B = a.B;
   p.H = a.H;

@@ -27,15 +27,17 @@ constexpr int GEMM_THREADS = 64 + 256;           // TMA warp, MMA warp, 8 epilog
 constexpr size_t GEMM_SMEM_MAX = 232448;         // 227 KB opt-in limit per CTA
 // shared memory layout: [1 KB align slack][stages x (A 128x64 | B rows x 64)][2 x 16 KB output staging]
 // [residual tiles 2 x nch x 16 KB][barriers]; B rows per CTA = BN (single CTA) or BN / 2 (CTA pair)
-__host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid) {
+__host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid, bool f32 = false) {
   const size_t nch = (size_t)(BN + 63) / 64;
-  return 1024 + 2 * STAGE_OUT_BYTES + (resid ? 2 * nch * STAGE_OUT_BYTES : 0) + 2 * 256 * 4 + 256;
+  // f32 outputs: two more 16 KB staging boxes (a 64-column f32 chunk is two 128 x 32 boxes; two chunks in flight)
+  return 1024 + 2 * STAGE_OUT_BYTES + (resid ? 2 * nch * STAGE_OUT_BYTES : (f32 ? 2 * STAGE_OUT_BYTES : 0)) +
+         2 * 256 * 4 + 256;
 }
 __host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
   return A_STAGE_BYTES + (size_t)(pair ? BN / 2 : BN) * BK * 2;
 }
-__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid, bool pair, int stages) {
-  return gemm_fixed_bytes(BN, resid) + (size_t)stages * gemm_stage_bytes(BN, pair);
+__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid, bool pair, int stages, bool f32 = false) {
+  return gemm_fixed_bytes(BN, resid, f32) + (size_t)stages * gemm_stage_bytes(BN, pair);
 }
 }  // namespace
 
@@ -71,7 +73,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
   uint8_t* s_res = s_stage + 2 * STAGE_OUT_BYTES;   // 2 x nch x 16 KB residual tiles (TMA-loaded)
-  float* s_bias = reinterpret_cast<float*>(s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : 0));  // [2][256]
+  float* s_bias = reinterpret_cast<float*>(
+      s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 2 * 256);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
@@ -343,8 +346,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (tma_out) {
           if (issuer && gseq >= 2) bulk_wait_read1();
           named_bar_sync(1, 256);
-        } else if (f32_tma) {  // both staging buffers hold this chunk (two 128 x 32 f32 boxes): the previous
-          if (issuer && gseq >= 1) bulk_wait_read0();  // chunk's stores must have read them out
+        } else if (f32_tma) {  // a chunk = two 128 x 32 f32 boxes; buffers of parity gseq & 1 (two chunks in
+          if (issuer && gseq >= 2) bulk_wait_read1();  // flight): the chunk before last must have been read out
           named_bar_sync(1, 256);
         }
         uint32_t r[32];
@@ -373,7 +376,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
         if (EK == EK_F32 && p.softplus) {  // Delta = softplus(delta_low W_dt^T + b_dt) (f32 output path)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = v[j] > 20.f ? v[j] : log1pf(__expf(v[j]));
+          for (int j = 0; j < 32; ++j) {  // log1p(t) = log(u) t / (u - 1), u = 1 + t (exact where u rounds to 1)
+            const float t = __expf(v[j]), u = 1.f + t;
+            const float lp = u == 1.f ? t : __logf(u) * __fdividef(t, u - 1.f);
+            v[j] = v[j] > 20.f ? v[j] : lp;
+          }
         }
         if (EK == EK_GELU) {  // FFN fc1: GELU (erf form, reading Q21)
 #pragma unroll
@@ -412,7 +419,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         } else if (f32_tma) {
           // f32: this thread's 32 values are one 128-byte row of box `half` (128B-swizzled like the bf16 staging)
-          uint8_t* sh = s_stage + half * STAGE_OUT_BYTES;
+          uint8_t* sf = s_stage + (gseq & 1) * 2 * STAGE_OUT_BYTES;
+          uint8_t* sh = sf + half * STAGE_OUT_BYTES;
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<uint4*>(sh + swz_offset(row_local, q, 128)) =
@@ -422,8 +430,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           named_bar_sync(1, 256);
           if (issuer) {
             if (mb < p.M && n0 + cc * 64 < p.N) {
-              tma_store_2d(&tmOut, s_stage, n0 + cc * 64, mb);
-              if (n0 + cc * 64 + 32 < p.N) tma_store_2d(&tmOut, s_stage + STAGE_OUT_BYTES, n0 + cc * 64 + 32, mb);
+              tma_store_2d(&tmOut, sf, n0 + cc * 64, mb);
+              if (n0 + cc * 64 + 32 < p.N) tma_store_2d(&tmOut, sf + STAGE_OUT_BYTES, n0 + cc * 64 + 32, mb);
             }
             bulk_commit();
           }
@@ -584,8 +592,9 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (resid && p.BN > 128) return -2;
   if (pair && (p.BN % 16)) return -2;
   // ring depth: as many stages as fit next to the staging / residual buffers
+  const bool f32o = p.epi == EPI_STORE_F32;
   {
-    const size_t fixed = gemm_fixed_bytes(p.BN, resid), st = gemm_stage_bytes(p.BN, pair);
+    const size_t fixed = gemm_fixed_bytes(p.BN, resid, f32o), st = gemm_stage_bytes(p.BN, pair);
     int stages = (int)((GEMM_SMEM_MAX - fixed) / st);
     if (stages > MAX_STAGES) stages = MAX_STAGES;
     if (stages < 2) return -2;
@@ -632,7 +641,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
     attr_set = true;
   }
   const int ek = p.epi == EPI_QKV_ROPE ? EK_ROPE : (p.gelu ? EK_GELU : (p.epi == EPI_STORE_F32 ? EK_F32 : EK_PLAIN));
-  const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages);
+  const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages, f32o);
   if (smem > GEMM_SMEM_MAX) return -2;
   const long long tiles = (long long)m_tiles * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);

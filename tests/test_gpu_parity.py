@@ -129,6 +129,7 @@ ATTN_CASES = [
     synth.vitb(64, pad_mode=synth.PAD_MASKED),
     synth.vitb(64, shift_x=0, shift_y=0),
     synth.tiny(H=64, W=64, C=128, heads=2, window=32, shift_x=16, shift_y=16),  # w=32: 4 q x 4 kv tiles
+    synth.tiny(H=64, W=64, C=128, heads=2, window=64, shift_x=0, shift_y=0),    # global attention at 1024^2
 ]
 
 
@@ -164,6 +165,19 @@ def test_window_attention_4096_sampled(pl, mode):
     assert sel.sum() > 0
     assert np.all(np.isfinite(O))
     assert float(np.max(np.abs(O[sel] - ref[sel])) / np.max(np.abs(ref[sel]))) < BF16_TOL
+
+
+@pytest.mark.parametrize("C,heads", [(64, 2), (768, 12)])
+def test_global_attention_2048_sampled(pl, C, heads):
+    # Table 3's "Global" comparator at 2048^2: window = H = W = 128 (16384 keys); sampled query tokens vs the
+    # oracle's plain definition over all keys
+    cfg = synth.tiny(H=128, W=128, C=C, heads=heads, window=128, shift_x=0, shift_y=0)
+    qkv, qkv_p, gpu_qkv = _attn_inputs(cfg)
+    O = host(pl.window_attention(pl.LayerDesc.from_config(cfg), dev(gpu_qkv), None)).reshape(-1, C)
+    toks = np.array([0, 127, 128 * 64 + 63, 128 * 127, 128 * 128 - 1, 5000, 9999])
+    ref = oracle.global_attention_rows(qkv, 128, 128, heads, toks, cfg.rope)
+    assert np.all(np.isfinite(O))
+    assert float(np.max(np.abs(O[toks] - ref)) / np.max(np.abs(ref))) < BF16_TOL
 
 
 def test_attention_guard_and_invariants(pl):

@@ -1,9 +1,8 @@
-# profiling session: launch list of the bench step + one ncu --set full capture (outputs under gpurun_out/)
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-graph > gpurun_out/ncu_launch.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -o gpurun_out/step_full -f \
-  python tools/run_stage.py 1 > gpurun_out/ncu_full.log 2>&1
-python tools/ncu_summary.py launches gpurun_out/launches.csv > gpurun_out/launches.md 2>&1
-python tools/ncu_summary.py full gpurun_out/step_full.ncu-rep gpurun_out/dram_traffic.json > gpurun_out/full_step.md 2>&1
-tail -3 gpurun_out/ncu_full.log; cat gpurun_out/launches.md gpurun_out/full_step.md
+# one gpurun session: parity tests, benches (outputs under gpurun_out/)
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1
+timeout 600 python bench.py --breakdown --no-cpu-baseline > gpurun_out/bench1024.log 2>&1
+PSCWIN_DT_FFMA=1 timeout 600 python bench.py --no-cpu-baseline --steps 100 > gpurun_out/bench1024_dtffma.log 2>&1
+timeout 600 python bench.py --workload 4096 --steps 20 --breakdown --no-cpu-baseline > gpurun_out/bench4096.log 2>&1
+timeout 1200 python bench.py --ablation --steps 10 > gpurun_out/ablation.log 2>&1
+for f in gpurun_out/*.log; do echo "== $f"; tail -n 1 $f | cut -c1-200; done
