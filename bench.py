@@ -729,6 +729,74 @@ def run_ablation(args):
         print(f"| {r['variant']} | {r['input']} | {r['value']:.3f} | {r['paper_ms_context']} |", file=sys.stderr)
 
 
+# ----------------------------------------------------------------------------------------------- encoder
+def run_encoder(args):
+    """--encoder: the whole HRSAM encoder on one image: patch embedding -> the 12-block stack with FFN
+    (global alternation, cycle scan before blocks 2, 5, 8, 11) -> fusion of the four stage outputs (neck) ->
+    [H/16, W/16, 256] embeddings. One CUDA graph; the image [1, 3, 16H, 16W] is resident (value)
+    or copied from pinned host memory with the embedding copied back (e2e)."""
+    import torch
+    import paper_2407_02109_b200 as pl
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    side = {"1024": 64, "2048": 128, "4096": 256}[args.workload]
+    layers = []
+    for i in range(12):
+        shifted, cs = synth.stack_layer_kind(i)
+        cfg = synth.vitb(side, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, cycle_scan=int(cs),
+                         mlp_hidden=3072)
+        w = synth.make_weights(cfg, layer=i)
+        dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
+              for k, v in w.items()}
+        layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dw))
+    ew = synth.make_ends_weights()
+    ends = {k: torch.tensor(v, dtype=torch.float32 if v.ndim == 1 else torch.bfloat16, device=dev)
+            for k, v in ew.items()}
+    ends["w_neck_conv"] = ends["w_neck_conv"].permute(0, 2, 3, 1).contiguous()
+    enc = pl.HRSAMEncoder(layers, ends, 1, side, side, graph=True)
+    img = torch.tensor(synth.make_image(1, side, side), dtype=torch.bfloat16, device=dev)
+    enc.img.copy_(img)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        enc.graph.replay()
+    torch.cuda.synchronize()
+    ts = []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            enc.graph.replay()
+            b.record()
+            ts.append((a, b))
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ts) / args.steps
+    img_pin = img.cpu().pin_memory()
+    out_pin = torch.empty(enc.out.shape, dtype=torch.bfloat16).pin_memory()
+    te = []
+    for _ in range(args.steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        y = enc(img_pin)
+        out_pin.copy_(y, non_blocking=True)
+        b.record()
+        te.append((a, b))
+    torch.cuda.synchronize()
+    e2e = sum(a.elapsed_time(b) for a, b in te) / args.steps
+    line = {"metric": "HRSAM encoder latency ms/image (patch embedding + 12 blocks with FFN + neck)",
+            "value": round(ms, 4), "unit": "ms/image", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic image and random-init weights",
+            "config": {"workload": f"{16 * side}^2 image -> {side}x{side}x256 embeddings", "blocks": 12,
+                       "ffn": 3072, "stage_ends": [2, 5, 8, 11], "launch": "CUDA graph",
+                       "l2": "flushed before every timed step (256 MiB write)"},
+            "e2e": {"value": round(e2e, 4), "unit": "ms/image", "h2d_bytes_per_step": int(img.numel() * 2),
+                    "d2h_bytes_per_step": int(enc.out.numel() * 2)},
+            "gpu_launches": int(enc.launches_per_step * args.steps), "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -748,6 +816,8 @@ def main():
     ap.add_argument("--ablation", action="store_true",
                     help="Table 3 rendition: the 12-block encoder body per attention / cycle-scan variant at 1024^2 and "
                          "2048^2 (one JSON line per variant; SURVEY NEXT-4)")
+    ap.add_argument("--encoder", action="store_true",
+                    help="the whole HRSAM encoder on one image: patch embedding + 12 blocks with FFN + neck (NEXT-3)")
     ap.add_argument("--ffn", action="store_true",
                     help="add the FFN sub-layer (hidden 768 x 4, P:L625; SURVEY NEXT-2) after every attention sub-layer")
     args = ap.parse_args()
@@ -766,6 +836,10 @@ def main():
     if args.ablation:
         if rank == 0:
             run_ablation(args)
+        return
+    if args.encoder:
+        if rank == 0:
+            run_encoder(args)
         return
 
     if world > 1:

@@ -198,6 +198,37 @@ size_t pscwin_ms_workspace_bytes(const pscwin_ms_desc* desc);
 int pscwin_ms_forward(const pscwin_ms_desc* desc, const pscwin_layer_weights* wts, const void* x_in, void* x_out,
                       void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------ encoder ends */
+/* Patch embedding (ViT; a 1024^2 image gives 64 x 64 tokens): img [B, 3, 16H, 16W] bf16 (NCHW),
+ * w_patch [C, 768] bf16 = a Conv2d(3, C, 16, stride 16) weight [C, 3, 16, 16] flattened, b_patch [C] f32 ->
+ * out [B, H, W, C] bf16. No absolute position embedding (RoPE carries positions; reading Q22).
+ * Internally a patchify gather into the workspace and one tcgen05 GEMM with the bias in its epilogue. */
+size_t pscwin_patch_embed_workspace_bytes(int32_t B, int32_t H, int32_t W);
+int pscwin_patch_embed(const void* img, int32_t B, int32_t H, int32_t W, int32_t C, const void* w_patch,
+                       const float* b_patch, void* out, void* workspace, size_t ws_bytes, void* stream);
+/* Bilinear resize (align_corners = False: half-pixel centres, clamped), channels-last bf16
+ * in [B, h, w, Cx] -> out [B, H, W, Cx]; accumulate != 0 adds into out (f32 sum, one rounding). Cx % 8 == 0. */
+int pscwin_resize_bilinear(const void* in, int32_t B, int32_t h, int32_t w, int32_t Cx, int32_t H, int32_t W,
+                           int32_t accumulate, void* out, void* stream);
+/* Output fusion of the four stages ("fusing outputs from all four stages through summation, followed by a
+ * convolutional block"; P:L625 stage output dimension 256; reading Q22):
+ *   f = sum_s stage_s W_s^T  (1x1 projections C -> C_out, no bias) on the main grid (scale 0);
+ *   HRSAM++ (n_scales > 1): every other scale's f is bilinearly resized to the main grid and added;
+ *   out = LN2d(conv3x3(LN2d(f))) (SAM neck block; conv zero padding 1, no bias).
+ * stage_outs[s]: device pointer to stage s's output, packed [B * sum_j H[j] W[j], C] bf16 (scale-outermost, the
+ * pscwin_ms_forward layout; one scale = [B, H, W, C]); w_stage[s] [C_out, C] bf16; ln* [C_out] f32;
+ * w_conv [C_out, 3, 3, C_out] bf16 (o, dy, dx, i); out [B, H[0], W[0], C_out] bf16. The pointer arrays are host
+ * arrays of device pointers. Workspace: pscwin_neck_workspace_bytes. */
+typedef struct {
+  int32_t B, C, C_out, n_stages, n_scales;
+  int32_t H[PSCWIN_MAX_SCALES], W[PSCWIN_MAX_SCALES];
+  float ln_eps;
+} pscwin_neck_desc;
+size_t pscwin_neck_workspace_bytes(const pscwin_neck_desc* desc);
+int pscwin_neck(const pscwin_neck_desc* desc, const void* const* stage_outs, const void* const* w_stage,
+                const float* ln1_g, const float* ln1_b, const void* w_conv, const float* ln2_g, const float* ln2_b,
+                void* out, void* workspace, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------- row bands (multi-GPU, §8(e)) */
 /* Window-row sharding of ONE image (B = 1) over `world` ranks, one band of token rows per rank (SURVEY §8(e),
  * config 4; cycle-scan carries per SURVEY Appendix A). row_begin / row_end are multiples of the window (the

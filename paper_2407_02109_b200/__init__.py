@@ -4,8 +4,9 @@ The compute lives in libpscwin.so (CUDA C++, C ABI in include/pscwin.h); this pa
 binding with the same call names. Importing it loads the library and fails loudly if it is missing.
 """
 from ._lib import (CS_MULTI_SCALE, CS_NONE, CS_SINGLE_SCALE, LIB_PATH, LayerDesc, LayerWeights,  # noqa: F401
-                   MSDesc, PscwinError, ScanDesc, launch_count, lib, ms_index_map, profile_enable, profile_read)
-from .api import (PSCWinLayer, PSCWinMSLayer, PSCWinStack, ms_forward, ms_workspace_bytes, Workspace, cycle_scan, forward, index_map, layer_norm, linear,  # noqa: F401
+                   MSDesc, NeckDesc, PscwinError, ScanDesc, launch_count, lib, ms_index_map, profile_enable, profile_read)
+from .api import (HRSAMEncoder, PSCWinLayer, PSCWinMSLayer, PSCWinStack, ms_forward, ms_workspace_bytes, neck,
+                  neck_workspace_bytes, patch_embed, resize_bilinear, Workspace, cycle_scan, forward, index_map, layer_norm, linear,  # noqa: F401
                   qkv_project, scan_workspace_bytes, shifted_pad_partition, window_attention, window_count,
                   window_merge, window_partition, workspace_bytes)
 

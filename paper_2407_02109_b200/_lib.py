@@ -31,6 +31,8 @@ EXPORTS = [
     "pscwin_band_workspace_bytes", "pscwin_band_io_offsets", "pscwin_band_scan_begin", "pscwin_band_scan_mid",
     "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
     "pscwin_ms_window_count", "pscwin_ms_index_map", "pscwin_ms_workspace_bytes", "pscwin_ms_forward",
+    "pscwin_patch_embed_workspace_bytes", "pscwin_patch_embed", "pscwin_resize_bilinear", "pscwin_neck_workspace_bytes",
+    "pscwin_neck",
 ]
 
 
@@ -100,6 +102,21 @@ class MSDesc(ctypes.Structure):
         return sum(self.H[i] * self.W[i] for i in range(self.n_scales))
 
 
+class NeckDesc(ctypes.Structure):
+    """pscwin_neck_desc: output fusion of the stages (1x1 projections summed, HRSAM++ scales resized, conv block)."""
+    _fields_ = [("B", ctypes.c_int32), ("C", ctypes.c_int32), ("C_out", ctypes.c_int32), ("n_stages", ctypes.c_int32),
+                ("n_scales", ctypes.c_int32), ("H", ctypes.c_int32 * MAX_SCALES), ("W", ctypes.c_int32 * MAX_SCALES),
+                ("ln_eps", ctypes.c_float)]
+
+    @classmethod
+    def make(cls, B, C, C_out, scales, n_stages=4, eps=1e-6) -> "NeckDesc":
+        d = cls()
+        d.B, d.C, d.C_out, d.n_stages, d.n_scales, d.ln_eps = B, C, C_out, n_stages, len(scales), eps
+        for i, (h, w) in enumerate(scales):
+            d.H[i], d.W[i] = h, w
+        return d
+
+
 class ScanDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in ("B", "H", "W", "D", "N", "R", "conv_k", "scan_order", "bbar_mode",
                                               "dtype", "window")]
@@ -167,6 +184,12 @@ def lib() -> ctypes.CDLL:
         "pscwin_ms_workspace_bytes": ([ctypes.POINTER(MSDesc)], sz),
         "pscwin_ms_forward": ([ctypes.POINTER(MSDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
                               ctypes.c_int),
+        "pscwin_patch_embed_workspace_bytes": ([i32, i32, i32], sz),
+        "pscwin_patch_embed": ([vp, i32, i32, i32, i32, vp, vp, vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_resize_bilinear": ([vp, i32, i32, i32, i32, i32, i32, i32, vp, vp], ctypes.c_int),
+        "pscwin_neck_workspace_bytes": ([ctypes.POINTER(NeckDesc)], sz),
+        "pscwin_neck": ([ctypes.POINTER(NeckDesc), ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, vp, vp, vp, vp,
+                         sz, vp], ctypes.c_int),
         "pscwin_launch_count": ([], ctypes.c_int64),
         "pscwin_profile_enable": ([ctypes.c_int], None),
         "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],

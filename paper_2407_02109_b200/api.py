@@ -12,7 +12,7 @@ from typing import Dict, Optional
 import torch
 
 from ._lib import (BF16, CS_MULTI_SCALE, CS_NONE, CS_SINGLE_SCALE, F32, LayerDesc, LayerWeights,  # noqa: F401
-                   MSDesc, ScanDesc, check, index_map, lib, ms_index_map, window_count)
+                   MSDesc, NeckDesc, ScanDesc, check, index_map, lib, ms_index_map, window_count)
 
 
 def _stream() -> int:
@@ -240,3 +240,107 @@ class PSCWinStack:
     def __call__(self, x: torch.Tensor) -> torch.Tensor:
         self.x_in.copy_(x, non_blocking=True)
         return self.replay()
+
+
+# ------------------------------------------------------------------------------------------- encoder ends
+
+def patch_embed(img: torch.Tensor, w_patch: torch.Tensor, b_patch: torch.Tensor,
+                ws: Optional[Workspace] = None) -> torch.Tensor:
+    """pscwin_patch_embed: img [B, 3, 16H, 16W] bf16 -> tokens [B, H, W, C] bf16 (w_patch [C, 768] bf16)."""
+    B, _, Hi, Wi = img.shape
+    H, W, C = Hi // 16, Wi // 16, w_patch.shape[0]
+    ws = ws or Workspace(int(lib().pscwin_patch_embed_workspace_bytes(B, H, W)), img.device)
+    out = torch.empty(B, H, W, C, dtype=torch.bfloat16, device=img.device)
+    check(lib().pscwin_patch_embed(_ptr(img), B, H, W, C, _ptr(w_patch), _ptr(b_patch), _ptr(out), ws.ptr, ws.nbytes,
+                                   _stream()), "patch_embed")
+    return out
+
+
+def resize_bilinear(x: torch.Tensor, H: int, W: int, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """pscwin_resize_bilinear: x [B, h, w, C] bf16 -> [B, H, W, C] (accumulates into `out` when given)."""
+    B, h, w, C = x.shape
+    acc = out is not None
+    if out is None:
+        out = torch.empty(B, H, W, C, dtype=x.dtype, device=x.device)
+    check(lib().pscwin_resize_bilinear(_ptr(x), B, h, w, C, H, W, int(acc), _ptr(out), _stream()), "resize_bilinear")
+    return out
+
+
+def neck_workspace_bytes(desc: NeckDesc) -> int:
+    return int(lib().pscwin_neck_workspace_bytes(ctypes.byref(desc)))
+
+
+def neck(desc: NeckDesc, stage_outs, w: Dict[str, torch.Tensor], ws: Optional[Workspace] = None,
+         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """pscwin_neck: stage outputs (device tensors) -> fused image embedding [B, H0, W0, C_out] bf16.
+    w: w_stage{i} [C_out, C], neck_ln1_g/b, w_neck_conv [C_out, 3, 3, C_out] (channels-last), neck_ln2_g/b."""
+    dev = stage_outs[0].device
+    ws = ws or Workspace(neck_workspace_bytes(desc), dev)
+    if out is None:
+        out = torch.empty(desc.B, desc.H[0], desc.W[0], desc.C_out, dtype=torch.bfloat16, device=dev)
+    n = desc.n_stages
+    xs = (ctypes.c_void_p * n)(*[_ptr(t) for t in stage_outs])
+    wsv = (ctypes.c_void_p * n)(*[_ptr(w[f"w_stage{i}"]) for i in range(n)])
+    check(lib().pscwin_neck(ctypes.byref(desc), xs, wsv, _ptr(w["neck_ln1_g"]), _ptr(w["neck_ln1_b"]),
+                            _ptr(w["w_neck_conv"]), _ptr(w["neck_ln2_g"]), _ptr(w["neck_ln2_b"]), _ptr(out), ws.ptr,
+                            ws.nbytes, _stream()), "neck")
+    return out
+
+
+class HRSAMEncoder:
+    """The whole HRSAM encoder: patch embedding -> the layers (stage outputs after every layer listed in
+    `stage_ends`) -> output fusion (neck). All buffers static; optionally captured once into a CUDA graph.
+
+        enc = HRSAMEncoder(layers, ends_weights, B, H, W, stage_ends=(2, 5, 8, 11))
+        emb = enc(img)     # img [B, 3, 16H, 16W] bf16 -> [B, H, W, 256]
+    """
+
+    def __init__(self, layers, ends: Dict[str, torch.Tensor], B: int, H: int, W: int, stage_ends=(2, 5, 8, 11),
+                 C: int = 768, C_out: int = 256, graph: bool = True):
+        dev = ends["w_patch"].device
+        self.layers, self.ends, self.stage_ends = list(layers), ends, tuple(stage_ends)
+        self.img = torch.empty(B, 3, 16 * H, 16 * W, dtype=torch.bfloat16, device=dev)
+        self.x0 = torch.empty(B, H, W, C, dtype=torch.bfloat16, device=dev)
+        self.bufs = [torch.empty_like(self.x0), torch.empty_like(self.x0)]
+        self.stage = [torch.empty_like(self.x0) for _ in self.stage_ends]
+        self.desc = NeckDesc.make(B, C, C_out, [(H, W)], n_stages=len(self.stage_ends))
+        self.ws_pe = Workspace(int(lib().pscwin_patch_embed_workspace_bytes(B, H, W)), dev)
+        self.ws_neck = Workspace(neck_workspace_bytes(self.desc), dev)
+        self.out = torch.empty(B, H, W, C_out, dtype=torch.bfloat16, device=dev)
+        self.w_patch = ends["w_patch"].reshape(C, -1).contiguous()
+        from ._lib import launch_count
+        n0 = launch_count()
+        self._run()
+        torch.cuda.synchronize()
+        self.launches_per_step = launch_count() - n0
+        self.graph = None
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._run()
+            torch.cuda.synchronize()
+            self.graph = g
+
+    def _run(self):
+        check(lib().pscwin_patch_embed(_ptr(self.img), self.x0.shape[0], self.x0.shape[1], self.x0.shape[2],
+                                       self.x0.shape[3], _ptr(self.w_patch), _ptr(self.ends["b_patch"]),
+                                       _ptr(self.x0), self.ws_pe.ptr, self.ws_pe.nbytes, _stream()), "patch_embed")
+        cur, k = self.x0, 0
+        for j, layer in enumerate(self.layers):
+            if j in self.stage_ends:
+                nxt = self.stage[self.stage_ends.index(j)]
+            else:
+                nxt = self.bufs[k & 1] if self.bufs[k & 1] is not cur else self.bufs[(k + 1) & 1]
+                k += 1
+            layer(cur, out=nxt)
+            cur = nxt
+        neck(self.desc, self.stage, self.ends, ws=self.ws_neck, out=self.out)
+        return self.out
+
+    def __call__(self, img: torch.Tensor) -> torch.Tensor:
+        self.img.copy_(img, non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._run()
+        return self.out
