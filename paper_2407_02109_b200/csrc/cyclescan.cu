@@ -847,6 +847,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
     const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
+    float ypart[NS > 1 ? TSUB : 1];  // NS > 1: this thread's partial C . h per token of the sub-chunk
     auto tstep = [&](int j) {
       const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);      // B pairs
       const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + N + n0);  // C pairs
@@ -871,20 +872,44 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
         }
         y2[k & 1] = __ffma2_rn(__fmul2_rn(ck, invA[k]), h[k], y2[k & 1]);  // C . h = C . (h~ / A)
       }
-      float y = (y2[0].x + y2[1].x) + (y2[0].y + y2[1].y);
-#pragma unroll
-      for (int o = 1; o < NS; o <<= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
-      if (sub == 0) {
-        y = fmaf(D3, v, y);
+      const float y = (y2[0].x + y2[1].x) + (y2[0].y + y2[1].y);
+      if constexpr (NS > 1) {
+        ypart[j] = y;  // combined across the channel's NS threads once per sub-chunk (no per-token shuffle)
+      } else {
         const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
-        p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(y * g);
+        p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(fmaf(D3, v, y) * g);
       }
     };
-    if (nt == TSUB) {  // full sub-chunk: partially unrolled
+    if constexpr (NS > 1) {  // fully unrolled with a guard: ypart stays in registers
+#pragma unroll
+      for (int j = 0; j < TSUB; ++j)
+        if (j < nt) tstep(j);
+    } else if (nt == TSUB) {  // full sub-chunk: partially unrolled
 #pragma unroll 4
       for (int j = 0; j < TSUB; ++j) tstep(j);
     } else {
       for (int j = 0; j < nt; ++j) tstep(j);
+    }
+    if constexpr (NS > 1) {
+      // deferred reduction: partial sums to shared memory, then thread `sub` of each channel finishes the tokens
+      // j = sub, sub + NS, ... (y = sum of the NS partials + 3 D v, gate, bf16 store)
+      float* red = reinterpret_cast<float*>(s_raw + 2 * SB);  // [DPB][NS][TSUB]
+#pragma unroll
+      for (int j = 0; j < TSUB; ++j)
+        if (j < nt) red[(c * NS + sub) * TSUB + j] = ypart[j];
+      __syncthreads();
+#pragma unroll
+      for (int j0 = 0; j0 < TSUB; j0 += NS) {
+        const int j = j0 + sub;
+        if (j < nt) {
+          float y = 0.f;
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2) y += red[(c * NS + s2) * TSUB + j];
+          const float v = __bfloat162float(sv[j * DPB + c]);
+          const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
+          p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(fmaf(D3, v, y) * g);
+        }
+      }
     }
     __syncthreads();
   }
@@ -919,10 +944,16 @@ static int pass_ns() {
   return ns;
 }
 
+// pass-2 dynamic shared memory: two stage buffers (+ the [DPB][NS][TSUB] partial sums when NS > 1)
+template <int NS>
+static size_t pass2_smem(int W) {
+  return 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(W) + (NS > 1 ? (size_t)PASS_DPB * NS * TSUB * 4 : 0);
+}
+
 template <int N, int NS>
 static int pass2_slots_t(int W) {
   int n = 0;
-  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(W);
+  const size_t smem = pass2_smem<NS>(W);
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<N, PASS_DPB, NS, true>,
                                                                 PASS_DPB * NS, smem);
   if (e != cudaSuccess || n <= 0) {
@@ -1027,7 +1058,7 @@ static void launch_pass1(ScanParams& p, cudaStream_t s) {
 template <int N, int NS>
 static void launch_pass2(ScanParams& p, cudaStream_t s) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
-  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(p.R + 2 * N);
+  const size_t smem = pass2_smem<NS>(p.R + 2 * N);
   if (p.bbar == 0)
     launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
   else
