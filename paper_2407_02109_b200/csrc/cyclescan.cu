@@ -847,7 +847,10 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
     const float* sdt = reinterpret_cast<const float*>(buf + St::off_dt(W));
     const __nv_bfloat16* sz = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_z(W));
-    float ypart[NS > 1 ? TSUB : 1];  // NS > 1: this thread's partial C . h per token of the sub-chunk
+    // NS > 1: this thread's partial C . h per token goes to shared memory [TSUB][NS][DPB + 32 / NS] (the padding
+    // puts the NS sub-rows of a warp's channels in disjoint banks)
+    constexpr int RSTR = DPB + 32 / NS;
+    float* red = reinterpret_cast<float*>(s_raw + 2 * SB);
     auto tstep = [&](int j) {
       const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);      // B pairs
       const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + N + n0);  // C pairs
@@ -874,17 +877,13 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
       }
       const float y = (y2[0].x + y2[1].x) + (y2[0].y + y2[1].y);
       if constexpr (NS > 1) {
-        ypart[j] = y;  // combined across the channel's NS threads once per sub-chunk (no per-token shuffle)
+        red[(j * NS + sub) * RSTR + c] = y;  // combined across the channel's NS threads once per sub-chunk
       } else {
         const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
         p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(fmaf(D3, v, y) * g);
       }
     };
-    if constexpr (NS > 1) {  // fully unrolled with a guard: ypart stays in registers
-#pragma unroll
-      for (int j = 0; j < TSUB; ++j)
-        if (j < nt) tstep(j);
-    } else if (nt == TSUB) {  // full sub-chunk: partially unrolled
+    if (nt == TSUB) {  // full sub-chunk: partially unrolled
 #pragma unroll 4
       for (int j = 0; j < TSUB; ++j) tstep(j);
     } else {
@@ -893,10 +892,6 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     if constexpr (NS > 1) {
       // deferred reduction: partial sums to shared memory, then thread `sub` of each channel finishes the tokens
       // j = sub, sub + NS, ... (y = sum of the NS partials + 3 D v, gate, bf16 store)
-      float* red = reinterpret_cast<float*>(s_raw + 2 * SB);  // [DPB][NS][TSUB]
-#pragma unroll
-      for (int j = 0; j < TSUB; ++j)
-        if (j < nt) red[(c * NS + sub) * TSUB + j] = ypart[j];
       __syncthreads();
 #pragma unroll
       for (int j0 = 0; j0 < TSUB; j0 += NS) {
@@ -904,7 +899,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
         if (j < nt) {
           float y = 0.f;
 #pragma unroll
-          for (int s2 = 0; s2 < NS; ++s2) y += red[(c * NS + s2) * TSUB + j];
+          for (int s2 = 0; s2 < NS; ++s2) y += red[(j * NS + s2) * RSTR + c];
           const float v = __bfloat162float(sv[j * DPB + c]);
           const float g = p.gz ? __bfloat162float(sz[j * DPB + c]) : 1.f;
           p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(fmaf(D3, v, y) * g);
@@ -926,8 +921,8 @@ static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 // channels per CTA of the passes and threads per channel (the chunk plan depends on them)
 constexpr int PASS_DPB = 64;
 // threads per channel of the passes (each owns N / NS states). Measured at ViT-B 1024^2: pass 1 is fastest with
-// NS = 4 (more warps, MUFU-bound), pass 2 with NS = 1 (its per-token work -- output reduction, gate, store -- is
-// amortised over all N states). PSCWIN_SCAN_NS1 / PSCWIN_SCAN_NS2 = 1, 2 or 4 override (tuning knobs).
+// NS = 4 (more warps, MUFU-bound), pass 2 with NS = 2 since its output reduction is deferred to one shared-memory
+// combine per 16-token sub-chunk (82 vs 85 us at 1024^2, 1.04 vs 1.08 ms at 4096^2 with two waves). PSCWIN_SCAN_NS1 / PSCWIN_SCAN_NS2 = 1, 2 or 4 override (tuning knobs).
 static int ns_env(const char* name, int dflt) {
   const char* e = getenv(name);
   const int v = e ? atoi(e) : dflt;
@@ -940,14 +935,15 @@ static int pass1_ns() {
 }
 static int pass_ns() {
   static int ns = 0;
-  if (!ns) ns = ns_env("PSCWIN_SCAN_NS2", 1);
+  if (!ns) ns = ns_env("PSCWIN_SCAN_NS2", 2);
   return ns;
 }
 
 // pass-2 dynamic shared memory: two stage buffers (+ the [DPB][NS][TSUB] partial sums when NS > 1)
 template <int NS>
 static size_t pass2_smem(int W) {
-  return 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(W) + (NS > 1 ? (size_t)PASS_DPB * NS * TSUB * 4 : 0);
+  return 2 * StageLayout<PASS_DPB, PASS_DPB * NS, true>::bytes(W) +
+         (NS > 1 ? (size_t)(PASS_DPB + 32 / NS) * NS * TSUB * 4 : 0);
 }
 
 template <int N, int NS>
@@ -979,9 +975,10 @@ static int choose_chunk(int B, int L, int D, int N, int W) {
   static int waves = 0;
   if (!waves) {
     const char* e = getenv("PSCWIN_SCAN_WAVES");
-    waves = e ? atoi(e) : 1;
-    if (waves <= 0) waves = 1;
+    waves = e ? atoi(e) : 0;  // 0 = automatic: two waves for long sequences (chunks stay >= 256 tokens)
+    if (waves < 0) waves = 0;
   }
+  const int wv = waves ? waves : (L >= 32768 ? 2 : 1);
   int sms = 148;
   {
     int dev = 0, v = 0;
@@ -991,7 +988,7 @@ static int choose_chunk(int B, int L, int D, int N, int W) {
       cudaGetLastError();
   }
   const long long cblocks = (long long)B * (D / PASS_DPB);
-  long long target_chunks = (long long)waves * sms * pass2_slots(N, W) / cblocks;
+  long long target_chunks = (long long)wv * sms * pass2_slots(N, W) / cblocks;
   if (target_chunks < 1) target_chunks = 1;
   const long long max_chunks = (48 * 1024) / ((long long)(N + 1) * 4);  // the carry stages one warp's summaries
   if (target_chunks > max_chunks) target_chunks = max_chunks;
