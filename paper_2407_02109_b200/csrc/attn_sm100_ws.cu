@@ -176,11 +176,33 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       if (elect_one()) umma_commit(&ld_empty[st]);
       __syncwarp();
     };
+    // Few items per CTA (1024^2: 1-2): the half-item stagger would serialise the two q tiles of the only items,
+    // so issue both q tiles in lockstep (S0, S1, PV0, PV1 per item); the stagger pays off only in long runs.
+    const bool lockstep = p.n_items <= 3 * (int)gridDim.x;
     bool have_prev = false, prev_act1 = false;
     int prev_stage = 0;
     uint32_t prev_sb = 0;
     bool first = true;
-    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (int item = blockIdx.x; lockstep && item < p.n_items; item += gridDim.x) {
+      int b, h, X0, Y0;
+      decode(item, b, h, X0, Y0);
+      const bool act0 = q_active(0, Y0), act1 = q_active(1, Y0);
+      mbar_wait(&ld_full[stage], phase);
+      if (p.patch) mbar_wait(&patch_done[stage], phase);
+      ATT_TS(32, ev);
+      tc_fence_after();
+      const uint32_t sb = smem_u32(smem + stage * STAGE);
+      if (act0) issue_s(0, sb);
+      if (act1) issue_s(1, sb);
+      if (act0) issue_pv(0, sb);
+      if (act1) issue_pv(1, sb);
+      release(stage);
+      if (++stage == 2) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+    for (int item = blockIdx.x; !lockstep && item < p.n_items; item += gridDim.x) {
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
       const bool act0 = q_active(0, Y0), act1 = q_active(1, Y0);
