@@ -445,30 +445,64 @@ def run_rows(args, rank, world, local_rank):
         if not tdist.is_initialized():
             tdist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % _free_port(), rank=0, world_size=1)
     exchange = TorchDistExchange()
+    lib_nccl = args.exchange == "nccl-lib"
+    comm = None
+    if lib_nccl:
+        from paper_2407_02109_b200.bands import DistLayer, NcclComm
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")  # one node: bootstrap over loopback (data over NVLink)
+        comm = NcclComm(rank, world)
     layers = []
     for i, cfg in enumerate(cfgs):
         w = synth.make_weights(cfg, layer=i)
         dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
               for k, v in w.items()}
-        layers.append(BandLayer(pl.LayerDesc.from_config(cfg), dw, r0, r1, rank, world))
+        if lib_nccl:
+            layers.append(DistLayer(pl.LayerDesc.from_config(cfg), dw, r0, r1, comm))
+        else:
+            layers.append(BandLayer(pl.LayerDesc.from_config(cfg), dw, r0, r1, rank, world))
     x_full = synth.make_input(cfgs[0], layer=0)
     xb = torch.tensor(x_full[:, r0:r1], dtype=torch.bfloat16, device=dev).contiguous()
     bufs = [torch.empty_like(xb), torch.empty_like(xb)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def step(x):
+    def step_eager(x):
         cur = x
         for j, layer in enumerate(layers):
             nxt = bufs[j & 1]
-            band_forward(layer, cur, exchange, out=nxt)
+            if lib_nccl:
+                layer(cur, out=nxt)
+            else:
+                band_forward(layer, cur, exchange, out=nxt)
             cur = nxt
         return cur
+
+    graph = None
+    xstatic = torch.empty_like(xb)
+    if lib_nccl:  # kernels and NCCL exchanges of the whole step in one CUDA graph
+        xstatic.copy_(xb)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step_eager(xstatic)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            gout = step_eager(xstatic)
+
+    def step(x):
+        if graph is None:
+            return step_eager(x)
+        if x is not xstatic:
+            xstatic.copy_(x, non_blocking=True)
+        graph.replay()
+        return gout
 
     for _ in range(args.warmup):
         step(xb)
     torch.cuda.synchronize()
     n0 = pl.launch_count()
-    step(xb)
+    step_eager(xb)
     torch.cuda.synchronize()
     launches_per_step = pl.launch_count() - n0
     stream = torch.cuda.current_stream()
@@ -813,6 +847,9 @@ def main():
     ap.add_argument("--shard", default="images", choices=["images", "rows"],
                     help="images: each rank its own image(s) (weak scaling, default); rows: one image split by "
                          "window rows over the ranks with halo / scan-carry exchange (config 4, strong scaling)")
+    ap.add_argument("--exchange", default="nccl-lib", choices=["nccl-lib", "torch"],
+                    help="--shard rows: exchanges inside libpscwin over NCCL (pscwin_dist_forward, graph-captured) or "
+                         "between the band phases via torch.distributed")
     ap.add_argument("--ablation", action="store_true",
                     help="Table 3 rendition: the 12-block encoder body per attention / cycle-scan variant at 1024^2 and "
                          "2048^2 (one JSON line per variant; SURVEY NEXT-4)")
@@ -844,6 +881,7 @@ def main():
 
     if world > 1:
         import torch
+        os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")  # one node (the contract): bootstrap over loopback
         torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if args.shard == "rows":
@@ -865,7 +903,9 @@ def main():
                            "grid": f"{c0.H}x{c0.W}", "layers": len(res["cfgs"]),
                            "parallelism": f"window-row bands x{world} (halo + scan-carry exchange)",
                            "rank0_band_rows": list(res["band"]),
-                           "l2": "flushed before every timed step (256 MiB write)", "launch": "eager"},
+                           "l2": "flushed before every timed step (256 MiB write)",
+                           "exchange": args.exchange,
+                           "launch": "CUDA graph (kernels + NCCL)" if args.exchange == "nccl-lib" else "eager"},
                 "e2e": {"value": round(res["e2e_ms"] / res["images"], 4), "unit": "ms/image",
                         "h2d_bytes_per_step": int(res["h2d"]), "d2h_bytes_per_step": int(res["d2h"])},
                 "gpu_launches": int(res["launches"]), "clocks": res["clocks"], "roofline": None}

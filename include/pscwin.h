@@ -271,6 +271,23 @@ int pscwin_band_attn_end(const pscwin_layer_desc* global_desc, const pscwin_band
                          const pscwin_layer_weights* wts, const void* x_band, void* x_out, void* workspace,
                          size_t ws_bytes, void* stream);
 
+/* One layer of a window-row-sharded image with the exchanges done inside the library over NCCL (SURVEY §8(b)
+ * pscwin_dist_forward; §8(e)): the rank / world come from the communicator (an ncclComm_t passed as void*, from
+ * the caller's own NCCL setup or pscwin_nccl_comm_init), the band is [row_begin, row_end) as for the band
+ * phases, and all kernels and NCCL operations (conv-history ring send/recv, ncclAllGather of the scan records,
+ * QKV halo send/recv with the neighbours) are enqueued on `stream` — the call is CUDA-graph capturable. Every
+ * rank of the communicator must call it for the same layer. x_band, x_band_out [rows, W, C] bf16 (no alias).
+ * Workspace: pscwin_dist_workspace_bytes (= pscwin_band_workspace_bytes). Errors: as the band phases;
+ * ERR_CUDA for an NCCL failure. */
+int pscwin_nccl_get_unique_id(void* id_out /* host, 128 bytes */);
+int pscwin_nccl_comm_init(const void* id /* host, 128 bytes */, int32_t world, int32_t rank, void** comm_out);
+int pscwin_nccl_comm_destroy(void* comm);
+size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* global_desc, int32_t row_begin, int32_t row_end,
+                                   int32_t rank, int32_t world);
+int pscwin_dist_forward(const pscwin_layer_desc* global_desc, const pscwin_layer_weights* wts, const void* x_band,
+                        void* x_band_out, int32_t row_begin, int32_t row_end, void* nccl_comm, void* workspace,
+                        size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this library since it was loaded (every launcher counts itself). */
 int64_t pscwin_launch_count(void);

@@ -32,7 +32,8 @@ EXPORTS = [
     "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
     "pscwin_ms_window_count", "pscwin_ms_index_map", "pscwin_ms_workspace_bytes", "pscwin_ms_forward",
     "pscwin_patch_embed_workspace_bytes", "pscwin_patch_embed", "pscwin_resize_bilinear", "pscwin_neck_workspace_bytes",
-    "pscwin_neck",
+    "pscwin_neck", "pscwin_nccl_get_unique_id", "pscwin_nccl_comm_init", "pscwin_nccl_comm_destroy",
+    "pscwin_dist_workspace_bytes", "pscwin_dist_forward",
 ]
 
 
@@ -190,6 +191,12 @@ def lib() -> ctypes.CDLL:
         "pscwin_neck_workspace_bytes": ([ctypes.POINTER(NeckDesc)], sz),
         "pscwin_neck": ([ctypes.POINTER(NeckDesc), ctypes.POINTER(vp), ctypes.POINTER(vp), vp, vp, vp, vp, vp, vp, vp,
                          sz, vp], ctypes.c_int),
+        "pscwin_nccl_get_unique_id": ([vp], ctypes.c_int),
+        "pscwin_nccl_comm_init": ([vp, i32, i32, ctypes.POINTER(vp)], ctypes.c_int),
+        "pscwin_nccl_comm_destroy": ([vp], ctypes.c_int),
+        "pscwin_dist_workspace_bytes": ([ctypes.POINTER(LayerDesc), i32, i32, i32, i32], sz),
+        "pscwin_dist_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, i32, i32, vp, vp, sz,
+                                 vp], ctypes.c_int),
         "pscwin_launch_count": ([], ctypes.c_int64),
         "pscwin_profile_enable": ([ctypes.c_int], None),
         "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],

@@ -121,3 +121,49 @@ class LoopbackBands:
         for g in range(G):
             L[g].attn_end(xs[g], outs[g])
         return torch.cat(outs, dim=1)
+
+
+class NcclComm:
+    """A communicator owned by libpscwin (pscwin_nccl_comm_init) for pscwin_dist_forward: rank 0 creates the NCCL
+    unique id and torch.distributed broadcasts it (any backend); world = 1 needs no process group."""
+
+    def __init__(self, rank: int = 0, world: int = 1):
+        import numpy as np
+        idb = np.zeros(128, dtype=np.uint8)
+        if rank == 0:
+            check(lib().pscwin_nccl_get_unique_id(idb.ctypes.data), "nccl_get_unique_id")
+        if world > 1:
+            import torch.distributed as tdist
+            obj = [idb.tobytes()]
+            tdist.broadcast_object_list(obj, src=0)
+            idb = np.frombuffer(obj[0], dtype=np.uint8).copy()
+        self.ptr = ctypes.c_void_p()
+        check(lib().pscwin_nccl_comm_init(idb.ctypes.data, world, rank, ctypes.byref(self.ptr)), "nccl_comm_init")
+        self.rank, self.world = rank, world
+
+    def close(self):
+        if self.ptr:
+            lib().pscwin_nccl_comm_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+
+class DistLayer:
+    """One PSCWin layer on this rank's band, exchanges inside the library over NCCL (pscwin_dist_forward)."""
+
+    def __init__(self, desc: LayerDesc, weights: Dict[str, torch.Tensor], row_begin: int, row_end: int,
+                 comm: NcclComm):
+        self.desc, self.weights, self.comm = desc, weights, comm
+        self.wts = LayerWeights.from_tensors(weights)
+        self.r0, self.r1 = row_begin, row_end
+        n = int(lib().pscwin_dist_workspace_bytes(ctypes.byref(desc), row_begin, row_end, comm.rank, comm.world))
+        if n == 0:
+            raise ValueError("invalid band for this layer")
+        dev = next(iter(weights.values())).device
+        self.ws = torch.empty(n, dtype=torch.uint8, device=dev)
+
+    def __call__(self, x_band: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
+        out = torch.empty_like(x_band) if out is None else out
+        check(lib().pscwin_dist_forward(ctypes.byref(self.desc), ctypes.byref(self.wts), _ptr(x_band), _ptr(out),
+                                        self.r0, self.r1, self.comm.ptr, self.ws.data_ptr(), self.ws.numel(),
+                                        _stream()), "dist_forward")
+        return out

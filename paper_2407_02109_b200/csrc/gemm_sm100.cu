@@ -29,9 +29,11 @@ constexpr size_t GEMM_SMEM_MAX = 232448;         // 227 KB opt-in limit per CTA
 // [residual tiles 2 x nch x 16 KB][barriers]; B rows per CTA = BN (single CTA) or BN / 2 (CTA pair)
 __host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid, bool f32 = false) {
   const size_t nch = (size_t)(BN + 63) / 64;
-  // f32 outputs: two more 16 KB staging boxes (a 64-column f32 chunk is two 128 x 32 boxes; two chunks in flight)
-  return 1024 + 2 * STAGE_OUT_BYTES + (resid ? 2 * nch * STAGE_OUT_BYTES : (f32 ? 2 * STAGE_OUT_BYTES : 0)) +
-         2 * 256 * 4 + 256;
+  // f32 outputs: two more 16 KB staging boxes (a 64-column f32 chunk is two 128 x 32 boxes; two chunks in flight).
+  // residual with BN > 128 ("in place"): ONE set of residual chunks, the output overwrites them and is stored from
+  // there (the two output staging boxes stay allocated but unused; the layout offsets do not change).
+  const size_t res = resid ? (BN > 128 ? nch : 2 * nch) * STAGE_OUT_BYTES : (f32 ? 2 * STAGE_OUT_BYTES : 0);
+  return 1024 + 2 * STAGE_OUT_BYTES + res + 2 * 256 * 4 + 256;
 }
 __host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
   return A_STAGE_BYTES + (size_t)(pair ? BN / 2 : BN) * BK * 2;
@@ -73,8 +75,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
   uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
   uint8_t* s_res = s_stage + 2 * STAGE_OUT_BYTES;   // 2 x nch x 16 KB residual tiles (TMA-loaded)
+  // residual tiles: double-buffered (BN <= 128) or one set written over in place by the output (BN > 128)
+  const bool res_inplace = resid_tma && BN > 128;
   float* s_bias = reinterpret_cast<float*>(
-      s_res + (resid_tma ? 2 * nch * STAGE_OUT_BYTES : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256]
+      s_res + (resid_tma ? (res_inplace ? 1 : 2) * nch * STAGE_OUT_BYTES
+                         : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256]
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 2 * 256);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs of a pair)
       mbar_init(&rfull[i], 1);
-      mbar_init(&rempty[i], 256);
+      mbar_init(&rempty[i], res_inplace ? 1 : 256);  // in place: the store issuer, after the stores read out
     }
     if (resid_tma) tma_prefetch_desc(&tmRes);
     fence_barrier_init();
@@ -146,10 +151,30 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int rbuf = 0;
       uint32_t rphase = 0;
+      auto load_res = [&](int m0, int n0, int buf) {  // this CTA's residual rows of the tile
+        if (m0 + mrow < p.M) {
+          mbar_arrive_expect_tx(&rfull[buf], nch * STAGE_OUT_BYTES);
+          for (int c = 0; c < nch; ++c)
+            tma_load_2d(s_res + (buf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[buf], n0 + c * 64, m0 + mrow, pol_a);
+        } else {
+          mbar_arrive(&rfull[buf]);
+        }
+      };
       for (int tile = tile0; tile < n_tiles; tile += tstride) {
         int m0, n0, kb0, kb1, s;
         coords(tile, m0, n0, kb0, kb1, s);
-        if (resid_tma) {
+        // in place: the single residual set is refilled once the previous tile's stores have read it out; probe
+        // that between k-block loads so the mainloop never waits for it
+        bool res_pending = res_inplace;
+        auto try_res = [&](bool block) {
+          if (!res_pending) return;
+          if (block) mbar_wait(&rempty[0], rphase ^ 1);
+          else if (!mbar_test(&rempty[0], rphase ^ 1)) return;
+          load_res(m0, n0, 0);
+          rphase ^= 1;
+          res_pending = false;
+        };
+        if (resid_tma && !res_inplace) {
           // residual tile of this CTA's rows (double-buffered, consumed by the epilogue), issued ahead of the k-loop
           mbar_wait(&rempty[rbuf], rphase ^ 1);
           if (m0 + mrow < p.M) {
@@ -172,6 +197,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t bytes = ((int)a0_in + (int)a1_in) * A_STAGE_BYTES + ((int)b0_in + (int)b1_in) * B_STAGE_BYTES;
           const bool a_mine = rank ? a1_in : a0_in, b_mine = rank ? b1_in : b0_in;
           for (int kb = kb0; kb < kb1; ++kb) {
+            try_res(false);
             mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
             const uint32_t fb = full0 + stage * 8;
@@ -185,6 +211,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
         } else {
           for (int kb = kb0; kb < kb1; ++kb) {
+            try_res(false);
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], A_STAGE_BYTES + B_STAGE_BYTES);
             tma_load_2d(sA + stage * A_STAGE_BYTES, &tmA, &full[stage], kb * BKe, m0, pol_a);
@@ -195,6 +222,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
           }
         }
+        try_res(true);
       }
     }
   } else if (warp == 1) {
@@ -342,8 +370,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) res[q] = *reinterpret_cast<const uint4*>(rt + swz_offset(row_local, half * 4 + q, 128));
         }
-        uint8_t* stg = s_stage + (gseq & 1) * STAGE_OUT_BYTES;
-        if (tma_out) {
+        // in place: each thread overwrites exactly the residual bytes it just read, and the chunk is stored from there
+        uint8_t* stg = res_inplace ? s_res + cc * STAGE_OUT_BYTES : s_stage + (gseq & 1) * STAGE_OUT_BYTES;
+        if (tma_out && !res_inplace) {
           if (issuer && gseq >= 2) bulk_wait_read1();
           named_bar_sync(1, 256);
         } else if (f32_tma) {  // a chunk = two 128 x 32 f32 boxes; buffers of parity gseq & 1 (two chunks in
@@ -461,7 +490,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (resid_tma) {
+      if (res_inplace) {  // the residual set may be refilled once this tile's stores have read it out
+        if (issuer) {
+          bulk_wait_read0();
+          mbar_arrive(&rempty[0]);
+        }
+        rphase ^= 1;
+      } else if (resid_tma) {
         mbar_arrive(&rempty[rbuf]);
         if (++rbuf == 2) {
           rbuf = 0;
@@ -572,11 +607,8 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   // tile N: one tile when N <= 256 (<= 128 with a residual, whose tiles are staged in shared memory); else the
   // width (256 or 128) with the fewest scheduling rounds, weighting a round by its tile width
   if (p.BN <= 0) {
-    const int cap = resid ? 128 : 256;
-    if (p.N <= cap) {
+    if (p.N <= 256) {
       p.BN = ((p.N + 15) / 16) * 16;
-    } else if (resid) {
-      p.BN = 128;
     } else {
       auto cost = [&](int bn) {
         const long long tiles = (long long)m_tiles * ((p.N + bn - 1) / bn);
@@ -589,7 +621,6 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
       }
     }
   }
-  if (resid && p.BN > 128) return -2;
   if (pair && (p.BN % 16)) return -2;
   // ring depth: as many stages as fit next to the staging / residual buffers
   const bool f32o = p.epi == EPI_STORE_F32;

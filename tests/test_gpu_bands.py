@@ -60,3 +60,59 @@ def test_band_contract(pl):
     dw = dev_weights(synth.make_weights(cfg), cfg)
     with pytest.raises(ValueError):
         BandLayer(desc, dw, 4, 20, 1, 2)  # not whole window rows
+
+
+_NCCL_CASE = r"""
+import os, sys
+os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")   # single-node bootstrap over loopback
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import torch, numpy as np, synth, oracle
+import paper_2407_02109_b200 as pl
+from paper_2407_02109_b200.bands import DistLayer, NcclComm
+from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+cfg = [synth.tiny(H=32, W=16), synth.tiny(H=32, W=16, cycle_scan=1, mlp_hidden=128), synth.vitb(64, cycle_scan=1)][{i}]
+x, w = synth.make_input(cfg), synth.make_weights(cfg)
+dw = dev_weights(w, cfg)
+desc = pl.LayerDesc.from_config(cfg)
+xd = dev(x)
+whole = pl.PSCWinLayer(desc, dw)(xd)
+comm = NcclComm(0, 1)
+layer = DistLayer(desc, dw, 0, cfg.H, comm)
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+xin = xd[0].contiguous()
+with torch.cuda.stream(s):
+    got = layer(xin)
+torch.cuda.current_stream().wait_stream(s)
+torch.cuda.synchronize()
+if cfg.cycle_scan:
+    assert rel_err(host(got), host(whole[0])) < 8e-3
+else:
+    assert torch.equal(got, whole[0])
+assert rel_err(host(got)[None], oracle.pscwin_layer(x, w, cfg)) < BF16_TOL
+out = torch.empty_like(got)
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g):
+    layer(xin, out=out)
+out.zero_()
+g.replay()
+torch.cuda.synchronize()
+assert torch.equal(out, got)
+comm.close()
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("i", [0, 1, 2])
+def test_dist_forward_nccl_world1(pl, i):
+    # pscwin_dist_forward with a library-owned NCCL communicator of one rank: the in-library ring / all-gather
+    # exchanges run for real; the whole image as one band equals pscwin_forward, and the call captures into a
+    # CUDA graph (NCCL operations on the layer's stream). Run in a subprocess with a timeout: an NCCL bootstrap
+    # problem must fail the test, not hang the suite.
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _NCCL_CASE.format(root=root, tests=os.path.join(root, "tests"), i=i)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
