@@ -281,7 +281,7 @@ int pscwin_band_attn_end(const pscwin_layer_desc* global_desc, const pscwin_band
  * ERR_CUDA for an NCCL failure. */
 int pscwin_nccl_get_unique_id(void* id_out /* host, 128 bytes */);
 int pscwin_nccl_comm_init(const void* id /* host, 128 bytes */, int32_t world, int32_t rank, void** comm_out);
-int pscwin_nccl_comm_destroy(void* comm);
+int pscwin_nccl_comm_destroy(void* comm);  /* after every CUDA graph holding its operations is destroyed */
 size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* global_desc, int32_t row_begin, int32_t row_end,
                                    int32_t rank, int32_t world);
 int pscwin_dist_forward(const pscwin_layer_desc* global_desc, const pscwin_layer_weights* wts, const void* x_band,

@@ -142,6 +142,8 @@ class NcclComm:
         self.rank, self.world = rank, world
 
     def close(self):
+        """ncclCommDestroy; call only after every CUDA graph that captured operations on this communicator has
+        been destroyed (NCCL waits for them)."""
         if self.ptr:
             lib().pscwin_nccl_comm_destroy(self.ptr)
             self.ptr = ctypes.c_void_p()

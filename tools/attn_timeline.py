@@ -1,4 +1,8 @@
-"""Run one attention layer with PSCWIN_ATTN_TIMELINE and print per-CTA phase timings (debug)."""
+"""Run one attention layer with PSCWIN_ATTN_TIMELINE and print per-CTA phase timings (debug).
+
+    python tools/attn_timeline.py [side=64]      # ViT-B, side x side token grid, plain and shifted layers
+Events per CTA (globaltimer ns): loader = item load issued; mma = S issued / PV issued; wg0/wg1 = S ready,
+P written, O ready, O stored (per q-tile slot)."""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -9,8 +13,9 @@ os.environ["PSCWIN_ATTN_TIMELINE"] = path
 import torch, synth
 import paper_2407_02109_b200 as pl
 from gpu_util import dev
+side = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 for shift in (0, 8):
-    cfg = synth.vitb(64, shift_x=shift, shift_y=shift)
+    cfg = synth.vitb(side, shift_x=shift, shift_y=shift)
     qkv = dev(synth.make_qkv(cfg)); qp = dev(synth.make_pad_qkv(cfg), "f32")
     d = pl.LayerDesc.from_config(cfg)
     for _ in range(3):
@@ -25,4 +30,13 @@ for run in (2, 5):
         row = t[cta]
         def ev(base):
             v = row[base:base + 32]; v = v[v > 0]; return ((v - t0) / 1e3).round(2).tolist()
-        print(f"cta {cta}: load {ev(0)}\n   mma {ev(32)}\n   wg0 {ev(64)}\n   wg1 {ev(96)}")
+        print(f"cta {cta}: load {ev(0)[:12]}\n   mma {ev(32)[:12]}\n   wg0 {ev(64)[:12]}\n   wg1 {ev(96)[:12]}")
+    # steady-state per-item spacing of slot 0's "S ready" events (every 4th wg0 event), median over CTAs
+    gaps = []
+    for cta in range(148):
+        v = np.sort(t[cta][64:96]); v = v[v > 0]
+        if len(v) >= 12:
+            s = v[::4]
+            gaps.append(np.median(np.diff(s)) / 1e3)
+    if gaps:
+        print(f"median per-item period (slot 0): {np.median(gaps):.2f} us over {len(gaps)} CTAs")
