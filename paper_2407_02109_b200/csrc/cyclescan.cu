@@ -380,7 +380,15 @@ __global__ void __launch_bounds__(DT_THREADS) scan_dt_kernel(ScanParams p) {
 // ------------------------------------------------------------------------------------------------- pass 1
 // NS threads per channel, each owning NH = N / NS of its states (NS = 2 halves the registers per thread, which
 // doubles the resident warps that hide the MUFU / FMA latencies).
-template <int N, int DPB, int NS, bool ZOH>
+// PK > 0: every PK-th state pair takes its decay factor from the degree-5 polynomial on the FMA pipe instead of MUFU
+// ex2 (the MUFU pipe bounds the passes while the FMA pipe has slack; same accuracy, exp2_poly5x2)
+template <int PK>
+__device__ __forceinline__ float2 decay2(int k, float2 x) {
+  if (PK > 0 && k % PK == PK - 1) return exp2_poly5x2(x);
+  return make_float2(ex2_approx(x.x), ex2_approx(x.y));
+}
+
+template <int N, int DPB, int NS, bool ZOH, int PK>
 __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
   pdl_trigger();
   pdl_wait();
@@ -438,7 +446,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
         const float4 bq = b4[k / 2];
         const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
-        const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 dA = decay2<PK>(k, x);
         const float2 wn = __fmul2_rn(bk, nv2);                    // -w = -B v
         if (ZOH) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);               // h~ + w
@@ -790,7 +798,7 @@ __global__ void __launch_bounds__(256) scan_dist_carry_kernel(ScanParams p, cons
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
-template <int N, int DPB, int NS, bool ZOH>
+template <int N, int DPB, int NS, bool ZOH, int PK>
 __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
   pdl_trigger();
   pdl_wait();
@@ -864,7 +872,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
         const float2 bk = (k & 1) ? make_float2(bq.z, bq.w) : make_float2(bq.x, bq.y);
         const float2 ck = (k & 1) ? make_float2(cq.z, cq.w) : make_float2(cq.x, cq.y);
         const float2 x = __fmul2_rn(dt2, A2[k]);
-        const float2 dA = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+        const float2 dA = decay2<PK>(k, x);
         const float2 wn = __fmul2_rn(bk, nv3);                    // -3 B v
         if (ZOH) {
           const float2 t = __ffma2_rn(wn, m1, h[k]);
@@ -939,6 +947,24 @@ static int pass_ns() {
   return ns;
 }
 
+// Polynomial-exp2 period (state pairs) of the ZOH passes: every PK-th pair's decay factors come from the FMA pipe
+// (decay2). PSCWIN_SCAN_POLY1 / PSCWIN_SCAN_POLY2 override (0 = all MUFU; pass 1: 2 or 4, pass 2: 4 or 8).
+static int pk_env(const char* name, int dflt, int a, int b) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  return (v == 0 || v == a || v == b) ? v : dflt;
+}
+static int pass1_pk() {
+  static int pk = -1;
+  if (pk < 0) pk = pk_env("PSCWIN_SCAN_POLY1", 0, 2, 4);
+  return pk;
+}
+static int pass2_pk() {
+  static int pk = -1;
+  if (pk < 0) pk = pk_env("PSCWIN_SCAN_POLY2", 0, 4, 8);
+  return pk;
+}
+
 // pass-2 dynamic shared memory: two stage buffers (+ the [DPB][NS][TSUB] partial sums when NS > 1)
 template <int NS>
 static size_t pass2_smem(int W) {
@@ -950,7 +976,7 @@ template <int N, int NS>
 static int pass2_slots_t(int W) {
   int n = 0;
   const size_t smem = pass2_smem<NS>(W);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<N, PASS_DPB, NS, true>,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, scan_pass2_kernel<N, PASS_DPB, NS, true, 0>,
                                                                 PASS_DPB * NS, smem);
   if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
@@ -1046,20 +1072,30 @@ template <int N, int NS>
 static void launch_pass1(ScanParams& p, cudaStream_t s) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
   const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false>::bytes(p.R + 2 * N);
-  if (p.bbar == 0)
-    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  const int pk = pass1_pk();
+  if (p.bbar != 0)
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, false, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else if (pk == 2)
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true, 2>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else if (pk == 4)
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true, 4>, grid, dim3(PASS_DPB * NS), smem, s, p);
   else
-    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, false>, grid, dim3(PASS_DPB * NS), smem, s, p);
+    launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);
 }
 
 template <int N, int NS>
 static void launch_pass2(ScanParams& p, cudaStream_t s) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
   const size_t smem = pass2_smem<NS>(p.R + 2 * N);
-  if (p.bbar == 0)
-    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  const int pk = pass2_pk();
+  if (p.bbar != 0)
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, false, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else if (pk == 4)
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true, 4>, grid, dim3(PASS_DPB * NS), smem, s, p);
+  else if (pk == 8)
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true, 8>, grid, dim3(PASS_DPB * NS), smem, s, p);
   else
-    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, false>, grid, dim3(PASS_DPB * NS), smem, s, p);
+    launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, true, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);
 }
 
 template <int N>
