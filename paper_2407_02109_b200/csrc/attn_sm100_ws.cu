@@ -16,6 +16,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -38,6 +40,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct AttnWsArgs {
   int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
   int rpt, n_tiles, tile_slots, n_items;
+  int tma_out;  // 1: O tiles staged in smem and TMA-stored; 0: 16-byte global stores of the real rows
   float sl2;
   const __nv_bfloat16 *kx, *ky, *vp;
   __nv_bfloat16* out;
@@ -46,7 +49,8 @@ struct AttnWsArgs {
 
 template <int D, bool MASKED>
 __global__ void __launch_bounds__(WS_THREADS, 1)
-    window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, AttnWsArgs p) {
+    window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmO,
+                          AttnWsArgs p) {
   pdl_trigger();
   constexpr int ROWB = D * 2;
   constexpr int TILE = 128 * ROWB;           // smem bytes reserved per 128-slot tile
@@ -73,9 +77,12 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmQKV);
+    tma_prefetch_desc(&tmO);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&ld_full[i], 1);
-      mbar_init(&ld_empty[i], 1);
+      // a stage is free once its MMAs completed (commit) AND both q-tile slots' O tiles, staged in the slot's Q
+      // region of the stage, have been read out by their TMA stores (one arrival per slot)
+      mbar_init(&ld_empty[i], 3);
       mbar_init(&patch_done[i], 256);  // slot 0's threads patch (slot 1 runs half an item behind)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 256);
@@ -294,6 +301,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         }
         fence_proxy_async_smem();
         mbar_arrive(&patch_done[stage]);
+        __syncwarp();
       }
       if (active) {
         // MASKED: valid-key bitmask per 32-column chunk (real slots only); columns past the window are never read
@@ -356,12 +364,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // pass 2: p = 2^(s log2(e)/sqrt(d) - base) (packed fp32x2 scale, MUFU ex2), partial sums, P (bf16 pairs)
         // written over the consumed S columns
         float2 ls = make_float2(0.f, 0.f);
-        auto exp_chunk = [&](const uint32_t (&r)[32], uint32_t m, uint32_t (&pk)[16]) {
+        // 16 columns: pairs of global index (OFF + j) / 2 with (OFF + j) / 2 % 3 == 2 go to the FMA pipe (a third of
+        // each 32-column chunk; the MUFU ex2 rate bounds this loop)
+        auto exp16 = [&](auto off_c, const uint32_t (&r)[16], uint32_t m, uint32_t (&pk)[8]) {
+          constexpr int OFF = decltype(off_c)::value;
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
+          for (int j = 0; j < 16; j += 2) {
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl2, nb);
             float e0, e1;
-            if ((j / 2) % 3 == 2) {  // every third pair on the FMA pipe: the MUFU ex2 rate bounds this loop
+            if (((OFF + j) / 2) % 3 == 2) {
               const float2 e = exp2_poly2(x);
               e0 = e.x;
               e1 = e.y;
@@ -370,8 +381,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
               e1 = ex2_approx(x.y);
             }
             if (MASKED || m != 0xFFFFFFFFu) {  // invalid keys, or stale columns past a 16-key window
-              e0 = ((m >> j) & 1u) ? e0 : 0.f;
-              e1 = ((m >> (j + 1)) & 1u) ? e1 : 0.f;
+              e0 = ((m >> (OFF + j)) & 1u) ? e0 : 0.f;
+              e1 = ((m >> (OFF + j + 1)) & 1u) ? e1 : 0.f;
             }
             ls = __fadd2_rn(ls, make_float2(e0, e1));
             pk[j / 2] = pack_bf16(e0, e1);
@@ -380,12 +391,21 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // P for key k goes to TMEM column k/2 (keys < 128) or 64 + k/2 (keys >= 128): each thread overwrites only S
         // columns it has already consumed (the PV MMA reads A from columns [0,64) and [128,192)).
         const int p_off = (split && hc) ? 64 : 0;
-        for (int c0 = c_lo; c0 < c_lo + nc; c0 += 32) {
-          uint32_t r0[32], pk[16];
-          tmem_ld32(tS + c0, r0);
-          tmem_wait_ld();
-          exp_chunk(r0, (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask, pk);
-          tmem_st16(tS + p_off + c0 / 2, pk);
+        {  // two 16-column register sets: the TMEM load of the next 16 columns is in flight while these are
+           // exponentiated (the 96-register budget of 18 warps rules out 32-column double buffering)
+          uint32_t ra[16], rb[16], pk[8];
+          if (nc > 0) tmem_ld16(tS + c_lo, ra);
+          for (int c0 = c_lo; c0 < c_lo + nc; c0 += 32) {
+            const uint32_t m = (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask;
+            tmem_wait_ld_dep16(ra);
+            tmem_ld16(tS + c0 + 16, rb);  // (a 16-key window reads 16 stale columns here, masked by tail_mask)
+            exp16(std::integral_constant<int, 0>(), ra, m, pk);
+            tmem_st8(tS + p_off + c0 / 2, pk);
+            tmem_wait_ld_dep16(rb);
+            if (c0 + 32 < c_lo + nc) tmem_ld16(tS + c0 + 32, ra);
+            exp16(std::integral_constant<int, 16>(), rb, m, pk);
+            tmem_st8(tS + p_off + c0 / 2 + 8, pk);
+          }
         }
         tmem_wait_st();
         tc_fence_before();
@@ -414,11 +434,14 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         mbar_arrive(&o_free[a]);
         named_bar_sync(1 + a, 256);  // partial sums of both halves are in shared memory
         const float lsum = red_sum[row] + (split ? red_sum[128 + row] : 0.f);
-        const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
-        const int Y = Y0 + iy, X = X0 + ix;
-        if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+        // merge / crop: the normalised O tile is staged in this slot's Q region of the stage (Q_a is dead
+        // once S_a has been computed) in the TMA box layout, and ONE 5-D tensor store writes the window's rows back
+        // to the [B,H,W,C] grid; rows outside the grid (the pads) fall outside the tensor and are clipped by TMA
+        // (a TMA tensor store whose box starts at a negative coordinate traps: windows of the first padded row /
+        // column store their real rows directly instead; boxes running past the far edges are clipped)
+        if (p.tma_out && X0 >= 0 && Y0 + a * p.rpt >= 0) {
           const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
-          uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D + hc * DH);
+          uint8_t* so = smem + stage * STAGE + a * TILE;
 #pragma unroll
           for (int c = 0; c < DH / 8; ++c) {
             uint4 v;
@@ -426,11 +449,40 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
             v.y = pack_bf16(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
             v.z = pack_bf16(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
             v.w = pack_bf16(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
-            dst[c] = v;
+            *reinterpret_cast<uint4*>(so + swz_offset(row, hc * (DH / 8) + c, ROWB)) = v;
           }
+          fence_proxy_async_smem();
+          named_bar_sync(1 + a, 256);
+          if (gtid == 0) {
+            tma_store_5d(&tmO, so, 0, h, X0, Y0 + a * p.rpt, b);
+            bulk_commit();
+            bulk_wait_read0();  // the stage's Q region may be refilled once the store has read it
+            mbar_arrive(&ld_empty[stage]);
+          }
+        } else {
+          const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
+          const int Y = Y0 + iy, X = X0 + ix;
+          if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+            const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+            uint4* dst =
+                reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D + hc * DH);
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(o[c * 8 + 0]) * inv, __uint_as_float(o[c * 8 + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(o[c * 8 + 2]) * inv, __uint_as_float(o[c * 8 + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(o[c * 8 + 4]) * inv, __uint_as_float(o[c * 8 + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(o[c * 8 + 6]) * inv, __uint_as_float(o[c * 8 + 7]) * inv);
+              dst[c] = v;
+            }
+          }
+          if (gtid == 0) mbar_arrive(&ld_empty[stage]);
         }
         if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
+      } else if (gtid == 0) {
+        mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
       }
+      __syncwarp();  // lane 0's store / arrival branch rejoins before the next item's .sync.aligned tcgen05 ops
       if (++stage == 2) {
         stage = 0;
         phase ^= 1;
@@ -475,6 +527,8 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   p.vp = reinterpret_cast<const __nv_bfloat16*>(vp);
   p.out = reinterpret_cast<__nv_bfloat16*>(a.out);
   p.dbg = nullptr;
+  static const int direct_store = getenv("PSCWIN_ATTN_DIRECT_STORE") ? 1 : 0;  // A/B knob
+  p.tma_out = !direct_store;
   static unsigned long long* dbg_buf = nullptr;
   const char* tl = getenv("PSCWIN_ATTN_TIMELINE");
   if (tl) {
@@ -483,7 +537,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
     p.dbg = dbg_buf;
   }
   if (p.n_tiles > 2 || p.tile_slots < 16) return -2;
-  CUtensorMap tmQKV;
+  CUtensorMap tmQKV, tmO;
   const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
   const uint64_t sq[4] = {(uint64_t)d * 2, (uint64_t)3 * a.C * 2, (uint64_t)a.W * 3 * a.C * 2,
                           (uint64_t)a.H * a.W * 3 * a.C * 2};
@@ -491,12 +545,19 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   int rc = make_tmap_5d(&tmQKV, a.qkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dq, sq, box,
                         d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
   if (rc) return rc;
+  {  // O [B,H,W,heads,d]: the same window box, stored
+    const uint64_t dout[5] = {(uint64_t)d, (uint64_t)a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
+    const uint64_t sout[4] = {(uint64_t)d * 2, (uint64_t)a.C * 2, (uint64_t)a.W * a.C * 2, (uint64_t)a.H * a.W * a.C * 2};
+    rc = make_tmap_5d(&tmO, a.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, dout, sout, box,
+                      d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+  }
   const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8 + 1024 * 4;
   const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
   PSCWIN_PROF("window_attention", stream);
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(kern, dim3(grid), dim3(WS_THREADS), smem, stream, tmQKV, p);
+    launch_k(kern, dim3(grid), dim3(WS_THREADS), smem, stream, tmQKV, tmO, p);
   };
   const bool masked = p.pad_mode == 1;
   if (d == 64)

@@ -50,7 +50,8 @@ struct ScanParams {
   const __nv_bfloat16* hist;
 };
 
-__device__ __forceinline__ float silu_f(float x) { return x / (1.f + __expf(-x)); }
+// SiLU(x) = x / (1 + e^-x) with the fast division (MUFU rcp; -> 0 as e^-x overflows for very negative x)
+__device__ __forceinline__ float silu_f(float x) { return __fdividef(x, 1.f + __expf(-x)); }
 __device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log1pf(__expf(x)); }
 
 // ------------------------------------------------------------------------------------------------- conv
@@ -259,10 +260,16 @@ struct StageLayout {
   __device__ static void load(uint8_t* buf, const ScanParams& p, int W, long long rbase, long long tok0, int t, int nt,
                               int d0) {
     const int tid = threadIdx.x;
+    // only the (B, C) columns of the x_proj rows are staged (W = 2N floats per token; delta_low is consumed by
+    // the dt GEMM alone): row stride R + 2N in global memory, column offset R
     float* sd = reinterpret_cast<float*>(buf);
     __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(buf + off_v(W));
-    const float* gd = p.dbc + (rbase + t) * W;
-    for (int i = tid; i < nt * W / 4; i += NT) cp_async16(sd + 4 * i, gd + 4 * i);
+    const int gw = p.R + W, W4 = W / 4;
+    const float* gd = p.dbc + (rbase + t) * gw + p.R;
+    for (int i = tid; i < nt * W4; i += NT) {
+      const int j = i / W4, q = i - j * W4;
+      cp_async16(sd + 4 * i, gd + (long long)j * gw + 4 * q);
+    }
     constexpr int VPR = DPB / 8;  // 16-byte chunks per token row of bf16
     for (int i = tid; i < nt * VPR; i += NT) {
       const int j = i / VPR, cc = i - j * VPR;
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
   constexpr int NT = DPB * NS, NH = N / NS;
   using St = StageLayout<DPB, NT, false>;
   extern __shared__ __align__(128) uint8_t s_raw[];
-  const int W = p.R + 2 * N;
+  const int W = 2 * N;  // staged (B, C) row
   const size_t SB = St::bytes(W);
   const int c = threadIdx.x / NS, sub = threadIdx.x % NS;
   const int d0 = blockIdx.x * DPB;
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
       const float v = __bfloat162float(sv[j * DPB + c]);
       const float dt = sdelta[j * DPB + c];
       sdt += dt;
-      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);  // two state pairs per load
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + n0);  // two state pairs per load
       const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
       for (int k = 0; k < NH / 2; ++k) {
@@ -798,14 +805,19 @@ __global__ void __launch_bounds__(256) scan_dist_carry_kernel(ScanParams p, cons
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
+// resident CTAs per SM the register allocation of the NS = 2 pass 2 is sized for (5: 96 registers; occupancy
+// experiments: -DPSCWIN_PASS2_MINB=6 via PSCWIN_NVCC_FLAGS)
+#ifndef PSCWIN_PASS2_MINB
+#define PSCWIN_PASS2_MINB 5
+#endif
 template <int N, int DPB, int NS, bool ZOH, int PK>
-__global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
+__global__ void __launch_bounds__(DPB * NS, NS == 2 ? PSCWIN_PASS2_MINB : 1) scan_pass2_kernel(ScanParams p) {
   pdl_trigger();
   pdl_wait();
   constexpr int NT = DPB * NS, NH = N / NS;
   using St = StageLayout<DPB, NT, true>;
   extern __shared__ __align__(128) uint8_t s_raw[];
-  const int W = p.R + 2 * N;
+  const int W = 2 * N;  // staged (B, C) row
   const size_t SB = St::bytes(W);
   const int c = threadIdx.x / NS, sub = threadIdx.x % NS;
   const int d0 = blockIdx.x * DPB;
@@ -860,8 +872,8 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass2_kernel(ScanParams p) {
     constexpr int RSTR = DPB + 32 / NS;
     float* red = reinterpret_cast<float*>(s_raw + 2 * SB);
     auto tstep = [&](int j) {
-      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + n0);      // B pairs
-      const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + p.R + N + n0);  // C pairs
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + n0);      // B pairs
+      const float4* c4 = reinterpret_cast<const float4*>(sdbc + j * W + N + n0);  // C pairs
       const float v = __bfloat162float(sv[j * DPB + c]);
       const float dt = sdt[j * DPB + c];
       const float2 dt2 = f2(dt), nv3 = f2(-3.f * v);
@@ -1026,7 +1038,7 @@ static int choose_chunk(int B, int L, int D, int N, int W) {
 static ScanPlan plan_scan_p(int B, int L, int D, int N, int R, int k, int P) {
   ScanPlan s;
   s.P = P;
-  s.Lc = choose_chunk(B, L, D, N, R + 2 * N);
+  s.Lc = choose_chunk(B, L, D, N, 2 * N);  // staged (B, C) row width
   s.n_chunks = (L + s.Lc - 1) / s.Lc;
   s.W = R + 2 * N;
   const size_t rows = (size_t)B * (L + s.P);
@@ -1071,7 +1083,7 @@ static int check_scan(int B, int L, int D, int N, int R, int k) {
 template <int N, int NS>
 static void launch_pass1(ScanParams& p, cudaStream_t s) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
-  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false>::bytes(p.R + 2 * N);
+  const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false>::bytes(2 * N);
   const int pk = pass1_pk();
   if (p.bbar != 0)
     launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, false, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);
@@ -1086,7 +1098,7 @@ static void launch_pass1(ScanParams& p, cudaStream_t s) {
 template <int N, int NS>
 static void launch_pass2(ScanParams& p, cudaStream_t s) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
-  const size_t smem = pass2_smem<NS>(p.R + 2 * N);
+  const size_t smem = pass2_smem<NS>(2 * N);
   const int pk = pass2_pk();
   if (p.bbar != 0)
     launch_k_even(scan_pass2_kernel<N, PASS_DPB, NS, false, 0>, grid, dim3(PASS_DPB * NS), smem, s, p);

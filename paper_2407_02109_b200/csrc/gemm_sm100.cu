@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // bias of the tile's columns staged once in shared memory (read back as broadcasts), double-buffered by
       // accumulator so the next tile's staging never races this tile's readers
       float* sb = s_bias + acc * 256;
-      if (p.bias) {
+      if (p.bias && !f32_tma) {  // (f32 tiles read the bias straight from L1: no CTA-wide barrier in that path)
         if (etid < BN / 4) {
           const int c = n0 + 4 * etid;
           float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -375,9 +375,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (tma_out && !res_inplace) {
           if (issuer && gseq >= 2) bulk_wait_read1();
           named_bar_sync(1, 256);
-        } else if (f32_tma) {  // a chunk = two 128 x 32 f32 boxes; buffers of parity gseq & 1 (two chunks in
-          if (issuer && gseq >= 2) bulk_wait_read1();  // flight): the chunk before last must have been read out
-          named_bar_sync(1, 256);
+        } else if (f32_tma) {  // each warp stores its own 32 x 32 box (buffers of parity gseq & 1, two chunks in
+          if (lane == 0 && gseq >= 2) bulk_wait_read1();  // flight per warp): its store from two chunks ago has been
+          __syncwarp();                                    // read out; no barrier couples the epilogue warps
         }
         uint32_t r[32];
         if (cl < BN) {
@@ -390,11 +390,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.bias && cl < BN) {  // shared-memory broadcast reads (zero past N)
+        if (p.bias && cl < BN) {
+          if (f32_tma) {  // L1-cached broadcast loads (zero past N)
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
-            v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = col0 + j + 4 <= p.N ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
+                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+          } else {  // shared-memory broadcast reads (zero past N)
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
           }
         }
         if constexpr (EK == EK_ROPE) {
@@ -456,12 +465,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
                            __float_as_uint(v[4 * q + 3]));
           fence_proxy_async_smem();
-          named_bar_sync(1, 256);
-          if (issuer) {
-            if (mb < p.M && n0 + cc * 64 < p.N) {
-              tma_store_2d(&tmOut, sf, n0 + cc * 64, mb);
-              if (n0 + cc * 64 + 32 < p.N) tma_store_2d(&tmOut, sf + STAGE_OUT_BYTES, n0 + cc * 64 + 32, mb);
-            }
+          __syncwarp();
+          if (lane == 0) {  // this warp's 32 rows of box `half`
+            const int r0 = mb + quarter * 32;
+            if (r0 < p.M && col0 < p.N) tma_store_2d(&tmOut, sh + quarter * 32 * 128, col0, r0);
             bulk_commit();
           }
         } else if (row_ok && cl < BN) {
@@ -539,7 +546,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         named_bar_sync(1, 256);
       }
     }
-    if (issuer && (tma_out || f32_tma)) bulk_wait0();
+    if (issuer && tma_out) bulk_wait0();
+    if (lane == 0 && f32_tma) bulk_wait0();
   }
   __syncthreads();
   if (PAIR) cluster_sync();  // the peer may still read this CTA's shared memory / signal its barriers until here
@@ -645,8 +653,8 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   p.f32_tma = (p.epi == EPI_STORE_F32 && p.splits <= 1 && (p.ldo * 4) % 16 == 0 && !getenv("PSCWIN_GEMM_F32_DIRECT"))
                   ? 1 : 0;
   if (p.f32_tma) {
-    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.N, p.M, (uint64_t)p.ldo * 4, 32, BM,
-                      CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.N, p.M, (uint64_t)p.ldo * 4, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_128B);  // one 32 x 32 box per epilogue warp
     if (rc) return rc;
   }
   if (p.epi != EPI_STORE_F32) {
