@@ -607,8 +607,10 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (p.tf32 && (p.K % 4 || (p.lda * 4) % 16 || (p.ldb * 4) % 16)) return -1;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
-  // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K
-  const bool pair = pair_enabled() && p.splits <= 1 && p.M > BM;
+  // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K; not for the
+  // TF32 dt GEMM (K = R = 48: nothing to share, and the cluster-scope barrier traffic slows its epilogue-bound
+  // tiles: 4096^2 226 -> 208 us single-CTA)
+  const bool pair = pair_enabled() && p.splits <= 1 && p.M > BM && !p.tf32;
   const int TMr = pair ? 2 * BM : BM;
   const int m_tiles = (p.M + TMr - 1) / TMr;
   const int slots = pair ? num_sms() / 2 : num_sms();

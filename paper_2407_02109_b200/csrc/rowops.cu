@@ -108,6 +108,26 @@ __global__ void pad_qkv_kernel(const T* __restrict__ pad, const T* __restrict__ 
   if (j >= 3 * C) return;
   int lane = threadIdx.x & 31;
   float acc = 0.f;
+  if constexpr (sizeof(T) == 2) {
+    if (C % 8 == 0) {  // 16-byte vectors: the warp's row loads are independent (C = 768: 3 per lane)
+      const uint4* w4 = reinterpret_cast<const uint4*>(w + (size_t)j * C);
+      const uint4* p4 = reinterpret_cast<const uint4*>(pad);
+      for (int i = lane; i < C / 8; i += 32) {
+        const uint4 wv = __ldg(w4 + i), pv = __ldg(p4 + i);
+        const uint32_t* ww = reinterpret_cast<const uint32_t*>(&wv);
+        const uint32_t* pw = reinterpret_cast<const uint32_t*>(&pv);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc = fmaf(__uint_as_float(pw[q] << 16), __uint_as_float(ww[q] << 16), acc);
+          acc = fmaf(__uint_as_float(pw[q] & 0xFFFF0000u), __uint_as_float(ww[q] & 0xFFFF0000u), acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) out[j] = acc + (bias ? bias[j] : 0.f);
+      return;
+    }
+  }
   for (int c = lane; c < C; c += 32) {
     float a, bw;
     if constexpr (sizeof(T) == 2) {
