@@ -181,11 +181,15 @@ PSCWIN_DEVICE uint32_t smem_in_cta(const void* p, uint32_t rank) {
 PSCWIN_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Wait on a barrier that the peer CTA of a pair also signals (TMA complete_tx, multicast tcgen05.commit, remote
+// arrivals after tcgen05 fences). Everything it orders is async-proxy work (TMA, UMMA, TMEM), which the mbarrier
+// itself orders, so the default .acquire.cta semantics suffice (as CUTLASS's cluster pipelines wait); the
+// .acquire.cluster form made every successful wait invalidate L1 (CCTL.IVALL), a top stall of the pair GEMMs.
 PSCWIN_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");

@@ -1,7 +1,8 @@
 // Kernel launch helper: every library kernel is launched with programmatic stream serialization (PDL), so its
 // CTAs can be scheduled (and run their prologue: barrier init, TMEM allocation, descriptor prefetch) while the
 // previous kernel drains; the kernel body starts at pdl_wait() (common.cuh), which restores stream order.
-// Measured on the graph-captured step: no gain (1% slower), so the attribute is off unless PSCWIN_PDL=1.
+// Measured on the graph-captured step (B200, round 1): 1024^2 stage 0.404 -> 0.394 ms, 4096^2 stack neutral, so the
+// attribute is on by default; PSCWIN_PDL=0 turns it off (A/B knob).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdlib.h>
@@ -14,7 +15,7 @@ inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
     const char* e = getenv("PSCWIN_PDL");
-    on = (e && e[0] == '1') ? 1 : 0;
+    on = (e && e[0] == '0') ? 0 : 1;
   }
   return on == 1;
 }
