@@ -175,13 +175,18 @@ def peaks():
     return p
 
 
-def traffic_table():
+def traffic_table(workload="1024"):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum, one ncu --set full capture) by kernel
+    label, for this workload: profiles/dram_traffic.json holds {workload: {label: bytes}} (a flat table = 1024^2)."""
     path = os.path.join(ROOT, "profiles", "dram_traffic.json")
     try:
         with open(path) as f:
-            return json.load(f)
+            t = json.load(f)
     except Exception:
         return {}
+    if t and all(isinstance(v, dict) for v in t.values()):
+        return t.get(str(workload), {})
+    return t if str(workload) == "1024" else {}
 
 
 # ----------------------------------------------------------------------------------------------- clocks
@@ -392,7 +397,7 @@ def roofline(res, args):
         rows.append(row)
     rows.sort(key=lambda r: -r["share"])
     dom = next((r for r in rows if "bound" in r), None)
-    traffic = traffic_table()
+    traffic = traffic_table("ms" if args.workload == "ms" else args.workload)
     out = None
     if dom:
         tr = traffic.get(dom["kernel"])

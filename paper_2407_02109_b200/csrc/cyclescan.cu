@@ -518,13 +518,34 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
     A2[j] = A * kLog2e;
     invA[j] = 1.f / A;
   }
-  auto step = [&](float (&h)[NPL], long long row) {
-    const float dt = p.delta[row * p.D + d];
-    const float v = __bfloat162float(p.v[row * p.D + d]);
+  // The P <= KMAX - 1 prefix rows of copy 1 (r1 = L + t) and of copies 2/3 (r2 = t) are read once, all up front
+  // (independent loads in flight together, overlapping the summaries' cp.async), instead of one dependent global
+  // round trip per recurrence step.
+  constexpr int PM = KMAX - 1;
+  float pdt1[PM], pdt2[PM], pv1[PM], pv2[PM], pb1[PM][NPL], pb2[PM][NPL], pc1[PM][NPL], pc2[PM][NPL], pg[PM];
+#pragma unroll
+  for (int t = 0; t < PM; ++t) {
+    if (t >= p.P) break;
+    const long long r1 = rbase + p.L + t, r2 = rbase + t;
+    pdt1[t] = p.delta[r1 * p.D + d];
+    pdt2[t] = p.delta[r2 * p.D + d];
+    pv1[t] = __bfloat162float(p.v[r1 * p.D + d]);
+    pv2[t] = __bfloat162float(p.v[r2 * p.D + d]);
+#pragma unroll
+    for (int j = 0; j < NPL; ++j) {
+      const int n = act[j] ? lane + 32 * j : 0;
+      pb1[t][j] = p.dbc[r1 * W + p.R + n];
+      pb2[t][j] = p.dbc[r2 * W + p.R + n];
+      pc1[t][j] = p.dbc[r1 * W + p.R + N + n];
+      pc2[t][j] = p.dbc[r2 * W + p.R + N + n];
+    }
+    pg[t] = p.gz ? __bfloat162float(p.gz[((long long)b * p.L + t) * p.ld_gz + d]) : 1.f;
+  }
+  auto step = [&](float (&h)[NPL], float dt, float v, const float (&bv)[NPL]) {
 #pragma unroll
     for (int j = 0; j < NPL; ++j) {
       if (!act[j]) continue;
-      const float w = p.dbc[row * W + p.R + lane + 32 * j] * v;
+      const float w = bv[j] * v;
       const float x = dt * A2[j];
       const float dA = ex2_approx(x);
       h[j] = zoh ? fmaf(dA, h[j] + w, -w) : fmaf(dA, h[j], x * 0.69314718055994531f * w);
@@ -535,10 +556,12 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
 #pragma unroll
   for (int j = 0; j < NPL; ++j) beta1[j] = beta2[j] = 0.f;
   float sdt2 = 0.f;
-  for (int t = 0; t < p.P; ++t) {
-    step(beta1, rbase + p.L + t);
-    step(beta2, rbase + t);
-    sdt2 += p.delta[(rbase + t) * p.D + d];
+#pragma unroll
+  for (int t = 0; t < PM; ++t) {
+    if (t >= p.P) break;
+    step(beta1, pdt1[t], pv1[t], pb1[t]);
+    step(beta2, pdt2[t], pv2[t], pb2[t]);
+    sdt2 += pdt2[t];
   }
 #pragma unroll
   for (int j = 0; j < NPL; ++j) alpha2[j] = ex2_approx(sdt2 * A2[j]);
@@ -574,25 +597,21 @@ __global__ void __launch_bounds__(256) scan_carry_kernel(ScanParams p) {
       h3[j] = c3[j];
     }
     const float Ds = p.d_skip[d];
-    for (int t = 0; t < p.P; ++t) {
-      const long long r1 = rbase + p.L + t, r2 = rbase + t;
-      step(h1, r1);
-      step(h2, r2);
-      step(h3, r2);
+#pragma unroll
+    for (int t = 0; t < PM; ++t) {
+      if (t >= p.P) break;
+      step(h1, pdt1[t], pv1[t], pb1[t]);
+      step(h2, pdt2[t], pv2[t], pb2[t]);
+      step(h3, pdt2[t], pv2[t], pb2[t]);
       float y = 0.f;
 #pragma unroll
       for (int j = 0; j < NPL; ++j)
-        if (act[j]) {
-          const int n = lane + 32 * j;
-          y += invA[j] * (p.dbc[r1 * W + p.R + N + n] * h1[j] + p.dbc[r2 * W + p.R + N + n] * (h2[j] + h3[j]));
-        }
+        if (act[j]) y += invA[j] * (pc1[t][j] * h1[j] + pc2[t][j] * (h2[j] + h3[j]));
 #pragma unroll
       for (int o = 16; o; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
       if (lane == 0) {
-        y += Ds * (__bfloat162float(p.v[r1 * p.D + d]) + 2.f * __bfloat162float(p.v[r2 * p.D + d]));
-        const long long tok = (long long)b * p.L + t;
-        const float g = p.gz ? __bfloat162float(p.gz[tok * p.ld_gz + d]) : 1.f;
-        p.out[tok * p.ld_out + d] = __float2bfloat16_rn(y * g);
+        y += Ds * (pv1[t] + 2.f * pv2[t]);
+        p.out[((long long)b * p.L + t) * p.ld_out + d] = __float2bfloat16_rn(y * pg[t]);
       }
     }
   }

@@ -64,7 +64,7 @@ def launches(path):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     agg = collections.OrderedDict()
     for r in rows[h + 1:]:
-        if len(r) > vi:
+        if len(r) > vi and "::" not in short(r[ki]):  # library kernels only (torch's L2-flush fills excluded)
             agg.setdefault(short(r[ki]), []).append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
     print("| kernel | launches | mean us | share of GPU time |\n|---|---|---|---|")
