@@ -149,3 +149,37 @@ def test_cycle_scan_layer_forward(pl, cfg):
     assert rel_err(got, ref) < BF16_TOL
     inc = ref - x
     assert float(np.max(np.abs((got - x) - inc))) < BF16_TOL * np.max(np.abs(inc)) + 2.0 ** -8 * np.max(np.abs(ref))
+
+
+_PDL_CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["PSCWIN_ROOT"]); sys.path.insert(0, os.path.join(os.environ["PSCWIN_ROOT"], "tests"))
+import numpy as np, torch, synth
+import paper_2407_02109_b200 as pl
+from gpu_util import dev, dev_weights
+cfgs = [synth.tiny(), synth.tiny(shift_x=0, shift_y=0, cycle_scan=1), synth.vitb(64, cycle_scan=1)]
+outs = []
+for i, c in enumerate(cfgs):
+    layer = pl.PSCWinLayer(pl.LayerDesc.from_config(c), dev_weights(synth.make_weights(c, layer=i), c))
+    outs.append(layer(dev(synth.make_input(c))).float().cpu().numpy())
+np.savez(sys.argv[1], *outs)
+'''
+
+
+def test_pdl_on_equals_off(pl, tmp_path):
+    # Every kernel is launched with programmatic stream serialization and waits (griddepcontrol.wait) before its
+    # first global access; the results must be byte-identical to plain stream-ordered launches (PSCWIN_PDL=0).
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "child.py"
+    script.write_text(_PDL_CHILD)
+    res = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, PSCWIN_PDL=flag, PSCWIN_ROOT=root)
+        out = tmp_path / f"pdl{flag}.npz"
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        res[flag] = np.load(out)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["0"][k]), k
