@@ -824,10 +824,15 @@ __global__ void __launch_bounds__(256) scan_dist_carry_kernel(ScanParams p, cons
 }
 
 // ------------------------------------------------------------------------------------------------- pass 2
-// resident CTAs per SM the register allocation of the NS = 2 pass 2 is sized for (5: 96 registers; occupancy
-// experiments: -DPSCWIN_PASS2_MINB=6 via PSCWIN_NVCC_FLAGS)
+#ifndef PSCWIN_P2_UNROLL
+#define PSCWIN_P2_UNROLL 8
+#endif
+constexpr int kP2Unroll = PSCWIN_P2_UNROLL;  // (#pragma unroll takes a constant expression, not a macro)
+// resident CTAs per SM the register allocation of the NS = 2 pass 2 is sized for, and its token unroll. Swept on
+// B200 (PSCWIN_NVCC_FLAGS rebuilds): 4 CTAs (<= 128 registers) with 8-token unroll beats 5 CTAs / 96 registers
+// (1024^2 82.2 -> 78.4 us, 4096^2 1.047 -> 1.005 ms); 3 and 6 CTAs / SM and unroll 2 / 16 are slower or equal.
 #ifndef PSCWIN_PASS2_MINB
-#define PSCWIN_PASS2_MINB 5
+#define PSCWIN_PASS2_MINB 4
 #endif
 template <int N, int DPB, int NS, bool ZOH, int PK>
 __global__ void __launch_bounds__(DPB * NS, NS == 2 ? PSCWIN_PASS2_MINB : 1) scan_pass2_kernel(ScanParams p) {
@@ -922,8 +927,8 @@ __global__ void __launch_bounds__(DPB * NS, NS == 2 ? PSCWIN_PASS2_MINB : 1) sca
         p.out[(tok0 + ts + j) * p.ld_out + d] = __float2bfloat16_rn(fmaf(D3, v, y) * g);
       }
     };
-    if (nt == TSUB) {  // full sub-chunk: partially unrolled
-#pragma unroll 4
+    if (nt == TSUB) {  // full sub-chunk: partially unrolled (PSCWIN_P2_UNROLL: A/B experiments via PSCWIN_NVCC_FLAGS)
+#pragma unroll kP2Unroll
       for (int j = 0; j < TSUB; ++j) tstep(j);
     } else {
       for (int j = 0; j < nt; ++j) tstep(j);
