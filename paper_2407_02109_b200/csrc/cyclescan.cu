@@ -60,7 +60,10 @@ __device__ __forceinline__ float softplus_f(float x) { return x > 20.f ? x : log
 // CONV_T + k - 1 input loads of its window up front (independent 16-byte loads, coalesced across the warp's channel
 // groups), keeps its 8 x k taps in registers, and slides the window in registers.
 constexpr int KMAX = 4;  // conv width supported (Mamba default 4)
-constexpr int CONV_T = 8;
+#ifndef PSCWIN_CONV_T
+#define PSCWIN_CONV_T 8  // rows per thread (sweeps: PSCWIN_NVCC_FLAGS)
+#endif
+constexpr int CONV_T = PSCWIN_CONV_T;
 __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
   pdl_trigger();
   pdl_wait();
