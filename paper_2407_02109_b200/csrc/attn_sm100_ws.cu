@@ -40,6 +40,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct AttnWsArgs {
   int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
   int rpt, n_tiles, tile_slots, n_items;
+  int lockstep;  // -1: automatic (few items per CTA), 0 / 1 forced (PSCWIN_ATTN_LOCKSTEP knob)
   int tma_out;  // 1: O tiles staged in smem and TMA-stored; 0: 16-byte global stores of the real rows
   float sl2;
   const __nv_bfloat16 *kx, *ky, *vp;
@@ -185,7 +186,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     };
     // Few items per CTA (1024^2: 1-2): the half-item stagger would serialise the two q tiles of the only items,
     // so issue both q tiles in lockstep (S0, S1, PV0, PV1 per item); the stagger pays off only in long runs.
-    const bool lockstep = p.n_items <= 3 * (int)gridDim.x;
+    const bool lockstep = p.lockstep >= 0 ? p.lockstep == 1 : p.n_items <= 3 * (int)gridDim.x;
     bool have_prev = false, prev_act1 = false;
     int prev_stage = 0;
     uint32_t prev_sb = 0;
@@ -529,6 +530,8 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   p.dbg = nullptr;
   static const int direct_store = getenv("PSCWIN_ATTN_DIRECT_STORE") ? 1 : 0;  // A/B knob
   p.tma_out = !direct_store;
+  static const int lockstep_knob = getenv("PSCWIN_ATTN_LOCKSTEP") ? atoi(getenv("PSCWIN_ATTN_LOCKSTEP")) : -1;
+  p.lockstep = lockstep_knob;
   static unsigned long long* dbg_buf = nullptr;
   const char* tl = getenv("PSCWIN_ATTN_TIMELINE");
   if (tl) {
