@@ -25,6 +25,10 @@ namespace pscwin {
 
 namespace {
 constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroups
+#ifndef PSCWIN_ATTN_POLY_MOD
+#define PSCWIN_ATTN_POLY_MOD 0  // k > 0: every k-th exp2 pair on the FMA pipe; swept 0 / 2 / 3 / 4 at 4096^2: 125 / 133 / 128.5 / 127 us
+#endif
+constexpr int kPolyMod = PSCWIN_ATTN_POLY_MOD;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -365,15 +369,15 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         // pass 2: p = 2^(s log2(e)/sqrt(d) - base) (packed fp32x2 scale, MUFU ex2), partial sums, P (bf16 pairs)
         // written over the consumed S columns
         float2 ls = make_float2(0.f, 0.f);
-        // 16 columns: pairs of global index (OFF + j) / 2 with (OFF + j) / 2 % 3 == 2 go to the FMA pipe (a third of
-        // each 32-column chunk; the MUFU ex2 rate bounds this loop)
+        // 16 columns per call; with kPolyMod = k > 0 the pairs of global index (OFF + j) / 2 = k - 1 (mod k) take the
+        // FMA-pipe polynomial instead of MUFU ex2 (off: the softmax is latency-, not MUFU-bound, see the sweep)
         auto exp16 = [&](auto off_c, const uint32_t (&r)[16], uint32_t m, uint32_t (&pk)[8]) {
           constexpr int OFF = decltype(off_c)::value;
 #pragma unroll
           for (int j = 0; j < 16; j += 2) {
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl2, nb);
             float e0, e1;
-            if (((OFF + j) / 2) % 3 == 2) {
+            if (kPolyMod > 0 && ((OFF + j) / 2) % kPolyMod == kPolyMod - 1) {
               const float2 e = exp2_poly2(x);
               e0 = e.x;
               e1 = e.y;
