@@ -1088,6 +1088,7 @@ static ScanPlan plan_scan_p(int B, int L, int D, int N, int R, int k, int P) {
   if (const char* e = getenv("PSCWIN_XPROJ_SPLITS")) {  // tuning knob (1..8)
     const int v = atoi(e);
     if (v >= 1 && v <= 8) s.xsplits = v;
+    if (s.xsplits > D / 64) s.xsplits = D / 64 > 0 ? D / 64 : 1;  // every split needs >= 1 K block (D / 64 of them)
   }
   s.partial = off;
   off += s.xsplits > 1 ? al256((size_t)s.xsplits * rows * s.W * 4) : 0;
