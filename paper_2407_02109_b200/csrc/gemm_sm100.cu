@@ -607,6 +607,10 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (p.tf32 && (p.K % 4 || (p.lda * 4) % 16 || (p.ldb * 4) % 16)) return -1;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))
     return -3;
+  {  // every split needs at least one K block (a split without any would never commit its accumulator)
+    const int nk = (p.K + (p.tf32 ? BK / 2 : BK) - 1) / (p.tf32 ? BK / 2 : BK);
+    if (p.splits > nk) p.splits = nk;
+  }
   // CTA pairs (256-row tiles, cta_group::2) whenever there are at least two row tiles and no split-K; not for the
   // TF32 dt GEMM (K = R = 48: nothing to share, and the cluster-scope barrier traffic slows its epilogue-bound
   // tiles: 4096^2 226 -> 208 us single-CTA)
