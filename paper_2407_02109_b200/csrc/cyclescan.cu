@@ -248,7 +248,10 @@ __global__ void __launch_bounds__(256) ms_permute_rows_kernel(const __nv_bfloat1
 // sequential recurrence never waits on a global load. The state is kept scaled, h~ = A h (per (d, n) constant),
 // which turns the ZOH update into h~ <- dA (h~ + w) - w with w = B_t[n] v_t (no 1/A per element), and pairs of
 // states are updated with packed fp32x2 instructions (FFMA2 / FMUL2 on sm_100a).
-constexpr int TSUB = 16;
+#ifndef PSCWIN_TSUB
+#define PSCWIN_TSUB 16  // tokens per staged sub-chunk of the passes (sweeps: PSCWIN_NVCC_FLAGS)
+#endif
+constexpr int TSUB = PSCWIN_TSUB;
 template <int DPB, int NT, bool PASS2>  // DPB channels per CTA, NT threads
 struct StageLayout {
   // byte offsets inside one stage buffer
