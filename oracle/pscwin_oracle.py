@@ -284,16 +284,18 @@ def global_attention_rows(qkv: np.ndarray, H: int, W: int, heads: int, tokens, r
     return out.reshape(len(tokens), C)
 
 
-def attention_sublayer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False):
+def attention_sublayer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False,
+                       window_rows=None):
     """One PSCWin attention sub-layer (a4-a7), pre-LN residual:
     u = LN1(x); qkv = u W_qkv^T + b_qkv; qkv_p = p W_qkv^T + b_qkv (p not normalised, Q14);
     O = window attention (plain if shift == 0, else padded shift; P:L110, L116-119);
-    x_out = x + O W_o^T + b_o (P:L104 outer "Linear")."""
+    x_out = x + O W_o^T + b_o (P:L104 outer "Linear").
+    window_rows: evaluate only these padded-grid window rows (attention_core_padded); other tokens are NaN."""
     u = layer_norm(x, wt["ln1_g"], wt["ln1_b"], cfg.ln_eps)
     qkv = u @ wt["w_qkv"].T + wt["b_qkv"]
     qkv_p = wt["pad"] @ wt["w_qkv"].T + wt["b_qkv"]
     O = attention_core_padded(qkv, qkv_p, cfg.H, cfg.W, cfg.heads, cfg.window,
-                              cfg.shift_x, cfg.shift_y, cfg.pad_mode, cfg.rope)
+                              cfg.shift_x, cfg.shift_y, cfg.pad_mode, cfg.rope, window_rows=window_rows)
     y = O @ wt["w_o"].T + wt["b_o"]
     out = x + y
     if return_parts:
@@ -382,14 +384,15 @@ def scan_permutation(H: int, W: int, order: int, window: int = 0) -> np.ndarray:
 
 
 def cycle_ssm_3L(xin3: np.ndarray, z3: Optional[np.ndarray], wt: Dict[str, np.ndarray], bbar_mode: int,
-                 channels=None) -> np.ndarray:
+                 channels=None, z_sampled: bool = False) -> np.ndarray:
     """The Mamba SSM operator over the literal cycled sequence of 3L tokens ("repeats the image
     token sequence three times and connects them sequentially. The Mamba SSM operator then scans the
     tokens in this order"). Mamba-1 block internals per reading Q9:
       v = SiLU(causal_conv(xin));  (delta_low, B, C) = v W_x^T;  Delta = softplus(delta_low W_dt^T + b_dt);
       A = -exp(A_log);  y = selective scan (Eqs. 3-4) + D_skip v;  g = y * SiLU(z)  (no gate if z3 is None).
     xin3, z3 [3L, D]. Returns g3 [3L, D] (or [3L, len(channels)]: channels are independent, so a
-    subset is exact for those channels — used to sample full-size cases)."""
+    subset is exact for those channels — used to sample full-size cases). z_sampled: z3 holds only the
+    sampled channels' columns [3L, len(channels)]."""
     R = wt["w_dt"].shape[1]
     N = wt["a_log"].shape[1]
     v = silu(causal_conv1d(xin3, wt["conv_w"], wt["conv_b"]))
@@ -399,7 +402,7 @@ def cycle_ssm_3L(xin3: np.ndarray, z3: Optional[np.ndarray], wt: Dict[str, np.nd
     delta = softplus(delta_low @ wt["w_dt"][ch].T + wt["b_dt"][ch])
     A = -np.exp(wt["a_log"][ch])
     y = selective_scan_sequential(v[:, ch], delta, A, Bm, Cm, wt["d_skip"][ch], bbar_mode)
-    return y if z3 is None else y * silu(z3[:, ch])
+    return y if z3 is None else y * silu(z3 if z_sampled else z3[:, ch])
 
 
 def cycle_scan(xin: np.ndarray, z: Optional[np.ndarray], wt: Dict[str, np.ndarray], H: int, W: int,
@@ -421,14 +424,24 @@ def cycle_scan(xin: np.ndarray, z: Optional[np.ndarray], wt: Dict[str, np.ndarra
     return out
 
 
-def cycle_scan_module(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False):
+def cycle_scan_module(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_parts: bool = False,
+                      channels=None):
     """Cycle-scan module before the attention block (a1-a3; SURVEY §8c oracle step 1):
     u0 = LN_s(x); flatten in scan order; MATERIALISE X3_j = s_{j mod L} (j < 3L); [xin, z] = X3 W_in^T
     (W_in applied to all 3L tokens); g3 = SSM(X3); o = g3 W_out^T; out_t = o_t + o_{L+t} + o_{2L+t};
-    x[pi(t)] += out_t (pre-LN residual, Q13)."""
+    x[pi(t)] += out_t (pre-LN residual, Q13).
+    channels: full-size sampling. Valid only for weights whose W_out columns outside `channels` are zero:
+    then o = g[:, channels] W_out[:, channels]^T exactly, and the SSM runs on those channels alone (channels
+    are independent given v, Delta, B, C)."""
     B, H, W, C = x.shape
     D = cfg.D
     L = H * W
+    if channels is not None:
+        ch = np.asarray(channels)
+        rest = np.ones(D, dtype=bool)
+        rest[ch] = False
+        if np.any(wt["w_out"][:, rest] != 0):
+            raise ValueError("channel sampling needs W_out to be zero outside the sampled channels")
     u0 = layer_norm(x, wt["lns_g"], wt["lns_b"], cfg.ln_eps).reshape(B, L, C)
     pi = scan_permutation(H, W, cfg.scan_order, cfg.window)
     out = x.reshape(B, L, C).copy()
@@ -436,9 +449,15 @@ def cycle_scan_module(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, return_part
     for b in range(B):
         s = u0[b][pi]
         X3 = np.concatenate([s, s, s])
-        xz = X3 @ wt["w_in"].T
-        g3 = cycle_ssm_3L(xz[:, :D], xz[:, D:], wt, cfg.bbar_mode)
-        o3 = g3 @ wt["w_out"].T
+        if channels is None:
+            xz = X3 @ wt["w_in"].T
+            g3 = cycle_ssm_3L(xz[:, :D], xz[:, D:], wt, cfg.bbar_mode)
+            o3 = g3 @ wt["w_out"].T
+        else:  # xin on every channel (conv, x_proj need them), z only on the sampled ones (row subset of W_in)
+            xin3 = X3 @ wt["w_in"][:D].T
+            z3 = X3 @ wt["w_in"][D + ch].T
+            g3 = cycle_ssm_3L(xin3, z3, wt, cfg.bbar_mode, channels=ch, z_sampled=True)
+            o3 = g3 @ wt["w_out"][:, ch].T
         o = o3[:L] + o3[L:2 * L] + o3[2 * L:]
         out[b][pi] += o
         parts.append(dict(g=(g3[:L] + g3[L:2 * L] + g3[2 * L:])))
@@ -462,12 +481,14 @@ def ffn_sublayer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg) -> np.ndarray:
     return x + h @ wt["w_fc2"].T + wt["b_fc2"]
 
 
-def pscwin_layer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg) -> np.ndarray:
+def pscwin_layer(x: np.ndarray, wt: Dict[str, np.ndarray], cfg, window_rows=None, channels=None) -> np.ndarray:
     """One PSCWin layer: optional cycle-scan module ("prior to the final block of each stage")
-    followed by the plain or padded-shift attention sub-layer, then (cfg.mlp_hidden > 0) the FFN sub-layer."""
+    followed by the plain or padded-shift attention sub-layer, then (cfg.mlp_hidden > 0) the FFN sub-layer.
+    Full-size sampling (exact for what it evaluates): window_rows = padded-grid window rows of the attention
+    sub-layer (other tokens NaN); channels = SSM channels of the cycle-scan module (cycle_scan_module)."""
     if cfg.cycle_scan:
-        x = cycle_scan_module(x, wt, cfg)
-    x = attention_sublayer(x, wt, cfg)
+        x = cycle_scan_module(x, wt, cfg, channels=channels)
+    x = attention_sublayer(x, wt, cfg, window_rows=window_rows)
     if getattr(cfg, "mlp_hidden", 0):
         x = ffn_sublayer(x, wt, cfg)
     return x
@@ -520,31 +541,35 @@ def ms_index_map(scales, w: int, sx: int = 0, sy: int = 0) -> np.ndarray:
     return np.concatenate(maps).astype(np.uint32)
 
 
-def ms_attention_sublayer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales) -> np.ndarray:
+def ms_attention_sublayer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, window_rows=None) -> np.ndarray:
     """Multi-scale attention: "computationally equivalent to performing attention on isolated
     windows" — every scale's grid gets its own (plain / padded-shift) windows with the layer's window,
     shift and pad token, RoPE at the scale's own grid coordinates (reading Q20); no window spans two
-    scales (block-diagonal mask). xp packed [B * sum L_s, C]."""
+    scales (block-diagonal mask). xp packed [B * sum L_s, C].
+    window_rows: per scale, the padded-grid window rows to evaluate (None = all; sampling, other tokens NaN)."""
     B = xp.shape[0] // int(ms_offsets(scales)[-1])
     outs = []
-    for g, (h, w) in zip(ms_unpack(xp, B, scales), scales):
-        outs.append(attention_sublayer(g, wt, cfg.replace(B=B, H=h, W=w)))
+    for i, (g, (h, w)) in enumerate(zip(ms_unpack(xp, B, scales), scales)):
+        rows = None if window_rows is None else window_rows[i]
+        outs.append(attention_sublayer(g, wt, cfg.replace(B=B, H=h, W=w), window_rows=rows))
     return ms_pack(outs)
 
 
-def ms_cycle_scan_module(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, mode: int) -> np.ndarray:
+def ms_cycle_scan_module(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, mode: int,
+                         channels=None) -> np.ndarray:
     """Cycle-scan module over a packed multi-scale sequence:
     SINGLE-SCALE "first splits the tokens by scale, scan each scale's tokens separately by the SSM, and
     then concatenates them" -> the single-scale module on every scale grid;
     MULTI-SCALE "directly performs the SSM across the tokens from all the scales": per sample, the
     scan-order sequences of all scales are concatenated (scale order) into ONE sequence of sum L_s tokens,
     which is cycled three times, scanned, split and summed like a single-scale sequence.
-    Pre-LN residual (Q13). xp packed [B * sum L_s, C]."""
+    Pre-LN residual (Q13). xp packed [B * sum L_s, C].
+    channels: SSM channel sampling, valid when W_out is zero outside them (see cycle_scan_module)."""
     off = ms_offsets(scales)
     B = xp.shape[0] // int(off[-1])
     grids = ms_unpack(xp, B, scales)
     if mode == CS_SINGLE_SCALE:
-        return ms_pack([cycle_scan_module(g, wt, cfg.replace(B=B, H=h, W=w))
+        return ms_pack([cycle_scan_module(g, wt, cfg.replace(B=B, H=h, W=w), channels=channels)
                         for g, (h, w) in zip(grids, scales)])
     if mode != CS_MULTI_SCALE:
         raise ValueError(mode)
@@ -559,9 +584,20 @@ def ms_cycle_scan_module(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales,
             pis.append(pi)
         s = np.concatenate(seq)
         X3 = np.concatenate([s, s, s])
-        xz = X3 @ wt["w_in"].T
-        g3 = cycle_ssm_3L(xz[:, :D], xz[:, D:], wt, cfg.bbar_mode)
-        o3 = g3 @ wt["w_out"].T
+        if channels is None:
+            xz = X3 @ wt["w_in"].T
+            g3 = cycle_ssm_3L(xz[:, :D], xz[:, D:], wt, cfg.bbar_mode)
+            o3 = g3 @ wt["w_out"].T
+        else:
+            ch = np.asarray(channels)
+            rest = np.ones(D, dtype=bool)
+            rest[ch] = False
+            if np.any(wt["w_out"][:, rest] != 0):
+                raise ValueError("channel sampling needs W_out to be zero outside the sampled channels")
+            xin3 = X3 @ wt["w_in"][:D].T
+            z3 = X3 @ wt["w_in"][D + ch].T
+            g3 = cycle_ssm_3L(xin3, z3, wt, cfg.bbar_mode, channels=ch, z_sampled=True)
+            o3 = g3 @ wt["w_out"][:, ch].T
         o = o3[:Ltot] + o3[Ltot:2 * Ltot] + o3[2 * Ltot:]
         for i, pi in enumerate(pis):
             outs[i][b][pi] += o[off[i]:off[i + 1]]
@@ -569,13 +605,14 @@ def ms_cycle_scan_module(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales,
 
 
 def ms_layer(xp: np.ndarray, wt: Dict[str, np.ndarray], cfg, scales, attention: int = 1,
-             cycle_scan: int = CS_NONE) -> np.ndarray:
+             cycle_scan: int = CS_NONE, window_rows=None, channels=None) -> np.ndarray:
     """One HRSAM++ layer over a packed multi-scale sequence: optional cycle-scan module (single- or
-    multi-scale) followed (attention = 1) by the multi-scale window-attention sub-layer."""
+    multi-scale) followed (attention = 1) by the multi-scale window-attention sub-layer.
+    window_rows (per scale) / channels: full-size sampling as in pscwin_layer."""
     if cycle_scan:
-        xp = ms_cycle_scan_module(xp, wt, cfg, scales, cycle_scan)
+        xp = ms_cycle_scan_module(xp, wt, cfg, scales, cycle_scan, channels=channels)
     if attention:
-        xp = ms_attention_sublayer(xp, wt, cfg, scales)
+        xp = ms_attention_sublayer(xp, wt, cfg, scales, window_rows=window_rows)
         if getattr(cfg, "mlp_hidden", 0):
             xp = ffn_sublayer(xp, wt, cfg)
     return xp

@@ -182,17 +182,24 @@ def _store(x: np.ndarray, kind: str, cfg: LayerConfig) -> np.ndarray:
     return round_f32(x)
 
 
-def make_input(cfg: LayerConfig, layer: int = 0) -> np.ndarray:
-    """x ~ N(0,1), shape [B,H,W,C] (seed 1 + layer)."""
+def make_input(cfg: LayerConfig, layer: int = 0, scale: float = 1.0) -> np.ndarray:
+    """x ~ N(0, scale^2), shape [B,H,W,C] (seed 1 + layer). The layer-level parity gates use a small residual
+    stream (scale 0.02): LayerNorm makes every sub-layer's increment independent of the scale of x, so the
+    increment dominates x_out and a layer that returns its input (or drops a sub-layer) fails the gate."""
     n = cfg.B * cfg.H * cfg.W * cfg.C
-    return _store(normal(stream_seed(1 + layer, 0), n).reshape(cfg.B, cfg.H, cfg.W, cfg.C), "mat", cfg)
+    return _store(scale * normal(stream_seed(1 + layer, 0), n).reshape(cfg.B, cfg.H, cfg.W, cfg.C), "mat", cfg)
 
 
-def make_weights(cfg: LayerConfig, layer: int = 0, peaky: bool = False) -> Dict[str, np.ndarray]:
+def make_weights(cfg: LayerConfig, layer: int = 0, peaky: bool = False,
+                 scan_params: str = "varied") -> Dict[str, np.ndarray]:
     """Weights of one PSCWin layer (SURVEY §8(d) recipe). Linear weights are nn.Linear-style [out, in].
 
     GEMM matrices and the pad token p are stored in the activation dtype; LN parameters, biases,
-    conv, dt_proj, A_log and D_skip are f32."""
+    conv, dt_proj, A_log and D_skip are f32.
+
+    scan_params: "varied" (default) draws channel-dependent SSM parameters, A_log[d,n] = log(n+1) + U(-0.5, 0.5)
+    and D_skip[d] ~ U(0.5, 1.5), so a kernel that indexes them by the wrong channel fails parity; "mamba" is the
+    channel-uniform S4D-real init (A_log = log(n+1), D_skip = 1) of round 1."""
     C, D, N, R, K = cfg.C, cfg.D, cfg.N, cfg.R, cfg.ssm_conv
     s = 100 + layer
     g = lambda idx, n: normal(stream_seed(s, idx), n)
@@ -219,8 +226,15 @@ def make_weights(cfg: LayerConfig, layer: int = 0, peaky: bool = False) -> Dict[
     w["w_dt"] = _store((2.0 * u(17, D * R) - 1.0).reshape(D, R) / math.sqrt(R), "f32", cfg)
     dt0 = np.exp(math.log(1e-3) + u(18, D) * (math.log(1e-1) - math.log(1e-3)))
     w["b_dt"] = _store(dt0 + np.log(-np.expm1(-dt0)), "f32", cfg)  # softplus^{-1}(dt0)
-    w["a_log"] = _store(np.log(np.tile(np.arange(1, N + 1, dtype=np.float64), (D, 1))), "f32", cfg)
-    w["d_skip"] = _store(np.ones(D), "f32", cfg)
+    a_log = np.log(np.tile(np.arange(1, N + 1, dtype=np.float64), (D, 1)))
+    if scan_params == "varied":
+        w["a_log"] = _store(a_log + (u(27, D * N).reshape(D, N) - 0.5), "f32", cfg)
+        w["d_skip"] = _store(0.5 + u(28, D), "f32", cfg)
+    elif scan_params == "mamba":
+        w["a_log"] = _store(a_log, "f32", cfg)
+        w["d_skip"] = _store(np.ones(D), "f32", cfg)
+    else:
+        raise ValueError(scan_params)
     w["w_out"] = _store(0.02 * g(19, C * D).reshape(C, D), "mat", cfg)
     # FFN sub-layer ("the typical FFN has a hidden layer dimension of 768x4"; reading Q21)
     Hd = cfg.mlp_hidden if cfg.mlp_hidden > 0 else 4 * C

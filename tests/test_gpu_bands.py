@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import synth
-from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+from gpu_util import BF16_TOL, X_SCALE, dev, dev_weights, host, layer_gate, n_residual, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -39,7 +39,7 @@ CASES = [
 def test_bands_equal_whole_image(pl, cfg, world):
     import torch
     from paper_2407_02109_b200.bands import LoopbackBands
-    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    x, w = synth.make_input(cfg, scale=X_SCALE), synth.make_weights(cfg)
     dw = dev_weights(w, cfg)
     desc = pl.LayerDesc.from_config(cfg)
     xd = dev(x)
@@ -50,7 +50,9 @@ def test_bands_equal_whole_image(pl, cfg, world):
         assert rel_err(host(banded), host(whole)) < 8e-3
     else:
         assert torch.equal(banded, whole)
-    assert rel_err(host(banded), oracle.pscwin_layer(x, w, cfg)) < BF16_TOL
+    ref = oracle.pscwin_layer(x, w, cfg)
+    assert rel_err(host(banded), ref) < BF16_TOL
+    assert layer_gate(host(banded), x, ref, n_residual(cfg)) < 1.0
 
 
 def test_band_contract(pl):
@@ -69,9 +71,9 @@ sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
 import torch, numpy as np, synth, oracle
 import paper_2407_02109_b200 as pl
 from paper_2407_02109_b200.bands import DistLayer, NcclComm
-from gpu_util import BF16_TOL, dev, dev_weights, host, rel_err
+from gpu_util import BF16_TOL, X_SCALE, dev, dev_weights, host, layer_gate, n_residual, rel_err
 cfg = [synth.tiny(H=32, W=16), synth.tiny(H=32, W=16, cycle_scan=1, mlp_hidden=128), synth.vitb(64, cycle_scan=1)][{i}]
-x, w = synth.make_input(cfg), synth.make_weights(cfg)
+x, w = synth.make_input(cfg, scale=X_SCALE), synth.make_weights(cfg)
 dw = dev_weights(w, cfg)
 desc = pl.LayerDesc.from_config(cfg)
 xd = dev(x)
@@ -89,7 +91,9 @@ if cfg.cycle_scan:
     assert rel_err(host(got), host(whole[0])) < 8e-3
 else:
     assert torch.equal(got, whole[0])
-assert rel_err(host(got)[None], oracle.pscwin_layer(x, w, cfg)) < BF16_TOL
+ref = oracle.pscwin_layer(x, w, cfg)
+assert rel_err(host(got)[None], ref) < BF16_TOL
+assert layer_gate(host(got)[None], x, ref, n_residual(cfg)) < 1.0
 out = torch.empty_like(got)
 g = torch.cuda.CUDAGraph()
 with torch.cuda.graph(g):

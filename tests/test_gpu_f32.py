@@ -6,7 +6,7 @@ import pytest
 
 import oracle
 import synth
-from gpu_util import F32_TOL, dev, dev_weights, host, rel_err
+from gpu_util import F32_TOL, X_SCALE, dev, dev_weights, host, layer_gate, n_residual, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -46,19 +46,22 @@ LAYERS = [
 @pytest.mark.parametrize("cfg", LAYERS, ids=lambda c: f"B{c.B}{c.H}x{c.W}C{c.C}w{c.window}s{c.shift_x},{c.shift_y}"
                                                       f"m{c.pad_mode}r{c.rope}cs{c.cycle_scan}o{c.scan_order}b{c.bbar_mode}f{c.mlp_hidden}")
 def test_forward_f32(pl, cfg):
-    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    x, w = synth.make_input(cfg, scale=X_SCALE), synth.make_weights(cfg)
     layer = pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))
     got = host(layer(dev(x, "f32")))
     ref = oracle.pscwin_layer(x, w, cfg)
     assert rel_err(got, ref) < F32_TOL
+    assert layer_gate(got, x, ref, n_residual(cfg), tol=F32_TOL, storage="f32") < 1.0
 
 
 def test_forward_f32_vitb_mid(pl):
     # ViT-B widths (C = 768, 12 heads, N = 32, R = 48) on a 16 x 16 grid, shifted + cycle scan
     cfg = synth.vitb(16, dtype="f32", cycle_scan=1)
-    x, w = synth.make_input(cfg), synth.make_weights(cfg)
+    x, w = synth.make_input(cfg, scale=X_SCALE), synth.make_weights(cfg)
     got = host(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dev_weights(w, cfg))(dev(x, "f32")))
-    assert rel_err(got, oracle.pscwin_layer(x, w, cfg)) < F32_TOL
+    ref = oracle.pscwin_layer(x, w, cfg)
+    assert rel_err(got, ref) < F32_TOL
+    assert layer_gate(got, x, ref, n_residual(cfg), tol=F32_TOL, storage="f32") < 1.0
 
 
 def test_window_attention_f32_peaky(pl):
