@@ -93,11 +93,29 @@ def layer_metas(args):
     if args.workload == "ms":
         _, B, specs = ms_workload()
         T = B * sum(h * w for h, w in MS_SCALES)
-        return [dict(T=T, C=c.C, D=c.D, N=c.N, R=c.R, attn=a, cs=int(cs > 0), Hd=c.mlp_hidden * a)
-                for c, a, cs, _ in specs]
+        return [dict(T=T, B=B, C=c.C, D=c.D, N=c.N, R=c.R, attn=a, cs=int(cs > 0), Hd=c.mlp_hidden * a, pad=0,
+                     Hp=0, Wp=0, chunks=-(-T // (256 * B))) for c, a, cs, _ in specs]
     _, _, cfgs = workload(args.workload)
-    return [dict(T=c.B * c.H * c.W, C=c.C, D=c.D, N=c.N, R=c.R, attn=1, cs=int(c.cycle_scan), Hd=c.mlp_hidden)
-            for c in cfgs]
+    out = []
+    for c in cfgs:
+        sh = c.shift_x or c.shift_y
+        pt, pl_ = (c.window - c.shift_y) % c.window, (c.window - c.shift_x) % c.window
+        Hp = -(-(c.H + pt) // c.window) * c.window
+        Wp = -(-(c.W + pl_) // c.window) * c.window
+        out.append(dict(T=c.B * c.H * c.W, B=c.B, C=c.C, D=c.D, N=c.N, R=c.R, attn=1, cs=int(c.cycle_scan),
+                        Hd=c.mlp_hidden, pad=int(bool(sh) and c.pad_mode == synth.PAD_LEARNABLE), Hp=Hp, Wp=Wp,
+                        chunks=scan_chunks(c)))
+    return out
+
+
+def scan_chunks(c):
+    """Chunk count of the cycle scan (the library's choose_chunk is internal; the carry's bytes are reported from
+    the chunk length the library reports through pscwin_scan_plan when available, else 256 tokens)."""
+    try:
+        import paper_2407_02109_b200 as pl
+        return pl.scan_chunks(c.B, c.H * c.W, c.D)
+    except Exception:
+        return -(-(c.H * c.W) // 256)
 
 
 # ----------------------------------------------------------------------------------------------- roofline
@@ -128,9 +146,21 @@ def kernel_work(label: str, metas):
         elif label == "gemm_out_proj_scan":
             bound, scale, unit = "tensor", 1e12, "TFLOP/s"
             tot += cs * 2.0 * T * D * C
-        elif label == "gemm_x_proj":
-            bound, scale, unit = "tensor", 1e12, "TFLOP/s"
-            tot += cs * 2.0 * T * D * (R + 2 * N)
+        elif label == "gemm_x_proj":     # AI = 2(R+2N)D / (2D + 4(R+2N)) ~ 100 FLOP/B < ridge 255: HBM-bound
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += cs * T * (2.0 * D + 4.0 * (R + 2 * N))   # v read (bf16) + (delta, B, C) write (f32)
+        elif label == "scan_dt":         # Delta = softplus(delta W_dt^T + b): delta read, Delta write (f32)
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += cs * T * (4.0 * R + 4.0 * D)
+        elif label == "scan_carry":      # chunk summaries read (a = sum Delta, b = end state), entry states written
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += cs * m["B"] * m["chunks"] * (4.0 * D + 2 * 4.0 * D * N)
+        elif label == "pad_qkv":         # p W_qkv^T + b: W_qkv read once (bf16), 3C f32 written
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += m["pad"] * (2.0 * 3 * C * C + 4.0 * 3 * C)
+        elif label == "pad_tables":      # rotated pad keys per padded column / row and the pad value (bf16)
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            tot += m["pad"] * 2.0 * (m["Hp"] + m["Wp"] + 2) * C
         elif label == "gemm_fc1_gelu":
             bound, scale, unit = "tensor", 1e12, "TFLOP/s"
             tot += 2.0 * T * C * Hd
@@ -170,8 +200,16 @@ def peaks():
                  sm_max_mhz=m.get("sm_max_mhz", 1965.0))
     except Exception:
         p["sm_max_mhz"] = 1965.0
-    # MUFU ex2: 16 / clk / SM (B200: 148 SMs), at the max SM clock
+    # MUFU ex2: the rate measured by tools/ubench/pipes.cu on a B200 (profiles/alu_peaks.json); else derived from
+    # 16 / clk / SM x 148 SMs at the max SM clock
     p["ex2_gps"] = 16 * 148 * p["sm_max_mhz"] * 1e6 / 1e9
+    p["ex2_src"] = "derived: 16 ex2/clk/SM x 148 SMs x max SM clock"
+    try:
+        with open(os.path.join(ROOT, "profiles", "alu_peaks.json")) as f:
+            p["ex2_gps"] = float(json.load(f)["ex2_gps"])
+            p["ex2_src"] = "measured: MUFU.EX2 rate, tools/ubench/pipes.cu (profiles/alu_peaks.json)"
+    except Exception:
+        pass
     return p
 
 
@@ -406,8 +444,53 @@ def roofline(res, args):
         out = {"kernel": dom["kernel"], "bound": dom["bound"], "achieved": round(dom["achieved"], 2),
                "peak": round(dom["peak"], 2), "unit": dom["unit"], "frac": round(dom["frac"], 4),
                "traffic": tr, "share_of_step": round(dom["share"], 4),
-               "peak_src": src if dom["bound"] != "alu" else "derived: 16 ex2/clk/SM x 148 SMs x max SM clock"}
+               "peak_src": src if dom["bound"] != "alu" else pk["ex2_src"]}
     return out, rows
+
+
+def attention_sublayer_roofline(res, args):
+    """The north-star attention target (">= 60 % of B200 dense-bf16 tensor peak in attention") graded on the attention
+    SUB-LAYER: LN1 + QKV GEMM (+ RoPE) + pad work + window attention + out-proj with residual, timed per layer with
+    CUDA events (eager, L2 flushed) on the layers that have no cycle-scan module and no FFN. Algorithmic FLOPs per
+    token: QKV 2*C*3C, out-proj 2*C*C, attention 4*w^2*C (QK^T and PV over the w^2 slots of the token's window)."""
+    if args.workload == "ms":
+        return None
+    pk = peaks()
+    cfgs, layer_ms = res["cfgs"], res["layer_ms"]
+    out = {}
+    for name, want_shift in (("P", False), ("S", True)):
+        ts = [t for c, t in zip(cfgs, layer_ms)
+              if not c.cycle_scan and not c.mlp_hidden and bool(c.shift_x or c.shift_y) == want_shift]
+        if not ts:
+            continue
+        c = next(c for c in cfgs if not c.cycle_scan and bool(c.shift_x or c.shift_y) == want_shift)
+        T = c.B * c.H * c.W
+        flops = T * (2.0 * c.C * 3 * c.C + 2.0 * c.C * c.C + 4.0 * c.window ** 2 * c.C)
+        ms = float(np.median(ts))
+        tf = flops / (ms * 1e-3) / 1e12
+        out[name] = {"ms": round(ms, 4), "gflop": round(flops / 1e9, 2), "tflops": round(tf, 1),
+                     "frac": round(tf / pk["bf16_tflops"], 4)}
+    if not out:
+        return None
+    return {"unit": "TFLOP/s", "peak": pk["bf16_tflops"], "peak_src": "of measured (MEASURED_PEAKS.json, burst)",
+            "scope": "LN1 + QKV/RoPE + pad + window attention + out-proj + residual, per layer", **out}
+
+
+def scan_roofline(rows):
+    """Scan passes against the measured MUFU ex2 rate (one ex2 per (token, channel, state) per pass) and the dt /
+    x_proj / conv steps against HBM (north-star scan target: ">= 70 % of HBM peak in the scan")."""
+    pk = peaks()
+    out = {}
+    for r in rows:
+        if r["kernel"] in ("scan_pass1", "scan_pass2", "scan_dt", "gemm_x_proj", "conv_silu", "scan_carry") \
+                and "frac" in r:
+            out[r["kernel"]] = {"ms_per_launch": round(r["ms_per_launch"], 4), "achieved": round(r["achieved"], 1),
+                                "unit": r["unit"], "frac": round(r["frac"], 4)}
+    if not out:
+        return None
+    out["ex2_peak_gps"] = pk["ex2_gps"]
+    out["hbm_peak_gbs"] = pk["hbm_gbs"]
+    return out
 
 
 # ----------------------------------------------------------------------------------------------- oracle (CPU)
@@ -560,16 +643,18 @@ def _free_port():
 def cpu_baseline(args):
     """The fp64 oracle as it stands, timed on this host: one image through one layer of each kind (summed per
     image) — or, for the multi-scale workload, each bounded oracle piece of one sample timed once and scaled."""
-    if args.workload == "ms":
+    if args.workload != "1024":
         items = reference_items(reference_entries(args))
         tot = 0.0
         for name, fn, scale in items:
             t0 = time.perf_counter()
             fn()
             tot += (time.perf_counter() - t0) * scale
+        what = "sample" if args.workload == "ms" else "image"
         return {"value": round(1e3 * tot, 1), "unit": "ms/image", "cores": oracle_threads(), "kind": "oracle",
-                "sample": f"one sample; {len(items)} bounded oracle pieces (1/16 of the projection rows, one window "
-                          f"row, 1/16 of the 3L scan) timed once each and scaled to the full stack"}
+                "sample": f"one {what}; {len(items)} bounded oracle pieces (1/16 of the projection rows, one window "
+                          f"row per attention kind, 1/16 (1/64 at 4096^2) of the 3L scan tokens) timed once each and "
+                          f"scaled to the full stack"}
     label, B, cfgs = workload(args.workload)
     one = [c.replace(B=1) for c in cfgs]
     kinds = {}
@@ -596,7 +681,15 @@ def reference_entries(args):
         ents.append((synth.vitb(64, B=1, H=1, W=Lt, shift_x=0, shift_y=0, cycle_scan=1), 0, 4))  # multi-scale
         return ents
     _, _, cfgs = workload(args.workload)
-    return [(c.replace(B=1), 1, 1 if c.cycle_scan else 0) for c in cfgs]
+    # one entry per distinct piece (the oracle's cost of a piece depends only on its kind): plain attention,
+    # shifted attention, cycle-scan module, each with its repeat count in the stack
+    ents = {}
+    for c in cfgs:
+        one = c.replace(B=1, cycle_scan=0)
+        ents.setdefault(("att", one.shift_x), [one, 0, 0])[1] += 1
+        if c.cycle_scan:
+            ents.setdefault(("cs",), [c.replace(B=1, shift_x=0, shift_y=0), 0, 0])[2] += 1
+    return [tuple(v) for v in ents.values()]
 
 
 def reference_items(entries):
@@ -637,6 +730,7 @@ def reference_items(entries):
                 items.append((f"E{j} FFN", ffn, na * T / len(rows)))
         if ncs:
             L, D = T, c.D
+            frac = 16 if L <= 16384 else 64      # the SSM sample: 1/16 (1/64 at 4096^2) of the 3L tokens
             rows3 = np.arange(0, 3 * L, 16)
 
             def cs_proj(x=x, w=w, c=c, rows3=rows3, L=L):
@@ -646,10 +740,10 @@ def reference_items(entries):
                 return xz[:, :c.D] @ w["w_out"].T
             items.append((f"E{j} cycle-scan LN+in/out-proj", cs_proj, ncs * 3 * L / len(rows3)))
             u0 = oracle.layer_norm(x, w["lns_g"], w["lns_b"], c.ln_eps).reshape(L, c.C)
-            n3 = 3 * L // 16
+            n3 = 3 * L // frac
             xz = np.concatenate([u0, u0, u0])[:n3] @ w["w_in"].T
 
-            def cs_ssm(xz=xz, w=w, c=c, D=D):  # the recurrence over the first 1/16 of the 3L tokens
+            def cs_ssm(xz=xz, w=w, c=c, D=D):  # the recurrence over the first 1/frac of the 3L tokens
                 return oracle.cycle_ssm_3L(xz[:, :D], xz[:, D:], w, c.bbar_mode)
             items.append((f"E{j} cycle-scan SSM", cs_ssm, ncs * 3 * L / n3))
     return items
@@ -675,8 +769,8 @@ def run_reference(args):
     ms_img = 1e3 * sum(np.mean(times[name]) * scale for name, _, scale in items)
     cores = oracle_threads()
     sample = (f"{n_run} steps round-robin over {len(items)} oracle pieces of one image (projections on 1/16 of "
-              f"the token rows, attention on one window row, the SSM on 1/16 of the 3L tokens), each scaled to the full "
-              f"layer")
+              f"the token rows, attention on one window row per attention kind, the SSM on 1/16 (1/64 at 4096^2) of "
+              f"the 3L tokens), each scaled to its repeats in the full stack")
     line = {"metric": METRIC, "value": round(ms_img, 2), "unit": "ms/image", "n_gpus": 0, "steps": n_run,
             "warmup": args.warmup, "ms_per_step": round(1e3 * wall / max(n_run, 1), 2),
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -842,9 +936,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--workload", default="1024", choices=["1024", "2048", "4096", "ms"],
-                    help="1024: configs[1] (default); 2048 / 4096: the 12-layer stacks (configs[2], [3]); "
-                         "ms: HRSAM++ multi-scale (configs[4])")
+    ap.add_argument("--workload", default="4096", choices=["1024", "2048", "4096", "ms"],
+                    help="4096: the north-star 12-layer stack on one 4096^2 image (configs[3], default); 1024: "
+                         "HRSAM stage 1 (configs[1]); 2048: the 12-layer stack, batch 8 (configs[2]); ms: HRSAM++ "
+                         "multi-scale (configs[4])")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="also print the per-kernel table to stderr")
@@ -867,9 +962,17 @@ def main():
     global FFN_HIDDEN
     FFN_HIDDEN = 3072 if args.ffn else 0
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: re-run under torch.distributed.run with one rank per GPU (the
+        # driver's own launch is the same command, already under torchrun)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)]
+        raise SystemExit(subprocess.call(cmd + sys.argv[1:]))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} rank(s)", file=sys.stderr)
 
     if args.impl == "reference":
         if rank == 0:
@@ -892,8 +995,6 @@ def main():
     if args.shard == "rows":
         if args.workload == "ms":
             raise SystemExit("--shard rows splits one image (config 4); the multi-scale workload shards by sample")
-        if args.workload == "1024" and "--workload" not in sys.argv:
-            args.workload = "4096"  # config 4 is the row-sharded 4096^2 stack
         res = run_rows(args, rank, world, local_rank)
         if rank == 0:
             c0 = res["cfgs"][0]
@@ -945,6 +1046,8 @@ def main():
             "gpu_launches": int(res["launches"]),
             "clocks": res["clocks"],
             "roofline": rl,
+            "attention_sublayer": attention_sublayer_roofline(res, args),
+            "scan": scan_roofline(rows),
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args)

@@ -153,6 +153,10 @@ int pscwin_cycle_scan(const pscwin_scan_desc* desc, const void* xin, const void*
                       const float* a_log, const float* d_skip, void* out, void* workspace, size_t ws_bytes,
                       void* stream);
 size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* desc);
+/* Instrumentation: the chunk length (tokens) the bf16 two-pass scan would use for desc on the current device
+ * (chosen from the pass-2 occupancy so the chunk x channel-block CTAs fill the SMs); 0 for an invalid desc or the
+ * F32 path. Lets a caller account the carry's bytes (chunks x D x (N + 1) floats per image). */
+int32_t pscwin_scan_chunk_length(const pscwin_scan_desc* desc);
 
 /* ----------------------------------------------------------------------------------- the whole layer */
 /* One PSCWin layer: [cycle-scan module: x += (cycle_scan(in_proj(LN_s(x)))) W_out^T] then

@@ -7,7 +7,7 @@ from ._lib import (CS_MULTI_SCALE, CS_NONE, CS_SINGLE_SCALE, LIB_PATH, LayerDesc
                    MSDesc, NeckDesc, PscwinError, ScanDesc, launch_count, lib, ms_index_map, profile_enable, profile_read)
 from .api import (HRSAMEncoder, PSCWinLayer, PSCWinMSLayer, PSCWinStack, ms_forward, ms_workspace_bytes, neck,
                   neck_workspace_bytes, patch_embed, resize_bilinear, Workspace, cycle_scan, forward, index_map, layer_norm, linear,  # noqa: F401
-                  qkv_project, scan_workspace_bytes, shifted_pad_partition, window_attention, window_count,
+                  qkv_project, scan_chunks, scan_workspace_bytes, shifted_pad_partition, window_attention, window_count,
                   window_merge, window_partition, workspace_bytes)
 
 lib()  # no silent fallback: the CUDA library must be present

@@ -26,7 +26,7 @@ EXPORTS = [
     "pscwin_version", "pscwin_status_string", "pscwin_last_async_error", "pscwin_window_count",
     "pscwin_index_map", "pscwin_window_partition", "pscwin_shifted_pad_partition", "pscwin_window_merge",
     "pscwin_layer_norm", "pscwin_linear", "pscwin_qkv_project", "pscwin_window_attention", "pscwin_cycle_scan",
-    "pscwin_scan_workspace_bytes", "pscwin_workspace_bytes", "pscwin_forward",
+    "pscwin_scan_workspace_bytes", "pscwin_scan_chunk_length", "pscwin_workspace_bytes", "pscwin_forward",
     "pscwin_launch_count", "pscwin_profile_enable", "pscwin_profile_read",
     "pscwin_band_workspace_bytes", "pscwin_band_io_offsets", "pscwin_band_scan_begin", "pscwin_band_scan_mid",
     "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
@@ -164,6 +164,7 @@ def lib() -> ctypes.CDLL:
         "pscwin_cycle_scan": ([ctypes.POINTER(ScanDesc), vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
                               ctypes.c_int),
         "pscwin_scan_workspace_bytes": ([ctypes.POINTER(ScanDesc)], sz),
+        "pscwin_scan_chunk_length": ([ctypes.POINTER(ScanDesc)], ctypes.c_int32),
         "pscwin_workspace_bytes": ([ctypes.POINTER(LayerDesc)], sz),
         "pscwin_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, vp, sz, vp],
                            ctypes.c_int),

@@ -129,6 +129,14 @@ def scan_workspace_bytes(sd: ScanDesc) -> int:
     return int(lib().pscwin_scan_workspace_bytes(ctypes.byref(sd)))
 
 
+def scan_chunks(B: int, L: int, D: int, N: int = 32, R: int = 48, conv_k: int = 4) -> int:
+    """Number of chunks the bf16 cycle scan splits each image's L tokens into (pscwin_scan_chunk_length)."""
+    sd = ScanDesc()
+    sd.B, sd.H, sd.W, sd.D, sd.N, sd.R, sd.conv_k = B, 1, L, D, N, R, conv_k
+    lc = int(lib().pscwin_scan_chunk_length(ctypes.byref(sd)))
+    return -(-L // lc) if lc > 0 else 0
+
+
 def cycle_scan(sd: ScanDesc, xin: torch.Tensor, z: Optional[torch.Tensor], w: Dict[str, torch.Tensor],
                ws: Optional[Workspace] = None) -> torch.Tensor:
     ws = ws or Workspace(scan_workspace_bytes(sd), xin.device)

@@ -752,6 +752,9 @@ BandGeo band_geo(const pscwin_layer_desc* d, const pscwin_band* b) {
   g.hb = pt ? w - pt : 0;
   g.ht_eff = b->rank > 0 ? g.ht : 0;
   g.hb_eff = b->rank < b->world - 1 ? g.hb : 0;
+  // the band must hold the halo its neighbours read from it: its first hb rows go to rank - 1, its last ht rows
+  // to rank + 1 (a shorter ragged band would send rows past its own into the workspace)
+  if ((b->rank > 0 && g.rows < g.hb) || (b->rank < b->world - 1 && g.rows < g.ht)) return g;
   g.e0 = g.r0 - g.ht_eff;
   g.ext_rows = g.ht_eff + g.rows + g.hb_eff;
   // the extended buffer's window grid must coincide with the global one: local pad_top = (pt + e0) mod w

@@ -1594,6 +1594,13 @@ extern "C" size_t pscwin_scan_workspace_bytes(const pscwin_scan_desc* d) {
   return scan_ws_bytes(d->B, L, d->D, d->N, d->R, d->conv_k, d->scan_order);
 }
 
+extern "C" int32_t pscwin_scan_chunk_length(const pscwin_scan_desc* d) {
+  if (!d || d->dtype != PSCWIN_BF16) return 0;
+  const int L = d->H * d->W;
+  if (check_scan(d->B, L, d->D, d->N, d->R, d->conv_k) != PSCWIN_OK) return 0;
+  return choose_chunk(d->B, L, d->D, d->N, 2 * d->N);
+}
+
 extern "C" int pscwin_cycle_scan(const pscwin_scan_desc* d, const void* xin, const void* z, const float* conv_w,
                                  const float* conv_b, const void* w_x, const float* w_dt, const float* b_dt,
                                  const float* a_log, const float* d_skip, void* out, void* ws, size_t ws_bytes,

@@ -53,15 +53,17 @@ def sum_over_ranks(value: float, device=None) -> float:
 
 # ------------------------------------------------------------------------------------- window-row bands
 def band_rows(H: int, window: int, world: int):
-    """Split the H token rows of one image into `world` contiguous bands of whole window rows (the last band
-    takes the ragged remainder). Returns [(row_begin, row_end)] in rank order."""
-    nwin = -(-H // window)
-    if world <= 0 or world > nwin:
-        raise ValueError(f"cannot split {nwin} window rows over {world} ranks")
+    """Split the H token rows of one image into `world` contiguous bands of whole window rows. A ragged remainder
+    (H % window rows) joins the last full window row, so every band holds at least `window` rows: a band must hold
+    the halo rows its neighbours need (up to window - 1 from each edge; pscwin_band_io_offsets rejects a band
+    shorter than that). Returns [(row_begin, row_end)] in rank order."""
+    units = max(H // window, 1)        # window rows; the last one absorbs the ragged tail
+    if world <= 0 or world > units:
+        raise ValueError(f"cannot split {H} rows ({units} whole window rows) over {world} ranks")
     out = []
     for r in range(world):
-        lo, hi = shard_range(nwin, world, r)
-        out.append((lo * window, min(hi * window, H)))
+        lo, hi = shard_range(units, world, r)
+        out.append((lo * window, H if hi == units else hi * window))
     return out
 
 

@@ -107,6 +107,15 @@ def test_band_plan_and_io_offsets(pl):
            BandDesc(224, 256, 6, 8)]  # rank 6 cannot end at H
     for b in bad:
         assert L.pscwin_band_workspace_bytes(ctypes.byref(d), ctypes.byref(b)) == 0
+    # a ragged last band shorter than the halo it sends to the previous rank: H = 34, w = 8, shift 4
+    # sends w - pt = 4 rows from a 2-row band; H = 36 with shift_y = 5 sends 5 rows from a 4-row band
+    for H, sy, r0 in ((34, 4, 32), (36, 5, 32)):
+        t = LayerDesc.from_config(synth.tiny(H=H, W=16, shift_x=4, shift_y=sy))
+        io = BandIO()
+        assert L.pscwin_band_io_offsets(ctypes.byref(t), ctypes.byref(BandDesc(r0, H, 2, 3)), ctypes.byref(io)) != 0
+        assert L.pscwin_band_workspace_bytes(ctypes.byref(t), ctypes.byref(BandDesc(r0, H, 2, 3))) == 0
+    ok = LayerDesc.from_config(synth.tiny(H=34, W=16, shift_x=4, shift_y=4))
+    assert L.pscwin_band_io_offsets(ctypes.byref(ok), ctypes.byref(BandDesc(24, 34, 2, 3)), ctypes.byref(BandIO())) == 0
     col = LayerDesc.from_config(cfg.replace(scan_order=synth.SCAN_COL_MAJOR))
     assert L.pscwin_band_workspace_bytes(ctypes.byref(col), ctypes.byref(BandDesc(0, 32, 0, 8))) == 0
 

@@ -110,12 +110,21 @@ def test_band_exchange_gloo(world):
         assert rn == ([30 + g + 1] * 3 if g < world - 1 else [])
 
 
-@pytest.mark.parametrize("H,w,world", [(256, 16, 8), (64, 16, 4), (20, 8, 3), (32, 8, 1)])
+@pytest.mark.parametrize("H,w,world", [(256, 16, 8), (64, 16, 4), (28, 8, 3), (34, 8, 3), (32, 8, 1), (36, 8, 4)])
 def test_band_rows_cover_whole_window_rows(H, w, world):
     d = _load_dist()
     rows = d.band_rows(H, w, world)
     assert rows[0][0] == 0 and rows[-1][1] == H and len(rows) == world
     for (a, b), (c, _) in zip(rows, rows[1:]):
         assert b == c and a % w == 0 and b % w == 0 and b > a
+    assert all(r1 - r0 >= w for r0, r1 in rows)      # every band can serve a halo of up to w - 1 rows
     with pytest.raises(ValueError):
-        d.band_rows(H, w, -(-H // w) + 1)
+        d.band_rows(H, w, H // w + 1)
+
+
+def test_band_rows_ragged_tail_joins_last_band():
+    # a ragged last band shorter than the halo it must send (H = 34, w = 8, 3 ranks) is never produced
+    d = _load_dist()
+    assert d.band_rows(34, 8, 3) == [(0, 16), (16, 24), (24, 34)]
+    with pytest.raises(ValueError):
+        d.band_rows(20, 8, 3)                          # 2 whole window rows (+ 4 ragged) cannot feed 3 ranks

@@ -25,7 +25,9 @@ CASES = [
     (synth.tiny(H=32, W=16), 2),                                           # S, learnable
     (synth.tiny(H=32, W=16), 4),
     (synth.tiny(H=40, W=24, shift_x=3, shift_y=5), 3),                     # asymmetric shift: 5 / 3 halo rows
-    (synth.tiny(H=36, W=16, pad_mode=synth.PAD_MASKED), 3),                # ragged last band (4 rows)
+    (synth.tiny(H=36, W=16, pad_mode=synth.PAD_MASKED), 3),                # ragged tail joins the last band
+    (synth.tiny(H=34, W=16), 3),                                           # 2-row ragged tail, shift 4
+    (synth.tiny(H=36, W=16, shift_x=4, shift_y=5, cycle_scan=1), 3),       # 5-row halo to the previous rank
     (synth.tiny(H=32, W=16, cycle_scan=1, shift_x=0, shift_y=0), 2),       # CS + P
     (synth.tiny(H=32, W=16, cycle_scan=1), 4),                             # CS + S
     (synth.tiny(H=32, W=16, cycle_scan=1, bbar_mode=synth.BBAR_EULER), 3),

@@ -22,7 +22,7 @@ for v in "${vals[@]}"; do
   envs=""
   case $kind in
     env:*)  envs="${kind#env:}=$v" ;;
-    flag:*) PSCWIN_NVCC_FLAGS="-D${kind#flag:}=$v" python -m paper_2407_02109_b200._build --force > /dev/null 2>&1 \
+    flag:*) PSCWIN_NVCC_FLAGS="-D${kind#flag:}=$v" python paper_2407_02109_b200/_build.py --force > /dev/null 2>&1 \
               || { echo "== $kind=$v: build failed" >> "$log"; continue; }
             timeout 900 python -m pytest ${PSCWIN_SWEEP_TESTS:-tests/test_gpu_scan.py} -x -q -m gpu > gpurun_out/$name.tests.log 2>&1
             echo "== $kind=$v tests: $(tail -n 1 gpurun_out/$name.tests.log)" >> "$log" ;;
@@ -43,5 +43,5 @@ for l in sys.stdin:
         print('   STEP %s ms/image' % d['value'])" >> "$log"
   done
 done
-case $kind in flag:*) python -m paper_2407_02109_b200._build --force > /dev/null 2>&1 ;; esac
+case $kind in flag:*) python paper_2407_02109_b200/_build.py --force > /dev/null 2>&1 ;; esac
 cat "$log"
