@@ -930,6 +930,59 @@ def run_encoder(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------------------------- micro
+def run_partition_micro(args):
+    """--micro partition: the standalone a5 / a7 data-movement entry points (pscwin_window_partition,
+    pscwin_shifted_pad_partition, pscwin_window_merge with and without the residual) on a 4096^2 token grid
+    (256 x 256, w = 16, s = 8) for the QKV width (Cx = 3C = 2304) and the model width (Cx = 768), L2 flushed
+    before every launch, CUDA events on the launching stream. Algorithmic bytes: partition = grid read + every
+    window slot written (pads included); merge = the real window rows read + the grid written (+ residual read).
+    One JSON line per case (GB/s and fraction of the measured HBM copy bandwidth)."""
+    import torch
+    import paper_2407_02109_b200 as pl
+    torch.cuda.set_device(0)
+    pk = peaks()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    H = W = 256
+    w, s_ = 16, 8
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(max(5, min(args.steps, 50))):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    for Cx in (2304, 768):
+        x = torch.randn(1, H, W, Cx, device="cuda").to(torch.bfloat16)
+        pad = torch.randn(Cx, device="cuda").to(torch.bfloat16)
+        res = torch.randn_like(x)
+        grid = H * W * Cx * 2
+        n_s = pl.window_count(H, W, w, s_, s_)
+        win_p = pl.window_partition(x, w)
+        win_s = pl.shifted_pad_partition(x, pad, w, s_, s_)
+        cases = [("window_partition", lambda: pl.window_partition(x, w), 2 * grid),
+                 ("shifted_pad_partition", lambda: pl.shifted_pad_partition(x, pad, w, s_, s_),
+                  grid + n_s * w * w * Cx * 2),
+                 ("window_merge", lambda: pl.window_merge(win_p, 1, H, W, w), 2 * grid),
+                 ("window_merge_shifted_residual", lambda: pl.window_merge(win_s, 1, H, W, w, s_, s_, residual=res),
+                  3 * grid)]
+        for name, fn, nbytes in cases:
+            ms = timed(fn)
+            gbs = nbytes / (ms * 1e-3) / 1e9
+            print(json.dumps({"micro": name, "grid": f"{H}x{W}", "Cx": Cx, "window": w, "shift": s_ if "shift" in name else 0,
+                              "ms": round(ms, 4), "bytes": int(nbytes), "GB/s": round(gbs, 1),
+                              "frac_hbm": round(gbs / pk["hbm_gbs"], 4), "peak_gbs": pk["hbm_gbs"],
+                              "l2": "flushed before every launch"}), flush=True)
+
+
 # ----------------------------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -955,6 +1008,7 @@ def main():
                          "2048^2 (one JSON line per variant; SURVEY NEXT-4)")
     ap.add_argument("--encoder", action="store_true",
                     help="the whole HRSAM encoder on one image: patch embedding + 12 blocks with FFN + neck (NEXT-3)")
+    ap.add_argument("--micro", choices=["partition"], help="micro-benchmark of one standalone entry point family")
     ap.add_argument("--ffn", action="store_true",
                     help="add the FFN sub-layer (hidden 768 x 4, P:L625; SURVEY NEXT-2) after every attention sub-layer")
     args = ap.parse_args()
@@ -985,6 +1039,10 @@ def main():
     if args.encoder:
         if rank == 0:
             run_encoder(args)
+        return
+    if args.micro:
+        if rank == 0:
+            run_partition_micro(args)
         return
 
     if world > 1:

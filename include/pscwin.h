@@ -10,11 +10,18 @@
  *   - `stream` is a cudaStream_t passed as void*. Calls enqueue work on it and return immediately;
  *     argument/contract validation is synchronous. A launch failure returns PSCWIN_ERR_CUDA; a fault inside a
  *     kernel surfaces later through pscwin_last_async_error() or the next call.
- *   - No exceptions or C++ types cross the boundary. Calls are reentrant; the only global state is a cached
- *     SM count and per-kernel attribute flags.
- *   - dtype PSCWIN_BF16: activations and GEMM weights are bf16; LayerNorm parameters, biases, conv, dt_proj,
- *     A_log, D_skip are f32. PSCWIN_F32 (all f32) is accepted by the partition / merge / layer-norm calls;
- *     the fused layer and attention calls currently require PSCWIN_BF16 (PSCWIN_ERR_UNSUPPORTED otherwise).
+ *   - No exceptions or C++ types cross the boundary. Calls are reentrant and may run concurrently on different
+ *     host threads and streams: the library's only state is a cached SM count, per-(device, kernel)
+ *     shared-memory attributes set once under a lock, and helper streams / fork-join events that are private to
+ *     each host thread and device (thread_local; e.g. the side stream of the pad work). The A/B tuning knobs
+ *     (PSCWIN_* environment variables) are read once per process.
+ *   - dtype PSCWIN_BF16 (the product path): activations and GEMM weights are bf16; LayerNorm parameters, biases,
+ *     conv, dt_proj, A_log, D_skip are f32; accumulation and the scan state are f32. PSCWIN_F32 (everything f32,
+ *     the 1e-4 correctness path of DESIGN.md §6b) is accepted by the partition / merge / layer-norm calls, the
+ *     attention, cycle-scan and whole-layer calls; the multi-scale, band and encoder-end calls require BF16
+ *     (PSCWIN_ERR_UNSUPPORTED otherwise).
+ *   - Head width d = C / heads must be 32 or 64 (tcgen05 tiles of the attention kernels); d = 128 is a contract
+ *     limit of this library (PSCWIN_ERR_UNSUPPORTED): ViT-B / HRSAM use d = 64.
  */
 #ifndef PSCWIN_H_
 #define PSCWIN_H_
@@ -274,15 +281,32 @@ int pscwin_band_attn_begin(const pscwin_layer_desc* global_desc, const pscwin_ba
 int pscwin_band_attn_end(const pscwin_layer_desc* global_desc, const pscwin_band* band,
                          const pscwin_layer_weights* wts, const void* x_band, void* x_out, void* workspace,
                          size_t ws_bytes, void* stream);
+/* pscwin_band_attn_end split for overlapping the halo exchange with compute (pscwin_dist_forward does this on two
+ * streams): the band's extended image has *nwy padded-grid window rows; rows [*top, *bot) read no halo row (they
+ * can run before the halo arrives), rows [0, *top) and [*bot, *nwy) read halo rows. pscwin_band_attn_windows runs
+ * the window attention of rows [wy_begin, wy_end) (wy_begin == wy_end: nothing); after every row has run once,
+ * pscwin_band_out_proj runs the out-proj + residual (+ FFN). Together they equal pscwin_band_attn_end. */
+int pscwin_band_window_split(const pscwin_layer_desc* global_desc, const pscwin_band* band, int32_t* top,
+                             int32_t* bot, int32_t* nwy);
+int pscwin_band_attn_windows(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                             const pscwin_layer_weights* wts, void* workspace, size_t ws_bytes, int32_t wy_begin,
+                             int32_t wy_end, void* stream);
+int pscwin_band_out_proj(const pscwin_layer_desc* global_desc, const pscwin_band* band,
+                         const pscwin_layer_weights* wts, const void* x_band, void* x_out, void* workspace,
+                         size_t ws_bytes, void* stream);
 
 /* One layer of a window-row-sharded image with the exchanges done inside the library over NCCL (SURVEY §8(b)
  * pscwin_dist_forward; §8(e)): the rank / world come from the communicator (an ncclComm_t passed as void*, from
  * the caller's own NCCL setup or pscwin_nccl_comm_init), the band is [row_begin, row_end) as for the band
- * phases, and all kernels and NCCL operations (conv-history ring send/recv, ncclAllGather of the scan records,
- * QKV halo send/recv with the neighbours) are enqueued on `stream` — the call is CUDA-graph capturable. Every
- * rank of the communicator must call it for the same layer. x_band, x_band_out [rows, W, C] bf16 (no alias).
- * Workspace: pscwin_dist_workspace_bytes (= pscwin_band_workspace_bytes). Errors: as the band phases;
- * ERR_CUDA for an NCCL failure. */
+ * phases. Kernels and the latency-sized scan exchanges (conv-history ring send/recv, ncclAllGather of the scan
+ * records) run on `stream` (compute). The QKV halo send/recv with the neighbours runs on `comm_stream` when it is
+ * non-NULL and differs from `stream`: it waits (event) for this band's QKV rows, the windows that need no halo row
+ * are computed on `stream` meanwhile, then `stream` waits (event) for the halo and computes the band-edge windows
+ * and the out-proj (SURVEY §8(e) overlap). comm_stream NULL: everything on `stream`. Both streams must be usable
+ * by the caller's CUDA graph capture (the call is capturable: the fork / join are event edges). Every rank of the
+ * communicator must call it for the same layer. x_band, x_band_out [rows, W, C] bf16 (no alias). Workspace:
+ * pscwin_dist_workspace_bytes (= pscwin_band_workspace_bytes). Errors: as the band phases; ERR_CUDA for an NCCL
+ * failure. */
 int pscwin_nccl_get_unique_id(void* id_out /* host, 128 bytes */);
 int pscwin_nccl_comm_init(const void* id /* host, 128 bytes */, int32_t world, int32_t rank, void** comm_out);
 int pscwin_nccl_comm_destroy(void* comm);  /* after every CUDA graph holding its operations is destroyed */
@@ -290,7 +314,7 @@ size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* global_desc, int32_t
                                    int32_t rank, int32_t world);
 int pscwin_dist_forward(const pscwin_layer_desc* global_desc, const pscwin_layer_weights* wts, const void* x_band,
                         void* x_band_out, int32_t row_begin, int32_t row_end, void* nccl_comm, void* workspace,
-                        size_t ws_bytes, void* stream);
+                        size_t ws_bytes, void* stream, void* comm_stream);
 
 /* ------------------------------------------------------------------------------------ instrumentation */
 /* Kernel launches issued by this library since it was loaded (every launcher counts itself). */

@@ -29,7 +29,8 @@ EXPORTS = [
     "pscwin_scan_workspace_bytes", "pscwin_scan_chunk_length", "pscwin_workspace_bytes", "pscwin_forward",
     "pscwin_launch_count", "pscwin_profile_enable", "pscwin_profile_read",
     "pscwin_band_workspace_bytes", "pscwin_band_io_offsets", "pscwin_band_scan_begin", "pscwin_band_scan_mid",
-    "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end",
+    "pscwin_band_scan_end", "pscwin_band_attn_begin", "pscwin_band_attn_end", "pscwin_band_window_split",
+    "pscwin_band_attn_windows", "pscwin_band_out_proj",
     "pscwin_ms_window_count", "pscwin_ms_index_map", "pscwin_ms_workspace_bytes", "pscwin_ms_forward",
     "pscwin_patch_embed_workspace_bytes", "pscwin_patch_embed", "pscwin_resize_bilinear", "pscwin_neck_workspace_bytes",
     "pscwin_neck", "pscwin_nccl_get_unique_id", "pscwin_nccl_comm_init", "pscwin_nccl_comm_destroy",
@@ -181,6 +182,12 @@ def lib() -> ctypes.CDLL:
                                     vp, vp, sz, vp], ctypes.c_int),
         "pscwin_band_attn_end": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
                                   vp, vp, vp, sz, vp], ctypes.c_int),
+        "pscwin_band_window_split": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(i32),
+                                      ctypes.POINTER(i32), ctypes.POINTER(i32)], ctypes.c_int),
+        "pscwin_band_attn_windows": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc),
+                                      ctypes.POINTER(LayerWeights), vp, sz, i32, i32, vp], ctypes.c_int),
+        "pscwin_band_out_proj": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(BandDesc), ctypes.POINTER(LayerWeights),
+                                  vp, vp, vp, sz, vp], ctypes.c_int),
         "pscwin_ms_window_count": ([ctypes.POINTER(MSDesc), ctypes.POINTER(i32)], ctypes.c_int),
         "pscwin_ms_index_map": ([ctypes.POINTER(MSDesc), vp], ctypes.c_int),
         "pscwin_ms_workspace_bytes": ([ctypes.POINTER(MSDesc)], sz),
@@ -197,7 +204,7 @@ def lib() -> ctypes.CDLL:
         "pscwin_nccl_comm_destroy": ([vp], ctypes.c_int),
         "pscwin_dist_workspace_bytes": ([ctypes.POINTER(LayerDesc), i32, i32, i32, i32], sz),
         "pscwin_dist_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, i32, i32, vp, vp, sz,
-                                 vp], ctypes.c_int),
+                                 vp, vp], ctypes.c_int),
         "pscwin_launch_count": ([], ctypes.c_int64),
         "pscwin_profile_enable": ([ctypes.c_int], None),
         "pscwin_profile_read": ([ctypes.c_char_p, sz, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32), i32],

@@ -58,6 +58,21 @@ class BandLayer:
     def attn_end(self, x, out):
         self._call("attn_end", _ptr(x), _ptr(out))
 
+    # attn_end split around the halo exchange (what pscwin_dist_forward overlaps on two streams)
+    def window_split(self):
+        t, b, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(lib().pscwin_band_window_split(ctypes.byref(self.desc), ctypes.byref(self.band), ctypes.byref(t),
+                                             ctypes.byref(b), ctypes.byref(n)), "band_window_split")
+        return t.value, b.value, n.value
+
+    def attn_windows(self, wy0, wy1):
+        check(lib().pscwin_band_attn_windows(ctypes.byref(self.desc), ctypes.byref(self.band), ctypes.byref(self.wts),
+                                             self.ws.data_ptr(), self.ws.numel(), wy0, wy1, _stream()),
+              "band_attn_windows")
+
+    def out_proj(self, x, out):
+        self._call("out_proj", _ptr(x), _ptr(out))
+
     # exchange buffers
     def hist(self):
         return self.view("hist_send", "hist_bytes"), self.view("hist_recv", "hist_bytes")
@@ -89,7 +104,8 @@ class LoopbackBands:
     """All `world` bands of one image on one GPU, phases run in lockstep and the exchanges done as device copies
     (the same byte movements NCCL performs across GPUs). Used to check the band path against pscwin_forward."""
 
-    def __init__(self, desc: LayerDesc, weights: Dict[str, torch.Tensor], world: int):
+    def __init__(self, desc: LayerDesc, weights: Dict[str, torch.Tensor], world: int, overlap: bool = False):
+        self.overlap = overlap  # interior windows before the halo copies, band-edge windows after (dist schedule)
         self.rows = band_rows(desc.H, desc.window, world)
         self.layers: List[BandLayer] = [BandLayer(desc, weights, r0, r1, g, world)
                                         for g, (r0, r1) in enumerate(self.rows)]
@@ -112,6 +128,11 @@ class LoopbackBands:
                 L[g].scan_end(xs[g])
         for g in range(G):
             L[g].attn_begin(xs[g])
+        split = [L[g].window_split() for g in range(G)] if self.overlap else None
+        if self.overlap:
+            for g in range(G):
+                top, bot, _ = split[g]
+                L[g].attn_windows(top, bot)
         for g in range(G):
             sp, sn, rp, rn = L[g].halo()
             if rp.numel():
@@ -119,7 +140,13 @@ class LoopbackBands:
             if rn.numel():
                 rn.copy_(L[g + 1].halo()[0])
         for g in range(G):
-            L[g].attn_end(xs[g], outs[g])
+            if self.overlap:
+                top, bot, nwy = split[g]
+                L[g].attn_windows(0, top)
+                L[g].attn_windows(bot, nwy)
+                L[g].out_proj(xs[g], outs[g])
+            else:
+                L[g].attn_end(xs[g], outs[g])
         return torch.cat(outs, dim=1)
 
 
@@ -150,10 +177,11 @@ class NcclComm:
 
 
 class DistLayer:
-    """One PSCWin layer on this rank's band, exchanges inside the library over NCCL (pscwin_dist_forward)."""
+    """One PSCWin layer on this rank's band, exchanges inside the library over NCCL (pscwin_dist_forward). With
+    overlap=True the QKV halo exchange runs on a second (comm) stream while the interior windows compute."""
 
     def __init__(self, desc: LayerDesc, weights: Dict[str, torch.Tensor], row_begin: int, row_end: int,
-                 comm: NcclComm):
+                 comm: NcclComm, overlap: bool = True, comm_stream: "torch.cuda.Stream" = None):
         self.desc, self.weights, self.comm = desc, weights, comm
         self.wts = LayerWeights.from_tensors(weights)
         self.r0, self.r1 = row_begin, row_end
@@ -162,10 +190,12 @@ class DistLayer:
             raise ValueError("invalid band for this layer")
         dev = next(iter(weights.values())).device
         self.ws = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.comm_stream = (comm_stream or torch.cuda.Stream(device=dev)) if overlap else None
 
     def __call__(self, x_band: torch.Tensor, out: torch.Tensor = None) -> torch.Tensor:
         out = torch.empty_like(x_band) if out is None else out
         check(lib().pscwin_dist_forward(ctypes.byref(self.desc), ctypes.byref(self.wts), _ptr(x_band), _ptr(out),
                                         self.r0, self.r1, self.comm.ptr, self.ws.data_ptr(), self.ws.numel(),
-                                        _stream()), "dist_forward")
+                                        _stream(), self.comm_stream.cuda_stream if self.comm_stream else None),
+              "dist_forward")
         return out

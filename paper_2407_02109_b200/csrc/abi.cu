@@ -1,6 +1,10 @@
 // C-ABI entry points of libpscwin.so (declared and documented in include/pscwin.h): argument / contract
 // validation, workspace planning, TMA descriptor encoding and the per-layer launch sequence.
 #include <stdio.h>
+
+#include <map>
+#include <mutex>
+#include <utility>
 #include <stdlib.h>
 #include <string.h>
 
@@ -266,29 +270,55 @@ int attention_impl(const pscwin_layer_desc* d, const void* qkv, const float* qkv
   return launch_window_attention(a, s);
 }
 
-// A side stream (one per process, created on first use) for the weight-only pad work of a shifted LEARNABLE layer
-// (qkv_pad = p W_qkv^T + b and its rotated pad-key / value tables): forked from the caller's stream at the start
-// of the attention sub-layer and joined before the attention kernel, so it overlaps LN1 + the QKV GEMM instead of
-// sitting on the critical path. Event fork / join is captured into CUDA graphs as graph edges.
-struct Side {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  bool ok = false;
-};
-Side& side() {
-  static Side sd;
-  if (!sd.ok && !sd.s) {
-    if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) == cudaSuccess &&
-        cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) == cudaSuccess &&
-        cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) == cudaSuccess)
-      sd.ok = getenv("PSCWIN_NO_SIDE_STREAM") == nullptr;
-    else
-      cudaGetLastError();
-  }
-  return sd;
+// The side stream (aux_stream slot 0) for the weight-only pad work of a shifted LEARNABLE layer (qkv_pad =
+// p W_qkv^T + b and its rotated pad-key / value tables): forked from the caller's stream at the start of the
+// attention sub-layer and joined before the attention kernel, so it overlaps LN1 + the QKV GEMM instead of sitting
+// on the critical path. Event fork / join is captured into CUDA graphs as graph edges. PSCWIN_NO_SIDE_STREAM=1 runs
+// the pad work on the caller's stream (A/B knob, read once).
+AuxStream* side() {
+  static const bool off = getenv("PSCWIN_NO_SIDE_STREAM") != nullptr;
+  return off ? nullptr : aux_stream(0);
 }
 
 }  // namespace
+
+namespace pscwin {
+void func_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{dev, fn}];
+  if (bytes > have && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    have = bytes;
+}
+
+AuxStream* aux_stream(int slot) {
+  constexpr int kDev = 16, kSlots = 3;
+  thread_local AuxStream tab[kDev][kSlots];
+  int dev = 0;
+  if (slot < 0 || slot >= kSlots || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDev) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  AuxStream& a = tab[dev][slot];
+  if (!a.ok) {
+    if (!a.s && cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) a.s = nullptr;
+    if (!a.fork && cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) a.fork = nullptr;
+    if (!a.join && cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) a.join = nullptr;
+    a.ok = a.s && a.fork && a.join;
+    if (!a.ok) {
+      cudaGetLastError();
+      return nullptr;
+    }
+  }
+  return &a;
+}
+}  // namespace pscwin
 
 extern "C" {
 
@@ -468,21 +498,21 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   float* qkv_pad = reinterpret_cast<float*>(wsp(ws, L.qkv_pad));
   void* O = wsp(ws, L.O);
   const bool learn_pad = shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE;
-  Side& sd = side();
-  const bool fork = learn_pad && sd.ok;
+  AuxStream* sd = learn_pad ? side() : nullptr;
+  const bool fork = sd != nullptr;
   if (fork) {  // weight-only pad work overlaps LN1 + the QKV GEMM (see side())
-    if (cudaEventRecord(sd.fork, s) != cudaSuccess || cudaStreamWaitEvent(sd.s, sd.fork, 0) != cudaSuccess)
+    if (cudaEventRecord(sd->fork, s) != cudaSuccess || cudaStreamWaitEvent(sd->s, sd->fork, 0) != cudaSuccess)
       return PSCWIN_ERR_CUDA;
-    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, sd.s);
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, sd->s);
     if (rc) return status_from(rc);
     AttnArgs pa = attn_args(d, qkv, qkv_pad, O, wsp(ws, L.pad_tab));
-    rc = launch_pad_tables(pa, sd.s);
+    rc = launch_pad_tables(pa, sd->s);
     if (rc) return status_from(rc);
-    if (cudaEventRecord(sd.join, sd.s) != cudaSuccess) return PSCWIN_ERR_CUDA;
+    if (cudaEventRecord(sd->join, sd->s) != cudaSuccess) return PSCWIN_ERR_CUDA;
   }
   rc = qkv_project_impl(d, wt, x, qkv, (learn_pad && !fork) ? qkv_pad : nullptr, ws, L, s);
   if (rc) return status_from(rc);
-  if (fork && cudaStreamWaitEvent(s, sd.join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  if (fork && cudaStreamWaitEvent(s, sd->join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
   rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s, fork ? 1 : 0);
   if (rc) return status_from(rc);
   GemmArgs a;
@@ -993,27 +1023,31 @@ int pscwin_band_attn_begin(const pscwin_layer_desc* d, const pscwin_band* b, con
   return PSCWIN_OK;
 }
 
-int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
-                         const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+}  // extern "C"
+
+namespace pscwin {
+
+// Window attention of a band over the extended QKV buffer, padded-grid window rows [wy0, wy1) of the extended
+// image (wy1 <= 0: all), and the band's out-proj + residual (+ FFN). pscwin_band_attn_end runs both; the NCCL path
+// splits the attention into interior and halo window rows to overlap the halo exchange (distnccl.cu).
+int band_attention(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt, void* ws,
+                   size_t ws_bytes, int wy0, int wy1, int tables_ready, void* stream) {
   BandGeo g;
   int rc = band_check(d, b, &g);
   if (rc) return rc;
-  if (!wt || !x_band || !x_out || !wt->w_o || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  if (!wt) return PSCWIN_ERR_SHAPE;
   const BandWs w = plan_band(d, b, g);
   if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
-  if (!aligned16(x_out)) return PSCWIN_ERR_ALIGN;
-  cudaStream_t s = (cudaStream_t)stream;
-  const long long T = (long long)g.rows * d->W;
-  const int C = d->C;
   // the extended buffer is an image of ext_rows rows whose window grid matches the global one (band_geo)
   const pscwin_layer_desc e = sub_desc(d, g.ext_rows, g.sy_local);
   AttnArgs a;
+  memset(&a, 0, sizeof(a));
   a.B = 1;
   a.H = g.ext_rows;
   a.W = d->W;
-  a.C = C;
+  a.C = d->C;
   a.heads = d->heads;
-  a.d = C / d->heads;
+  a.d = d->C / d->heads;
   a.w = d->window;
   a.sx = e.shift_x;
   a.sy = e.shift_y;
@@ -1024,9 +1058,42 @@ int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const
   a.qkv_pad = reinterpret_cast<const float*>(wsp(ws, w.qkv_pad));
   a.out = wsp(ws, w.O);
   a.pad_tab = wsp(ws, w.pad_tab);
-  a.tables_ready = 0;
-  rc = launch_window_attention(a, s);
-  if (rc) return status_from(rc);
+  a.tables_ready = tables_ready;
+  a.wy_begin = wy0;
+  a.wy_end = wy1;
+  return status_from(launch_window_attention(a, (cudaStream_t)stream));
+}
+
+// Window-row ranges of the extended band image: [0, top) and [bot, nwy) hold the windows that read halo rows,
+// [top, bot) the interior ones (computable before the halo arrives).
+void band_window_rows(const pscwin_layer_desc* d, const pscwin_band* b, int* top, int* bot, int* nwy) {
+  BandGeo g;
+  *top = *bot = *nwy = 0;
+  if (band_check(d, b, &g)) return;
+  const int w = d->window;
+  const int pt = (w - g.sy_local) % w;
+  const int Hp = pt + g.ext_rows + ((-(pt + g.ext_rows)) % w + w) % w;
+  *nwy = Hp / w;
+  // window row j covers local token rows [j w - pt, (j + 1) w - pt); own rows are [ht_eff, ht_eff + rows)
+  int t = 0, bo = *nwy;
+  while (t < *nwy && g.ht_eff > 0 && t * w - pt < g.ht_eff) ++t;
+  while (bo > t && g.hb_eff > 0 && bo * w - pt > g.ht_eff + g.rows) --bo;
+  *top = t;
+  *bot = bo;
+}
+
+int band_out_proj(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                  const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!wt || !x_band || !x_out || !wt->w_o || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  const BandWs w = plan_band(d, b, g);
+  if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
+  if (!aligned16(x_out)) return PSCWIN_ERR_ALIGN;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long T = (long long)g.rows * d->W;
+  const int C = d->C;
   const void* x = d->cycle_scan ? wsp(ws, w.x1) : x_band;
   GemmArgs o;
   memset(&o, 0, sizeof(o));
@@ -1050,6 +1117,44 @@ int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const
     return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, w.u), wsp(ws, w.h), s);
   }
   return PSCWIN_OK;
+}
+
+}  // namespace pscwin
+
+extern "C" {
+
+int pscwin_band_window_split(const pscwin_layer_desc* d, const pscwin_band* b, int32_t* top, int32_t* bot,
+                             int32_t* nwy) {
+  BandGeo g;
+  int rc = band_check(d, b, &g);
+  if (rc) return rc;
+  if (!top || !bot || !nwy) return PSCWIN_ERR_SHAPE;
+  int t, bo, n;
+  pscwin::band_window_rows(d, b, &t, &bo, &n);
+  *top = t;
+  *bot = bo;
+  *nwy = n;
+  return PSCWIN_OK;
+}
+
+int pscwin_band_attn_windows(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                             void* ws, size_t ws_bytes, int32_t wy_begin, int32_t wy_end, void* stream) {
+  if (wy_begin < 0 || wy_end < wy_begin) return PSCWIN_ERR_SHAPE;
+  if (wy_end == wy_begin) return PSCWIN_OK;
+  return pscwin::band_attention(d, b, wt, ws, ws_bytes, wy_begin, wy_end, 0, stream);
+}
+
+int pscwin_band_out_proj(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                         const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+  return pscwin::band_out_proj(d, b, wt, x_band, x_out, ws, ws_bytes, stream);
+}
+
+int pscwin_band_attn_end(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                         const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!wt || !x_band || !x_out || !wt->w_o || !wt->b_o) return PSCWIN_ERR_SHAPE;
+  int rc = band_attention(d, b, wt, ws, ws_bytes, 0, 0, 0, stream);
+  if (rc) return rc;
+  return band_out_proj(d, b, wt, x_band, x_out, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

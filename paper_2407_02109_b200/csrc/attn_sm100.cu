@@ -33,6 +33,7 @@ struct AttnKArgs {
   const __nv_bfloat16* ky;  // [Hp][heads][d/2]  rotated second half at y = Y (index Y + pt)
   const __nv_bfloat16* vp;  // [heads][d]
   int Wp, Hp;
+  int win0, nw_run;         // windows [win0, win0 + nw_run) of every image (a window-row range; all by default)
   __nv_bfloat16* out;       // [B,H,W,C]
 };
 
@@ -48,8 +49,8 @@ __global__ void __launch_bounds__(ATT_THREADS, 2)
 
   const int qt = blockIdx.x;
   const int h = blockIdx.y;
-  const int b = blockIdx.z / p.nw;
-  const int win = blockIdx.z - b * p.nw;
+  const int b = blockIdx.z / p.nw_run;
+  const int win = p.win0 + (blockIdx.z - b * p.nw_run);
   const int wy = win / p.nwx, wx = win - (win / p.nwx) * p.nwx;
   const int X0 = wx * p.w - p.pl;
   const int Y0 = wy * p.w - p.pt;
@@ -364,8 +365,8 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
   }
   // windows of <= 256 slots: persistent warp-specialised kernel (attn_sm100_ws.cu); PSCWIN_ATTN_V1=1 forces this
   // file's one-CTA-per-(q tile, head, window) kernel, which also serves larger windows.
-  const char* force_v1 = getenv("PSCWIN_ATTN_V1");
-  if (p.n_tiles <= 2 && !(force_v1 && force_v1[0] == '1'))
+  static const bool force_v1 = env_knob("PSCWIN_ATTN_V1", 0) == 1;
+  if (p.n_tiles <= 2 && !force_v1)
     return launch_window_attention_ws(a, p.kx, p.ky, p.vp, p.patch, stream);
   CUtensorMap tmQKV;
   const uint64_t dq[5] = {(uint64_t)d, (uint64_t)3 * a.heads, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.B};
@@ -377,21 +378,20 @@ int launch_window_attention(const AttnArgs& a, cudaStream_t stream) {
   if (rc) return rc;
   p.out = reinterpret_cast<__nv_bfloat16*>(a.out);
   const size_t smem = 1024 + 3 * 128 * d * 2 + 128 * 256 + 64;
-  dim3 grid(p.n_tiles, a.heads, a.B * p.nw);
+  {
+    const int nwy = p.nw / p.nwx;
+    const int wy0 = a.wy_end > 0 ? a.wy_begin : 0, wy1 = a.wy_end > 0 ? (a.wy_end < nwy ? a.wy_end : nwy) : nwy;
+    if (wy0 < 0 || wy0 >= wy1) return 0;
+    p.win0 = wy0 * p.nwx;
+    p.nw_run = (wy1 - wy0) * p.nwx;
+  }
+  dim3 grid(p.n_tiles, a.heads, a.B * p.nw_run);
   PSCWIN_PROF("window_attention", stream);
   if (d == 64) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(window_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
-    }
+    func_smem_once((const void*)window_attn_kernel<64>, (int)smem);
     launch_k(window_attn_kernel<64>, dim3(grid), dim3(ATT_THREADS), smem, stream, tmQKV, p);
   } else {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(window_attn_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      set = true;
-    }
+    func_smem_once((const void*)window_attn_kernel<32>, (int)smem);
     launch_k(window_attn_kernel<32>, dim3(grid), dim3(ATT_THREADS), smem, stream, tmQKV, p);
   }
   return (int)cudaGetLastError();

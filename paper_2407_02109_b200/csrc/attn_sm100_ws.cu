@@ -44,6 +44,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct AttnWsArgs {
   int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
   int rpt, n_tiles, tile_slots, n_items;
+  int win0, nw_run;  // windows [win0, win0 + nw_run) of every image are run (a window-row range; all by default)
   int lockstep;  // -1: automatic (few items per CTA), 0 / 1 forced (PSCWIN_ATTN_LOCKSTEP knob)
   int tma_out;  // 1: O tiles staged in smem and TMA-stored; 0: 16-byte global stores of the real rows
   float sl2;
@@ -106,8 +107,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   auto decode = [&](int item, int& b, int& h, int& X0, int& Y0) {
     h = item % p.heads;
     const int r = item / p.heads;
-    const int win = r % p.nw;
-    b = r / p.nw;
+    const int win = p.win0 + r % p.nw_run;
+    b = r / p.nw_run;
     const int wy = win / p.nwx, wx = win - wy * p.nwx;
     X0 = wx * p.w - p.pl;
     Y0 = wy * p.w - p.pt;
@@ -525,7 +526,14 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   p.rpt = w * w <= 128 ? w : 128 / w;
   p.n_tiles = w / p.rpt;
   p.tile_slots = w * p.rpt;
-  p.n_items = a.B * p.nw * a.heads;
+  {
+    const int nwy = p.nw / p.nwx;
+    const int wy0 = a.wy_end > 0 ? a.wy_begin : 0, wy1 = a.wy_end > 0 ? (a.wy_end < nwy ? a.wy_end : nwy) : nwy;
+    if (wy0 < 0 || wy0 >= wy1) return 0;  // empty range: nothing to run
+    p.win0 = wy0 * p.nwx;
+    p.nw_run = (wy1 - wy0) * p.nwx;
+  }
+  p.n_items = a.B * p.nw_run * a.heads;
   p.sl2 = 1.4426950408889634f / sqrtf((float)d);
   p.kx = reinterpret_cast<const __nv_bfloat16*>(kx);
   p.ky = reinterpret_cast<const __nv_bfloat16*>(ky);
@@ -537,7 +545,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   static const int lockstep_knob = getenv("PSCWIN_ATTN_LOCKSTEP") ? atoi(getenv("PSCWIN_ATTN_LOCKSTEP")) : -1;
   p.lockstep = lockstep_knob;
   static unsigned long long* dbg_buf = nullptr;
-  const char* tl = getenv("PSCWIN_ATTN_TIMELINE");
+  static const char* tl = getenv("PSCWIN_ATTN_TIMELINE");  // debug knob, read once
   if (tl) {
     if (!dbg_buf) cudaMalloc(&dbg_buf, 148 * 128 * sizeof(unsigned long long));
     cudaMemsetAsync(dbg_buf, 0, 148 * 128 * sizeof(unsigned long long), stream);
@@ -563,7 +571,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
   PSCWIN_PROF("window_attention", stream);
   auto launch = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    func_smem_once((const void*)kern, (int)smem);
     launch_k(kern, dim3(grid), dim3(WS_THREADS), smem, stream, tmQKV, tmO, p);
   };
   const bool masked = p.pad_mode == 1;

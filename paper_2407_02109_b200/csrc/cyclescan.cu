@@ -1088,9 +1088,9 @@ static ScanPlan plan_scan_p(int B, int L, int D, int N, int R, int k, int P) {
   // x_proj split-K (measured: the partial round trip costs more than the idle SMs it fills, so off by default)
   const int m_tiles = (int)((rows + 127) / 128);
   s.xsplits = 1;
-  if (const char* e = getenv("PSCWIN_XPROJ_SPLITS")) {  // tuning knob (1..8)
-    const int v = atoi(e);
-    if (v >= 1 && v <= 8) s.xsplits = v;
+  static const int xsplit_knob = env_knob("PSCWIN_XPROJ_SPLITS", 1);  // tuning knob (1..8)
+  if (xsplit_knob >= 1 && xsplit_knob <= 8) {
+    s.xsplits = xsplit_knob;
     if (s.xsplits > D / 64) s.xsplits = D / 64 > 0 ? D / 64 : 1;  // every split needs >= 1 K block (D / 64 of them)
   }
   s.partial = off;

@@ -52,33 +52,30 @@ size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* d, int32_t row_begin
 
 static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x_band,
                            void* x_band_out, int32_t row_begin, int32_t row_end, void* nccl_comm, void* ws,
-                           size_t ws_bytes, void* stream);
+                           size_t ws_bytes, void* stream, void* comm_stream);
 
 int pscwin_dist_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x_band,
                         void* x_band_out, int32_t row_begin, int32_t row_end, void* nccl_comm, void* ws,
-                        size_t ws_bytes, void* stream) {
-  if (stream) return dist_forward_on(d, wt, x_band, x_band_out, row_begin, row_end, nccl_comm, ws, ws_bytes, stream);
+                        size_t ws_bytes, void* stream, void* comm_stream) {
+  if (stream)
+    return dist_forward_on(d, wt, x_band, x_band_out, row_begin, row_end, nccl_comm, ws, ws_bytes, stream,
+                           comm_stream);
   // the legacy default stream: NCCL's send / recv to self have been seen to stall there, so the layer runs on a
-  // library-owned non-blocking stream joined to it by events (same stream order for the caller)
-  static cudaStream_t own = nullptr;
-  static cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-  if (!own) {
-    if (cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming) != cudaSuccess)
-      return PSCWIN_ERR_CUDA;
-  }
-  if (cudaEventRecord(ev_in, 0) != cudaSuccess || cudaStreamWaitEvent(own, ev_in, 0) != cudaSuccess)
+  // library-owned non-blocking stream (per thread and device, aux_stream slot 1) joined to it by events
+  pscwin::AuxStream* own = pscwin::aux_stream(1);
+  if (!own) return PSCWIN_ERR_CUDA;
+  if (cudaEventRecord(own->fork, 0) != cudaSuccess || cudaStreamWaitEvent(own->s, own->fork, 0) != cudaSuccess)
     return PSCWIN_ERR_CUDA;
-  const int rc = dist_forward_on(d, wt, x_band, x_band_out, row_begin, row_end, nccl_comm, ws, ws_bytes, own);
-  if (cudaEventRecord(ev_out, own) != cudaSuccess || cudaStreamWaitEvent(0, ev_out, 0) != cudaSuccess)
+  const int rc = dist_forward_on(d, wt, x_band, x_band_out, row_begin, row_end, nccl_comm, ws, ws_bytes, own->s,
+                                 comm_stream);
+  if (cudaEventRecord(own->join, own->s) != cudaSuccess || cudaStreamWaitEvent(0, own->join, 0) != cudaSuccess)
     return PSCWIN_ERR_CUDA;
   return rc;
 }
 
 static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x_band,
                            void* x_band_out, int32_t row_begin, int32_t row_end, void* nccl_comm, void* ws,
-                           size_t ws_bytes, void* stream) {
+                           size_t ws_bytes, void* stream, void* comm_stream) {
   if (!nccl_comm) return PSCWIN_ERR_SHAPE;
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
   int rank = 0, world = 1;
@@ -95,6 +92,9 @@ static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weight
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int prev = (rank - 1 + world) % world, next = (rank + 1) % world;
   if (d->cycle_scan) {
+    // The two scan exchanges are latency-sized (k - 1 xin rows; one record of D (N + 2) floats per rank) and the
+    // work after each depends on them (the band's first conv rows; every chunk's entry state), so they stay on the
+    // compute stream.
     rc = pscwin_band_scan_begin(d, &b, wt, x_band, ws, ws_bytes, stream);
     if (rc) return rc;
     // conv history ring: rank g -> g+1 (rank 0 receives the global sequence tail from the last rank)
@@ -113,13 +113,38 @@ static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weight
   rc = pscwin_band_attn_begin(d, &b, wt, x_band, ws, ws_bytes, stream);
   if (rc) return rc;
   // QKV halo rows of the shifted windows straddling the band edges (sizes are 0 for plain layers / image edges)
-  if (io.send_prev_bytes || io.send_next_bytes || io.recv_prev_bytes || io.recv_next_bytes) {
+  const bool halo = io.send_prev_bytes || io.send_next_bytes || io.recv_prev_bytes || io.recv_next_bytes;
+  cudaStream_t c = reinterpret_cast<cudaStream_t>(comm_stream);
+  pscwin::AuxStream* ev = (halo && c && c != s) ? pscwin::aux_stream(2) : nullptr;
+  cudaStream_t hs = ev ? c : s;  // the stream the halo exchange runs on
+  if (ev) {  // the exchange waits for this band's QKV rows; interior windows run meanwhile on the compute stream
+    if (cudaEventRecord(ev->fork, s) != cudaSuccess || cudaStreamWaitEvent(c, ev->fork, 0) != cudaSuccess)
+      return PSCWIN_ERR_CUDA;
+  }
+  if (halo) {
     if (ncclGroupStart() != ncclSuccess) return PSCWIN_ERR_CUDA;
-    if (io.send_prev_bytes) ncclSend(at(ws, io.send_prev), io.send_prev_bytes, ncclUint8, rank - 1, comm, s);
-    if (io.send_next_bytes) ncclSend(at(ws, io.send_next), io.send_next_bytes, ncclUint8, rank + 1, comm, s);
-    if (io.recv_prev_bytes) ncclRecv(at(ws, io.recv_prev), io.recv_prev_bytes, ncclUint8, rank - 1, comm, s);
-    if (io.recv_next_bytes) ncclRecv(at(ws, io.recv_next), io.recv_next_bytes, ncclUint8, rank + 1, comm, s);
+    if (io.send_prev_bytes) ncclSend(at(ws, io.send_prev), io.send_prev_bytes, ncclUint8, rank - 1, comm, hs);
+    if (io.send_next_bytes) ncclSend(at(ws, io.send_next), io.send_next_bytes, ncclUint8, rank + 1, comm, hs);
+    if (io.recv_prev_bytes) ncclRecv(at(ws, io.recv_prev), io.recv_prev_bytes, ncclUint8, rank - 1, comm, hs);
+    if (io.recv_next_bytes) ncclRecv(at(ws, io.recv_next), io.recv_next_bytes, ncclUint8, rank + 1, comm, hs);
     if (ncclGroupEnd() != ncclSuccess) return PSCWIN_ERR_CUDA;
+  }
+  if (ev) {
+    if (cudaEventRecord(ev->join, c) != cudaSuccess) return PSCWIN_ERR_CUDA;
+    int top = 0, bot = 0, nwy = 0;
+    pscwin::band_window_rows(d, &b, &top, &bot, &nwy);
+    if (bot > top) {  // interior window rows: no halo row inside
+      rc = pscwin::band_attention(d, &b, wt, ws, ws_bytes, top, bot, 0, stream);
+      if (rc) return rc;
+    }
+    if (cudaStreamWaitEvent(s, ev->join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
+    // the window rows that read halo rows (the pad tables, if any, were written by the interior launch)
+    const int tab = bot > top ? 1 : 0;
+    if (top > 0 && (rc = pscwin::band_attention(d, &b, wt, ws, ws_bytes, 0, top, tab, stream))) return rc;
+    if (bot < nwy && bot >= top &&
+        (rc = pscwin::band_attention(d, &b, wt, ws, ws_bytes, bot, nwy, tab || top > 0, stream)))
+      return rc;
+    return pscwin::band_out_proj(d, &b, wt, x_band, x_band_out, ws, ws_bytes, stream);
   }
   return pscwin_band_attn_end(d, &b, wt, x_band, x_band_out, ws, ws_bytes, stream);
 }

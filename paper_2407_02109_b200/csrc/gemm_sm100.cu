@@ -629,10 +629,8 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
         return ((tiles + slots - 1) / slots) * (bn + 32);
       };
       p.BN = cost(256) <= cost(128) ? 256 : 128;
-      if (const char* e = getenv("PSCWIN_GEMM_BN")) {  // tuning knob for the multi-tile case: 128 or 256
-        const int v = atoi(e);
-        if (v == 128 || v == 256) p.BN = v;
-      }
+      static const int bn_knob = env_knob("PSCWIN_GEMM_BN", 0);  // tuning knob for the multi-tile case: 128 or 256
+      if (bn_knob == 128 || bn_knob == 256) p.BN = bn_knob;
     }
   }
   if (pair && (p.BN % 16)) return -2;
@@ -656,8 +654,8 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (rc) return rc;
   memset(&tmOut, 0, sizeof(tmOut));
   // f32 outputs without split-K go through a TMA store when the row stride allows it (16-byte multiple)
-  p.f32_tma = (p.epi == EPI_STORE_F32 && p.splits <= 1 && (p.ldo * 4) % 16 == 0 && !getenv("PSCWIN_GEMM_F32_DIRECT"))
-                  ? 1 : 0;
+  static const bool f32_direct = getenv("PSCWIN_GEMM_F32_DIRECT") != nullptr;  // A/B knob
+  p.f32_tma = (p.epi == EPI_STORE_F32 && p.splits <= 1 && (p.ldo * 4) % 16 == 0 && !f32_direct) ? 1 : 0;
   if (p.f32_tma) {
     rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p.N, p.M, (uint64_t)p.ldo * 4, 32, 32,
                       CU_TENSOR_MAP_SWIZZLE_128B);  // one 32 x 32 box per epilogue warp
@@ -676,14 +674,12 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
                       CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
+  {
     const void* fns[8] = {(const void*)gemm_bf16_kernel<false, EK_PLAIN>, (const void*)gemm_bf16_kernel<false, EK_ROPE>,
                           (const void*)gemm_bf16_kernel<false, EK_GELU>, (const void*)gemm_bf16_kernel<false, EK_F32>,
                           (const void*)gemm_bf16_kernel<true, EK_PLAIN>, (const void*)gemm_bf16_kernel<true, EK_ROPE>,
                           (const void*)gemm_bf16_kernel<true, EK_GELU>, (const void*)gemm_bf16_kernel<true, EK_F32>};
-    for (const void* f : fns) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM_MAX);
-    attr_set = true;
+    for (const void* f : fns) func_smem_once(f, (int)GEMM_SMEM_MAX);
   }
   const int ek = p.epi == EPI_QKV_ROPE ? EK_ROPE : (p.gelu ? EK_GELU : (p.epi == EPI_STORE_F32 ? EK_F32 : EK_PLAIN));
   const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages, f32o);

@@ -11,6 +11,13 @@
 
 namespace pscwin {
 
+// Tuning knob from the environment, read ONCE per call site (`static const int v = env_knob(...)`): the A/B knobs
+// are fixed for the life of the process, so a workspace query and the run it sizes always see the same plan.
+inline int env_knob(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
 inline bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
@@ -47,8 +54,8 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k_even(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                                  Args&&... args) {
-  const char* e = getenv("PSCWIN_PDL_EVEN");  // tuning knob: 1 = PDL for these launches too
-  return launch_kernel(e && e[0] == '1', kern, grid, block, smem, s, std::forward<Args>(args)...);
+  static const bool pdl_even = env_knob("PSCWIN_PDL_EVEN", 0) == 1;  // tuning knob: 1 = PDL for these launches too
+  return launch_kernel(pdl_even, kern, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 }  // namespace pscwin

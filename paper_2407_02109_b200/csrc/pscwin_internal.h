@@ -50,6 +50,26 @@ struct GemmArgs {
 
 // host helpers (abi.cu)
 int num_sms();
+// A helper stream with a fork / join event pair, private to the calling host thread and to the current device
+// (thread_local, indexed by device): concurrent callers on other threads never share its events, and one process
+// can drive several GPUs. Slot 0: the side stream of the weight-only pad work; slot 1: the default-stream proxy of
+// pscwin_dist_forward; slot 2: the halo-overlap events of pscwin_dist_forward. Created on first use, never
+// destroyed (one set per thread and device). nullptr when creation fails.
+struct AuxStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+};
+AuxStream* aux_stream(int slot);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `fn` on the current device, once per (device,
+// function) and only when `bytes` exceeds what was set before (thread-safe; abi.cu).
+void func_smem_once(const void* fn, int bytes);
+// row-band attention phases (abi.cu), used by pscwin_dist_forward to overlap the QKV halo exchange
+int band_attention(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt, void* ws,
+                   size_t ws_bytes, int wy0, int wy1, int tables_ready, void* stream);
+void band_window_rows(const pscwin_layer_desc* d, const pscwin_band* b, int* top, int* bot, int* nwy);
+int band_out_proj(const pscwin_layer_desc* d, const pscwin_band* b, const pscwin_layer_weights* wt,
+                  const void* x_band, void* x_out, void* ws, size_t ws_bytes, void* stream);
 int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint64_t inner, uint64_t outer,
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
 int make_tmap_5d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const uint64_t dims[5],
@@ -74,6 +94,7 @@ struct AttnArgs {
   void* out;             // [B,H,W,C] bf16
   void* pad_tab;         // workspace for rotated pad K halves + V (bf16)
   int tables_ready;      // 1: pad_tab was already filled by launch_pad_tables (e.g. on a side stream)
+  int wy_begin, wy_end;  // padded-grid window rows to run, [wy_begin, wy_end); wy_end <= 0: all (row-band overlap)
 };
 size_t attn_pad_table_bytes(int H, int W, int C, int w);
 // rotated pad-key / pad-value tables of a shifted LEARNABLE layer (depends only on qkv_pad and the geometry)

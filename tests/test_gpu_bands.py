@@ -57,6 +57,33 @@ def test_bands_equal_whole_image(pl, cfg, world):
     assert layer_gate(host(banded), x, ref, n_residual(cfg)) < 1.0
 
 
+@pytest.mark.parametrize("cfg,world", [(synth.tiny(H=32, W=16), 4), (synth.tiny(H=40, W=24, shift_x=3, shift_y=5), 3),
+                                       (synth.tiny(H=34, W=16, cycle_scan=1), 3), (synth.vitb(64, B=1), 4)],
+                         ids=["S4", "asym3", "ragged_cs3", "vitb4"])
+def test_bands_overlap_schedule_equals_whole_image(pl, cfg, world):
+    # the pscwin_dist_forward overlap schedule: interior window rows before the halo arrives, band-edge window rows
+    # after, then out-proj — stitched bit-identical to the one-launch band schedule (and the whole image for
+    # attention layers); the interior rows must not read any halo row: the halo buffers hold garbage until copied
+    import torch
+    from paper_2407_02109_b200.bands import LoopbackBands
+    x, w = synth.make_input(cfg, scale=X_SCALE), synth.make_weights(cfg)
+    dw = dev_weights(w, cfg)
+    desc = pl.LayerDesc.from_config(cfg)
+    xd = dev(x)
+    plain = LoopbackBands(desc, dw, world)(xd)
+    ov = LoopbackBands(desc, dw, world, overlap=True)
+    for layer in ov.layers:
+        layer.ws.fill_(0x7F)   # NaN-ish bf16 garbage everywhere, including the halo rows, before the first call
+    got = ov(xd)
+    torch.cuda.synchronize()
+    assert torch.equal(got, plain)
+    tops = [layer.window_split() for layer in ov.layers]
+    assert all(0 <= t <= b <= n for t, b, n in tops)
+    assert tops[0][0] == 0 and tops[-1][1] == tops[-1][2]          # image edges have no halo
+    if not cfg.cycle_scan:
+        assert torch.equal(got, pl.PSCWinLayer(desc, dw)(xd))
+
+
 def test_band_contract(pl):
     from paper_2407_02109_b200.bands import BandLayer
     cfg = synth.tiny(H=32, W=16)
