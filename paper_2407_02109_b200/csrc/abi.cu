@@ -70,11 +70,26 @@ int make_tmap_5d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, const
   return r == CUDA_SUCCESS ? 0 : -11;
 }
 
+int ln_gemm(const void* x, const float* g, const float* be, float eps, const void* W, GemmArgs a, void* u,
+            const LnFold* lnf, cudaStream_t s) {
+  if (!lnf) {
+    int rc = launch_layer_norm(x, a.M, a.K, g, be, eps, 0, u, s);
+    if (rc) return rc;
+    return launch_gemm_bf16(u, W, a, s);
+  }
+  int rc = launch_row_stats(x, a.M, a.K, eps, lnf->stats, s);
+  if (rc) return rc;
+  if (lnf->ready && cudaStreamWaitEvent(s, lnf->ready, 0) != cudaSuccess) return (int)cudaErrorUnknown;
+  a.bias = lnf->bias;
+  a.ln_stats = lnf->stats;
+  a.ln_colsum = lnf->colsum;
+  return launch_gemm_bf16(x, lnf->wf, a, s);
+}
+
 int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts_v, void* x, void* u, void* h,
-             cudaStream_t s) {
+             cudaStream_t s, const LnFold* lnf) {
   const pscwin_layer_weights* w = reinterpret_cast<const pscwin_layer_weights*>(wts_v);
-  int rc = launch_layer_norm(x, T, C, (const float*)w->ln2_g, (const float*)w->ln2_b, eps, 0, u, s);
-  if (rc) return PSCWIN_ERR_CUDA;
+  int rc;
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.prof_name = "gemm_fc1_gelu";
@@ -88,7 +103,8 @@ int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts_v, void*
   a.epi = EPI_STORE_BF16;
   a.bias = (const float*)w->b_fc1;
   a.gelu = 1;
-  if (launch_gemm_bf16(u, w->w_fc1, a, s)) return PSCWIN_ERR_CUDA;
+  rc = ln_gemm(x, (const float*)w->ln2_g, (const float*)w->ln2_b, eps, w->w_fc1, a, u, lnf, s);
+  if (rc) return PSCWIN_ERR_CUDA;
   memset(&a, 0, sizeof(a));
   a.prof_name = "gemm_fc2";
   a.M = (int)T;
@@ -164,7 +180,31 @@ bool ffn_weights_ok(const pscwin_layer_weights* w) {
 // Workspace layout shared by qkv_project / window_attention / forward.
 struct LayerWs {
   size_t u, qkv, qkv_pad, O, pad_tab, xz, g, h, scan, total;
+  size_t stats, f_qkv, f_in, f_fc1;  // folded-LayerNorm scratch: row stats [T] float2; W' | s | c per projection
 };
+
+// LayerNorm folded into the projection after it (rowops.cu; PSCWIN_LN_FOLD=0 restores the separate LayerNorm
+// pass: A/B knob, read once)
+bool ln_fold_enabled() {
+  static const bool on = env_knob("PSCWIN_LN_FOLD", 1) != 0;
+  return on;
+}
+size_t fold_bytes(size_t N, size_t K) { return align256(N * K * 2) + align256(N * 4) * 2; }
+LnFold fold_at(void* ws, size_t off, size_t N, size_t K, size_t stats_off) {
+  LnFold f;
+  uint8_t* b = reinterpret_cast<uint8_t*>(ws) + off;
+  f.wf = b;
+  f.colsum = reinterpret_cast<const float*>(b + align256(N * K * 2));
+  f.bias = reinterpret_cast<const float*>(b + align256(N * K * 2) + align256(N * 4));
+  f.stats = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(ws) + stats_off);
+  f.ready = nullptr;
+  return f;
+}
+int fold_launch(const LnFold& f, const void* W, int N, int K, const void* g, const void* be, const void* bias,
+                cudaStream_t s) {
+  return launch_ln_fold(W, N, K, (const float*)g, (const float*)be, (const float*)bias, const_cast<void*>(f.wf),
+                        const_cast<float*>(f.colsum), const_cast<float*>(f.bias), s);
+}
 
 LayerWs plan_layer(const pscwin_layer_desc* d) {
   LayerWs w;
@@ -201,6 +241,10 @@ LayerWs plan_layer(const pscwin_layer_desc* d) {
     sd.window = d->window;
     w.scan = take(pscwin_scan_workspace_bytes(&sd));
   }
+  w.stats = take(T * 8);
+  w.f_qkv = take(fold_bytes(3 * C, C));
+  w.f_in = d->cycle_scan ? take(fold_bytes(2 * (size_t)d->ssm_expand * C, C)) : 0;
+  w.f_fc1 = d->mlp_hidden > 0 ? take(fold_bytes(d->mlp_hidden, C)) : 0;
   w.total = off;
   return w;
 }
@@ -208,12 +252,11 @@ LayerWs plan_layer(const pscwin_layer_desc* d) {
 uint8_t* wsp(void* base, size_t off) { return reinterpret_cast<uint8_t*>(base) + off; }
 
 int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, const void* x, void* qkv,
-                     float* qkv_pad, void* ws, const LayerWs& L, cudaStream_t s) {
+                     float* qkv_pad, void* ws, const LayerWs& L, cudaStream_t s, const LnFold* lnf = nullptr) {
   const long long T = (long long)d->B * d->H * d->W;
   const int C = d->C;
   void* u = wsp(ws, L.u);
-  int rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, 0, u, s);
-  if (rc) return rc;
+  int rc;
   const int dh = C / d->heads;
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -232,7 +275,7 @@ int qkv_project_impl(const pscwin_layer_desc* d, const pscwin_layer_weights* wt,
   a.Wgrid = d->W;
   a.C = C;
   a.d_head = dh;
-  rc = launch_gemm_bf16(u, wt->w_qkv, a, s);
+  rc = ln_gemm(x, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, wt->w_qkv, a, u, lnf, s);
   if (rc) return rc;
   if (qkv_pad && wt->pad) {
     rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, s);
@@ -488,32 +531,53 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   cudaStream_t s = (cudaStream_t)stream;
   const long long T = (long long)d->B * d->H * d->W;
   const int C = d->C;
-  const void* x = x_in;
-  if (d->cycle_scan) {
-    rc = cycle_scan_module(d, wt, x_in, x_out, ws, L.u, L.xz, L.g, L.scan, L.total - L.scan, s);
-    if (rc) return rc;
-    x = x_out;
-  }
   void* qkv = wsp(ws, L.qkv);
   float* qkv_pad = reinterpret_cast<float*>(wsp(ws, L.qkv_pad));
   void* O = wsp(ws, L.O);
   const bool learn_pad = shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE;
-  AuxStream* sd = learn_pad ? side() : nullptr;
+  const bool fold = ln_fold_enabled();
+  const int D2 = 2 * d->ssm_expand * C;
+  // Weight-only work on the side stream, forked at the start of the layer: the LayerNorm folds of the projections
+  // (cycle-scan in_proj, QKV, fc1) and the learnable pad token's projection + rotated tables. Each consumer waits
+  // on its own event, so the fold of a projection overlaps everything before it.
+  AuxStream* sd = (learn_pad || fold) ? side() : nullptr;
   const bool fork = sd != nullptr;
-  if (fork) {  // weight-only pad work overlaps LN1 + the QKV GEMM (see side())
-    if (cudaEventRecord(sd->fork, s) != cudaSuccess || cudaStreamWaitEvent(sd->s, sd->fork, 0) != cudaSuccess)
-      return PSCWIN_ERR_CUDA;
-    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, sd->s);
+  cudaStream_t aux = fork ? sd->s : s;
+  LnFold f_in = fold_at(ws, L.f_in, D2, C, L.stats), f_qkv = fold_at(ws, L.f_qkv, 3 * C, C, L.stats);
+  LnFold f_fc1 = fold_at(ws, L.f_fc1, d->mlp_hidden, C, L.stats);
+  if (fork && (cudaEventRecord(sd->fork, s) != cudaSuccess || cudaStreamWaitEvent(sd->s, sd->fork, 0) != cudaSuccess))
+    return PSCWIN_ERR_CUDA;
+  if (fold && d->cycle_scan) {
+    if ((rc = fold_launch(f_in, wt->w_in, D2, C, wt->lns_g, wt->lns_b, nullptr, aux))) return status_from(rc);
+    if (fork && cudaEventRecord(f_in.ready = sd->ev[0], aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  }
+  if (fold) {
+    if ((rc = fold_launch(f_qkv, wt->w_qkv, 3 * C, C, wt->ln1_g, wt->ln1_b, wt->b_qkv, aux))) return status_from(rc);
+    if (fork && cudaEventRecord(f_qkv.ready = sd->ev[1], aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  }
+  if (learn_pad && fork) {  // the pad work overlaps everything up to the attention kernel
+    rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, aux);
     if (rc) return status_from(rc);
     AttnArgs pa = attn_args(d, qkv, qkv_pad, O, wsp(ws, L.pad_tab));
-    rc = launch_pad_tables(pa, sd->s);
-    if (rc) return status_from(rc);
-    if (cudaEventRecord(sd->join, sd->s) != cudaSuccess) return PSCWIN_ERR_CUDA;
+    if ((rc = launch_pad_tables(pa, aux))) return status_from(rc);
+    if (cudaEventRecord(sd->join, aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
   }
-  rc = qkv_project_impl(d, wt, x, qkv, (learn_pad && !fork) ? qkv_pad : nullptr, ws, L, s);
+  if (fold && d->mlp_hidden > 0) {
+    if ((rc = fold_launch(f_fc1, wt->w_fc1, d->mlp_hidden, C, wt->ln2_g, wt->ln2_b, wt->b_fc1, aux)))
+      return status_from(rc);
+    if (fork && cudaEventRecord(f_fc1.ready = sd->ev[2], aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  }
+  const void* x = x_in;
+  if (d->cycle_scan) {
+    rc = cycle_scan_module(d, wt, fold ? &f_in : nullptr, x_in, x_out, ws, L.u, L.xz, L.g, L.scan,
+                           L.total - L.scan, s);
+    if (rc) return rc;
+    x = x_out;
+  }
+  rc = qkv_project_impl(d, wt, x, qkv, (learn_pad && !fork) ? qkv_pad : nullptr, ws, L, s, fold ? &f_qkv : nullptr);
   if (rc) return status_from(rc);
-  if (fork && cudaStreamWaitEvent(s, sd->join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
-  rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s, fork ? 1 : 0);
+  if (learn_pad && fork && cudaStreamWaitEvent(s, sd->join, 0) != cudaSuccess) return PSCWIN_ERR_CUDA;
+  rc = attention_impl(d, qkv, qkv_pad, O, ws, L, s, (learn_pad && fork) ? 1 : 0);
   if (rc) return status_from(rc);
   GemmArgs a;
   memset(&a, 0, sizeof(a));
@@ -532,7 +596,7 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   rc = launch_gemm_bf16(O, wt->w_o, a, s);
   if (rc) return status_from(rc);
   if (d->mlp_hidden > 0)
-    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, L.u), wsp(ws, L.h), s);
+    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, L.u), wsp(ws, L.h), s, fold ? &f_fc1 : nullptr);
   return PSCWIN_OK;
 }
 

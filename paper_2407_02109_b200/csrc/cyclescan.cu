@@ -1409,8 +1409,8 @@ static int run_cycle_scan_ordered(int B, int H, int W, int order, int window, in
   return cudaGetLastError() == cudaSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA;
 }
 
-int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, void* x_out, void* ws, size_t off_u,
-                      size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s) {
+int cycle_scan_module(const void* desc_v, const void* wts_v, const LnFold* lnf, const void* x_in, void* x_out, void* ws,
+                      size_t off_u, size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s) {
   const pscwin_layer_desc* d = reinterpret_cast<const pscwin_layer_desc*>(desc_v);
   const pscwin_layer_weights* w = reinterpret_cast<const pscwin_layer_weights*>(wts_v);
   if (!w->lns_g || !w->lns_b || !w->w_in || !w->conv_w || !w->conv_b || !w->w_x || !w->w_dt || !w->b_dt ||
@@ -1428,9 +1428,7 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   __nv_bfloat16* u = reinterpret_cast<__nv_bfloat16*>(base + off_u);
   __nv_bfloat16* xz = reinterpret_cast<__nv_bfloat16*>(base + off_xz);
   __nv_bfloat16* g = reinterpret_cast<__nv_bfloat16*>(base + off_g);
-  // a1: u0 = LN_s(x); [xin, z] = u0 W_in^T
-  rc = launch_layer_norm(x_in, T, C, (const float*)w->lns_g, (const float*)w->lns_b, d->ln_eps, 0, u, s);
-  if (rc) return PSCWIN_ERR_CUDA;
+  // a1: u0 = LN_s(x); [xin, z] = u0 W_in^T (the LayerNorm folded into the projection when lnf is given)
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.prof_name = "gemm_in_proj";
@@ -1443,7 +1441,7 @@ int cycle_scan_module(const void* desc_v, const void* wts_v, const void* x_in, v
   a.ldo = 2 * D;
   a.epi = EPI_STORE_BF16;
   a.silu_col = D;  // the z half leaves the epilogue as the output gate SiLU(z)
-  rc = launch_gemm_bf16(u, w->w_in, a, s);
+  rc = ln_gemm(x_in, (const float*)w->lns_g, (const float*)w->lns_b, d->ln_eps, w->w_in, a, u, lnf, s);
   if (rc) return PSCWIN_ERR_CUDA;
   // a2: cycle scan -> g = sum over copies of y * SiLU(z)
   rc = run_cycle_scan_ordered(d->B, d->H, d->W, d->scan_order, d->window, D, N, R, d->ssm_conv, d->bbar_mode, xz,

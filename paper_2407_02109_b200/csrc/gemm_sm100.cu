@@ -33,7 +33,7 @@ __host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid, bool f32 
   // residual with BN > 128 ("in place"): ONE set of residual chunks, the output overwrites them and is stored from
   // there (the two output staging boxes stay allocated but unused; the layout offsets do not change).
   const size_t res = resid ? (BN > 128 ? nch : 2 * nch) * STAGE_OUT_BYTES : (f32 ? 2 * STAGE_OUT_BYTES : 0);
-  return 1024 + 2 * STAGE_OUT_BYTES + res + 2 * 256 * 4 + 256;
+  return 1024 + 2 * STAGE_OUT_BYTES + res + 4 * 256 * 4 + 256;  // bias + LN column sums, double-buffered
 }
 __host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
   return A_STAGE_BYTES + (size_t)(pair ? BN / 2 : BN) * BK * 2;
@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const bool res_inplace = resid_tma && BN > 128;
   float* s_bias = reinterpret_cast<float*>(
       s_res + (resid_tma ? (res_inplace ? 1 : 2) * nch * STAGE_OUT_BYTES
-                         : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 2 * 256);
+                         : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256] bias, then [2][256] LN s_n
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 4 * 256);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -339,17 +339,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // bias of the tile's columns staged once in shared memory (read back as broadcasts), double-buffered by
       // accumulator so the next tile's staging never races this tile's readers
       float* sb = s_bias + acc * 256;
+      float* sc = s_bias + 512 + acc * 256;              // LN column sums s_n (folded LayerNorm)
+      const bool ln = EK != EK_F32 && p.ln_stats != nullptr;
+      float ln_r = 1.f, ln_nmr = 0.f;                    // rstd and -mu * rstd of this row
+      if (ln && row_ok) {
+        const float2 st = __ldg(p.ln_stats + row);
+        ln_r = st.y;
+        ln_nmr = -st.x * st.y;
+      }
       if (p.bias && !f32_tma) {  // (f32 tiles read the bias straight from L1: no CTA-wide barrier in that path)
         if (etid < BN / 4) {
           const int c = n0 + 4 * etid;
-          float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
           if (c + 4 <= p.N) {
             b4 = __ldg(reinterpret_cast<const float4*>(p.bias + c));
+            if (ln) s4 = __ldg(reinterpret_cast<const float4*>(p.ln_colsum + c));
           } else {
             float* bp = reinterpret_cast<float*>(&b4);
-            for (int e = 0; e < 4 && c + e < p.N; ++e) bp[e] = __ldg(p.bias + c + e);
+            float* sp = reinterpret_cast<float*>(&s4);
+            for (int e = 0; e < 4 && c + e < p.N; ++e) {
+              bp[e] = __ldg(p.bias + c + e);
+              if (ln) sp[e] = __ldg(p.ln_colsum + c + e);
+            }
           }
           reinterpret_cast<float4*>(sb)[etid] = b4;
+          if (ln) reinterpret_cast<float4*>(sc)[etid] = s4;
         }
         if (!tma_out && !f32_tma) named_bar_sync(1, 256);  // (the staged paths' chunk barrier orders it otherwise)
       }
@@ -397,6 +411,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               const float4 b4 = col0 + j + 4 <= p.N ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
               v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+            }
+          } else if (ln) {  // folded LayerNorm: rstd (acc - mu s_n) + c_n
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+              const float4 s4 = *reinterpret_cast<const float4*>(sc + cl + j);
+              v[j] = fmaf(v[j], ln_r, fmaf(ln_nmr, s4.x, b4.x));
+              v[j + 1] = fmaf(v[j + 1], ln_r, fmaf(ln_nmr, s4.y, b4.y));
+              v[j + 2] = fmaf(v[j + 2], ln_r, fmaf(ln_nmr, s4.z, b4.z));
+              v[j + 3] = fmaf(v[j + 3], ln_r, fmaf(ln_nmr, s4.w, b4.w));
             }
           } else {  // shared-memory broadcast reads (zero past N)
 #pragma unroll
@@ -603,6 +627,7 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
   if (p.silu_col && (p.silu_col % 32 || p.epi == EPI_STORE_F32)) return -2;
   if (p.gelu && p.epi != EPI_STORE_BF16) return -2;
+  if (p.ln_stats && (!p.ln_colsum || !p.bias || p.epi == EPI_STORE_F32 || p.splits > 1)) return -2;
   if ((p.tf32 || p.softplus) && (p.epi != EPI_STORE_F32 || p.splits > 1)) return -2;
   if (p.tf32 && (p.K % 4 || (p.lda * 4) % 16 || (p.ldb * 4) % 16)) return -1;
   if (p.splits > 1 && (p.epi != EPI_STORE_F32 || !p.partial || !p.sem || p.splits > 8 || p.N % 4 || p.ldo % 4))

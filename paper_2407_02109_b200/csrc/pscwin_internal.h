@@ -46,6 +46,10 @@ struct GemmArgs {
   int stages;  // smem ring depth (set by the launcher)
   int f32_tma;  // f32 output staged in smem and TMA-stored (set by the launcher)
   int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
+  // LayerNorm folded into this projection (bf16 epilogues; rowops.cu ln_fold_kernel): A = x (not normalised),
+  // B = W' = W diag(gamma), bias = c = W beta + b; the epilogue computes rstd_m (acc - mu_m s_n) + c_n
+  const float2* ln_stats;  // [M] (mu, rstd) per A row, or null (no folding)
+  const float* ln_colsum;  // [N] s_n = sum_k W'[n,k]
 };
 
 // host helpers (abi.cu)
@@ -58,7 +62,18 @@ int num_sms();
 struct AuxStream {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // extra join points (one per consumer)
   bool ok = false;
+};
+// A LayerNorm folded into the projection that follows it (rowops.cu): W' = W diag(gamma) [N, K] bf16, s [N],
+// c = W beta + b [N] (weight-only, produced by launch_ln_fold, ready once `ready` has been waited on; null =
+// stream-ordered), and a [T] float2 scratch for the row statistics of the projection's input.
+struct LnFold {
+  const void* wf;
+  const float* colsum;
+  const float* bias;
+  float2* stats;
+  cudaEvent_t ready;
 };
 AuxStream* aux_stream(int slot);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) for `fn` on the current device, once per (device,
@@ -81,6 +96,9 @@ int launch_partition(const void* x, const void* pad_row, int B, int H, int W, in
 int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, int sy, const void* residual,
                  int is_f32, void* out, cudaStream_t stream);
 int launch_gemm_bf16(const void* A, const void* B, const GemmArgs& args, cudaStream_t stream);
+int launch_row_stats(const void* x, long long rows, int C, float eps, float2* stats, cudaStream_t stream);
+int launch_ln_fold(const void* W, int N, int K, const float* g, const float* beta, const float* bias, void* Wf,
+                   float* s, float* c, cudaStream_t stream);
 int launch_layer_norm(const void* x, long long rows, int C, const float* g, const float* b, float eps, int is_f32,
                       void* out, cudaStream_t stream);
 int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C, int is_f32, float* out,
@@ -152,8 +170,15 @@ int ms_cycle_scan_module(const void* desc, const void* wts, const MsGeo& g, int 
                          cudaStream_t s);
 // FFN sub-layer (NEXT-2): x += GELU(LN2(x) W_fc1^T + b_fc1) W_fc2^T + b_fc2 over T rows, in place; u [T, C] and
 // h [T, hidden] bf16 scratch
-int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts, void* x, void* u, void* h, cudaStream_t s);
+int ffn_bf16(long long T, int C, int hidden, float eps, const void* wts, void* x, void* u, void* h, cudaStream_t s,
+             const LnFold* lnf = nullptr);
+// GEMM whose A operand is LayerNorm(x) (gamma g, beta be, eps): with lnf, the row statistics of x and the folded
+// projection (A = x itself); without, the LayerNorm pass into u and the plain projection. a.bias is the
+// projection's own bias (replaced by lnf->bias when folded); a.M / a.K are the rows / width of x.
+int ln_gemm(const void* x, const float* g, const float* be, float eps, const void* W, GemmArgs a, void* u,
+            const LnFold* lnf, cudaStream_t s);
 // cycle-scan module of a layer (a1-a3): x_out = x_in + out_proj(cycle_scan(in_proj(LN_s(x_in))))
-int cycle_scan_module(const void* desc, const void* wts, const void* x_in, void* x_out, void* ws, size_t off_u,
+int cycle_scan_module(const void* desc, const void* wts, const LnFold* lnf, const void* x_in, void* x_out, void* ws,
+                      size_t off_u,
                       size_t off_xz, size_t off_g, size_t off_scan, size_t scan_bytes, cudaStream_t s);
 }  // namespace pscwin

@@ -156,4 +156,121 @@ int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C
   return (int)cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------------------------------------------
+// LayerNorm folded into the following projection (a1 LN_s -> in_proj, a4 LN1 -> QKV, FFN LN2 -> fc1):
+//   LN(x) W^T + b = rstd (x W'^T - mu s) + c,   W' = W diag(gamma),  s_n = sum_k W'[n,k],  c = W beta + b
+// (exact algebra of LN(x)_k = (x_k - mu) rstd gamma_k + beta_k). The GEMM reads x itself; its epilogue applies the
+// row statistics (mu, rstd) and the folded column terms (s, c). Two small kernels feed it:
+//   row_stats_kernel: (mu, rstd) per row of x, two-pass in registers (warp per row) -> 8 bytes per row instead of
+//                     the C-element normalised row (the LayerNorm pass it replaces reads AND writes C elements);
+//   ln_fold_kernel:   W' (bf16), s (from the rounded W' so x W'^T - mu s vanishes for a constant row) and c, from
+//                     the weights alone (weight-only work: it runs on the side stream, off the critical path).
+// ---------------------------------------------------------------------------------------------------------------
+__global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long rows, int C, float eps,
+                                 float2* __restrict__ stats) {
+  pdl_trigger();
+  pdl_wait();
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int nvec = C / 8;
+  const uint4* src = reinterpret_cast<const uint4*>(x + row * C);
+  uint4 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // all loads in flight before any arithmetic
+    const int i = lane + 32 * k;
+    if (i < nvec) v[k] = __ldcs(src + i);
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (lane + 32 * k < nvec) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) sum += bf16_lo(w[j]) + bf16_hi(w[j]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const float mean = sum / C;
+  float sq = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (lane + 32 * k < nvec) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float a = bf16_lo(w[j]) - mean, b = bf16_hi(w[j]) - mean;
+        sq = fmaf(a, a, fmaf(b, b, sq));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  if (lane == 0) stats[row] = make_float2(mean, rsqrtf(sq / C + eps));
+}
+
+// one warp per output row n of W [N, K] (nn.Linear layout): W'[n,:] = bf16(W[n,:] * gamma), s[n] = sum W'[n,:],
+// c[n] = sum_k beta_k W[n,k] + b[n]
+__global__ void ln_fold_kernel(const __nv_bfloat16* __restrict__ Wt, int N, int K, const float* __restrict__ g,
+                               const float* __restrict__ beta, const float* __restrict__ bias,
+                               __nv_bfloat16* __restrict__ Wf, float* __restrict__ s, float* __restrict__ c) {
+  pdl_trigger();
+  pdl_wait();
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (n >= N) return;
+  const int lane = threadIdx.x & 31;
+  const uint4* src = reinterpret_cast<const uint4*>(Wt + (size_t)n * K);
+  uint4* dst = reinterpret_cast<uint4*>(Wf + (size_t)n * K);
+  float ss = 0.f, cc = 0.f;
+  for (int i = lane; i < K / 8; i += 32) {
+    const uint4 w = __ldg(src + i);
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(g + 8 * i));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(g + 8 * i + 4));
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta + 8 * i));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta + 8 * i + 4));
+    const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    const uint32_t* wi = reinterpret_cast<const uint32_t*>(&w);
+    uint4 o;
+    uint32_t* wo = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float w0 = bf16_lo(wi[j]), w1 = bf16_hi(wi[j]);
+      wo[j] = pack_bf16(w0 * gg[2 * j], w1 * gg[2 * j + 1]);
+      ss += bf16_lo(wo[j]) + bf16_hi(wo[j]);
+      cc = fmaf(w0, bb[2 * j], fmaf(w1, bb[2 * j + 1], cc));
+    }
+    dst[i] = o;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    cc += __shfl_xor_sync(0xffffffffu, cc, o);
+  }
+  if (lane == 0) {
+    s[n] = ss;
+    c[n] = cc + (bias ? bias[n] : 0.f);
+  }
+}
+
+int launch_row_stats(const void* x, long long rows, int C, float eps, float2* stats, cudaStream_t stream) {
+  if (rows == 0) return 0;
+  if (C % 8 || C > 2048) return -1;
+  PSCWIN_PROF("row_stats", stream);
+  launch_k(row_stats_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C,
+           eps, stats);
+  return (int)cudaGetLastError();
+}
+
+int launch_ln_fold(const void* W, int N, int K, const float* g, const float* beta, const float* bias, void* Wf,
+                   float* s, float* c, cudaStream_t stream) {
+  if (K % 8) return -1;
+  PSCWIN_PROF("ln_fold", stream);
+  launch_k(ln_fold_kernel, dim3((unsigned)((N + 7) / 8)), dim3(256), 0, stream, (const __nv_bfloat16*)W, N, K, g, beta,
+           bias, (__nv_bfloat16*)Wf, s, c);
+  return (int)cudaGetLastError();
+}
+
 }  // namespace pscwin

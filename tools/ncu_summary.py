@@ -89,7 +89,7 @@ METRICS = [
 ]
 
 
-def full(path, traffic_out=None):
+def full(path, traffic_out=None, labels_override=None):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
@@ -99,7 +99,7 @@ def full(path, traffic_out=None):
     print("| kernel | " + " | ".join(m[1] for m in METRICS) + " | top stalls (warps per issue) |")
     print("|---" * (len(METRICS) + 2) + "|")
     traffic = {}
-    labels = gemm_labels([short(r[ki]) for r in rows[2:]])
+    labels = labels_override or gemm_labels([short(r[ki]) for r in rows[2:]])
     for r, lab in zip(rows[2:], labels):
         vals = []
         for key, _, scale in METRICS:
@@ -128,4 +128,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
-        full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
+        # optional 4th argument: comma-separated labels of the captured launches, in order (a -k filtered capture
+        # has no neighbouring kernels to infer the GEMM labels from)
+        full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 and sys.argv[3] != "-" else None,
+             sys.argv[4].split(",") if len(sys.argv) > 4 else None)
