@@ -183,10 +183,13 @@ struct LayerWs {
   size_t stats, f_qkv, f_in, f_fc1;  // folded-LayerNorm scratch: row stats [T] float2; W' | s | c per projection
 };
 
-// LayerNorm folded into the projection after it (rowops.cu; PSCWIN_LN_FOLD=0 restores the separate LayerNorm
-// pass: A/B knob, read once)
+// LayerNorm folded into the projection after it (rowops.cu). Off by default (PSCWIN_LN_FOLD=1 enables it; A/B
+// knob, read once): measured at 4096^2 (ncu, one eager step, profiles/r02/ln_fold_r02c.md) the row-stats pass
+// saves 19 us per LayerNorm but the folded epilogue (two more FMAs per element, s_n from shared memory, register
+// spills in the RoPE variant) makes the QKV GEMM 186 -> 213 us and in_proj 235 -> 272 us: the projections'
+// epilogues, not their tensor pipes, bound them once the LayerNorm work moves in.
 bool ln_fold_enabled() {
-  static const bool on = env_knob("PSCWIN_LN_FOLD", 1) != 0;
+  static const bool on = env_knob("PSCWIN_LN_FOLD", 0) != 0;
   return on;
 }
 size_t fold_bytes(size_t N, size_t K) { return align256(N * K * 2) + align256(N * 4) * 2; }
@@ -353,7 +356,10 @@ AuxStream* aux_stream(int slot) {
     if (!a.s && cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) a.s = nullptr;
     if (!a.fork && cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) a.fork = nullptr;
     if (!a.join && cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) a.join = nullptr;
-    a.ok = a.s && a.fork && a.join;
+    bool evs = true;
+    for (cudaEvent_t& e : a.ev)
+      if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr, evs = false;
+    a.ok = a.s && a.fork && a.join && evs;
     if (!a.ok) {
       cudaGetLastError();
       return nullptr;

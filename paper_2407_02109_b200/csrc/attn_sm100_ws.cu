@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
         red_max[hc * 128 + row] = mx;
         named_bar_sync(1 + a, 256);
         mx = fmaxf(mx, red_max[(hc ^ 1) * 128 + row]);
+        if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);  // max pass done (debug timeline)
         const float base = (mx == -INFINITY) ? 0.f : mx * p.sl2;
         const float2 nb = make_float2(-base, -base);
         // pass 2: p = 2^(s log2(e)/sqrt(d) - base) (packed fp32x2 scale, MUFU ex2), partial sums, P (bf16 pairs)

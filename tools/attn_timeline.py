@@ -2,7 +2,7 @@
 
     python tools/attn_timeline.py [side=64]      # ViT-B, side x side token grid, plain and shifted layers
 Events per CTA (globaltimer ns): loader = item load issued; mma = S issued / PV issued; wg0/wg1 = S ready,
-P written, O ready, O stored (per q-tile slot)."""
+max done, P written, O ready, O stored (per q-tile slot)."""
 import os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -36,7 +36,16 @@ for run in (2, 5):
     for cta in range(148):
         v = np.sort(t[cta][64:96]); v = v[v > 0]
         if len(v) >= 12:
-            s = v[::4]
+            s = v[::5]
             gaps.append(np.median(np.diff(s)) / 1e3)
     if gaps:
         print(f"median per-item period (slot 0): {np.median(gaps):.2f} us over {len(gaps)} CTAs")
+    # median phase durations of slot 0: S ready -> max done -> P written -> O ready -> O stored -> next S ready
+    ph = [[] for _ in range(5)]
+    for cta in range(148):
+        v = np.sort(t[cta][64:96]); v = v[v > 0]
+        for i in range(0, len(v) - 5, 5):
+            for k in range(5):
+                ph[k].append((v[i + k + 1] - v[i + k]) / 1e3)
+    names = ["max pass", "exp pass", "PV wait", "O readout+store", "to next S"]
+    print("slot-0 phase medians (us): " + ", ".join(f"{n} {np.median(x):.2f}" for n, x in zip(names, ph) if x))

@@ -58,3 +58,16 @@ for name, M, K, N, f32 in shapes:
     kb = (K + 63) // 64
     print(f"{name:14s} M={M:6d} K={K:5d} N={N:5d} {us:8.2f} us  {tf:7.1f} TF/s  {us / kb:6.3f} us/kblock(if 1 tile/CTA)",
           flush=True)
+
+# 4096^2 shapes (M = 65536 tokens) against cuBLAS (torch.matmul, no epilogue) as the library-GEMM yardstick
+if not only or "cublas" in only:
+    for name, M, K, N in [("qkv4096", 65536, 768, 2304), ("out4096", 65536, 768, 768), ("in4096", 65536, 768, 3072),
+                          ("outscan4096", 65536, 1536, 768), ("fc1_4096", 65536, 768, 3072),
+                          ("fc2_4096", 65536, 3072, 768)]:
+        A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+        W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        ours = graph_time(lambda: pl.linear(A, W))
+        cub = graph_time(lambda: torch.matmul(A, W.t()))
+        f = 2 * M * N * K / 1e6
+        print(f"{name:12s} M={M} K={K} N={N}  ours {ours:8.2f} us {f / ours:7.1f} TF/s   cuBLAS {cub:8.2f} us "
+              f"{f / cub:7.1f} TF/s", flush=True)

@@ -1,9 +1,13 @@
 // Pipe-throughput microbenchmark (sm_100a): MUFU.EX2, FFMA, FFMA2 and the scan's mix, per SM per clock.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipes pipes.cu && ./pipes
 #include <cstdio>
+#include <cstdint>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+// packed half-precision exp2: two results per lane per instruction (MODE 4: f16x2, MODE 5: bf16x2)
+__device__ __forceinline__ uint32_t ex2h2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.f16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
+__device__ __forceinline__ uint32_t ex2b2(uint32_t x) { uint32_t y; asm volatile("ex2.approx.ftz.bf16x2 %0, %1;" : "=r"(y) : "r"(x)); return y; }
 
 template <int MODE>
 __global__ void kern(float* out, int iters, long long* clk) {
@@ -19,6 +23,16 @@ __global__ void kern(float* out, int iters, long long* clk) {
       if (MODE == 0) a[i] = ex2(a[i]) * -0.5f;                       // MUFU + FMUL
       if (MODE == 1) a[i] = fmaf(a[i], 0.999f, 1e-4f);                // FFMA
       if (MODE == 2) b[i] = __ffma2_rn(b[i], m, c);                    // FFMA2
+      if (MODE == 4) {  // packed f16x2 exp2 (the chain keeps values in (0, 1): y = 2^x * -0.5 via the sign bit)
+        uint32_t h = __float_as_uint(a[i]);
+        h = ex2h2(h) ^ 0x80008000u;
+        a[i] = __uint_as_float(h);
+      }
+      if (MODE == 5) {
+        uint32_t h = __float_as_uint(a[i]);
+        h = ex2b2(h) ^ 0x80008000u;
+        a[i] = __uint_as_float(h);
+      }
       if (MODE == 3) {                                                 // scan pass-2 mix per pair: 2 MUFU, 3 FMUL2, 3 FFMA2
         float2 x = __fmul2_rn(b[i], m);
         float2 e = make_float2(ex2(x.x), ex2(x.y));
@@ -67,5 +81,7 @@ int main() {
   run<1>("ffma", 1, 256);
   run<2>("ffma2(x2)", 2, 256);
   run<3>("scanmix/el", 2, 256);
+  run<4>("ex2.f16x2(el)", 2, 256);
+  run<5>("ex2.bf16x2(el)", 2, 256);
   return 0;
 }
