@@ -99,6 +99,11 @@ PSCWIN_DEVICE void tma_store_2d(const CUtensorMap* m, const void* src, int c0, i
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// L2 prefetch of one tensor-map box (no shared memory, no barrier)
+PSCWIN_DEVICE void tma_prefetch_l2_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(m), "r"(c0), "r"(c1)
+               : "memory");
+}
 PSCWIN_DEVICE void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 PSCWIN_DEVICE void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 PSCWIN_DEVICE void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -178,8 +183,13 @@ PSCWIN_DEVICE uint32_t smem_in_cta(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// Arrival on a barrier of either CTA of the pair (the accumulator-free barrier of the leader). What it orders is
+// tcgen05 work (this warp's TMEM reads, already completed by tcgen05.wait::ld and fenced by
+// tcgen05.fence::before_thread_sync) against the leader's next MMAs, so the default .release.cta semantics suffice
+// (as CUTLASS's cluster barriers arrive); .release.cluster put a full memory barrier (ERRBAR) in front of every
+// arrival, the GEMM epilogue's top stall.
 PSCWIN_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // Wait on a barrier that the peer CTA of a pair also signals (TMA complete_tx, multicast tcgen05.commit, remote
 // arrivals after tcgen05 fences). Everything it orders is async-proxy work (TMA, UMMA, TMEM), which the mbarrier

@@ -7,7 +7,7 @@
 // Structure (B200-native): persistent grid (one CTA per SM), warp-specialised —
 //   warp 0: TMA producer (128B-swizzled A/B k-blocks of 64, 4-stage mbarrier ring)
 //   warp 1: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN<=256, K=16 per instruction)
-//   warps 2-9: epilogue (tcgen05.ld 32x32b -> registers -> fused op -> swizzled smem -> TMA tensor store),
+//   warps 2-9: epilogue (tcgen05.ld 32x32b -> registers -> fused op -> per-warp swizzled smem box -> TMA store),
 //   double-buffered TMEM accumulators (2 x 256 columns) so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <stdlib.h>
 #include <string.h>
@@ -25,21 +25,25 @@ constexpr int A_STAGE_BYTES = BM * BK * 2;       // 16 KB
 constexpr int STAGE_OUT_BYTES = BM * 64 * 2;     // one 128x64 bf16 output / residual chunk (16 KB)
 constexpr int GEMM_THREADS = 64 + 256;           // TMA warp, MMA warp, 8 epilogue warps
 constexpr size_t GEMM_SMEM_MAX = 232448;         // 227 KB opt-in limit per CTA
-// shared memory layout: [1 KB align slack][stages x (A 128x64 | B rows x 64)][2 x 16 KB output staging]
-// [residual tiles 2 x nch x 16 KB][barriers]; B rows per CTA = BN (single CTA) or BN / 2 (CTA pair)
-__host__ __device__ inline size_t gemm_fixed_bytes(int BN, bool resid, bool f32 = false) {
-  const size_t nch = (size_t)(BN + 63) / 64;
-  // f32 outputs: two more 16 KB staging boxes (a 64-column f32 chunk is two 128 x 32 boxes; two chunks in flight).
-  // residual with BN > 128 ("in place"): ONE set of residual chunks, the output overwrites them and is stored from
-  // there (the two output staging boxes stay allocated but unused; the layout offsets do not change).
-  const size_t res = resid ? (BN > 128 ? nch : 2 * nch) * STAGE_OUT_BYTES : (f32 ? 2 * STAGE_OUT_BYTES : 0);
-  return 1024 + 2 * STAGE_OUT_BYTES + res + 4 * 256 * 4 + 256;  // bias + LN column sums, double-buffered
+// shared memory layout: [1 KB align slack][stages x (A 128x64 | B rows x 64)][output staging][residual tiles]
+// [bias / LN sums][barriers]; B rows per CTA = BN (single CTA) or BN / 2 (CTA pair)
+struct EpiSmem {
+  size_t stg, res;  // output staging bytes, residual bytes
+};
+__host__ __device__ inline EpiSmem gemm_epi_smem(int BN, bool resid, bool f32, int warp_epi, int nbuf, int res_global) {
+  const size_t nbx = (size_t)(BN + 31) / 32;
+  // f32 outputs: four 16 KB staging boxes (a 64-column f32 chunk is two 128 x 32 boxes; two chunks in flight)
+  if (f32) return {2 * (size_t)STAGE_OUT_BYTES, 2 * (size_t)STAGE_OUT_BYTES};
+  // per-warp epilogue with the residual in shared memory: 32-column boxes of 128 rows, the output written over them
+  if (resid && !res_global) return {0, (BN > 128 ? 1 : 2) * nbx * (size_t)(STAGE_OUT_BYTES / 2)};
+  // per-warp epilogue, residual (if any) read from global memory: nbuf 2 KB staging boxes per epilogue warp
+  return {(size_t)8 * nbuf * 2048, 0};
+}
+__host__ __device__ inline size_t gemm_fixed_bytes(const EpiSmem& e) {
+  return 1024 + e.stg + e.res + 4 * 256 * 4 + 256;  // bias + LN column sums (double-buffered), barriers
 }
 __host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
   return A_STAGE_BYTES + (size_t)(pair ? BN / 2 : BN) * BK * 2;
-}
-__host__ __device__ inline size_t gemm_smem_bytes(int BN, bool resid, bool pair, int stages, bool f32 = false) {
-  return gemm_fixed_bytes(BN, resid, f32) + (size_t)stages * gemm_stage_bytes(BN, pair);
 }
 }  // namespace
 
@@ -68,18 +72,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int STAGES = p.stages;
   const int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
-  const bool resid_tma = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
+  const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
+  constexpr bool res_gmem_ek = EK == EK_PLAIN;                       // (only plain epilogues carry a residual)
+  const bool res_gmem = res_gmem_ek && resid && p.res_global;  // the epilogue reads the residual from global
+  const bool resid_tma = resid && !res_gmem;                   // residual tiles TMA-loaded into shared memory
   const int nch = (BN + 63) / 64;
+  const EpiSmem es = gemm_epi_smem(BN, resid, EK == EK_F32, p.warp_epi, p.nbuf, p.res_global);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_STAGE_BYTES;
-  uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // 2 x 16 KB output staging (1024-aligned)
-  uint8_t* s_res = s_stage + 2 * STAGE_OUT_BYTES;   // 2 x nch x 16 KB residual tiles (TMA-loaded)
+  uint8_t* s_stage = sB + STAGES * B_STAGE_BYTES;   // output staging (1024-aligned)
+  uint8_t* s_res = s_stage + es.stg;                // residual tiles (TMA-loaded)
   // residual tiles: double-buffered (BN <= 128) or one set written over in place by the output (BN > 128)
   const bool res_inplace = resid_tma && BN > 128;
-  float* s_bias = reinterpret_cast<float*>(
-      s_res + (resid_tma ? (res_inplace ? 1 : 2) * nch * STAGE_OUT_BYTES
-                         : (EK == EK_F32 ? 2 * STAGE_OUT_BYTES : 0)));  // [2][256] bias, then [2][256] LN s_n
+  float* s_bias = reinterpret_cast<float*>(s_res + es.res);  // [2][256] bias, then [2][256] LN s_n
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_bias + 4 * 256);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
@@ -121,9 +127,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs of a pair)
       mbar_init(&rfull[i], 1);
-      mbar_init(&rempty[i], res_inplace ? 1 : 256);  // in place: the store issuer, after the stores read out
+      // each epilogue warp's lane 0, once that warp's in-place stores have read the residual set out
+      mbar_init(&rempty[i], 8);
     }
-    if (resid_tma) tma_prefetch_desc(&tmRes);
+    if (resid) tma_prefetch_desc(&tmRes);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -152,12 +159,17 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int rbuf = 0;
       uint32_t rphase = 0;
       auto load_res = [&](int m0, int n0, int buf) {  // this CTA's residual rows of the tile
-        if (m0 + mrow < p.M) {
-          mbar_arrive_expect_tx(&rfull[buf], nch * STAGE_OUT_BYTES);
-          for (int c = 0; c < nch; ++c)
-            tma_load_2d(s_res + (buf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[buf], n0 + c * 64, m0 + mrow, pol_a);
-        } else {
-          mbar_arrive(&rfull[buf]);
+        if (m0 + mrow >= p.M) {
+          mbar_arrive(&rfull[buf]);  // no rows of this CTA in the tile: nothing to load
+        } else {  // 32-column SW64 boxes of 128 rows (the per-warp epilogue's layout)
+          const int nbx = (BN + 31) / 32;
+          int nb = 0;
+          for (int c = 0; c < nbx; ++c) nb += n0 + c * 32 < p.N;
+          mbar_arrive_expect_tx(&rfull[buf], nb * (STAGE_OUT_BYTES / 2));
+          for (int c = 0; c < nbx; ++c)
+            if (n0 + c * 32 < p.N)
+              tma_load_2d(s_res + (size_t)(buf * nbx + c) * (STAGE_OUT_BYTES / 2), &tmRes, &rfull[buf], n0 + c * 32,
+                          m0 + mrow, pol_a);
         }
       };
       for (int tile = tile0; tile < n_tiles; tile += tstride) {
@@ -174,17 +186,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           rphase ^= 1;
           res_pending = false;
         };
+        if (res_gmem) {  // the epilogue reads this tile's residual from global memory: warm L2 with it now
+          const int nbx = (BN + 31) / 32;
+          if (m0 + mrow < p.M)
+            for (int c = 0; c < nbx; ++c)
+              if (n0 + c * 32 < p.N) tma_prefetch_l2_2d(&tmRes, n0 + c * 32, m0 + mrow);
+        }
         if (resid_tma && !res_inplace) {
           // residual tile of this CTA's rows (double-buffered, consumed by the epilogue), issued ahead of the k-loop
           mbar_wait(&rempty[rbuf], rphase ^ 1);
-          if (m0 + mrow < p.M) {
-            mbar_arrive_expect_tx(&rfull[rbuf], nch * STAGE_OUT_BYTES);
-            for (int c = 0; c < nch; ++c)
-              tma_load_2d(s_res + (rbuf * nch + c) * STAGE_OUT_BYTES, &tmRes, &rfull[rbuf], n0 + c * 64, m0 + mrow,
-                          pol_a);
-          } else {
-            mbar_arrive(&rfull[rbuf]);  // no rows of this CTA in the tile: nothing to load
-          }
+          load_res(m0, n0, rbuf);
           if (++rbuf == 2) {
             rbuf = 0;
             rphase ^= 1;
@@ -286,9 +297,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else {
     // ------------------------------------------------------------------ epilogue warps 2..9
-    // Two warps per TMEM lane quarter (rows), each taking 32 of every 64 accumulator columns. bf16 outputs are
-    // staged in 128B-swizzled smem (two 128x64 buffers) and written by TMA tensor stores (coalesced, async);
-    // f32 outputs are stored directly.
+    // Two warps per TMEM lane quarter (rows), each taking 32 of every 64 accumulator columns. bf16 outputs: each
+    // warp stages its own 32 x 32 boxes (SW64) and TMA-stores them (no CTA-wide barrier per chunk); f32 outputs: per
+    // -warp 32 x 32 f32 boxes (SW128) or direct stores (split-K).
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int lane = lane_id();
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ln_r = st.y;
         ln_nmr = -st.x * st.y;
       }
-      if (p.bias && !f32_tma) {  // (f32 tiles read the bias straight from L1: no CTA-wide barrier in that path)
+      if (EK != EK_F32 && p.bias) {  // (f32 tiles read the bias straight from L1: no CTA-wide barrier there)
         if (etid < BN / 4) {
           const int c = n0 + 4 * etid;
           float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -365,33 +376,186 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           reinterpret_cast<float4*>(sb)[etid] = b4;
           if (ln) reinterpret_cast<float4*>(sc)[etid] = s4;
         }
-        if (!tma_out && !f32_tma) named_bar_sync(1, 256);  // (the staged paths' chunk barrier orders it otherwise)
       }
+      if constexpr (EK != EK_F32) {
+        // ---------------------------------------------------------- per-warp bf16 epilogue
+        // Warp (quarter, half) owns rows [32 quarter, +32) and the 32-column boxes i = half, half + 2, ... of the
+        // tile. Each box goes TMEM -> registers (the next box's TMEM load is in flight meanwhile) -> fused op ->
+        // a 2 KB SW64 staging box (this warp's own double buffer, or the residual box in place) -> one TMA store
+        // by the warp's lane 0. The only CTA-wide barrier is the one per tile that publishes the staged bias.
+        if (p.bias) named_bar_sync(1, 256);
+        const int nbx = p.dbg_noepi ? 0 : (BN + 31) / 32;  // (timing probe: no epilogue work at all)
+        // residual from global memory (L2-warm: the producer prefetched the tile): this thread's 64 bytes of row
+        // `row` per box, loaded one box ahead (the first box's before the accumulator wait). (Measured: loading all
+        // of a warp's boxes up front with the box loop unrolled was slower for every GEMM of the step.)
+        const __nv_bfloat16* rg =
+            res_gmem ? reinterpret_cast<const __nv_bfloat16*>(p.residual) + (size_t)row * p.ldr + n0 : nullptr;
+        uint4 rcur[res_gmem_ek ? 4 : 1], rnext[res_gmem_ek ? 4 : 1];
+        auto load_res4 = [&](int bx, uint4* r) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) r[q] = make_uint4(0u, 0u, 0u, 0u);
+          if (row_ok && n0 + bx * 32 < p.N) {
+            const uint4* src = reinterpret_cast<const uint4*>(rg + bx * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = __ldcs(src + q);
+          }
+        };
+        if constexpr (res_gmem_ek)
+          if (res_gmem && half < nbx) load_res4(half, rcur);
+        if (PAIR)
+          mbar_wait_cluster(&tfull[acc], acc_phase);
+        else
+          mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        if (resid_tma) mbar_wait(&rfull[rbuf], rphase);
+        const uint32_t t_row = tmem_base + acc * 256 + ((uint32_t)(quarter * 32) << 16);
+        const int ew = warp - 2;
+        // the next box's TMEM load is issued before this box's math
+        constexpr bool kPrefetch = true;
+        uint32_t ra[32];
+        if (kPrefetch && half < nbx) tmem_ld32(t_row + half * 32, ra);
+        for (int bx = half; bx < nbx; bx += 2) {
+          const int cl = bx * 32, col0 = n0 + cl;
+          if (!kPrefetch) tmem_ld32(t_row + cl, ra);
+          tmem_wait_ld_dep(ra);
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(ra[j]);
+          if (kPrefetch && bx + 2 < nbx) {
+            tmem_ld32(t_row + cl + 64, ra);
+          } else if (bx + 2 >= nbx) {  // this warp's last TMEM read of the tile: the accumulator may be reused
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (PAIR)
+                mbar_arrive_remote(tempty0 + acc * 8);
+              else
+                mbar_arrive(&tempty[acc]);
+            }
+          }
+          if (p.bias) {
+            if (ln) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+                const float4 s4 = *reinterpret_cast<const float4*>(sc + cl + j);
+                v[j] = fmaf(v[j], ln_r, fmaf(ln_nmr, s4.x, b4.x));
+                v[j + 1] = fmaf(v[j + 1], ln_r, fmaf(ln_nmr, s4.y, b4.y));
+                v[j + 2] = fmaf(v[j + 2], ln_r, fmaf(ln_nmr, s4.z, b4.z));
+                v[j + 3] = fmaf(v[j + 3], ln_r, fmaf(ln_nmr, s4.w, b4.w));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+                v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
+              }
+            }
+          }
+          if constexpr (EK == EK_ROPE) {
+            if (p.rope && col0 < 2 * p.C) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
+            }
+          }
+          if constexpr (EK == EK_GELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+          }
+          if (EK == EK_PLAIN && p.silu_col > 0 && col0 >= p.silu_col) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
+          }
+          // staging box: the residual box itself (written over in place) or one of this warp's nbuf buffers
+          const int nb = p.nbuf;
+          uint8_t* box = resid_tma ? s_res + ((size_t)(rbuf * nbx + bx) * 128 + quarter * 32) * 64
+                                   : s_stage + (size_t)(ew * nb + (nb == 2 ? (gseq & 1) : 0)) * 2048;
+          if constexpr (res_gmem_ek) if (res_gmem) {
+            if (bx + 2 < nbx) load_res4(bx + 2, rnext);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 rw = rcur[q];
+              rcur[q] = rnext[q];
+              v[8 * q + 0] += bf16_lo(rw.x); v[8 * q + 1] += bf16_hi(rw.x);
+              v[8 * q + 2] += bf16_lo(rw.y); v[8 * q + 3] += bf16_hi(rw.y);
+              v[8 * q + 4] += bf16_lo(rw.z); v[8 * q + 5] += bf16_hi(rw.z);
+              v[8 * q + 6] += bf16_lo(rw.w); v[8 * q + 7] += bf16_hi(rw.w);
+            }
+          }
+          if (resid_tma) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 rw = *reinterpret_cast<const uint4*>(box + swz_offset(lane, q, 64));
+              v[8 * q + 0] += bf16_lo(rw.x); v[8 * q + 1] += bf16_hi(rw.x);
+              v[8 * q + 2] += bf16_lo(rw.y); v[8 * q + 3] += bf16_hi(rw.y);
+              v[8 * q + 4] += bf16_lo(rw.z); v[8 * q + 5] += bf16_hi(rw.z);
+              v[8 * q + 6] += bf16_lo(rw.w); v[8 * q + 7] += bf16_hi(rw.w);
+            }
+          } else if (gseq >= nb) {  // the store from this buffer nb boxes ago has read it out
+            if (lane == 0) {
+              if (nb == 2)
+                bulk_wait_read1();
+              else
+                bulk_wait_read0();
+            }
+            __syncwarp();
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 w;
+            w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+            w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+            w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+            w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+            *reinterpret_cast<uint4*>(box + swz_offset(lane, q, 64)) = w;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (mb + quarter * 32 < p.M && col0 < p.N) tma_store_2d(&tmOut, box, col0, mb + quarter * 32);
+            bulk_commit();
+          }
+          ++gseq;
+        }
+        if (half >= nbx) {  // (a tile of one 32-column box: the second half's warps only release the accumulator)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (PAIR)
+              mbar_arrive_remote(tempty0 + acc * 8);
+            else
+              mbar_arrive(&tempty[acc]);
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+        if (resid_tma) {  // the residual set may be refilled once this warp's in-place stores have read it out
+          if (lane == 0) {
+            bulk_wait_read0();
+            mbar_arrive(&rempty[rbuf]);
+          }
+          if (res_inplace) {
+            rphase ^= 1;
+          } else if (++rbuf == 2) {
+            rbuf = 0;
+            rphase ^= 1;
+          }
+        }
+        continue;
+      }
+      // ---------------------------------------------------------- f32 epilogue (x_proj, dt)
       if (PAIR)
         mbar_wait_cluster(&tfull[acc], acc_phase);
       else
         mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (resid_tma) mbar_wait(&rfull[rbuf], rphase);
       const uint32_t t_row = tmem_base + acc * 256 + ((uint32_t)(quarter * 32) << 16);
       for (int cc = 0; cc < nch; ++cc, ++gseq) {
         const int cl = cc * 64 + half * 32;            // tile-local first column of this thread's 32
         const int col0 = n0 + cl;
-        // residual: this thread's 4 x 16B of the TMA-loaded tile (swizzled like the output staging)
-        uint4 res[4];
-        if (resid_tma) {
-          const uint8_t* rt = s_res + (rbuf * nch + cc) * STAGE_OUT_BYTES;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res[q] = *reinterpret_cast<const uint4*>(rt + swz_offset(row_local, half * 4 + q, 128));
-        }
-        // in place: each thread overwrites exactly the residual bytes it just read, and the chunk is stored from there
-        uint8_t* stg = res_inplace ? s_res + cc * STAGE_OUT_BYTES : s_stage + (gseq & 1) * STAGE_OUT_BYTES;
-        if (tma_out && !res_inplace) {
-          if (issuer && gseq >= 2) bulk_wait_read1();
-          named_bar_sync(1, 256);
-        } else if (f32_tma) {  // each warp stores its own 32 x 32 box (buffers of parity gseq & 1, two chunks in
-          if (lane == 0 && gseq >= 2) bulk_wait_read1();  // flight per warp): its store from two chunks ago has been
-          __syncwarp();                                    // read out; no barrier couples the epilogue warps
+        if (f32_tma) {  // each warp stores its own 32 x 32 box (buffers of parity gseq & 1, two chunks in flight per
+          if (lane == 0 && gseq >= 2) bulk_wait_read1();  // warp): its store from two chunks ago has been read out;
+          __syncwarp();                                    // no barrier couples the epilogue warps
         }
         uint32_t r[32];
         if (cl < BN) {
@@ -404,39 +568,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (p.bias && cl < BN) {
-          if (f32_tma) {  // L1-cached broadcast loads (zero past N)
+        if (p.bias && cl < BN) {  // L1-cached broadcast loads (zero past N)
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b4 = col0 + j + 4 <= p.N ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
-                                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
-          } else if (ln) {  // folded LayerNorm: rstd (acc - mu s_n) + c_n
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
-              const float4 s4 = *reinterpret_cast<const float4*>(sc + cl + j);
-              v[j] = fmaf(v[j], ln_r, fmaf(ln_nmr, s4.x, b4.x));
-              v[j + 1] = fmaf(v[j + 1], ln_r, fmaf(ln_nmr, s4.y, b4.y));
-              v[j + 2] = fmaf(v[j + 2], ln_r, fmaf(ln_nmr, s4.z, b4.z));
-              v[j + 3] = fmaf(v[j + 3], ln_r, fmaf(ln_nmr, s4.w, b4.w));
-            }
-          } else {  // shared-memory broadcast reads (zero past N)
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
-              v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
-            }
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b4 = col0 + j + 4 <= p.N ? __ldg(reinterpret_cast<const float4*>(p.bias + col0 + j))
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
           }
         }
-        if constexpr (EK == EK_ROPE) {
-          if (p.rope && col0 < 2 * p.C) {  // q = cols [0,C), k = [C,2C)
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj) rope_pair(v[2 * jj], v[2 * jj + 1], rc[jj], rs[jj]);
-          }
-        }
-        if (EK == EK_F32 && p.softplus) {  // Delta = softplus(delta_low W_dt^T + b_dt) (f32 output path)
+        if (p.softplus) {  // Delta = softplus(delta_low W_dt^T + b_dt)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {  // log1p(t) = log(u) t / (u - 1), u = 1 + t (exact where u rounds to 1)
             const float t = __expf(v[j]), u = 1.f + t;
@@ -444,43 +584,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             v[j] = v[j] > 20.f ? v[j] : lp;
           }
         }
-        if (EK == EK_GELU) {  // FFN fc1: GELU (erf form, reading Q21)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-        }
-        if (EK == EK_PLAIN && p.silu_col > 0 && col0 >= p.silu_col) {  // gate columns: SiLU(x) = x / (1 + e^-x)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __fdividef(v[j], 1.f + __expf(-v[j]));
-        }
-        if (resid_tma) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t* rw = reinterpret_cast<const uint32_t*>(&res[q]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              v[8 * q + 2 * e] += bf16_lo(rw[e]);
-              v[8 * q + 2 * e + 1] += bf16_hi(rw[e]);
-            }
-          }
-        }
-        if (tma_out) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 w;
-            w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-            w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-            w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-            w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-            *reinterpret_cast<uint4*>(stg + swz_offset(row_local, half * 4 + q, 128)) = w;
-          }
-          fence_proxy_async_smem();
-          named_bar_sync(1, 256);
-          if (issuer) {
-            if (mb < p.M) tma_store_2d(&tmOut, stg, n0 + cc * 64, mb);
-            bulk_commit();
-          }
-        } else if (f32_tma) {
-          // f32: this thread's 32 values are one 128-byte row of box `half` (128B-swizzled like the bf16 staging)
+        if (f32_tma) {
+          // this thread's 32 values are one 128-byte row of box `half` (128B-swizzled)
           uint8_t* sf = s_stage + (gseq & 1) * 2 * STAGE_OUT_BYTES;
           uint8_t* sh = sf + half * STAGE_OUT_BYTES;
 #pragma unroll
@@ -521,19 +626,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-      if (res_inplace) {  // the residual set may be refilled once this tile's stores have read it out
-        if (issuer) {
-          bulk_wait_read0();
-          mbar_arrive(&rempty[0]);
-        }
-        rphase ^= 1;
-      } else if (resid_tma) {
-        mbar_arrive(&rempty[rbuf]);
-        if (++rbuf == 2) {
-          rbuf = 0;
-          rphase ^= 1;
-        }
-      }
       if (S > 1) {
         // deterministic split-K fix-up: the last split to finish this output tile sums the S partials in split
         // order (no floating-point atomics) and resets the tile's counter for the next launch.
@@ -570,7 +662,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         named_bar_sync(1, 256);
       }
     }
-    if (issuer && tma_out) bulk_wait0();
+    if (tma_out && lane == 0) bulk_wait0();
     if (lane == 0 && f32_tma) bulk_wait0();
   }
   __syncthreads();
@@ -661,10 +753,30 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   if (pair && (p.BN % 16)) return -2;
   // ring depth: as many stages as fit next to the staging / residual buffers
   const bool f32o = p.epi == EPI_STORE_F32;
+  // bf16 outputs: per-warp epilogue (32 x 32 SW64 boxes). The residual is TMA-loaded into shared memory as 32-column
+  // boxes that the output overwrites in place (one 64 KB set at BN = 256: two ring stages fewer), or read from
+  // global memory by the epilogue threads one box ahead after an L2 prefetch of the tile (the ring keeps its depth,
+  // the epilogue waits on L2). Measured at 4096^2 (s5): K = 768 out-proj 86 us smem / 103 us global, K = 1536
+  // cycle-scan out-proj 133 / 126 us: a long mainloop hides the loads and profits from the deeper ring, so global
+  // iff K >= 1024. PSCWIN_GEMM_RES = 1 forces global, 2 shared memory (A/B knobs, read once).
+  static const int res_knob = env_knob("PSCWIN_GEMM_RES", 0);
+  const int res_smem = res_knob == 2 || (res_knob == 0 && p.K < 1024);
+  static const int nbuf_knob = env_knob("PSCWIN_GEMM_NBUF", 0);
+  p.warp_epi = f32o ? 0 : 1;
+  p.res_global = (p.warp_epi && !res_smem && p.N % 32 == 0 && p.ldr % 8 == 0) ? 1 : 0;
+  static const int noepi = env_knob("PSCWIN_GEMM_DBG_NOEPI", 0);  // timing probe only: output left unwritten
+  p.dbg_noepi = p.warp_epi && noepi ? 1 : 0;
   {
-    const size_t fixed = gemm_fixed_bytes(p.BN, resid, f32o), st = gemm_stage_bytes(p.BN, pair);
-    int stages = (int)((GEMM_SMEM_MAX - fixed) / st);
-    if (stages > MAX_STAGES) stages = MAX_STAGES;
+    // per-warp bf16 epilogue: two staging boxes per warp unless a single one buys another ring stage
+    const size_t st = gemm_stage_bytes(p.BN, pair);
+    auto ring = [&](int nbuf) {
+      const size_t fixed = gemm_fixed_bytes(gemm_epi_smem(p.BN, resid, f32o, p.warp_epi, nbuf, p.res_global));
+      const int n = (int)((GEMM_SMEM_MAX - fixed) / st);
+      return n > MAX_STAGES ? MAX_STAGES : n;
+    };
+    p.nbuf = ring(1) > ring(2) ? 1 : 2;
+    if (nbuf_knob == 1 || nbuf_knob == 2) p.nbuf = nbuf_knob;
+    const int stages = ring(p.nbuf);
     if (stages < 2) return -2;
     p.stages = stages;
   }
@@ -688,15 +800,15 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   }
   if (p.epi != EPI_STORE_F32) {
     if ((p.ldo * 2) % 16) return -1;
-    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldo * 2, 64, BM,
-                      CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_tmap_2d(&tmOut, p.out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldo * 2, 32, 32,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
   memset(&tmRes, 0, sizeof(tmRes));
-  if (resid) {
+  if (resid) {  // (TMA-loaded residual boxes, or the L2 prefetch of the global-memory residual path)
     if ((p.ldr * 2) % 16) return -1;
-    rc = make_tmap_2d(&tmRes, p.residual, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldr * 2, 64, BM,
-                      CU_TENSOR_MAP_SWIZZLE_128B);
+    rc = make_tmap_2d(&tmRes, p.residual, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, p.N, p.M, (uint64_t)p.ldr * 2, 32, BM,
+                      CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
   {
@@ -707,7 +819,8 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
     for (const void* f : fns) func_smem_once(f, (int)GEMM_SMEM_MAX);
   }
   const int ek = p.epi == EPI_QKV_ROPE ? EK_ROPE : (p.gelu ? EK_GELU : (p.epi == EPI_STORE_F32 ? EK_F32 : EK_PLAIN));
-  const size_t smem = gemm_smem_bytes(p.BN, resid, pair, p.stages, f32o);
+  const size_t smem = gemm_fixed_bytes(gemm_epi_smem(p.BN, resid, f32o, p.warp_epi, p.nbuf, p.res_global)) +
+                      (size_t)p.stages * gemm_stage_bytes(p.BN, pair);
   if (smem > GEMM_SMEM_MAX) return -2;
   const long long tiles = (long long)m_tiles * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);

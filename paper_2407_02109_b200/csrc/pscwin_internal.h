@@ -46,6 +46,10 @@ struct GemmArgs {
   int stages;  // smem ring depth (set by the launcher)
   int f32_tma;  // f32 output staged in smem and TMA-stored (set by the launcher)
   int pair;    // 1 = 2-CTA cluster tiles (set by the launcher; PSCWIN_GEMM_PAIR=0 disables)
+  int warp_epi;  // 1 = per-warp bf16 epilogue (32 x 32 boxes, no CTA-wide barrier per chunk; set by the launcher)
+  int nbuf;       // per-warp epilogue: 2 KB staging boxes per warp, 1 or 2 (set by the launcher)
+  int res_global;  // per-warp epilogue: residual read from global memory by the epilogue threads (launcher)
+  int dbg_noepi;  // timing probe (PSCWIN_GEMM_DBG_NOEPI=1): bf16 epilogue warps release the accumulator untouched
   // LayerNorm folded into this projection (bf16 epilogues; rowops.cu ln_fold_kernel): A = x (not normalised),
   // B = W' = W diag(gamma), bias = c = W beta + b; the epilogue computes rstd_m (acc - mu_m s_n) + c_n
   const float2* ln_stats;  // [M] (mu, rstd) per A row, or null (no folding)
