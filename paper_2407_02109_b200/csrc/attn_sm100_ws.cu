@@ -24,7 +24,9 @@
 namespace pscwin {
 
 namespace {
-constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroups
+constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroups (two threads per query row)
+constexpr int WS1_THREADS = 64 + 256 + 32;  // TMA warp, MMA warp (slot 0), 2 softmax warpgroups (one thread per
+                                            // query row), MMA warp (slot 1)
 #ifndef PSCWIN_ATTN_POLY_MOD
 #define PSCWIN_ATTN_POLY_MOD 0  // k > 0: every k-th exp2 pair on the FMA pipe; swept 0 / 2 / 3 / 4 at 4096^2: 125 / 133 / 128.5 / 127 us
 #endif
@@ -40,6 +42,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   do {                                                                                      \
     if (p.dbg && lane_id() == 0) p.dbg[blockIdx.x * 128 + (base) + ((cnt)++ & 31)] = gtimer(); \
   } while (0)
+// item-indexed variant (ROW1 softmax slots): event e (0..5) of the CTA's k-th item at slot (k % 5) * 6 + e
+#define ATT_TS6(base, k, e)                                                                          \
+  do {                                                                                               \
+    if (p.dbg && lane_id() == 0) p.dbg[blockIdx.x * 128 + (base) + ((k) % 5) * 6 + (e)] = gtimer(); \
+  } while (0)
 
 struct AttnWsArgs {
   int B, H, W, C, heads, w, lw, pt, pl, nwx, nw, pad_mode, patch;
@@ -47,14 +54,18 @@ struct AttnWsArgs {
   int win0, nw_run;  // windows [win0, win0 + nw_run) of every image are run (a window-row range; all by default)
   int lockstep;  // -1: automatic (few items per CTA), 0 / 1 forced (PSCWIN_ATTN_LOCKSTEP knob)
   int tma_out;  // 1: O tiles staged in smem and TMA-stored; 0: 16-byte global stores of the real rows
+  int pf;       // L2 prefetch distance of the TMA producer (items beyond the two staged ones; 0 = off)
+  int pingpong;  // ROW1: the two q-tile slots take turns for their exp passes
   float sl2;
   const __nv_bfloat16 *kx, *ky, *vp;
   __nv_bfloat16* out;
   unsigned long long* dbg;  // debug timeline (PSCWIN_ATTN_TIMELINE), else null
 };
 
-template <int D, bool MASKED>
-__global__ void __launch_bounds__(WS_THREADS, 1)
+// ROW1: one softmax thread per query row (8 softmax warps, 168 registers each: the whole 256-key row in one thread,
+// no cross-thread max / sum exchange); else two threads per row (16 softmax warps at the 96-register cap).
+template <int D, bool MASKED, bool ROW1>
+__global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
     window_attn_ws_kernel(const __grid_constant__ CUtensorMap tmQKV, const __grid_constant__ CUtensorMap tmO,
                           AttnWsArgs p) {
   pdl_trigger();
@@ -76,8 +87,10 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
   uint64_t* o_free = bars + 12;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   float* s_red = reinterpret_cast<float*>(bars + 16);  // [2 q tiles][2 halves][128 rows] partial row max / sum
+  uint64_t* turn = bars + 16;  // ROW1 (no s_red): [2] exp-pass turn of each q-tile slot (ping-pong)
 
   const int warp = warp_id();
+  constexpr int NTQ = ROW1 ? 128 : 256;  // softmax threads per q tile
   const int nt = p.n_tiles;
   const uint32_t tile_tx = (uint32_t)(p.tile_slots * ROWB);
 
@@ -88,12 +101,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       mbar_init(&ld_full[i], 1);
       // a stage is free once its MMAs completed (commit) AND both q-tile slots' O tiles, staged in the slot's Q
       // region of the stage, have been read out by their TMA stores (one arrival per slot)
-      mbar_init(&ld_empty[i], 3);
-      mbar_init(&patch_done[i], 256);  // slot 0's threads patch (slot 1 runs half an item behind)
+      mbar_init(&ld_empty[i], ROW1 ? 4 : 3);
+      mbar_init(&patch_done[i], NTQ);  // slot 0's threads patch (slot 1 runs half an item behind)
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 256);
+      mbar_init(&p_full[i], NTQ);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], 256);
+      mbar_init(&o_free[i], NTQ);
+      if (ROW1) mbar_init(&turn[i], NTQ);
     }
     fence_barrier_init();
   }
@@ -126,9 +140,22 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       const uint64_t pol = policy_evict_first();
       int stage = 0, ev = 0;
       uint32_t phase = 0;
+      // L2 prefetch p.pf items ahead of the loads: a stage is refilled only when its previous item is done, and a
+      // cold item's strided 128-byte rows took ~4 us to land from HBM (timeline r02e) — longer than an item
+      auto prefetch = [&](int item) {
+        if (item >= p.n_items) return;
+        int b, h, X0, Y0;
+        decode(item, b, h, X0, Y0);
+        for (int t = 0; t < nt; ++t) {
+          const int y = Y0 + t * p.rpt;
+          for (int q = 0; q < 3; ++q) tma_prefetch_l2_5d(&tmQKV, 0, q * p.heads + h, X0, y, b);
+        }
+      };
+      for (int k = 2; k < 2 + p.pf; ++k) prefetch(blockIdx.x + k * gridDim.x);
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         int b, h, X0, Y0;
         decode(item, b, h, X0, Y0);
+        if (p.pf) prefetch(item + (2 + p.pf) * gridDim.x);
         mbar_wait(&ld_empty[stage], phase ^ 1);
         ATT_TS(0, ev);
         mbar_arrive_expect_tx(&ld_full[stage], 3 * nt * tile_tx);
@@ -143,6 +170,59 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
           stage = 0;
           phase ^= 1;
         }
+      }
+    }
+  } else if (ROW1 && (warp == 1 || warp == 10)) {
+    // ------------------------------------------------------------------------------------------ MMA issuers (ROW1)
+    // One issuing warp per q-tile slot (warp 1: slot 0, warp 10: slot 1), so neither slot's S / PV MMAs wait behind
+    // the other slot's barriers: per item S_a = Q_a K^T (after the previous item's O_a, which aliases S columns, has
+    // been read out), then O_a = P_a V once P_a is in TMEM, then a commit that releases the stage (4 arrivals: both
+    // issuers' commits and both slots' O stores)
+    const int a = warp == 1 ? 0 : 1;
+    const int NK = nt * p.tile_slots;
+    const uint32_t idesc_s = make_idesc_bf16(128, NK, 0, 0);
+    const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
+    int stage = 0;
+    uint32_t phase = 0, ph_p = 0, ph_of = 0;
+    int ev = 0;
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      int b, h, X0, Y0;
+      decode(item, b, h, X0, Y0);
+      const bool act = q_active(a, Y0);
+      mbar_wait(&ld_full[stage], phase);
+      if (p.patch) mbar_wait(&patch_done[stage], phase);
+      if (a == 0) ATT_TS(32, ev);
+      const uint32_t sb = smem_u32(smem + stage * STAGE);
+      if (act) {
+        mbar_wait(&o_free[a], ph_of ^ 1);
+        ph_of ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t qa = sb + a * TILE, ka = sb + 2 * TILE;
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k)
+            umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT),
+                    make_sdesc(ka + k * 32, 16, SBO, LAYOUT), idesc_s, k > 0);
+          umma_commit(&s_full[a]);
+        }
+        __syncwarp();
+        mbar_wait(&p_full[a], ph_p);
+        ph_p ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t va = sb + 4 * TILE;
+          for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks
+            umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
+                    idesc_o, ks > 0);
+          umma_commit(&o_full[a]);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(&ld_empty[stage]);  // once this slot's MMAs have read the stage
+      __syncwarp();
+      if (++stage == 2) {
+        stage = 0;
+        phase ^= 1;
       }
     }
   } else if (warp == 1) {
@@ -178,8 +258,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
       tc_fence_after();
       if (elect_one()) {
         const uint32_t va = sb + 4 * TILE;
-        for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128)
-          umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (ks >= 8 ? 64 : 0),
+        for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128 unless ROW1)
+          umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (!ROW1 && ks >= 8 ? 64 : 0),
                   make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
         umma_commit(&o_full[a]);
       }
@@ -249,6 +329,245 @@ __global__ void __launch_bounds__(WS_THREADS, 1)
     if (have_prev) {
       if (prev_act1) issue_pv(1, prev_sb);
       release(prev_stage);
+    }
+  } else if constexpr (ROW1) {
+    // ------------------------------------------------------------------------------------------ softmax WGs (ROW1)
+    // 8 warps: q tile a = (warp - 2) >> 2; the thread of TMEM lane `row` owns query row `row` of its q tile and all
+    // of the window's keys: max pass, then exp pass (P bf16 pairs written over consumed S columns: keys 16ks..
+    // at column 8ks), then O read-out, normalisation and the merge / crop store.
+    const int sw = warp - 2;
+    const int a = sw >> 2;
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane_id();        // query slot within the q tile (= TMEM lane)
+    const int gtid = (sw & 3) * 32 + lane_id();      // 0..127 within the q tile's warpgroup
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tmem + 256 * a + lane_base;
+    const uint32_t tO = tmem + 256 * a + 192 + lane_base;
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t ph_s = 0, ph_o = 0;
+    int ev = 0;
+    const int NK = nt * p.tile_slots;                // keys of the window (one S tile): 16, 64 or 256
+    const uint32_t tail_mask = NK >= 32 ? 0xFFFFFFFFu : ((1u << NK) - 1u);  // 16-key windows (w = 4)
+    const float2 sl2 = make_float2(p.sl2, p.sl2);
+    const bool pingpong = p.pingpong && nt == 2;  // (one q tile per window: nothing to alternate with)
+    uint32_t ph_t = 0;
+    int kk = 0;  // this CTA's item count (debug timeline)
+    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++kk) {
+      int b, h, X0, Y0;
+      decode(item, b, h, X0, Y0);
+      const bool active = q_active(a, Y0);
+      if (p.patch && a == 0) {
+        // LEARNABLE pad patch of K/V rows outside the grid by slot 0's 128 threads (slot 1 runs half an item behind
+        // and never touches the stage's shared memory): entry e = key tile e>>7, slot e&127
+        mbar_wait(&ld_full[stage], phase);
+        for (int e = gtid; e < nt * 128; e += 128) {
+          const int kt = e >> 7, r = e & 127;
+          if (r >= p.tile_slots) continue;
+          const int Y = Y0 + kt * p.rpt + (r >> p.lw), X = X0 + (r & (p.w - 1));
+          if (Y < 0 || Y >= p.H || X < 0 || X >= p.W) {
+            uint8_t* sK = smem + stage * STAGE + (2 + kt) * TILE;
+            uint8_t* sV = smem + stage * STAGE + (4 + kt) * TILE;
+            const uint4* kx = reinterpret_cast<const uint4*>(p.kx + ((size_t)(X + p.pl) * p.heads + h) * (D / 2));
+            const uint4* ky = reinterpret_cast<const uint4*>(p.ky + ((size_t)(Y + p.pt) * p.heads + h) * (D / 2));
+            const uint4* vp = reinterpret_cast<const uint4*>(p.vp + (size_t)h * D);
+#pragma unroll
+            for (int c = 0; c < D / 16; ++c) {
+              *reinterpret_cast<uint4*>(sK + swz_offset(r, c, ROWB)) = kx[c];
+              *reinterpret_cast<uint4*>(sK + swz_offset(r, c + D / 16, ROWB)) = ky[c];
+            }
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4*>(sV + swz_offset(r, c, ROWB)) = vp[c];
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&patch_done[stage]);
+        __syncwarp();
+      }
+      if (active) {
+        // MASKED: valid-key bitmask per 32-column chunk (real slots only); columns past the window are never read
+        uint32_t xmask = 0xFFFFFFFFu;
+        int iy_lo = 0, iy_hi = 1 << 30;
+        if (MASKED) {
+          const int xl = max(0, -X0), xh = min(p.w, p.W - X0);
+          xmask = (xh > xl) ? (((1u << (xh - xl)) - 1u) << xl) : 0u;
+          iy_lo = -Y0;
+          iy_hi = p.H - Y0;
+        }
+        auto chunk_mask = [&](int c0) -> uint32_t {
+          uint32_t m = 0;
+          const int rows = 32 >> p.lw;
+#pragma unroll 8
+          for (int rr = 0; rr < rows; ++rr) {
+            const int iy = (c0 >> p.lw) + rr;
+            if (iy >= iy_lo && iy < iy_hi) m |= (xmask & ((1u << p.w) - 1u)) << (rr * p.w);
+          }
+          return m;
+        };
+        mbar_wait(&s_full[a], ph_s);
+        ph_s ^= 1;
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 0);
+        tc_fence_after();
+        // pass 1: row max over the window's keys (two 32-column TMEM loads per wait, four independent max chains)
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        for (int c0 = 0; c0 < NK; c0 += 64) {
+          uint32_t r0[32], r1[32];
+          const bool two = c0 + 32 < NK;
+          tmem_ld32(tS + c0, r0);
+          if (two) tmem_ld32(tS + c0 + 32, r1);
+          tmem_wait_ld();
+          if (MASKED || tail_mask != 0xFFFFFFFFu) {
+            const uint32_t m0 = (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if ((m0 >> j) & 1u) mx4[j & 3] = fmaxf(mx4[j & 3], __uint_as_float(r0[j]));
+            if (two) {
+              const uint32_t m1 = MASKED ? chunk_mask(c0 + 32) : 0xFFFFFFFFu;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((m1 >> j) & 1u) mx4[j & 3] = fmaxf(mx4[j & 3], __uint_as_float(r1[j]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              mx4[(j >> 1) & 3] = fmaxf(mx4[(j >> 1) & 3], fmaxf(__uint_as_float(r0[j]), __uint_as_float(r0[j + 1])));
+            }
+            if (two) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 2)
+                mx4[(j >> 1) & 3] =
+                    fmaxf(mx4[(j >> 1) & 3], fmaxf(__uint_as_float(r1[j]), __uint_as_float(r1[j + 1])));
+            }
+          }
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 1);  // max pass done (debug timeline)
+        const float base = (mx == -INFINITY) ? 0.f : mx * p.sl2;
+        const float2 nb = make_float2(-base, -base);
+        // pass 2: p = 2^(s log2(e)/sqrt(d) - base) (packed fp32x2 scale, MUFU ex2), row sum, P (bf16 pairs) written
+        // over the consumed S columns; 32-column TMEM loads double-buffered (the next chunk's load is in flight
+        // while this one is exponentiated)
+        float2 ls[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // ping-pong: the two slots' exp passes alternate (slot 0 of item i, slot 1 of item i, slot 0 of item i+1,
+        // ...), so one slot's MUFU-bound exponentials overlap the other slot's max pass, MMAs and O read-out instead
+        // of the two contending for the MUFU pipe and then idling together
+        if (pingpong) {
+          mbar_wait(&turn[a], a == 0 ? ph_t ^ 1 : ph_t);
+          ph_t ^= 1;
+        }
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 2);
+        auto exp32 = [&](const uint32_t (&r)[32], uint32_t m, uint32_t (&pk)[16]) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), sl2, nb);
+            float e0, e1;
+            if (kPolyMod > 0 && (j / 2) % kPolyMod == kPolyMod - 1) {
+              const float2 e = exp2_poly2(x);
+              e0 = e.x;
+              e1 = e.y;
+            } else {
+              e0 = ex2_approx(x.x);
+              e1 = ex2_approx(x.y);
+            }
+            if (MASKED || m != 0xFFFFFFFFu) {  // invalid keys, or stale columns past a 16-key window
+              e0 = ((m >> j) & 1u) ? e0 : 0.f;
+              e1 = ((m >> (j + 1)) & 1u) ? e1 : 0.f;
+            }
+            ls[(j >> 1) & 1] = __fadd2_rn(ls[(j >> 1) & 1], make_float2(e0, e1));
+            pk[j / 2] = pack_bf16(e0, e1);
+          }
+        };
+        {
+          uint32_t ra[32], rb[32], pk[16];
+          tmem_ld32(tS, ra);
+          for (int c0 = 0; c0 < NK; c0 += 64) {
+            tmem_wait_ld_dep(ra);
+            const bool two = c0 + 32 < NK;
+            if (two) tmem_ld32(tS + c0 + 32, rb);  // (a 16-key window reads 16 stale columns: masked by tail_mask)
+            exp32(ra, (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask, pk);
+            tmem_st16(tS + c0 / 2, pk);
+            if (two) {
+              tmem_wait_ld_dep(rb);
+              if (c0 + 64 < NK) tmem_ld32(tS + c0 + 64, ra);
+              exp32(rb, MASKED ? chunk_mask(c0 + 32) : 0xFFFFFFFFu, pk);
+              tmem_st16(tS + c0 / 2 + 16, pk);
+            }
+          }
+        }
+        if (pingpong) mbar_arrive(&turn[a ^ 1]);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[a]);
+        const float lsum = (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 3);
+        // O = P V lands in columns [192, 192 + d): copied to registers, the TMEM columns released (the next item's
+        // S may overwrite them), then normalised and written to the grid (merge / crop)
+        mbar_wait(&o_full[a], ph_o);
+        ph_o ^= 1;
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 4);
+        tc_fence_after();
+        uint32_t o0[32], o1[32];
+        tmem_ld32(tO, o0);
+        if constexpr (D == 64) tmem_ld32(tO + 32, o1);
+        tmem_wait_ld();
+        auto oval = [&](int j) { return __uint_as_float(j < 32 ? o0[j] : o1[j - 32]); };  // (j compile-time)
+        tc_fence_before();
+        mbar_arrive(&o_free[a]);
+        const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+        // the normalised O tile is staged in this slot's Q region of the stage (Q_a is dead once S_a has been
+        // computed) and ONE 5-D tensor store writes the window's rows back to the [B,H,W,C] grid; pad rows fall
+        // outside the tensor and are clipped (a box starting at a negative coordinate traps: windows of the first
+        // padded row / column store their real rows directly)
+        if (p.tma_out && X0 >= 0 && Y0 + a * p.rpt >= 0) {
+          uint8_t* so = smem + stage * STAGE + a * TILE;
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) {
+            uint4 v;
+            v.x = pack_bf16(oval(c * 8 + 0) * inv, oval(c * 8 + 1) * inv);
+            v.y = pack_bf16(oval(c * 8 + 2) * inv, oval(c * 8 + 3) * inv);
+            v.z = pack_bf16(oval(c * 8 + 4) * inv, oval(c * 8 + 5) * inv);
+            v.w = pack_bf16(oval(c * 8 + 6) * inv, oval(c * 8 + 7) * inv);
+            *reinterpret_cast<uint4*>(so + swz_offset(row, c, ROWB)) = v;
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1 + a, 128);
+          if (gtid == 0) {
+            tma_store_5d(&tmO, so, 0, h, X0, Y0 + a * p.rpt, b);
+            bulk_commit();
+            bulk_wait_read0();  // the stage's Q region may be refilled once the store has read it
+            mbar_arrive(&ld_empty[stage]);
+          }
+        } else {
+          const int iy = a * p.rpt + (row >> p.lw), ix = row & (p.w - 1);
+          const int Y = Y0 + iy, X = X0 + ix;
+          if (row < p.tile_slots && Y >= 0 && Y < p.H && X >= 0 && X < p.W) {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + (((size_t)b * p.H + Y) * p.W + X) * p.C + (size_t)h * D);
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+              uint4 v;
+              v.x = pack_bf16(oval(c * 8 + 0) * inv, oval(c * 8 + 1) * inv);
+              v.y = pack_bf16(oval(c * 8 + 2) * inv, oval(c * 8 + 3) * inv);
+              v.z = pack_bf16(oval(c * 8 + 4) * inv, oval(c * 8 + 5) * inv);
+              v.w = pack_bf16(oval(c * 8 + 6) * inv, oval(c * 8 + 7) * inv);
+              dst[c] = v;
+            }
+          }
+          if (gtid == 0) mbar_arrive(&ld_empty[stage]);
+        }
+        if (row == 0) ATT_TS6(64 + 32 * a, kk, 5);
+      } else {
+        if (pingpong) {  // an inactive q tile passes its exp turn on
+          mbar_wait(&turn[a], a == 0 ? ph_t ^ 1 : ph_t);
+          ph_t ^= 1;
+          mbar_arrive(&turn[a ^ 1]);
+        }
+        if (gtid == 0) mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
+      }
+      __syncwarp();  // lane 0's store / arrival branch rejoins before the next item's .sync.aligned tcgen05 ops
+      if (++stage == 2) {
+        stage = 0;
+        phase ^= 1;
+      }
     }
   } else {
     // ------------------------------------------------------------------------------------------ softmax WGs
@@ -545,6 +864,10 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   p.tma_out = !direct_store;
   static const int lockstep_knob = getenv("PSCWIN_ATTN_LOCKSTEP") ? atoi(getenv("PSCWIN_ATTN_LOCKSTEP")) : -1;
   p.lockstep = lockstep_knob;
+  static const int pf_knob = env_knob("PSCWIN_ATTN_PF", 0);  // A/B knob: L2 prefetch distance (0 = off)
+  p.pf = pf_knob < 0 ? 0 : pf_knob;
+  static const int pp_knob = env_knob("PSCWIN_ATTN_PINGPONG", 1);  // A/B knob
+  p.pingpong = pp_knob;
   static unsigned long long* dbg_buf = nullptr;
   static const char* tl = getenv("PSCWIN_ATTN_TIMELINE");  // debug knob, read once
   if (tl) {
@@ -571,15 +894,27 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
   const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8 + 1024 * 4;
   const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
   PSCWIN_PROF("window_attention", stream);
-  auto launch = [&](auto kern) {
+  // one softmax thread per query row (default) or two (PSCWIN_ATTN_ROW2=1, the round-1 layout; A/B knob)
+  static const bool row2 = env_knob("PSCWIN_ATTN_ROW2", 0) == 1;
+  auto launch = [&](auto kern, int threads) {
     func_smem_once((const void*)kern, (int)smem);
-    launch_k(kern, dim3(grid), dim3(WS_THREADS), smem, stream, tmQKV, tmO, p);
+    launch_k(kern, dim3(grid), dim3(threads), smem, stream, tmQKV, tmO, p);
   };
   const bool masked = p.pad_mode == 1;
-  if (d == 64)
-    masked ? launch(window_attn_ws_kernel<64, true>) : launch(window_attn_ws_kernel<64, false>);
-  else
-    masked ? launch(window_attn_ws_kernel<32, true>) : launch(window_attn_ws_kernel<32, false>);
+  if (!row2) {
+    if (d == 64)
+      masked ? launch(window_attn_ws_kernel<64, true, true>, WS1_THREADS)
+             : launch(window_attn_ws_kernel<64, false, true>, WS1_THREADS);
+    else
+      masked ? launch(window_attn_ws_kernel<32, true, true>, WS1_THREADS)
+             : launch(window_attn_ws_kernel<32, false, true>, WS1_THREADS);
+  } else if (d == 64) {
+    masked ? launch(window_attn_ws_kernel<64, true, false>, WS_THREADS)
+           : launch(window_attn_ws_kernel<64, false, false>, WS_THREADS);
+  } else {
+    masked ? launch(window_attn_ws_kernel<32, true, false>, WS_THREADS)
+           : launch(window_attn_ws_kernel<32, false, false>, WS_THREADS);
+  }
   if (tl) {  // debug: dump the per-CTA phase timeline (globaltimer ns)
     static unsigned long long host[148 * 128];
     cudaMemcpyAsync(host, dbg_buf, sizeof(host), cudaMemcpyDeviceToHost, stream);

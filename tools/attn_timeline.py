@@ -22,30 +22,29 @@ for shift in (0, 8):
         pl.window_attention(d, qkv, qp)
     torch.cuda.synchronize()
 raw = np.fromfile(path, dtype=np.uint64).reshape(-1, 148, 128).astype(np.int64)
+row2 = os.environ.get("PSCWIN_ATTN_ROW2") == "1"
+names = ["S->max", "max->turn", "exp", "P->O", "O->end", "end->nextS"]
 for run in (2, 5):
     t = raw[run]
     t0 = t[t > 0].min()
     print(f"--- run {run} (shift {'8' if run >= 3 else '0'}), kernel span {(t[t>0].max()-t0)/1e3:.1f} us")
-    for cta in (0, 1, 100, 147):
-        row = t[cta]
-        def ev(base):
-            v = row[base:base + 32]; v = v[v > 0]; return ((v - t0) / 1e3).round(2).tolist()
-        print(f"cta {cta}: load {ev(0)[:12]}\n   mma {ev(32)[:12]}\n   wg0 {ev(64)[:12]}\n   wg1 {ev(96)[:12]}")
-    # steady-state per-item spacing of slot 0's "S ready" events (every 4th wg0 event), median over CTAs
-    gaps = []
-    for cta in range(148):
-        v = np.sort(t[cta][64:96]); v = v[v > 0]
-        if len(v) >= 12:
-            s = v[::5]
-            gaps.append(np.median(np.diff(s)) / 1e3)
-    if gaps:
-        print(f"median per-item period (slot 0): {np.median(gaps):.2f} us over {len(gaps)} CTAs")
-    # median phase durations of slot 0: S ready -> max done -> P written -> O ready -> O stored -> next S ready
-    ph = [[] for _ in range(5)]
-    for cta in range(148):
-        v = np.sort(t[cta][64:96]); v = v[v > 0]
-        for i in range(0, len(v) - 5, 5):
-            for k in range(5):
-                ph[k].append((v[i + k + 1] - v[i + k]) / 1e3)
-    names = ["max pass", "exp pass", "PV wait", "O readout+store", "to next S"]
-    print("slot-0 phase medians (us): " + ", ".join(f"{n} {np.median(x):.2f}" for n, x in zip(names, ph) if x))
+    if row2:
+        continue
+    # ROW1: slot a's events of its k-th item at 64 + 32a + (k % 5) * 6 + e, e = S ready, max done, exp turn,
+    # P written, O ready, end
+    for a in (0, 1):
+        ph = [[] for _ in range(6)]
+        per = []
+        for cta in range(148):
+            ev = t[cta][64 + 32 * a: 64 + 32 * a + 30].reshape(5, 6)
+            ok = [i for i in range(5) if np.all(ev[i] > 0)]
+            items = sorted(ok, key=lambda i: ev[i][0])
+            for j, i in enumerate(items):
+                for e in range(5):
+                    ph[e].append((ev[i][e + 1] - ev[i][e]) / 1e3)
+                if j + 1 < len(items):
+                    nxt = ev[items[j + 1]][0]
+                    ph[5].append((nxt - ev[i][5]) / 1e3)
+                    per.append((nxt - ev[i][0]) / 1e3)
+        print(f"slot {a}: period {np.median(per):.2f} us; phase medians: " +
+              ", ".join(f"{n} {np.median(x):.2f}" for n, x in zip(names, ph) if x))

@@ -33,6 +33,18 @@ __global__ void kern(float* out, int iters, long long* clk) {
         h = ex2b2(h) ^ 0x80008000u;
         a[i] = __uint_as_float(h);
       }
+      if (MODE == 6) {  // F2FP: cvt.rn.bf16x2.f32 (the softmax's P pack), chained through a LOP3
+        uint32_t h;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(a[i]), "f"(b[i].x));
+        a[i] = __uint_as_float(h & 0x3f7f3f7fu);
+      }
+      if (MODE == 7) {  // softmax mix per pair: FFMA2 scale, 2 MUFU ex2, FADD2 sum, F2FP pack
+        const float2 x = __ffma2_rn(b[i], m, c);
+        const float2 e = make_float2(ex2(x.x), ex2(x.y));
+        uint32_t h;
+        asm volatile("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(e.x), "f"(e.y));
+        b[i] = __fadd2_rn(e, make_float2(__uint_as_float(h & 0x3f7f3f7fu), 0.f));
+      }
       if (MODE == 3) {                                                 // scan pass-2 mix per pair: 2 MUFU, 3 FMUL2, 3 FFMA2
         float2 x = __fmul2_rn(b[i], m);
         float2 e = make_float2(ex2(x.x), ex2(x.y));
@@ -53,12 +65,12 @@ __global__ void kern(float* out, int iters, long long* clk) {
 }
 
 template <int MODE>
-void run(const char* name, double ops_per_inner, int threads) {
+void run(const char* name, double ops_per_inner, int threads, int per_sm = 2048) {
   float* out; long long* clk;
   cudaMalloc(&out, 148 * 8 * 1024 * 4);
   cudaMalloc(&clk, 8);
   const int iters = 4096;
-  const int blocks = 148 * (2048 / threads);
+  const int blocks = 148 * (per_sm / threads);
   kern<MODE><<<blocks, threads>>>(out, 16, clk);
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
@@ -71,7 +83,7 @@ void run(const char* name, double ops_per_inner, int threads) {
   long long c; cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
   double total = (double)blocks * threads * iters * 16 * ops_per_inner;
   // per-SM per-clock from the cycle count of block 0 (blocks resident at once: 2048 threads / SM)
-  double per_sm_clk = (double)(2048) * iters * 16 * ops_per_inner / (double)c;
+  double per_sm_clk = (double)(per_sm) * iters * 16 * ops_per_inner / (double)c;
   printf("%-10s %8.3f ms  %8.1f G/s  %6.2f per SM-clk (clk %lld)\n", name, ms, total / ms / 1e6, per_sm_clk, c);
   cudaFree(out); cudaFree(clk);
 }
@@ -83,5 +95,14 @@ int main() {
   run<3>("scanmix/el", 2, 256);
   run<4>("ex2.f16x2(el)", 2, 256);
   run<5>("ex2.bf16x2(el)", 2, 256);
+  run<6>("f2fp.bf16x2", 1, 256);
+  run<7>("smaxmix/el", 2, 256);
+  // few warps per SM sub-partition (the attention softmax runs one or two warps per SMSP per q tile)
+  run<0>("ex2 1w/SMSP", 1, 128, 128);
+  run<0>("ex2 2w/SMSP", 1, 256, 256);
+  run<0>("ex2 4w/SMSP", 1, 512, 512);
+  run<7>("smax 1w/SMSP", 2, 128, 128);
+  run<7>("smax 2w/SMSP", 2, 256, 256);
+  run<7>("smax 4w/SMSP", 2, 512, 512);
   return 0;
 }
