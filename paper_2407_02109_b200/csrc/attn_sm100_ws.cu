@@ -352,38 +352,46 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
     const float2 sl2 = make_float2(p.sl2, p.sl2);
     const bool pingpong = p.pingpong && nt == 2;  // (one q tile per window: nothing to alternate with)
     uint32_t ph_t = 0;
+    // LEARNABLE pad patch of the K/V rows outside the grid by slot 0's 128 threads (slot 1 only reads the stage
+    // through its MMAs, after patch_done): entry e = key tile e>>7, slot e&127. It runs one item ahead — the next
+    // item's stage is patched while this item's PV MMA runs — so the next S MMA does not wait for it.
+    auto patch = [&](int pitem, int pstage, uint32_t pphase) {
+      int b, h, X0, Y0;
+      decode(pitem, b, h, X0, Y0);
+      mbar_wait(&ld_full[pstage], pphase);
+      for (int e = gtid; e < nt * 128; e += 128) {
+        const int kt = e >> 7, r = e & 127;
+        if (r >= p.tile_slots) continue;
+        const int Y = Y0 + kt * p.rpt + (r >> p.lw), X = X0 + (r & (p.w - 1));
+        if (Y < 0 || Y >= p.H || X < 0 || X >= p.W) {
+          uint8_t* sK = smem + pstage * STAGE + (2 + kt) * TILE;
+          uint8_t* sV = smem + pstage * STAGE + (4 + kt) * TILE;
+          const uint4* kx = reinterpret_cast<const uint4*>(p.kx + ((size_t)(X + p.pl) * p.heads + h) * (D / 2));
+          const uint4* ky = reinterpret_cast<const uint4*>(p.ky + ((size_t)(Y + p.pt) * p.heads + h) * (D / 2));
+          const uint4* vp = reinterpret_cast<const uint4*>(p.vp + (size_t)h * D);
+#pragma unroll
+          for (int c = 0; c < D / 16; ++c) {
+            *reinterpret_cast<uint4*>(sK + swz_offset(r, c, ROWB)) = kx[c];
+            *reinterpret_cast<uint4*>(sK + swz_offset(r, c + D / 16, ROWB)) = ky[c];
+          }
+#pragma unroll
+          for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4*>(sV + swz_offset(r, c, ROWB)) = vp[c];
+        }
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&patch_done[pstage]);
+      __syncwarp();
+    };
+    auto patch_next = [&](int item) {  // the stage after `stage` holds item + gridDim.x
+      if (p.patch && a == 0 && item + (int)gridDim.x < p.n_items)
+        patch(item + gridDim.x, stage ^ 1, stage == 1 ? phase ^ 1 : phase);
+    };
+    if (p.patch && a == 0 && (int)blockIdx.x < p.n_items) patch(blockIdx.x, 0, 0);
     int kk = 0;  // this CTA's item count (debug timeline)
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++kk) {
       int b, h, X0, Y0;
       decode(item, b, h, X0, Y0);
       const bool active = q_active(a, Y0);
-      if (p.patch && a == 0) {
-        // LEARNABLE pad patch of K/V rows outside the grid by slot 0's 128 threads (slot 1 runs half an item behind
-        // and never touches the stage's shared memory): entry e = key tile e>>7, slot e&127
-        mbar_wait(&ld_full[stage], phase);
-        for (int e = gtid; e < nt * 128; e += 128) {
-          const int kt = e >> 7, r = e & 127;
-          if (r >= p.tile_slots) continue;
-          const int Y = Y0 + kt * p.rpt + (r >> p.lw), X = X0 + (r & (p.w - 1));
-          if (Y < 0 || Y >= p.H || X < 0 || X >= p.W) {
-            uint8_t* sK = smem + stage * STAGE + (2 + kt) * TILE;
-            uint8_t* sV = smem + stage * STAGE + (4 + kt) * TILE;
-            const uint4* kx = reinterpret_cast<const uint4*>(p.kx + ((size_t)(X + p.pl) * p.heads + h) * (D / 2));
-            const uint4* ky = reinterpret_cast<const uint4*>(p.ky + ((size_t)(Y + p.pt) * p.heads + h) * (D / 2));
-            const uint4* vp = reinterpret_cast<const uint4*>(p.vp + (size_t)h * D);
-#pragma unroll
-            for (int c = 0; c < D / 16; ++c) {
-              *reinterpret_cast<uint4*>(sK + swz_offset(r, c, ROWB)) = kx[c];
-              *reinterpret_cast<uint4*>(sK + swz_offset(r, c + D / 16, ROWB)) = ky[c];
-            }
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4*>(sV + swz_offset(r, c, ROWB)) = vp[c];
-          }
-        }
-        fence_proxy_async_smem();
-        mbar_arrive(&patch_done[stage]);
-        __syncwarp();
-      }
       if (active) {
         // MASKED: valid-key bitmask per 32-column chunk (real slots only); columns past the window are never read
         uint32_t xmask = 0xFFFFFFFFu;
@@ -498,6 +506,7 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[a]);
+        patch_next(item);
         const float lsum = (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
         if (row == 0) ATT_TS6(64 + 32 * a, kk, 3);
         // O = P V lands in columns [192, 192 + d): copied to registers, the TMEM columns released (the next item's
@@ -562,6 +571,7 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
           mbar_arrive(&turn[a ^ 1]);
         }
         if (gtid == 0) mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
+        patch_next(item);
       }
       __syncwarp();  // lane 0's store / arrival branch rejoins before the next item's .sync.aligned tcgen05 ops
       if (++stage == 2) {
