@@ -45,6 +45,7 @@ struct ScanParams {
   float* hs;         // [B, n_chunks, D, N]
   __nv_bfloat16* out;
   long long ld_out;
+  int vec_out;  // pass 2 may store 16-byte vectors of 8 channels (ld_out % 8 == 0, 16-byte aligned out)
   // band mode (window-row sharding): the k-1 xin rows preceding this segment in the cycled sequence
   // (the previous rank's tail; rank 0: the global sequence tail) replace the local wrap-around; null = one segment
   const __nv_bfloat16* hist;
@@ -939,7 +940,36 @@ __global__ void __launch_bounds__(DPB * NS, NS == 2 ? PSCWIN_PASS2_MINB : 1) sca
     } else {
       for (int j = 0; j < nt; ++j) tstep(j);
     }
-    if constexpr (NS > 1) {
+    if (NS == 2 && TSUB * DPB / 8 == NT && p.vec_out) {
+      // deferred reduction, vectorised: thread (token j = tid / 8, channel group cg = tid % 8) finishes 8 channels of
+      // one token from shared memory (partials of both state halves, v, gate: 16-byte reads) and writes them with
+      // one 16-byte store (ld_out % 8 == 0 is checked on the host; the per-channel 2-byte stores were ~7 % of the
+      // kernel's stall samples, ncu r02f)
+      __syncthreads();
+      const int j = threadIdx.x >> 3, cg = (threadIdx.x & 7) * 8;
+      if (j < nt) {
+        const float4* r0 = reinterpret_cast<const float4*>(red + (j * NS) * RSTR + cg);
+        const float4* r1 = reinterpret_cast<const float4*>(red + (j * NS + 1) * RSTR + cg);
+        const float4 a0 = r0[0], a1 = r0[1], b0 = r1[0], b1 = r1[1];
+        const float y[8] = {a0.x + b0.x, a0.y + b0.y, a0.z + b0.z, a0.w + b0.w,
+                            a1.x + b1.x, a1.y + b1.y, a1.z + b1.z, a1.w + b1.w};
+        const uint4 vv = *reinterpret_cast<const uint4*>(sv + j * DPB + cg);
+        const uint4 gg = p.gz ? *reinterpret_cast<const uint4*>(sz + j * DPB + cg)
+                              : make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);  // bf16 1.0
+        const float4 k0 = __ldg(reinterpret_cast<const float4*>(p.d_skip + d0 + cg));  // (L1-resident)
+        const float4 k1 = __ldg(reinterpret_cast<const float4*>(p.d_skip + d0 + cg + 4));
+        const float d3v[8] = {3.f * k0.x, 3.f * k0.y, 3.f * k0.z, 3.f * k0.w, 3.f * k1.x, 3.f * k1.y, 3.f * k1.z, 3.f * k1.w};
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(&vv);
+        const uint32_t* gw = reinterpret_cast<const uint32_t*>(&gg);
+        uint4 o;
+        uint32_t* ow = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ow[q] = pack_bf16(fmaf(d3v[2 * q], bf16_lo(vw[q]), y[2 * q]) * bf16_lo(gw[q]),
+                            fmaf(d3v[2 * q + 1], bf16_hi(vw[q]), y[2 * q + 1]) * bf16_hi(gw[q]));
+        *reinterpret_cast<uint4*>(p.out + (tok0 + ts + j) * p.ld_out + d0 + cg) = o;
+      }
+    } else if constexpr (NS > 1) {
       // deferred reduction: partial sums to shared memory, then thread `sub` of each channel finishes the tokens
       // j = sub, sub + NS, ... (y = sum of the NS partials + 3 D v, gate, bf16 store)
       __syncthreads();
@@ -1244,6 +1274,7 @@ static ScanParams make_scan_params(const ScanPlan& pl, int B, int L, int D, int 
   p.hs = reinterpret_cast<float*>(base + pl.hs);
   p.out = out;
   p.ld_out = ld_out;
+  p.vec_out = (ld_out % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
   p.hist = nullptr;
   return p;
 }
