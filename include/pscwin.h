@@ -253,8 +253,11 @@ int pscwin_neck(const pscwin_neck_desc* desc, const void* const* stage_outs, con
  * Phase order: [cycle-scan layer: scan_begin, ring(hist), scan_mid, allgather(rec), scan_end]
  *              attn_begin, halo exchange, attn_end.
  * x_band, x_out [rows, W, C] bf16 (x_out may not alias x_band). Results equal pscwin_forward on the whole
- * image up to fp32 summation order in the scan (bit-identical elsewhere). bf16 only; scan_order ROW_MAJOR only
- * (other orders do not give contiguous segments: ERR_CONTRACT). Workspace: pscwin_band_workspace_bytes. */
+ * image up to fp32 summation order in the scan (bit-identical elsewhere). bf16 only; scan_order ROW_MAJOR, or
+ * WINDOW_MAJOR when H, W and both band edges are multiples of the window (a band of whole window rows is then a
+ * contiguous run of the window-major sequence, scanned in band-local window-major order; the exchanged conv
+ * history is the last k-1 tokens in that order); COL_MAJOR gives no contiguous segments: ERR_CONTRACT.
+ * Workspace: pscwin_band_workspace_bytes. */
 typedef struct {
   int32_t row_begin, row_end;  /* this rank's token rows [row_begin, row_end) */
   int32_t rank, world;

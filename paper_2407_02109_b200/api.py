@@ -301,21 +301,39 @@ class HRSAMEncoder:
 
         enc = HRSAMEncoder(layers, ends_weights, B, H, W, stage_ends=(2, 5, 8, 11))
         emb = enc(img)     # img [B, 3, 16H, 16W] bf16 -> [B, H, W, 256]
+
+    HRSAM++ (reading Q20 / Q22): pass `scales=[(H, W), (H1, W1), ...]` (scale 0 = the main grid, e.g. the
+    512^2 overview image as (32, 32)) and PSCWinMSLayer layers; every scale's image is patch-embedded straight into
+    its slice of the packed [B * sum H_s W_s, C] sequence, the layers run on the packed sequence, and the neck fuses
+    each scale's stage sum, resizing the other scales onto the main grid before the conv block.
+
+        enc = HRSAMEncoder(ms_layers, ends, B, 64, 64, scales=[(64, 64), (32, 32)])
+        emb = enc([img_1024, img_512])   # -> [B, 64, 64, 256]
     """
 
     def __init__(self, layers, ends: Dict[str, torch.Tensor], B: int, H: int, W: int, stage_ends=(2, 5, 8, 11),
-                 C: int = 768, C_out: int = 256, graph: bool = True):
+                 C: int = 768, C_out: int = 256, graph: bool = True, scales=None):
         dev = ends["w_patch"].device
         self.layers, self.ends, self.stage_ends = list(layers), ends, tuple(stage_ends)
-        self.img = torch.empty(B, 3, 16 * H, 16 * W, dtype=torch.bfloat16, device=dev)
-        self.x0 = torch.empty(B, H, W, C, dtype=torch.bfloat16, device=dev)
+        self.scales = [(H, W)] if scales is None else [tuple(s) for s in scales]
+        if self.scales[0] != (H, W):
+            raise ValueError("scale 0 is the main grid (H, W)")
+        T = B * sum(h * w for h, w in self.scales)
+        self.imgs = [torch.empty(B, 3, 16 * h, 16 * w, dtype=torch.bfloat16, device=dev) for h, w in self.scales]
+        self.img = self.imgs[0]
+        self.x0 = torch.empty(T, C, dtype=torch.bfloat16, device=dev)
         self.bufs = [torch.empty_like(self.x0), torch.empty_like(self.x0)]
         self.stage = [torch.empty_like(self.x0) for _ in self.stage_ends]
-        self.desc = NeckDesc.make(B, C, C_out, [(H, W)], n_stages=len(self.stage_ends))
-        self.ws_pe = Workspace(int(lib().pscwin_patch_embed_workspace_bytes(B, H, W)), dev)
+        self.desc = NeckDesc.make(B, C, C_out, self.scales, n_stages=len(self.stage_ends))
+        self.ws_pe = Workspace(max(int(lib().pscwin_patch_embed_workspace_bytes(B, h, w)) for h, w in self.scales), dev)
         self.ws_neck = Workspace(neck_workspace_bytes(self.desc), dev)
         self.out = torch.empty(B, H, W, C_out, dtype=torch.bfloat16, device=dev)
         self.w_patch = ends["w_patch"].reshape(C, -1).contiguous()
+        # packed rows of scale s: [B * off_s, B * off_{s+1}) as a [B, H_s, W_s, C] grid
+        off = [0]
+        for h, w in self.scales:
+            off.append(off[-1] + h * w)
+        self.x0_views = [self.x0[B * off[i]:B * off[i + 1]].view(B, h, w, C) for i, (h, w) in enumerate(self.scales)]
         from ._lib import launch_count
         n0 = launch_count()
         self._run()
@@ -330,9 +348,10 @@ class HRSAMEncoder:
             self.graph = g
 
     def _run(self):
-        check(lib().pscwin_patch_embed(_ptr(self.img), self.x0.shape[0], self.x0.shape[1], self.x0.shape[2],
-                                       self.x0.shape[3], _ptr(self.w_patch), _ptr(self.ends["b_patch"]),
-                                       _ptr(self.x0), self.ws_pe.ptr, self.ws_pe.nbytes, _stream()), "patch_embed")
+        for img, xv in zip(self.imgs, self.x0_views):
+            check(lib().pscwin_patch_embed(_ptr(img), xv.shape[0], xv.shape[1], xv.shape[2], xv.shape[3],
+                                           _ptr(self.w_patch), _ptr(self.ends["b_patch"]), _ptr(xv), self.ws_pe.ptr,
+                                           self.ws_pe.nbytes, _stream()), "patch_embed")
         cur, k = self.x0, 0
         for j, layer in enumerate(self.layers):
             if j in self.stage_ends:
@@ -345,8 +364,12 @@ class HRSAMEncoder:
         neck(self.desc, self.stage, self.ends, ws=self.ws_neck, out=self.out)
         return self.out
 
-    def __call__(self, img: torch.Tensor) -> torch.Tensor:
-        self.img.copy_(img, non_blocking=True)
+    def __call__(self, img) -> torch.Tensor:
+        imgs = img if isinstance(img, (list, tuple)) else [img]
+        if len(imgs) != len(self.imgs):
+            raise ValueError(f"{len(self.imgs)} images expected (one per scale)")
+        for dst, src in zip(self.imgs, imgs):
+            dst.copy_(src, non_blocking=True)
         if self.graph is not None:
             self.graph.replay()
         else:

@@ -875,6 +875,7 @@ pscwin_layer_desc sub_desc(const pscwin_layer_desc* d, int rows, int sy) {
 
 struct BandWs {
   size_t u, qkv, qkv_pad, O, pad_tab, h, xz, g, x1, hist_send, hist_recv, rec_send, rec_recv, scan, total;
+  size_t xzp, gs;  // window-major scan order: xz rows gathered into scan order, gated output in scan order
   size_t row_bytes_qkv;
   int D, N, R;
 };
@@ -903,6 +904,10 @@ BandWs plan_band(const pscwin_layer_desc* d, const pscwin_band* b, const BandGeo
     w.R = d->ssm_dt_rank > 0 ? d->ssm_dt_rank : (d->C + 15) / 16;
     const int k = d->ssm_conv;
     w.xz = take(T * 2 * w.D * 2);
+    if (d->scan_order == PSCWIN_SCAN_WINDOW_MAJOR) {
+      w.xzp = take(T * 2 * w.D * 2);
+      w.gs = take(T * w.D * 2);
+    }
     w.g = take(T * w.D * 2);
     w.x1 = take(T * C * 2);
     w.hist_send = take((size_t)(k - 1) * w.D * 2);
@@ -919,9 +924,16 @@ int band_check(const pscwin_layer_desc* d, const pscwin_band* b, BandGeo* g) {
   int rc = check_layer(d);
   if (rc) return rc;
   if (d->dtype != PSCWIN_BF16) return PSCWIN_ERR_UNSUPPORTED;  // bands run the bf16 product path
-  if (d->cycle_scan && d->scan_order != PSCWIN_SCAN_ROW_MAJOR) return PSCWIN_ERR_CONTRACT;  // contiguous segments
+  // a band's scan segment must be contiguous: row-major raster always; window-major when the band is whole window
+  // rows of a window-divisible grid (its windows are then a contiguous run of the window-major sequence, scanned
+  // in band-local window-major order); column-major never
+  if (d->cycle_scan && d->scan_order == PSCWIN_SCAN_COL_MAJOR) return PSCWIN_ERR_CONTRACT;
   *g = band_geo(d, b);
-  return g->ok ? PSCWIN_OK : PSCWIN_ERR_CONTRACT;
+  if (!g->ok) return PSCWIN_ERR_CONTRACT;
+  if (d->cycle_scan && d->scan_order == PSCWIN_SCAN_WINDOW_MAJOR &&
+      (d->H % d->window || d->W % d->window || g->r0 % d->window || g->r1 % d->window))
+    return PSCWIN_ERR_CONTRACT;
+  return PSCWIN_OK;
 }
 }  // namespace
 
@@ -989,7 +1001,13 @@ int pscwin_band_scan_begin(const pscwin_layer_desc* d, const pscwin_band* b, con
   a.epi = EPI_STORE_BF16;
   a.silu_col = D;
   if (launch_gemm_bf16(u, wt->w_in, a, s)) return PSCWIN_ERR_CUDA;
-  // conv history for the next rank: this band's last k-1 xin rows
+  if (d->scan_order == PSCWIN_SCAN_WINDOW_MAJOR) {  // [xin | SiLU(z)] rows into band-local window-major order
+    __nv_bfloat16* xzp = reinterpret_cast<__nv_bfloat16*>(wsp(ws, w.xzp));
+    if (launch_permute_rows(xz, 2 * D, xzp, 2 * D, 1, g.rows, d->W, 2 * D, d->scan_order, d->window, 0, s))
+      return PSCWIN_ERR_CUDA;
+    xz = xzp;
+  }
+  // conv history for the next rank: this band's last k-1 xin rows (in scan order)
   if (k > 1 && cudaMemcpy2DAsync(wsp(ws, w.hist_send), (size_t)D * 2, xz + (T - (k - 1)) * 2 * D, (size_t)2 * D * 2,
                                  (size_t)D * 2, k - 1, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return PSCWIN_ERR_CUDA;
@@ -1006,7 +1024,8 @@ int pscwin_band_scan_mid(const pscwin_layer_desc* d, const pscwin_band* b, const
   const BandWs w = plan_band(d, b, g);
   if (!ws || ws_bytes < w.total) return PSCWIN_ERR_WORKSPACE;
   const long long T = (long long)g.rows * d->W;
-  const __nv_bfloat16* xz = reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.xz));
+  const __nv_bfloat16* xz =
+      reinterpret_cast<const __nv_bfloat16*>(wsp(ws, d->scan_order == PSCWIN_SCAN_WINDOW_MAJOR ? w.xzp : w.xz));
   return band_scan_mid((int)T, w.D, w.N, w.R, d->ssm_conv, g.P, d->bbar_mode, xz, 2 * w.D,
                        reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.hist_recv)), (const float*)wt->conv_w,
                        (const float*)wt->conv_b, wt->w_x, (const float*)wt->w_dt, (const float*)wt->b_dt, wt->a_log,
@@ -1025,13 +1044,19 @@ int pscwin_band_scan_end(const pscwin_layer_desc* d, const pscwin_band* b, const
   cudaStream_t s = (cudaStream_t)stream;
   const long long T = (long long)g.rows * d->W;
   const int C = d->C, D = w.D;
-  const __nv_bfloat16* xz = reinterpret_cast<const __nv_bfloat16*>(wsp(ws, w.xz));
-  __nv_bfloat16* gb = reinterpret_cast<__nv_bfloat16*>(wsp(ws, w.g));
+  const bool wm = d->scan_order == PSCWIN_SCAN_WINDOW_MAJOR;
+  const __nv_bfloat16* xz = reinterpret_cast<const __nv_bfloat16*>(wsp(ws, wm ? w.xzp : w.xz));
+  __nv_bfloat16* gb = reinterpret_cast<__nv_bfloat16*>(wsp(ws, wm ? w.gs : w.g));
   rc = band_scan_end((int)T, D, w.N, w.R, d->ssm_conv, g.P, d->bbar_mode, xz, 2 * D, xz + D, 2 * D,
                      (const float*)wt->conv_w, (const float*)wt->conv_b, (const float*)wt->w_dt,
                      (const float*)wt->b_dt, wt->a_log, wt->d_skip, reinterpret_cast<const float*>(wsp(ws, w.rec_recv)),
                      b->rank, b->world, gb, D, wsp(ws, w.scan), w.total - w.scan, s);
   if (rc) return rc;
+  if (wm) {  // gated output rows back to grid order for the out-projection's residual
+    __nv_bfloat16* g_grid = reinterpret_cast<__nv_bfloat16*>(wsp(ws, w.g));
+    if (launch_permute_rows(gb, D, g_grid, D, 1, g.rows, d->W, D, d->scan_order, d->window, 1, s)) return PSCWIN_ERR_CUDA;
+    gb = g_grid;
+  }
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.prof_name = "gemm_out_proj_scan";

@@ -218,6 +218,17 @@ __global__ void __launch_bounds__(256) permute_rows_kernel(const __nv_bfloat16* 
   *reinterpret_cast<uint4*>(dst + to * ld_dst + c) = *reinterpret_cast<const uint4*>(src + from * ld_src + c);
 }
 
+int launch_permute_rows(const __nv_bfloat16* src, long long ld_src, __nv_bfloat16* dst, long long ld_dst, int B, int H,
+                        int W, int D, int order, int w, int scatter, cudaStream_t s) {
+  if (D % 8) return -1;
+  const long long n = (long long)B * H * W * (D / 8);
+  if (n == 0) return 0;
+  PSCWIN_PROF(scatter ? "scan_order_scatter" : "scan_order_gather", s);
+  launch_k(permute_rows_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, src, ld_src, dst, ld_dst, B, H, W, D,
+           order, w, scatter);
+  return (int)cudaGetLastError();
+}
+
 // Multi-scale row gather / scatter (HRSAM++ multi-scale cycle scan): sequence row (b, t) of the per-sample
 // concatenation of every scale's scan-order sequence <-> packed row B*off[s] + b*L_s + pi_s(t - off[s]) of the
 // scale-outermost packing (reading Q20). ncols % 8 == 0.

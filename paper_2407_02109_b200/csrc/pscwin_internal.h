@@ -100,6 +100,10 @@ int launch_partition(const void* x, const void* pad_row, int B, int H, int W, in
 int launch_merge(const void* win, int B, int H, int W, int Cx, int w, int sx, int sy, const void* residual,
                  int is_f32, void* out, cudaStream_t stream);
 int launch_gemm_bf16(const void* A, const void* B, const GemmArgs& args, cudaStream_t stream);
+// bf16 row gather (scan order <- grid order, scatter = 0) or scatter (grid order <- scan order) of B [H, W] grids of
+// D-channel rows in the given scan order (cyclescan.cu)
+int launch_permute_rows(const __nv_bfloat16* src, long long ld_src, __nv_bfloat16* dst, long long ld_dst, int B, int H,
+                        int W, int D, int order, int w, int scatter, cudaStream_t s);
 int launch_row_stats(const void* x, long long rows, int C, float eps, float2* stats, cudaStream_t stream);
 int launch_ln_fold(const void* W, int N, int K, const float* g, const float* beta, const float* bias, void* Wf,
                    float* s, float* c, cudaStream_t stream);

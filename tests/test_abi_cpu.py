@@ -118,6 +118,13 @@ def test_band_plan_and_io_offsets(pl):
     assert L.pscwin_band_io_offsets(ctypes.byref(ok), ctypes.byref(BandDesc(24, 34, 2, 3)), ctypes.byref(BandIO())) == 0
     col = LayerDesc.from_config(cfg.replace(scan_order=synth.SCAN_COL_MAJOR))
     assert L.pscwin_band_workspace_bytes(ctypes.byref(col), ctypes.byref(BandDesc(0, 32, 0, 8))) == 0
+    # window-major: bands of whole window rows of a window-divisible grid are contiguous segments (and need the
+    # permuted xz / gated-output buffers on top of the row-major plan); a ragged grid is rejected
+    wm = LayerDesc.from_config(cfg.replace(scan_order=synth.SCAN_WINDOW_MAJOR))
+    assert (L.pscwin_band_workspace_bytes(ctypes.byref(wm), ctypes.byref(BandDesc(32, 64, 1, 8))) >
+            L.pscwin_band_workspace_bytes(ctypes.byref(d), ctypes.byref(BandDesc(32, 64, 1, 8))) > 0)
+    wm_ragged = LayerDesc.from_config(synth.tiny(H=36, W=16, cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR))
+    assert L.pscwin_band_workspace_bytes(ctypes.byref(wm_ragged), ctypes.byref(BandDesc(24, 36, 2, 3))) == 0
 
 
 @pytest.mark.parametrize("scales,w,sx,sy", [([(4, 4), (2, 2)], 2, 0, 0), ([(16, 16), (8, 8), (24, 8)], 8, 4, 4),

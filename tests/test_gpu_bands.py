@@ -33,11 +33,14 @@ CASES = [
     (synth.tiny(H=32, W=16, cycle_scan=1, bbar_mode=synth.BBAR_EULER), 3),
     (synth.vitb(64, cycle_scan=1), 4),                                     # ViT-B 1024^2 as 4 bands
     (synth.tiny(H=32, W=16, cycle_scan=1, mlp_hidden=256), 2),             # CS + S + FFN
+    (synth.tiny(H=32, W=16, cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR), 4),   # window-major segments
+    (synth.tiny(H=48, W=24, cycle_scan=1, shift_x=0, shift_y=0, scan_order=synth.SCAN_WINDOW_MAJOR), 3),
 ]
 
 
 @pytest.mark.parametrize("cfg,world", CASES, ids=lambda c: str(c) if isinstance(c, int) else
-                         f"{c.H}x{c.W}C{c.C}s{c.shift_x},{c.shift_y}m{c.pad_mode}cs{c.cycle_scan}b{c.bbar_mode}f{c.mlp_hidden}")
+                         f"{c.H}x{c.W}C{c.C}s{c.shift_x},{c.shift_y}m{c.pad_mode}cs{c.cycle_scan}b{c.bbar_mode}f{c.mlp_hidden}"
+                         f"o{c.scan_order}")
 def test_bands_equal_whole_image(pl, cfg, world):
     import torch
     from paper_2407_02109_b200.bands import LoopbackBands

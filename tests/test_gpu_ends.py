@@ -105,3 +105,50 @@ def test_hrsam_encoder_tiny(pl):
     ref = oracle.encoder_neck(stages, ends)
     assert got.shape == (1, H, W, 64)
     assert rel_err(got, ref) < BF16_TOL
+
+
+def test_hrsampp_encoder_tiny(pl):
+    # HRSAM++ (P:L174-189): main 16x16 grid + 8x8 overview (the 512^2-overview role at tiny scale), each image
+    # patch-embedded into its slice of the packed sequence -> 6 multi-scale blocks (P, S, CS+P, S, P, CS+S; the
+    # cycle-scan blocks single-scale, each stage closed by a multi-scale cycle-scan module) -> neck over both scales
+    # (the overview's stage sum resized onto the main grid, reading Q22), against the oracle's composition.
+    import torch
+    C, B = 64, 1
+    scales = [(16, 16), (8, 8)]
+    base = synth.tiny(H=16, W=16, mlp_hidden=128)
+    specs = []  # (cfg, attention, cs mode, weight seed)
+    for i in range(6):
+        shifted, cs = synth.stack_layer_kind(i)
+        specs.append((base.replace(shift_x=4 if shifted else 0, shift_y=4 if shifted else 0), 1, 1 if cs else 0, i))
+        if cs:
+            specs.append((base.replace(shift_x=0, shift_y=0, mlp_hidden=0), 0, 2, 100 + i))
+    stage_ends = tuple(j for j, sp in enumerate(specs) if sp[1] == 0)   # after each stage's multi-scale module
+    ws = [synth.make_weights(c, layer=seed) for c, _, _, seed in specs]
+    ends = synth.make_ends_weights(C=C, C_out=64, n_stages=len(stage_ends))
+    layers = [pl.PSCWinMSLayer(pl.MSDesc.make(c, scales, att, cs), dev_weights(w, c))
+              for (c, att, cs, _), w in zip(specs, ws)]
+    enc = pl.HRSAMEncoder(layers, _ends_dev(ends, C), B, *scales[0], stage_ends=stage_ends, C=C, C_out=64,
+                          scales=scales)
+    imgs = [synth.make_image(B, h, w, seed=50 + i) for i, (h, w) in enumerate(scales)]
+    got = host(enc([dev(im) for im in imgs]))
+    torch.cuda.synchronize()
+    xp = oracle.ms_pack([oracle.patch_embed(im, ends["w_patch"], ends["b_patch"]) for im in imgs])
+    stages = []
+    for j, ((c, att, cs, _), w) in enumerate(zip(specs, ws)):
+        xp = oracle.ms_layer(synth.round_bf16(xp), w, c, scales, att, cs)   # the GPU stores x in bf16
+        if j in stage_ends:
+            stages.append(synth.round_bf16(xp))
+    off = oracle.ms_offsets(scales)
+    f = None
+    for s, (h, w) in enumerate(scales):
+        fs = sum(o[B * off[s]:B * off[s + 1]].reshape(B, h, w, C) @ ends[f"w_stage{i}"].T for i, o in enumerate(stages))
+        f = fs if f is None else f + oracle.resize_bilinear(fs, *scales[0])
+    f = oracle.layer_norm(f, ends["neck_ln1_g"], ends["neck_ln1_b"], 1e-6)
+    f = oracle.conv3x3(f, ends["w_neck_conv"])
+    ref = oracle.layer_norm(f, ends["neck_ln2_g"], ends["neck_ln2_b"], 1e-6)
+    assert got.shape == (B, *scales[0], 64)
+    assert rel_err(got, ref) < BF16_TOL
+    # the overview image matters: dropping its contribution moves the embedding by more than the tolerance
+    enc_only = [np.zeros_like(imgs[1])]
+    got0 = host(enc([dev(imgs[0]), dev(enc_only[0])]))
+    assert rel_err(got0, ref) > 3 * BF16_TOL
