@@ -64,6 +64,7 @@ def workload(name: str):
     return label, B, cfgs
 
 
+OVERVIEW = 32   # HRSAM++ overview image 512^2 -> 32 x 32 tokens
 MS_SCALES = [(64, 64), (128, 128), (256, 256)]   # config 5: 1024^2 + 2048^2 + 4096^2 token grids per sample
 
 
@@ -356,6 +357,18 @@ def run_ours(args, rank, world, local_rank):
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
     per_step = [a.elapsed_time(b) for a, b in ev]
 
+    # ---- L2-warm context (untimed for value): the same step back to back without the flush (at 1024^2 the
+    # whole working set, ~100 MB, can stay in the 126 MB L2; at 4096^2 it cannot)
+    warm = []
+    for _ in range(max(3, min(20, args.steps))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        warm.append(a.elapsed_time(b))
+    l2_warm_ms = float(np.median(warm))
+
     # ---- per-layer breakdown (untimed for value): each layer timed alone after an L2 flush
     layer_ms = []
     for j, layer in enumerate(layers):
@@ -406,6 +419,7 @@ def run_ours(args, rank, world, local_rank):
         total_ms, e2e_ms = float(t[0]), float(t[1])
     images = args.steps * B * world
     result = dict(total_ms=total_ms, e2e_ms=e2e_ms, images=images, per_step=per_step, layer_ms=layer_ms,
+                  l2_warm_ms=l2_warm_ms,
                   prof=prof, launches=launches, clocks=clk.summary(), label=label, B=B, cfgs=cfgs,
                   kinds=[_kind(l) for l in layers],
                   h2d=x0.numel() * 2 * B // B, d2h=x0.numel() * 2)
@@ -640,9 +654,37 @@ def _free_port():
     return port
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def tiny_single_thread_ms() -> float:
+    """configs[0] (tiny 16x16, dim 64) through the oracle's CS+S layer on ONE thread (SURVEY §8(d) baseline)."""
+    from threadpoolctl import threadpool_limits
+    cfg = synth.tiny(cycle_scan=1)
+    with threadpool_limits(1):
+        return round(1e3 * time_oracle_layer(cfg, 0), 1)
+
+
 def cpu_baseline(args):
     """The fp64 oracle as it stands, timed on this host: one image through one layer of each kind (summed per
-    image) — or, for the multi-scale workload, each bounded oracle piece of one sample timed once and scaled."""
+    image) — or, for the multi-scale workload, each bounded oracle piece of one sample timed once and scaled.
+    Adds the host CPU model and the single-thread time of the tiny configuration's CS+S layer."""
+    out = _cpu_baseline(args)
+    out["cpu_model"] = cpu_model()
+    out["tiny_cs_s_layer_1thread_ms"] = tiny_single_thread_ms()
+    return out
+
+
+def _cpu_baseline(args):
     if args.workload != "1024":
         items = reference_items(reference_entries(args))
         tot = 0.0
@@ -873,22 +915,40 @@ def run_encoder(args):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(0)
     side = {"1024": 64, "2048": 128, "4096": 256}[args.workload]
-    layers = []
-    for i in range(12):
-        shifted, cs = synth.stack_layer_kind(i)
-        cfg = synth.vitb(side, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, cycle_scan=int(cs),
-                         mlp_hidden=3072)
-        w = synth.make_weights(cfg, layer=i)
-        dw = {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)
-              for k, v in w.items()}
-        layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), dw))
+    todev = lambda w: {k: torch.tensor(v, dtype=torch.float32 if k in F32_KEYS else torch.bfloat16, device=dev)  # noqa
+                       for k, v in w.items()}
+    layers, stage_ends = [], [2, 5, 8, 11]
+    scales = [(side, side)] + ([(OVERVIEW, OVERVIEW)] if args.overview else [])
+    if args.overview:
+        # HRSAM++ (P:L174-189): the 512^2 overview image (32 x 32 tokens) packed after the main grid; blocks
+        # with a single-scale cycle scan, each stage closed by a multi-scale cycle-scan module (as --workload ms)
+        stage_ends = []
+        for i in range(12):
+            shifted, cs = synth.stack_layer_kind(i)
+            cfg = synth.vitb(side, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, mlp_hidden=3072)
+            layers.append(pl.PSCWinMSLayer(pl.MSDesc.make(cfg, scales, 1, 1 if cs else 0),
+                                           todev(synth.make_weights(cfg, layer=i))))
+            if cs:
+                ms = synth.vitb(side, shift_x=0, shift_y=0)
+                layers.append(pl.PSCWinMSLayer(pl.MSDesc.make(ms, scales, 0, 2),
+                                               todev(synth.make_weights(ms, layer=100 + i))))
+                stage_ends.append(len(layers) - 1)
+    else:
+        for i in range(12):
+            shifted, cs = synth.stack_layer_kind(i)
+            cfg = synth.vitb(side, shift_x=8 if shifted else 0, shift_y=8 if shifted else 0, cycle_scan=int(cs),
+                             mlp_hidden=3072)
+            layers.append(pl.PSCWinLayer(pl.LayerDesc.from_config(cfg), todev(synth.make_weights(cfg, layer=i))))
     ew = synth.make_ends_weights()
     ends = {k: torch.tensor(v, dtype=torch.float32 if v.ndim == 1 else torch.bfloat16, device=dev)
             for k, v in ew.items()}
     ends["w_neck_conv"] = ends["w_neck_conv"].permute(0, 2, 3, 1).contiguous()
-    enc = pl.HRSAMEncoder(layers, ends, 1, side, side, graph=True)
-    img = torch.tensor(synth.make_image(1, side, side), dtype=torch.bfloat16, device=dev)
-    enc.img.copy_(img)
+    enc = pl.HRSAMEncoder(layers, ends, 1, side, side, stage_ends=stage_ends, graph=True, scales=scales)
+    imgs = [torch.tensor(synth.make_image(1, h, w, seed=50 + i), dtype=torch.bfloat16, device=dev)
+            for i, (h, w) in enumerate(scales)]
+    img = imgs[0]
+    for dst, src in zip(enc.imgs, imgs):
+        dst.copy_(src)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
         enc.graph.replay()
@@ -904,27 +964,30 @@ def run_encoder(args):
             ts.append((a, b))
         torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ts) / args.steps
-    img_pin = img.cpu().pin_memory()
+    img_pins = [im.cpu().pin_memory() for im in imgs]
     out_pin = torch.empty(enc.out.shape, dtype=torch.bfloat16).pin_memory()
     te = []
     for _ in range(args.steps):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        y = enc(img_pin)
+        y = enc(img_pins)
         out_pin.copy_(y, non_blocking=True)
         b.record()
         te.append((a, b))
     torch.cuda.synchronize()
     e2e = sum(a.elapsed_time(b) for a, b in te) / args.steps
-    line = {"metric": "HRSAM encoder latency ms/image (patch embedding + 12 blocks with FFN + neck)",
+    name = "HRSAM++ encoder" if args.overview else "HRSAM encoder"
+    line = {"metric": f"{name} latency ms/image (patch embedding + 12 blocks with FFN + neck)",
             "value": round(ms, 4), "unit": "ms/image", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic image and random-init weights",
-            "config": {"workload": f"{16 * side}^2 image -> {side}x{side}x256 embeddings", "blocks": 12,
-                       "ffn": 3072, "stage_ends": [2, 5, 8, 11], "launch": "CUDA graph",
+            "config": {"workload": f"{16 * side}^2 image" + (f" + {16 * OVERVIEW}^2 overview (HRSAM++, multi-scale "
+                                                             f"cycle scan closing each stage)" if args.overview else "")
+                       + f" -> {side}x{side}x256 embeddings", "blocks": 12,
+                       "ffn": 3072, "stage_ends": stage_ends, "launch": "CUDA graph",
                        "l2": "flushed before every timed step (256 MiB write)"},
-            "e2e": {"value": round(e2e, 4), "unit": "ms/image", "h2d_bytes_per_step": int(img.numel() * 2),
+            "e2e": {"value": round(e2e, 4), "unit": "ms/image", "h2d_bytes_per_step": int(sum(im.numel() * 2 for im in imgs)),
                     "d2h_bytes_per_step": int(enc.out.numel() * 2)},
             "gpu_launches": int(enc.launches_per_step * args.steps), "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
@@ -1006,6 +1069,8 @@ def main():
     ap.add_argument("--ablation", action="store_true",
                     help="Table 3 rendition: the 12-block encoder body per attention / cycle-scan variant at 1024^2 and "
                          "2048^2 (one JSON line per variant; SURVEY NEXT-4)")
+    ap.add_argument("--overview", action="store_true",
+                    help="with --encoder: HRSAM++ (the 512^2 overview image packed with the main grid)")
     ap.add_argument("--encoder", action="store_true",
                     help="the whole HRSAM encoder on one image: patch embedding + 12 blocks with FFN + neck (NEXT-3)")
     ap.add_argument("--micro", choices=["partition"], help="micro-benchmark of one standalone entry point family")
@@ -1097,6 +1162,7 @@ def main():
                        "C": c0.C, "heads": c0.heads, "window": c0.window, "shift": 8, "ssm_state": c0.N,
                        "ssm_expand": c0.ssm_expand, "pad_mode": "learnable", "parallelism": f"images x{world}",
                        "l2": "flushed before every timed step (256 MiB write)",
+                       "l2_warm_ms_per_image": round(res["l2_warm_ms"] / res["B"], 4),
                        "launch": "eager" if args.no_graph else "CUDA graph of the whole step",
                        "per_layer_ms": [round(t, 4) for t in res["layer_ms"]]},
             "e2e": {"value": round(e2e_img, 4), "unit": "ms/image", "h2d_bytes_per_step": int(res["h2d"]),
