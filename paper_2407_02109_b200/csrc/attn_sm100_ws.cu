@@ -28,7 +28,10 @@ constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroup
 constexpr int WS1_THREADS = 64 + 256 + 32;  // TMA warp, MMA warp (slot 0), 2 softmax warpgroups (one thread per
                                             // query row), MMA warp (slot 1)
 #ifndef PSCWIN_ATTN_POLY_MOD
-#define PSCWIN_ATTN_POLY_MOD 0  // k > 0: every k-th exp2 pair on the FMA pipe; swept 0 / 2 / 3 / 4 at 4096^2: 125 / 133 / 128.5 / 127 us
+// k > 0: every k-th exp2 pair on the FMA pipe (degree-3 polynomial, 7.5e-5 relative, far below the bf16 rounding of
+// P). Round 1 (two threads per row, no ping-pong) swept 0 / 2 / 3 / 4: 125 / 133 / 128.5 / 127 us; round 2 (ROW1 with
+// the exp ping-pong, MUFU-bound exp passes) 0 / 4 / 8: 119.8 / 115.5 / 117.2 us at 4096^2 (profiles/r02)
+#define PSCWIN_ATTN_POLY_MOD 4
 #endif
 constexpr int kPolyMod = PSCWIN_ATTN_POLY_MOD;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -459,11 +462,15 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         // ping-pong: the two slots' exp passes alternate (slot 0 of item i, slot 1 of item i, slot 0 of item i+1,
         // ...), so one slot's MUFU-bound exponentials overlap the other slot's max pass, MMAs and O read-out instead
         // of the two contending for the MUFU pipe and then idling together
+        uint32_t ra[32], rb[32], pk[16];
+        tmem_ld32(tS, ra);  // (the first chunk's TMEM load is issued before waiting for the exp turn)
         if (pingpong) {
           mbar_wait(&turn[a], a == 0 ? ph_t ^ 1 : ph_t);
           ph_t ^= 1;
         }
         if (row == 0) ATT_TS6(64 + 32 * a, kk, 2);
+        long long clk_e0 = 0;
+        if (p.dbg && row == 0) clk_e0 = clock64();
         auto exp32 = [&](const uint32_t (&r)[32], uint32_t m, uint32_t (&pk)[16]) {
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -486,8 +493,6 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
           }
         };
         {
-          uint32_t ra[32], rb[32], pk[16];
-          tmem_ld32(tS, ra);
           for (int c0 = 0; c0 < NK; c0 += 64) {
             tmem_wait_ld_dep(ra);
             const bool two = c0 + 32 < NK;
@@ -509,6 +514,11 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         patch_next(item);
         const float lsum = (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
         if (row == 0) ATT_TS6(64 + 32 * a, kk, 3);
+        if (p.dbg && row == 0) {  // SM clocks of this exp pass + globaltimer ns (debug: effective clock)
+          p.dbg[blockIdx.x * 128 + 64 + 32 * a + 30] = (unsigned long long)(clock64() - clk_e0);
+          p.dbg[blockIdx.x * 128 + 64 + 32 * a + 31] = p.dbg[blockIdx.x * 128 + 64 + 32 * a + (kk % 5) * 6 + 3] -
+                                                      p.dbg[blockIdx.x * 128 + 64 + 32 * a + (kk % 5) * 6 + 2];
+        }
         // O = P V lands in columns [192, 192 + d): copied to registers, the TMEM columns released (the next item's
         // S may overwrite them), then normalised and written to the grid (merge / crop)
         mbar_wait(&o_full[a], ph_o);

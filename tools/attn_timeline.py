@@ -46,5 +46,11 @@ for run in (2, 5):
                     nxt = ev[items[j + 1]][0]
                     ph[5].append((nxt - ev[i][5]) / 1e3)
                     per.append((nxt - ev[i][0]) / 1e3)
+        clk = t[:, 64 + 32 * a + 30].astype(np.float64)
+        ns = t[:, 64 + 32 * a + 31].astype(np.float64)
+        ok = (clk > 0) & (ns > 0)
+        if ok.any():
+            print(f"slot {a}: last exp pass {np.median(clk[ok]):.0f} SM clocks in {np.median(ns[ok]):.0f} ns "
+                  f"-> {np.median(clk[ok] / ns[ok]) * 1e3:.0f} MHz effective")
         print(f"slot {a}: period {np.median(per):.2f} us; phase medians: " +
               ", ".join(f"{n} {np.median(x):.2f}" for n, x in zip(names, ph) if x))

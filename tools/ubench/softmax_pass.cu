@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../paper_2407_02109_b200/csrc/common.cuh"
+
 __device__ __forceinline__ float ex2(float x) { float y; asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ uint32_t pack(float a, float b) {
   uint32_t r; asm("cvt.rn.bf16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b)); return r;
@@ -79,6 +81,25 @@ __global__ void __launch_bounds__(320, 1) kern(int iters, long long* clk, float*
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+  } else if (MODE == 5) {  // warp 4: back-to-back tcgen05.mma (M 128, N 256, K 64 per group) into TMEM columns
+    // [256, 512) (the other q-tile slot's S), operands from shared memory, one commit + wait per group
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm) + 1023) & ~uintptr_t(1023));
+    const uint32_t idesc = pscwin::make_idesc_bf16(128, 256, 0, 0);
+    const uint32_t a0 = (uint32_t)__cvta_generic_to_shared(sm), b0 = a0 + 16384;
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      if (pscwin::elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          pscwin::umma_ss(slot + 256, pscwin::make_sdesc(a0 + k * 32, 16, 1024, pscwin::kLayoutSW128),
+                          pscwin::make_sdesc(b0 + k * 32, 16, 1024, pscwin::kLayoutSW128), idesc, k > 0);
+        pscwin::umma_commit(&bar);
+      }
+      __syncwarp();
+      pscwin::mbar_wait(&bar, ph);
+      ph ^= 1;
+    }
   } else if (MODE == 4) {  // idle warps spinning on an mbarrier (try_wait loop, as the kernel's waiting roles do)
     asm volatile(
         "{\n\t.reg .pred P1;\n"
@@ -120,9 +141,11 @@ void run(const char* name, int threads) {
   long long* clk; float* out;
   cudaMalloc(&clk, 8); cudaMalloc(&out, 148 * 320 * 4);
   const int iters = 2000;
-  kern<MODE><<<148, threads>>>(10, clk, out);
+  const int smem = MODE == 5 ? 50 * 1024 : 0;
+  if (smem) cudaFuncSetAttribute(kern<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  kern<MODE><<<148, threads, smem>>>(10, clk, out);
   cudaDeviceSynchronize();
-  kern<MODE><<<148, threads>>>(iters, clk, out);
+  kern<MODE><<<148, threads, smem>>>(iters, clk, out);
   cudaError_t e = cudaDeviceSynchronize();
   long long c; cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
   // MUFU floor per pass: 128 rows x 256 ex2 / 16 per clk = 2048 clk
@@ -137,5 +160,6 @@ int main() {
   run<3>("  + 4 warps of max passes", 256);
   run<4>("  + 4 warps spinning", 256);
   run<4>("  + 6 warps spinning", 320);
+  run<5>("  + MMAs into the other TMEM half", 160);
   return 0;
 }
