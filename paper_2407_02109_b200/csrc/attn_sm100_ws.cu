@@ -24,7 +24,8 @@
 namespace pscwin {
 
 namespace {
-constexpr int WS_THREADS = 64 + 512;  // TMA warp, MMA warp, 4 softmax warpgroups (two threads per query row)
+constexpr int WS_THREADS = 64 + 512 + 32;  // TMA warp, MMA warp (slot 0), 4 softmax warpgroups (two threads per query
+                                           // row), MMA warp (slot 1)
 constexpr int WS1_THREADS = 64 + 256 + 32;  // TMA warp, MMA warp (slot 0), 2 softmax warpgroups (one thread per
                                             // query row), MMA warp (slot 1)
 #ifndef PSCWIN_ATTN_POLY_MOD
@@ -89,8 +90,8 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
   uint64_t* o_full = bars + 10;      // [2]
   uint64_t* o_free = bars + 12;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  float* s_red = reinterpret_cast<float*>(bars + 16);  // [2 q tiles][2 halves][128 rows] partial row max / sum
-  uint64_t* turn = bars + 16;  // ROW1 (no s_red): [2] exp-pass turn of each q-tile slot (ping-pong)
+  uint64_t* turn = bars + 16;  // [2] exp-pass turn of each q-tile slot (ping-pong)
+  float* s_red = reinterpret_cast<float*>(bars + 18);  // ROW2: [2 q tiles][2 halves][128 rows] partial row max / sum
 
   const int warp = warp_id();
   constexpr int NTQ = ROW1 ? 128 : 256;  // softmax threads per q tile
@@ -104,13 +105,13 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
       mbar_init(&ld_full[i], 1);
       // a stage is free once its MMAs completed (commit) AND both q-tile slots' O tiles, staged in the slot's Q
       // region of the stage, have been read out by their TMA stores (one arrival per slot)
-      mbar_init(&ld_empty[i], ROW1 ? 4 : 3);
+      mbar_init(&ld_empty[i], 4);  // both issuers' commits + both slots' O stores
       mbar_init(&patch_done[i], NTQ);  // slot 0's threads patch (slot 1 runs half an item behind)
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], NTQ);
       mbar_init(&o_full[i], 1);
       mbar_init(&o_free[i], NTQ);
-      if (ROW1) mbar_init(&turn[i], NTQ);
+      mbar_init(&turn[i], NTQ);
     }
     fence_barrier_init();
   }
@@ -175,13 +176,13 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         }
       }
     }
-  } else if (ROW1 && (warp == 1 || warp == 10)) {
+  } else if (warp == 1 || warp == (ROW1 ? 10 : 18)) {
     // ------------------------------------------------------------------------------------------ MMA issuers (ROW1)
     // One issuing warp per q-tile slot (warp 1: slot 0, warp 10: slot 1), so neither slot's S / PV MMAs wait behind
     // the other slot's barriers: per item S_a = Q_a K^T (after the previous item's O_a, which aliases S columns, has
     // been read out), then O_a = P_a V once P_a is in TMEM, then a commit that releases the stage (4 arrivals: both
     // issuers' commits and both slots' O stores)
-    const int a = warp == 1 ? 0 : 1;
+    const int a = warp == 1 ? 0 : 1;  // (the issuer of slot 1 is the last warp)
     const int NK = nt * p.tile_slots;
     const uint32_t idesc_s = make_idesc_bf16(128, NK, 0, 0);
     const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
@@ -214,9 +215,9 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t va = sb + 4 * TILE;
-          for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks
-            umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8, make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT),
-                    idesc_o, ks > 0);
+          for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128 in ROW2)
+            umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (!ROW1 && ks >= 8 ? 64 : 0),
+                    make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
           umma_commit(&o_full[a]);
         }
         __syncwarp();
@@ -227,111 +228,6 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         stage = 0;
         phase ^= 1;
       }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------------------------------ MMA issuer
-    // The two q-tile slots run half an item apart so one slot's softmax (MUFU-bound) overlaps the other slot's
-    // PV MMA, O read-out and next S MMA. Issue order per item i: S(i,0), PV(i-1,1), S(i,1), PV(i,0); for the
-    // first item S(0,1) follows PV(0,0), which sets up the half-item offset.
-    const int NK = nt * p.tile_slots;
-    const uint32_t idesc_s = make_idesc_bf16(128, NK, 0, 0);
-    const uint32_t idesc_o = make_idesc_bf16(128, D, 0, 1);
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t ph_p[2] = {0, 0}, ph_of[2] = {0, 0};
-    int ev = 0;
-    auto issue_s = [&](int a, uint32_t sb) {
-      mbar_wait(&o_free[a], ph_of[a] ^ 1);  // the previous item's O (aliasing S columns) has been read
-      ph_of[a] ^= 1;
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t qa = sb + a * TILE, ka = sb + 2 * TILE;
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          umma_ss(tmem + 256 * a, make_sdesc(qa + k * 32, 16, SBO, LAYOUT), make_sdesc(ka + k * 32, 16, SBO, LAYOUT),
-                  idesc_s, k > 0);
-        umma_commit(&s_full[a]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int a, uint32_t sb) {
-      mbar_wait(&p_full[a], ph_p[a]);
-      ph_p[a] ^= 1;
-      ATT_TS(32, ev);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t va = sb + 4 * TILE;
-        for (int ks = 0; ks < NK / 16; ++ks)  // P of keys 16ks.. at column 8ks (+64 for keys >= 128 unless ROW1)
-          umma_ts(tmem + 256 * a + 192, tmem + 256 * a + ks * 8 + (!ROW1 && ks >= 8 ? 64 : 0),
-                  make_sdesc(va + ks * 16 * ROWB, TILE, SBO, LAYOUT), idesc_o, ks > 0);
-        umma_commit(&o_full[a]);
-      }
-      __syncwarp();
-    };
-    auto release = [&](int st) {  // all MMAs reading stage st have been issued: TMA may refill it when they finish
-      if (elect_one()) umma_commit(&ld_empty[st]);
-      __syncwarp();
-    };
-    // Few items per CTA (1024^2: 1-2): the half-item stagger would serialise the two q tiles of the only items,
-    // so issue both q tiles in lockstep (S0, S1, PV0, PV1 per item); the stagger pays off only in long runs.
-    const bool lockstep = p.lockstep >= 0 ? p.lockstep == 1 : p.n_items <= 3 * (int)gridDim.x;
-    bool have_prev = false, prev_act1 = false;
-    int prev_stage = 0;
-    uint32_t prev_sb = 0;
-    bool first = true;
-    for (int item = blockIdx.x; lockstep && item < p.n_items; item += gridDim.x) {
-      int b, h, X0, Y0;
-      decode(item, b, h, X0, Y0);
-      const bool act0 = q_active(0, Y0), act1 = q_active(1, Y0);
-      mbar_wait(&ld_full[stage], phase);
-      if (p.patch) mbar_wait(&patch_done[stage], phase);
-      ATT_TS(32, ev);
-      tc_fence_after();
-      const uint32_t sb = smem_u32(smem + stage * STAGE);
-      if (act0) issue_s(0, sb);
-      if (act1) issue_s(1, sb);
-      if (act0) issue_pv(0, sb);
-      if (act1) issue_pv(1, sb);
-      release(stage);
-      if (++stage == 2) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-    for (int item = blockIdx.x; !lockstep && item < p.n_items; item += gridDim.x) {
-      int b, h, X0, Y0;
-      decode(item, b, h, X0, Y0);
-      const bool act0 = q_active(0, Y0), act1 = q_active(1, Y0);
-      mbar_wait(&ld_full[stage], phase);
-      if (p.patch) mbar_wait(&patch_done[stage], phase);
-      ATT_TS(32, ev);
-      tc_fence_after();
-      const uint32_t sb = smem_u32(smem + stage * STAGE);
-      if (act0) issue_s(0, sb);
-      if (have_prev) {
-        if (prev_act1) issue_pv(1, prev_sb);
-        release(prev_stage);
-      }
-      if (first) {
-        if (act0) issue_pv(0, sb);
-        if (act1) issue_s(1, sb);
-      } else {
-        if (act1) issue_s(1, sb);
-        if (act0) issue_pv(0, sb);
-      }
-      first = false;
-      have_prev = true;
-      prev_act1 = act1;
-      prev_stage = stage;
-      prev_sb = sb;
-      if (++stage == 2) {
-        stage = 0;
-        phase ^= 1;
-      }
-    }
-    if (have_prev) {
-      if (prev_act1) issue_pv(1, prev_sb);
-      release(prev_stage);
     }
   } else if constexpr (ROW1) {
     // ------------------------------------------------------------------------------------------ softmax WGs (ROW1)
@@ -616,6 +512,8 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
     const bool col_active = split || hc == 0;
     const uint32_t tail_mask = NK >= 32 ? 0xFFFFFFFFu : ((1u << NK) - 1u);  // 16-key windows (w = 4)
     const int c_lo = hc * half_cols;
+    const bool pingpong = p.pingpong && nt == 2;
+    uint32_t ph_t = 0;
     const float2 sl2 = make_float2(p.sl2, p.sl2);
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       int b, h, X0, Y0;
@@ -741,6 +639,10 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
            // exponentiated (the 96-register budget of 18 warps rules out 32-column double buffering)
           uint32_t ra[16], rb[16], pk[8];
           if (nc > 0) tmem_ld16(tS + c_lo, ra);
+          if (pingpong) {  // the two slots' exp passes alternate (as in ROW1)
+            mbar_wait(&turn[a], a == 0 ? ph_t ^ 1 : ph_t);
+            ph_t ^= 1;
+          }
           for (int c0 = c_lo; c0 < c_lo + nc; c0 += 32) {
             const uint32_t m = (MASKED ? chunk_mask(c0) : 0xFFFFFFFFu) & tail_mask;
             tmem_wait_ld_dep16(ra);
@@ -753,6 +655,7 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
             tmem_st8(tS + p_off + c0 / 2 + 8, pk);
           }
         }
+        if (pingpong) mbar_arrive(&turn[a ^ 1]);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[a]);
@@ -825,8 +728,13 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
           if (gtid == 0) mbar_arrive(&ld_empty[stage]);
         }
         if (row == 0 && hc == 0) ATT_TS(64 + 32 * a, ev);
-      } else if (gtid == 0) {
-        mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
+      } else {
+        if (pingpong) {  // an inactive q tile passes its exp turn on
+          mbar_wait(&turn[a], a == 0 ? ph_t ^ 1 : ph_t);
+          ph_t ^= 1;
+          mbar_arrive(&turn[a ^ 1]);
+        }
+        if (gtid == 0) mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
       }
       __syncwarp();  // lane 0's store / arrival branch rejoins before the next item's .sync.aligned tcgen05 ops
       if (++stage == 2) {
@@ -911,7 +819,7 @@ int launch_window_attention_ws(const AttnArgs& a, const void* kx, const void* ky
                       d == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B);
     if (rc) return rc;
   }
-  const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 16 * 8 + 1024 * 4;
+  const size_t smem = 1024 + 2 * 6 * 128 * d * 2 + 18 * 8 + 1024 * 4;
   const int grid = p.n_items < num_sms() ? p.n_items : num_sms();
   PSCWIN_PROF("window_attention", stream);
   // one softmax thread per query row (default) or two (PSCWIN_ATTN_ROW2=1, the round-1 layout; A/B knob)
