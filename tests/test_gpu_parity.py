@@ -73,7 +73,11 @@ def test_layer_norm(pl):
 @pytest.mark.parametrize("M,K,N,bias,resid,f32", [
     (4096, 768, 2304, True, False, False), (4173, 768, 768, True, True, False), (100, 1536, 112, False, False, True),
     (1, 64, 36, False, False, True), (300, 64, 192, True, False, False), (4096, 768, 3072, False, False, False),
-    (777, 1536, 768, False, True, False), (130, 128, 256, True, True, False)])
+    (777, 1536, 768, False, True, False), (130, 128, 256, True, True, False),
+    # per-warp bf16 epilogue edges (round 2): ragged boxes (N % 32 = 16: residual in shared memory), the global-memory
+    # residual of long-K GEMMs with bias and two column tiles, a single 48-column tile whose second box is half outside
+    (500, 768, 80, True, True, False), (333, 1536, 208, True, True, False), (1000, 1536, 768, True, True, False),
+    (520, 2048, 512, False, True, False), (64, 64, 48, True, False, False)])
 def test_linear(pl, M, K, N, bias, resid, f32):
     g = lambda s, n: synth.round_bf16(synth.normal(synth.stream_seed(s, M, K, N), n))
     A = g(1, M * K).reshape(M, K)
