@@ -249,6 +249,47 @@ class PSCWinStack:
         self.x_in.copy_(x, non_blocking=True)
         return self.replay()
 
+    def run_job(self, xs_host, ys_host, before_step=None) -> None:
+        """A job of len(xs_host) inputs from pinned host memory through the stack into pinned host outputs, with the
+        host<->device copies overlapped with compute: the H2D copy of input i+1 (one copy stream) and the D2H copy of
+        output i-1 (another) run while the graph of input i runs on the current stream; device staging buffers are
+        double-buffered and ordered with events. Enqueues everything; the current stream ends after the last D2H.
+        before_step(i), if given, is called on the current stream before step i's compute (e.g. an L2 flush)."""
+        n = len(xs_host)
+        if n == 0:
+            return
+        cur = torch.cuda.current_stream()
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        if not hasattr(self, "_stage_in"):
+            self._stage_in = [torch.empty_like(self.x_in) for _ in range(2)]
+            self._stage_out = [torch.empty_like(self.out) for _ in range(2)]
+        ev = lambda: torch.cuda.Event()  # noqa: E731
+        in_ready, in_free = [ev() for _ in range(n)], [ev() for _ in range(n)]
+        out_ready, out_free = [ev() for _ in range(n)], [ev() for _ in range(n)]
+        s_in.wait_stream(cur)
+        s_out.wait_stream(cur)
+        for i in range(n):
+            with torch.cuda.stream(s_in):  # H2D of input i into staging slot i % 2 once step i-2 has consumed it
+                if i >= 2:
+                    s_in.wait_event(in_free[i - 2])
+                self._stage_in[i & 1].copy_(xs_host[i], non_blocking=True)
+                in_ready[i].record(s_in)
+            cur.wait_event(in_ready[i])
+            if before_step is not None:
+                before_step(i)
+            self.x_in.copy_(self._stage_in[i & 1], non_blocking=True)
+            in_free[i].record(cur)
+            self.replay()
+            if i >= 2:
+                cur.wait_event(out_free[i - 2])  # staging slot i % 2 read out by the D2H of output i-2
+            self._stage_out[i & 1].copy_(self.out, non_blocking=True)
+            out_ready[i].record(cur)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(out_ready[i])
+                ys_host[i].copy_(self._stage_out[i & 1], non_blocking=True)
+                out_free[i].record(s_out)
+        cur.wait_stream(s_out)
+
 
 # ------------------------------------------------------------------------------------------- encoder ends
 

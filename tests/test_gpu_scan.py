@@ -134,6 +134,24 @@ def test_stack_graph_replay_equals_eager(pl):
     assert rel_err(host(g1), ref) < BF16_TOL
 
 
+def test_stack_run_job_equals_per_step(pl):
+    # PSCWinStack.run_job (the e2e path of bench.py): pinned host inputs -> stack -> pinned host outputs with the
+    # copies of neighbouring steps overlapped with compute; every output equals the one-at-a-time result
+    import torch
+    cfgs = [synth.tiny(shift_x=0, shift_y=0), synth.tiny(shift_x=0, shift_y=0, cycle_scan=1)]
+    layers = [pl.PSCWinLayer(pl.LayerDesc.from_config(c), dev_weights(synth.make_weights(c, layer=i), c))
+              for i, c in enumerate(cfgs)]
+    xs = [dev(synth.make_input(cfgs[0], layer=k)) for k in range(5)]
+    stack = pl.PSCWinStack(layers, tuple(xs[0].shape), graph=True)
+    want = [stack(x).clone() for x in xs]
+    xs_h = [x.cpu().pin_memory() for x in xs]
+    ys_h = [torch.empty_like(x).pin_memory() for x in xs_h]
+    stack.run_job(xs_h, ys_h)
+    torch.cuda.synchronize()
+    for w, y in zip(want, ys_h):
+        assert torch.equal(w.cpu(), y)
+
+
 CS_LAYERS = [synth.tiny(cycle_scan=1, shift_x=0, shift_y=0), synth.tiny(cycle_scan=1),
              synth.tiny(cycle_scan=1, scan_order=synth.SCAN_WINDOW_MAJOR),
              synth.tiny(cycle_scan=1, shift_x=0, shift_y=0, scan_order=synth.SCAN_COL_MAJOR),
