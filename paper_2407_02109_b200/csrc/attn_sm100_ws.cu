@@ -254,10 +254,17 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
     // LEARNABLE pad patch of the K/V rows outside the grid by slot 0's 128 threads (slot 1 only reads the stage
     // through its MMAs, after patch_done): entry e = key tile e>>7, slot e&127. It runs one item ahead — the next
     // item's stage is patched while this item's PV MMA runs — so the next S MMA does not wait for it.
-    auto patch = [&](int pitem, int pstage, uint32_t pphase) {
+    // returns false (nothing done) when block is false and the stage has not landed yet
+    auto patch = [&](int pitem, int pstage, uint32_t pphase, bool block) -> bool {
       int b, h, X0, Y0;
       decode(pitem, b, h, X0, Y0);
-      mbar_wait(&ld_full[pstage], pphase);
+      if (X0 >= 0 && Y0 >= 0 && X0 + p.w <= p.W && Y0 + nt * p.rpt <= p.H) {  // no pad slot in this window
+        mbar_arrive(&patch_done[pstage]);
+        __syncwarp();
+        return true;
+      }
+      if (!block && !__all_sync(0xffffffffu, mbar_test(&ld_full[pstage], pphase))) return false;  // (warp-uniform)
+      mbar_wait(&ld_full[pstage], pphase);  // (TMA zero-fills the pad rows: patch only after it landed)
       for (int e = gtid; e < nt * 128; e += 128) {
         const int kt = e >> 7, r = e & 127;
         if (r >= p.tile_slots) continue;
@@ -280,12 +287,18 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
       fence_proxy_async_smem();
       mbar_arrive(&patch_done[pstage]);
       __syncwarp();
+      return true;
     };
-    auto patch_next = [&](int item) {  // the stage after `stage` holds item + gridDim.x
-      if (p.patch && a == 0 && item + (int)gridDim.x < p.n_items)
-        patch(item + gridDim.x, stage ^ 1, stage == 1 ? phase ^ 1 : phase);
+    // the stage after `stage` holds item + gridDim.x; if its data has not landed yet, the patch is deferred to the end
+    // of this item (block = true there) instead of stalling this slot's O read-out behind the next item's load
+    bool patch_deferred = false;
+    auto patch_next = [&](int item, bool block) {
+      if (p.patch && a == 0 && item + (int)gridDim.x < p.n_items) {
+        // (the defer decision is warp-uniform; warps may differ, each thread still arrives exactly once)
+        patch_deferred = !patch(item + gridDim.x, stage ^ 1, stage == 1 ? phase ^ 1 : phase, block);
+      }
     };
-    if (p.patch && a == 0 && (int)blockIdx.x < p.n_items) patch(blockIdx.x, 0, 0);
+    if (p.patch && a == 0 && (int)blockIdx.x < p.n_items) patch(blockIdx.x, 0, 0, true);
     int kk = 0;  // this CTA's item count (debug timeline)
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++kk) {
       int b, h, X0, Y0;
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[a]);
-        patch_next(item);
+        patch_next(item, false);
         const float lsum = (ls[0].x + ls[1].x) + (ls[0].y + ls[1].y);
         if (row == 0) ATT_TS6(64 + 32 * a, kk, 3);
         if (p.dbg && row == 0) {  // SM clocks of this exp pass + globaltimer ns (debug: effective clock)
@@ -477,9 +490,10 @@ __global__ void __launch_bounds__(ROW1 ? WS1_THREADS : WS_THREADS, 1)
           mbar_arrive(&turn[a ^ 1]);
         }
         if (gtid == 0) mbar_arrive(&ld_empty[stage]);  // nothing staged for an inactive q tile
-        patch_next(item);
+        patch_next(item, false);
       }
       __syncwarp();  // lane 0's store / arrival branch rejoins before the next item's .sync.aligned tcgen05 ops
+      if (patch_deferred) patch_next(item, true);
       if (++stage == 2) {
         stage = 0;
         phase ^= 1;
