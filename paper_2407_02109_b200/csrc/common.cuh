@@ -219,6 +219,17 @@ PSCWIN_DEVICE void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t ba
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "l"(hint)
       : "memory");
 }
+// The same, multicast: the box lands at this shared-memory offset in every CTA of cta_mask, and each destination's
+// bytes complete on the barrier at bar's offset in that destination's pair leader (bar = a pair leader's barrier:
+// with .cta_group::2 the barrier CTA of a destination is the destination with the peer bit taken from bar)
+PSCWIN_DEVICE void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m, uint32_t bar_cluster_addr, int c0, int c1,
+                                       uint16_t cta_mask, uint64_t hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "h"(cta_mask), "l"(hint)
+      : "memory");
+}
 PSCWIN_DEVICE void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

@@ -12,6 +12,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 #include "pscwin_internal.h"
 
@@ -61,7 +65,12 @@ __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) 
 // EK: epilogue kind, a compile-time specialisation so each variant's registers are allocated for its own work
 // (EK_ROPE keeps 32 cos / sin values per row live across the tile; EK_GELU inlines 32 GELUs per chunk).
 enum { EK_PLAIN = 0, EK_ROPE = 1, EK_GELU = 2, EK_F32 = 3 };
-template <bool PAIR, int EK>
+// MC = 2 (CTA pairs only): a 4-CTA cluster of two pairs takes two vertically adjacent 256-row tiles of the same
+// column tile; every B k-block is loaded once per cluster (each CTA loads a quarter and multicasts it to the CTA of
+// the same pair rank in both pairs), halving the B bytes moved from L2 (which would bound the big projections if
+// their ~10 TB/s of A + B tile reads at 4096^2 were at the L2 limit). Measured bit-identical but 2-4 % slower (the
+// 4-CTA clusters couple two pairs' rings and may leave SMs idle), so it is off by default (mc_enabled).
+template <bool PAIR, int EK, int MC = 1>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmRes,
@@ -71,7 +80,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int BN = p.BN;
   const int STAGES = p.stages;
   const int B_STAGE_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t rank = crank & 1u;              // rank inside the pair
+  const uint32_t pp = MC > 1 ? crank >> 1 : 0u;  // pair inside the cluster (MC = 2)
+  const uint32_t lead = pp * 2u;                 // cluster rank of this pair's leader
   const bool resid = p.epi == EPI_RESID_BF16 && p.residual != nullptr;
   constexpr bool res_gmem_ek = EK == EK_PLAIN;                       // (only plain epilogues carry a residual)
   const bool res_gmem = res_gmem_ek && resid && p.res_global;  // the epilogue reads the residual from global
@@ -100,16 +112,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int TM = PAIR ? 2 * BM : BM;          // tile rows (the pair's 256 or one CTA's 128)
   const int n_tiles_n = (p.N + BN - 1) / BN;
   const int S = p.splits > 1 ? p.splits : 1;  // split-K factor (f32 outputs only; single-CTA tiles)
-  const int n_tiles = ((p.M + TM - 1) / TM) * n_tiles_n * S;
-  const int tile0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;   // this CTA's (pair's) first tile
-  const int tstride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int n_tiles = ((p.M + MC * TM - 1) / (MC * TM)) * n_tiles_n * S;
+  const int tile0 = PAIR ? (int)(blockIdx.x / (2 * MC)) : (int)blockIdx.x;   // this CTA's (cluster's) first tile
+  const int tstride = PAIR ? (int)(gridDim.x / (2 * MC)) : (int)gridDim.x;
   const int BKe = p.tf32 ? BK / 2 : BK;  // K elements per 128-byte k-block row (bf16: 64, tf32: 32)
   const int nk = (p.K + BKe - 1) / BKe;
   // work tile -> output tile (m0, n0), k-block range [kb0, kb1) and split index
   auto coords = [&](int tile, int& m0, int& n0, int& kb0, int& kb1, int& s) {
     const int mn = tile / S;
     s = tile - mn * S;
-    m0 = (mn / n_tiles_n) * TM;
+    m0 = (mn / n_tiles_n) * (MC * TM) + (int)pp * TM;
     n0 = (mn % n_tiles_n) * BN;
     kb0 = (int)((long long)nk * s / S);
     kb1 = (int)((long long)nk * (s + 1) / S);
@@ -121,7 +133,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (p.epi != EPI_STORE_F32 || p.f32_tma) tma_prefetch_desc(&tmOut);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], MC);  // one multicast commit per pair that reads this CTA's stage
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -153,7 +165,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_a = policy_evict_normal();
       const uint64_t pol_b = policy_evict_last();
       // CTA pair: both CTAs' loads complete on the leader's full barrier (it issues the MMAs)
-      const uint32_t full0 = PAIR ? smem_in_cta(&full[0], 0) : 0u;
+      const uint32_t full0 = PAIR ? smem_in_cta(&full[0], lead) : 0u;
       int stage = 0;
       uint32_t phase = 0;
       int rbuf = 0;
@@ -205,16 +217,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // boxes entirely outside A (rows >= M) or B (rows >= N) are not loaded; their bytes are not expected
           const bool a0_in = m0 < p.M, a1_in = m0 + BM < p.M;
           const bool b0_in = n0 < p.N, b1_in = n0 + BN / 2 < p.N;
-          const uint32_t bytes = ((int)a0_in + (int)a1_in) * A_STAGE_BYTES + ((int)b0_in + (int)b1_in) * B_STAGE_BYTES;
-          const bool a_mine = rank ? a1_in : a0_in, b_mine = rank ? b1_in : b0_in;
+          uint32_t bytes = ((int)a0_in + (int)a1_in) * A_STAGE_BYTES + ((int)b0_in + (int)b1_in) * B_STAGE_BYTES;
+          const bool a_mine = rank ? a1_in : a0_in;
+          bool b_mine = rank ? b1_in : b0_in;
+          // MC = 2: B quarter (r, q) = rows n0 + r BN/2 + q BN/4 lands at offset q QB of the B stage of both pairs'
+          // rank-r CTAs; this CTA loads quarter (rank, pp)
+          const int QR = BN / 4;
+          const uint32_t QB = (uint32_t)QR * BK * 2;
+          const int qrow = n0 + (int)rank * (BN / 2) + (int)pp * QR;
+          if (MC > 1) {
+            bytes = ((int)a0_in + (int)a1_in) * A_STAGE_BYTES;
+            for (int q = 0; q < 4; ++q) bytes += (n0 + q * QR < p.N) ? QB : 0u;
+            b_mine = qrow < p.N;
+          }
+          const uint16_t qmask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
           for (int kb = kb0; kb < kb1; ++kb) {
             try_res(false);
             mbar_wait(&empty[stage], phase ^ 1);
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], bytes);
             const uint32_t fb = full0 + stage * 8;
             if (a_mine) tma_load_2d_pair(sA + stage * A_STAGE_BYTES, &tmA, fb, kb * BKe, m0 + mrow, pol_a);
-            if (b_mine)
+            if (MC > 1) {
+              if (b_mine)
+                tma_load_2d_pair_mc(sB + stage * B_STAGE_BYTES + pp * QB, &tmB, fb, kb * BKe, qrow, qmask, pol_b);
+            } else if (b_mine) {
               tma_load_2d_pair(sB + stage * B_STAGE_BYTES, &tmB, fb, kb * BKe, n0 + (int)rank * (BN / 2), pol_b);
+            }
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -278,8 +306,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               }
             }
             if (PAIR) {
-              umma_commit_pair_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
-              if (kb == kb1 - 1) umma_commit_pair_mc(&tfull[acc], 0x3);
+              // frees the stage in both CTAs (MC = 2: in all four, whose B quarters this pair's MMAs read)
+              umma_commit_pair_mc(&empty[stage], MC > 1 ? 0xF : 0x3);
+              if (kb == kb1 - 1) umma_commit_pair_mc(&tfull[acc], (uint16_t)(0x3u << lead));
             } else {
               umma_commit(&empty[stage]);
               if (kb == kb1 - 1) umma_commit(&tfull[acc]);
@@ -313,7 +342,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     int gseq = 0;
     int rbuf = 0;
     uint32_t rphase = 0;
-    const uint32_t tempty0 = PAIR ? smem_in_cta(&tempty[0], 0) : 0u;  // the leader's accumulator-free barriers
+    const uint32_t tempty0 = PAIR ? smem_in_cta(&tempty[0], lead) : 0u;  // the leader's accumulator-free barriers
     for (int tile = tile0; tile < n_tiles; tile += tstride) {
       int m0, n0, kb0, kb1, split;
       coords(tile, m0, n0, kb0, kb1, split);
@@ -690,29 +719,45 @@ static bool pair_enabled() {
   return on == 1;
 }
 
-// co-resident 2-CTA clusters of the pair kernel (an SM left alone in a GPC cannot host half a cluster)
-static int pair_clusters(size_t smem) {
-  static int cached = 0;
-  static size_t cached_smem = 0;
-  if (cached && cached_smem == smem) return cached;
+// B multicast across two CTA pairs (4-CTA clusters): PSCWIN_GEMM_MC=2 turns it on (A/B knob, read once). Off by
+// default: bit-identical but 2-4 % slower at every 4096^2 projection shape (profiles/r02/gemm_mc_r02m.log: QKV 183.9
+// -> 188.3 us, out-proj 78.9 -> 82.4, in_proj 237 -> 247), so the B tile reads from L2 are not what bounds them
+static bool mc_enabled() {
+  static const int on = env_knob("PSCWIN_GEMM_MC", 1);
+  return on == 2;
+}
+
+// co-resident clusters of `csize` CTAs (2: a pair, 4: two pairs) of the pair kernel (SMs left over in a GPC cannot
+// host part of a cluster); cached per (device, smem, cluster size)
+static int pair_clusters(size_t smem, int csize) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, size_t, int>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, smem, csize);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * (num_sms() / 2));
+  cfg.gridDim = dim3(csize * (num_sms() / csize));
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true, EK_PLAIN>, &cfg) != cudaSuccess || n <= 0) {
+  const cudaError_t e = csize == 4
+                            ? cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true, EK_PLAIN, 2>, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&n, gemm_bf16_kernel<true, EK_PLAIN>, &cfg);
+  if (e != cudaSuccess || n <= 0) {
     cudaGetLastError();
-    n = num_sms() / 2;
+    n = num_sms() / csize;
   }
-  cached = n;
-  cached_smem = smem;
+  cache[key] = n;
   return n;
 }
 
@@ -791,7 +836,9 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
   const int esz = p.tf32 ? 4 : 2, bke = p.tf32 ? BK / 2 : BK;
   int rc = make_tmap_2d(&tmA, A, in_t, p.K, p.M, (uint64_t)p.lda * esz, bke, BM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
-  rc = make_tmap_2d(&tmB, Bw, in_t, p.K, p.N, (uint64_t)p.ldb * esz, bke, pair ? p.BN / 2 : p.BN,
+  // B multicast across two pairs: bf16 epilogues, no split-K, whole 32-row quarters, at least two pair tiles
+  const int mc = (pair && mc_enabled() && p.epi != EPI_STORE_F32 && p.BN % 32 == 0 && p.M > 2 * TMr) ? 2 : 1;
+  rc = make_tmap_2d(&tmB, Bw, in_t, p.K, p.N, (uint64_t)p.ldb * esz, bke, pair ? p.BN / (2 * mc) : p.BN,
                     CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
   memset(&tmOut, 0, sizeof(tmOut));
@@ -817,17 +864,20 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
     if (rc) return rc;
   }
   {
-    const void* fns[8] = {(const void*)gemm_bf16_kernel<false, EK_PLAIN>, (const void*)gemm_bf16_kernel<false, EK_ROPE>,
+    const void* fns[11] = {(const void*)gemm_bf16_kernel<false, EK_PLAIN>, (const void*)gemm_bf16_kernel<false, EK_ROPE>,
                           (const void*)gemm_bf16_kernel<false, EK_GELU>, (const void*)gemm_bf16_kernel<false, EK_F32>,
                           (const void*)gemm_bf16_kernel<true, EK_PLAIN>, (const void*)gemm_bf16_kernel<true, EK_ROPE>,
-                          (const void*)gemm_bf16_kernel<true, EK_GELU>, (const void*)gemm_bf16_kernel<true, EK_F32>};
+                          (const void*)gemm_bf16_kernel<true, EK_GELU>, (const void*)gemm_bf16_kernel<true, EK_F32>,
+                          (const void*)gemm_bf16_kernel<true, EK_PLAIN, 2>, (const void*)gemm_bf16_kernel<true, EK_ROPE, 2>,
+                          (const void*)gemm_bf16_kernel<true, EK_GELU, 2>};
     for (const void* f : fns) func_smem_once(f, (int)GEMM_SMEM_MAX);
   }
   const int ek = p.epi == EPI_QKV_ROPE ? EK_ROPE : (p.gelu ? EK_GELU : (p.epi == EPI_STORE_F32 ? EK_F32 : EK_PLAIN));
   const size_t smem = gemm_fixed_bytes(gemm_epi_smem(p.BN, resid, f32o, p.warp_epi, p.nbuf, p.res_global)) +
                       (size_t)p.stages * gemm_stage_bytes(p.BN, pair);
   if (smem > GEMM_SMEM_MAX) return -2;
-  const long long tiles = (long long)m_tiles * ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
+  const long long tiles = (long long)(mc > 1 ? (p.M + 2 * TMr - 1) / (2 * TMr) : m_tiles) *
+                          ((p.N + p.BN - 1) / p.BN) * (p.splits > 1 ? p.splits : 1);
   PSCWIN_PROF(p.prof_name ? p.prof_name : "gemm", stream);
   if (!pair) {
     const int grid = tiles < num_sms() ? (int)tiles : num_sms();
@@ -841,23 +891,30 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
       launch_k(gemm_bf16_kernel<false, EK_PLAIN>, dim3(grid), dim3(GEMM_THREADS), smem, stream, tmA, tmB, tmOut, tmRes, p);
     return (int)cudaGetLastError();
   }
-  const int clusters_max = pair_clusters(smem);
+  const int csize = 2 * mc;
+  const int clusters_max = pair_clusters(smem, csize);
   const int clusters = tiles < clusters_max ? (int)tiles : clusters_max;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * clusters);
+  cfg.gridDim = dim3(csize * clusters);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = csize;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  if (ek == EK_ROPE)
+  if (mc > 1 && ek == EK_ROPE)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_ROPE, 2>, tmA, tmB, tmOut, tmRes, p);
+  else if (mc > 1 && ek == EK_GELU)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_GELU, 2>, tmA, tmB, tmOut, tmRes, p);
+  else if (mc > 1)
+    cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_PLAIN, 2>, tmA, tmB, tmOut, tmRes, p);
+  else if (ek == EK_ROPE)
     cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_ROPE>, tmA, tmB, tmOut, tmRes, p);
   else if (ek == EK_GELU)
     cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<true, EK_GELU>, tmA, tmB, tmOut, tmRes, p);
