@@ -264,7 +264,15 @@ __global__ void __launch_bounds__(256) ms_permute_rows_kernel(const __nv_bfloat1
 #define PSCWIN_TSUB 16  // tokens per staged sub-chunk of the passes (sweeps: PSCWIN_NVCC_FLAGS)
 #endif
 constexpr int TSUB = PSCWIN_TSUB;
-template <int DPB, int NT, bool PASS2>  // DPB channels per CTA, NT threads
+// FDT (pass 1 with the dt projection fused): the whole x_proj row (delta_low | B | C) is staged at the padded stride
+// W = fdt_stride(R + 2N) floats (an odd multiple of 4 mod 32: the tf32 mma's A-fragment loads hit 32 distinct banks)
+// and Delta is not loaded (pass 1 computes it into the stage's Delta slot).
+__host__ __device__ inline int fdt_stride(int w) {
+  int s = (w + 3) & ~3;
+  while ((s & 31) % 8 != 4) s += 4;
+  return s;
+}
+template <int DPB, int NT, bool PASS2, bool FDT = false>  // DPB channels per CTA, NT threads
 struct StageLayout {
   // byte offsets inside one stage buffer
   __host__ __device__ static size_t off_v(int W) { return (size_t)TSUB * W * 4; }
@@ -282,18 +290,27 @@ struct StageLayout {
     // the dt GEMM alone): row stride R + 2N in global memory, column offset R
     float* sd = reinterpret_cast<float*>(buf);
     __nv_bfloat16* sv = reinterpret_cast<__nv_bfloat16*>(buf + off_v(W));
-    const int gw = p.R + W, W4 = W / 4;
-    const float* gd = p.dbc + (rbase + t) * gw + p.R;
-    for (int i = tid; i < nt * W4; i += NT) {
-      const int j = i / W4, q = i - j * W4;
-      cp_async16(sd + 4 * i, gd + (long long)j * gw + 4 * q);
+    if (FDT) {  // whole rows (R + 2N floats) at stride W
+      const int gw = p.R + 2 * p.N, W4 = gw / 4;
+      const float* gd = p.dbc + (rbase + t) * gw;
+      for (int i = tid; i < nt * W4; i += NT) {
+        const int j = i / W4, q = i - j * W4;
+        cp_async16(sd + j * W + 4 * q, gd + (long long)j * gw + 4 * q);
+      }
+    } else {
+      const int gw = p.R + W, W4 = W / 4;
+      const float* gd = p.dbc + (rbase + t) * gw + p.R;
+      for (int i = tid; i < nt * W4; i += NT) {
+        const int j = i / W4, q = i - j * W4;
+        cp_async16(sd + 4 * i, gd + (long long)j * gw + 4 * q);
+      }
     }
     constexpr int VPR = DPB / 8;  // 16-byte chunks per token row of bf16
     for (int i = tid; i < nt * VPR; i += NT) {
       const int j = i / VPR, cc = i - j * VPR;
       cp_async16(sv + j * DPB + cc * 8, p.v + (rbase + t + j) * p.D + d0 + cc * 8);
     }
-    {
+    if (!FDT) {
       float* sdt = reinterpret_cast<float*>(buf + off_dt(W));
       constexpr int FPR = DPB / 4;
       for (int i = tid; i < nt * FPR; i += NT) {
@@ -413,14 +430,47 @@ __device__ __forceinline__ float2 decay2(int k, float2 x) {
   return make_float2(ex2_approx(x.x), ex2_approx(x.y));
 }
 
-template <int N, int DPB, int NS, bool ZOH, int PK>
-__global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
+// dt projection fused into pass 1 (FDT): Delta = softplus(delta_low W_dt^T + b_dt) (Q12) for the sub-chunk's 16
+// tokens x this warp's 8 channels as TF32 tensor-core MMAs (mma.sync m16n8k8: A = the staged delta_low rows,
+// B = the warp's W_dt rows held in registers as fragments), written into the stage's Delta slot for the recurrence
+// and to global memory for the carry and pass 2, in place of the separate dt GEMM (whose 400 MB f32 write at 4096^2
+// would happen inside a MUFU-bound kernel whose HBM is idle). Measured slower; off by default (launch_dt_pass1).
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return u;
+}
+__device__ __forceinline__ void mma_tf32_16x8x8(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                                uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+               "{%0,%1,%2,%3};"
+               : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+               : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// softplus with two MUFU: log1p(t), t = e^x, as t (1 - t/2 + t^2/3 - t^3/4 + t^4/5) below t = 1/32, else log(1 + t)
+// (same formula as the dt GEMM's f32 epilogue)
+__device__ __forceinline__ float softplus_dt(float x) {
+  const float t = __expf(x);
+  const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 0.2f, -0.25f), 0.33333334f), -0.5f), 1.f);
+  const float lp = t < 0.03125f ? poly : __logf(1.f + t);
+  return x > 20.f ? x : lp;
+}
+constexpr int FDT_KS = 8;  // k-steps of 8 (R <= 64)
+// resident CTAs per SM the fused pass 1 is register-bounded for (4: <= 64 registers, the unfused pass 1's occupancy)
+#ifndef PSCWIN_PASS1_FDT_MINB
+#define PSCWIN_PASS1_FDT_MINB 4
+#endif
+
+template <int N, int DPB, int NS, bool ZOH, int PK, bool FDT = false>
+__global__ void __launch_bounds__(DPB * NS, FDT ? PSCWIN_PASS1_FDT_MINB : 0) scan_pass1_kernel(ScanParams p) {
   pdl_trigger();
   pdl_wait();
   constexpr int NT = DPB * NS, NH = N / NS;
-  using St = StageLayout<DPB, NT, false>;
+  static_assert(!FDT || (NS == 4 && DPB == 64), "fused dt: one warp = 8 channels x 4 state groups");
+  using St = StageLayout<DPB, NT, false, FDT>;
   extern __shared__ __align__(128) uint8_t s_raw[];
-  const int W = 2 * N;  // staged (B, C) row
+  const int W = FDT ? fdt_stride(p.R + 2 * N) : 2 * N;  // staged row stride (floats)
+  const int boff = FDT ? p.R : 0;                         // B columns inside the staged row
   const size_t SB = St::bytes(W);
   const int c = threadIdx.x / NS, sub = threadIdx.x % NS;
   const int d0 = blockIdx.x * DPB;
@@ -444,6 +494,52 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
     St::load(s_raw, p, W, rbase, 0, tb, min(TSUB, t1 - tb), d0);
     cp_async_commit();
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // FDT: the warp's B fragments (W_dt rows of its 8 channels, tf32) live in shared memory after the two stage
+  // buffers, [warp][k-step][lane] pairs, reloaded per sub-chunk (kept in registers they cost the recurrence its ILP)
+  uint2* s_wf = reinterpret_cast<uint2*>(s_raw + 2 * SB) + wid * (FDT_KS * 32);
+  if constexpr (FDT) {
+    const int g = lane >> 2, tq = lane & 3;
+    const float* wr = p.w_dt + (size_t)(d0 + 8 * wid + g) * p.R;
+#pragma unroll
+    for (int ks = 0; ks < FDT_KS; ++ks) {
+      const int r0 = 8 * ks + tq, r1 = r0 + 4;
+      s_wf[ks * 32 + lane] = make_uint2(tf32_rna(r0 < p.R ? __ldg(wr + r0) : 0.f), tf32_rna(r1 < p.R ? __ldg(wr + r1) : 0.f));
+    }
+    __syncwarp();
+    if (chunk == 0) {
+      // the carry's prefix tokens, rows [0, P) (copies 2/3) and [L, L+P) (copy 1): plain dot products (delta_low
+      // truncated to tf32 as the MMA reads it, W_dt rounded as its fragments), 16-byte loads all issued up front;
+      // thread `sub` of each channel takes rows sub, sub + NS, ...
+      const int gw = p.R + 2 * N;
+      for (int i = sub; i < 2 * p.P; i += NS) {
+        const long long row = rbase + (i < p.P ? i : p.L + i - p.P);
+        const float4* dl = reinterpret_cast<const float4*>(p.dbc + row * gw);
+        const float4* wd = reinterpret_cast<const float4*>(p.w_dt + (size_t)d * p.R);
+        float acc = 0.f;
+        auto tr = [](float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); };
+        auto rn = [](float x) { return __uint_as_float(tf32_rna(x)); };
+        for (int q0 = 0; 4 * q0 < p.R; q0 += 4) {  // four 16-byte loads of each operand in flight per round
+          float4 xv[4], wv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * (q0 + q) < p.R) {
+              xv[q] = dl[q0 + q];
+              wv[q] = __ldg(wd + q0 + q);
+            }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (4 * (q0 + q) < p.R) {
+              acc = fmaf(tr(xv[q].x), rn(wv[q].x), acc);
+              acc = fmaf(tr(xv[q].y), rn(wv[q].y), acc);
+              acc = fmaf(tr(xv[q].z), rn(wv[q].z), acc);
+              acc = fmaf(tr(xv[q].w), rn(wv[q].w), acc);
+            }
+        }
+        p.delta[row * p.D + d] = softplus_dt(acc + __ldg(p.b_dt + d));
+      }
+    }
+  }
   const float2 m1 = f2(-1.f);
   for (int sc = 0; sc < nsub; ++sc) {
     const int ts = tb + sc * TSUB;
@@ -456,15 +552,40 @@ __global__ void __launch_bounds__(DPB * NS) scan_pass1_kernel(ScanParams p) {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const uint8_t* buf = s_raw + (sc & 1) * SB;
+    uint8_t* buf = s_raw + (sc & 1) * SB;
     const float* sdbc = reinterpret_cast<const float*>(buf);
     const __nv_bfloat16* sv = reinterpret_cast<const __nv_bfloat16*>(buf + St::off_v(W));
-    const float* sdelta = reinterpret_cast<const float*>(buf + St::off_dt(W));
+    float* sdelta = reinterpret_cast<float*>(buf + St::off_dt(W));
+    float* sdw = sdelta + wid * (TSUB * 8);  // FDT: this warp's [TSUB][8] Delta block
+    if constexpr (FDT) {
+      const int g = lane >> 2, tq = lane & 3;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int ks_n = (p.R + 7) / 8;
+      const float2 bdt = make_float2(__ldg(p.b_dt + d0 + 8 * wid + 2 * tq), __ldg(p.b_dt + d0 + 8 * wid + 2 * tq + 1));
+#pragma unroll
+      for (int ks = 0; ks < FDT_KS; ++ks)
+        if (ks < ks_n) {
+          // A = the f32 bit patterns (the tensor core reads their tf32 part, as the kind::tf32 dt GEMM did): a
+          // cvt.rna per element runs on the XU pipe that bounds this kernel (measured: +0.3 ms at 4096^2 with it)
+          const uint32_t* a = reinterpret_cast<const uint32_t*>(sdbc) + 8 * ks + tq;
+          const uint2 wf = s_wf[ks * 32 + lane];
+          mma_tf32_16x8x8(acc, a[g * W], a[(g + 8) * W], a[g * W + 4], a[(g + 8) * W + 4], wf.x, wf.y);
+        }
+      *reinterpret_cast<float2*>(sdw + g * 8 + 2 * tq) =
+          make_float2(softplus_dt(acc[0] + bdt.x), softplus_dt(acc[1] + bdt.y));
+      *reinterpret_cast<float2*>(sdw + (g + 8) * 8 + 2 * tq) =
+          make_float2(softplus_dt(acc[2] + bdt.x), softplus_dt(acc[3] + bdt.y));
+      __syncwarp();
+      const int j = lane >> 1, h4 = (lane & 1) * 4;  // Delta rows for the carry / pass 2: 32 bytes per token row
+      if (j < nt)
+        *reinterpret_cast<float4*>(p.delta + (rbase + ts + j) * p.D + d0 + 8 * wid + h4) =
+            *reinterpret_cast<const float4*>(sdw + j * 8 + h4);
+    }
     auto tstep = [&](int j) {
       const float v = __bfloat162float(sv[j * DPB + c]);
-      const float dt = sdelta[j * DPB + c];
+      const float dt = FDT ? sdw[j * 8 + (lane >> 2)] : sdelta[j * DPB + c];
       sdt += dt;
-      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + n0);  // two state pairs per load
+      const float4* b4 = reinterpret_cast<const float4*>(sdbc + j * W + boff + n0);  // two state pairs per load
       const float2 dt2 = f2(dt), nv2 = f2(-v);
 #pragma unroll
       for (int k = 0; k < NH / 2; ++k) {
@@ -1153,8 +1274,19 @@ static int check_scan(int B, int L, int D, int N, int R, int k) {
 }
 
 template <int N, int NS>
-static void launch_pass1(ScanParams& p, cudaStream_t s) {
+static void launch_pass1(ScanParams& p, cudaStream_t s, bool fdt = false) {
   const dim3 grid(p.D / PASS_DPB, p.n_chunks, p.B);
+  if constexpr (NS == 4) {
+    if (fdt) {
+      const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false, true>::bytes(fdt_stride(p.R + 2 * N)) +
+                          (size_t)(PASS_DPB * NS / 32) * FDT_KS * 32 * sizeof(uint2);  // + the W_dt fragments
+      if (p.bbar != 0)
+        launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, false, 0, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+      else
+        launch_k_even(scan_pass1_kernel<N, PASS_DPB, NS, true, 0, true>, grid, dim3(PASS_DPB * NS), smem, s, p);
+      return;
+    }
+  }
   const size_t smem = 2 * StageLayout<PASS_DPB, PASS_DPB * NS, false>::bytes(2 * N);
   const int pk = pass1_pk();
   if (p.bbar != 0)
@@ -1185,7 +1317,17 @@ static void launch_pass2(ScanParams& p, cudaStream_t s) {
 template <int N>
 static void launch_dt_pass1(ScanParams& p, cudaStream_t s) {
   static const bool dt_ffma = getenv("PSCWIN_DT_FFMA") != nullptr;  // A/B knob: the CUDA-core dt kernel
+  // A/B knob PSCWIN_DT_FUSE=1: the dt projection fused into pass 1 instead of the separate dt GEMM. Off: measured
+  // at 4096^2 the fused pass 1 takes 1.06 ms against 0.796 + 0.117 ms for pass 1 + the dt GEMM (its per-sub-chunk
+  // MMA / softplus phase stalls every warp of the CTA at once and adds MUFU work to the MUFU-bound loop)
+  static const int dt_fuse = env_knob("PSCWIN_DT_FUSE", 0);
   const long long rows = (long long)p.B * (p.L + p.P);
+  const bool fdt = dt_fuse != 0 && !dt_ffma && pass1_ns() == 4 && p.R % 4 == 0 && p.R <= 8 * FDT_KS;
+  if (fdt) {
+    PSCWIN_PROF("scan_pass1", s);
+    launch_pass1<N, 4>(p, s, true);
+    return;
+  }
   if (!dt_ffma && p.R % 4 == 0) {
     // Delta = softplus(delta_low W_dt^T + b_dt) as a TF32 tensor-core GEMM (M = rows, N = D, K = R) reading
     // delta_low straight out of the x_proj output (row stride R + 2N) with the softplus in the f32 epilogue

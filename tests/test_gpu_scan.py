@@ -200,3 +200,39 @@ def test_pdl_on_equals_off(pl, tmp_path):
         res[flag] = np.load(out)
     for k in res["1"].files:
         assert np.array_equal(res["1"][k], res["0"][k]), k
+
+
+_FDT_CHILD = r'''
+import os, sys
+sys.path.insert(0, os.environ["PSCWIN_ROOT"]); sys.path.insert(0, os.path.join(os.environ["PSCWIN_ROOT"], "tests"))
+import numpy as np
+import synth
+from gpu_util import dev, dev_weights, host
+import paper_2407_02109_b200 as pl
+from test_gpu_scan import SCAN_CASES, _desc, _scan_inputs
+outs = []
+for cfg in SCAN_CASES:
+    xin, z = _scan_inputs(cfg)
+    outs.append(host(pl.cycle_scan(_desc(pl, cfg), dev(xin), dev(z), dev_weights(synth.make_weights(cfg), cfg))))
+np.savez(sys.argv[1], *outs)
+'''
+
+
+def test_fused_dt_pass1(pl, tmp_path):
+    # A/B variant PSCWIN_DT_FUSE=1 (the dt projection as tf32 mma.sync inside pass 1, measured slower and off by
+    # default): every scan case still matches the oracle's literal 3L recurrence
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "child.py"
+    script.write_text(_FDT_CHILD)
+    out = tmp_path / "fdt.npz"
+    subprocess.run([sys.executable, str(script), str(out)], check=True, timeout=600,
+                   env=dict(os.environ, PSCWIN_DT_FUSE="1", PSCWIN_ROOT=root))
+    got = np.load(out)
+    for i, cfg in enumerate(SCAN_CASES):
+        xin, z = _scan_inputs(cfg)
+        ref = oracle.cycle_scan(xin, z, synth.make_weights(cfg), cfg.H, cfg.W, scan_order=cfg.scan_order,
+                                bbar_mode=cfg.bbar_mode, window=cfg.window)
+        assert rel_err(got[f"arr_{i}"], ref) < BF16_TOL, i
