@@ -86,22 +86,33 @@ __global__ void layer_norm_kernel(const T* __restrict__ x, long long rows, int C
 // issue-bound at 39 % of DRAM bandwidth); here each 16-byte vector is four (lo, hi) pairs: FADD2 sums, the centred
 // values d = x - mean kept for the variance and the output, FFMA2 d^2 sums, then y = d (rstd gamma) + beta as FMUL2 +
 // FFMA2 and one F2FP pack per pair (~4.5 instructions per element).
-template <int NV>  // 16-byte vectors per lane: ceil(C / 256)
+// RPW rows per warp: the loads of all RPW rows are issued up front, then the rows are normalised in turn (ncu r02n
+// shows long-scoreboard stalls of 11.7 warps per issue at one row per warp, but 2 / 4 rows per warp measured slower:
+// the occupancy they cost outweighs the loads in flight they add; RPW = 1 is the default).
+template <int NV, int RPW>  // 16-byte vectors per lane: ceil(C / 256)
 __global__ void layer_norm_bf16x2_kernel(const __nv_bfloat16* __restrict__ x, long long rows, int C,
                                          const float* __restrict__ g, const float* __restrict__ b, float eps,
                                          __nv_bfloat16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
-  long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const long long row0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW;
+  if (row0 >= rows) return;
   const int lane = threadIdx.x & 31;
   const int nvec = C / 8;
-  const uint4* src = reinterpret_cast<const uint4*>(x + row * C);
-  float2 d[NV][4];
-  uint4 v[NV];
+  uint4 vr[RPW][NV];
 #pragma unroll
-  for (int k = 0; k < NV; ++k)
-    if (lane + 32 * k < nvec) v[k] = src[lane + 32 * k];
+  for (int r = 0; r < RPW; ++r) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + (row0 + r) * C);
+#pragma unroll
+    for (int k = 0; k < NV; ++k)
+      if (row0 + r < rows && lane + 32 * k < nvec) vr[r][k] = src[lane + 32 * k];
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+  const long long row = row0 + r;
+  if (row >= rows) break;
+  const uint4 (&v)[NV] = vr[r];
+  float2 d[NV][4];
   float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
@@ -157,6 +168,7 @@ __global__ void layer_norm_bf16x2_kernel(const __nv_bfloat16* __restrict__ x, lo
       dst[i] = w;
     }
   }
+  }  // rows of this warp
 }
 
 int launch_layer_norm(const void* x, long long rows, int C, const float* g, const float* b, float eps, int is_f32,
@@ -164,6 +176,10 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
   if (rows == 0) return 0;
   unsigned grid = (unsigned)((rows + 7) / 8);
   PSCWIN_PROF("layer_norm", stream);
+  // rows per warp of the packed bf16 kernel (A/B knob PSCWIN_LN_RPW = 1, 2 or 4, read once). One: measured at
+  // 65536 x 768 (graph-timed, L2 flushed) 45.6 / 47.0 / 53.1 us for 1 / 2 / 4 rows per warp (profiles/r02/rowops_r02o.log)
+  static const int rpw_knob = env_knob("PSCWIN_LN_RPW", 1);
+  const int rpw = (rpw_knob == 2 || rpw_knob == 4) ? rpw_knob : 1;
   if (is_f32) {
     if (C % 4 || C > 1024) return -1;
     launch_k(layer_norm_kernel<float>, dim3(grid), dim3(256), 0, stream, (const float*)x, rows, C, g, b, eps, (float*)out);
@@ -172,16 +188,30 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
     static const int packed = env_knob("PSCWIN_LN_PACKED", 1);  // A/B knob: 0 = the scalar kernel
     if (packed) {
       const int nv = (C / 8 + 31) / 32;
-      auto go = [&](auto kern) {
-        launch_k(kern, dim3(grid), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, g, b, eps, (__nv_bfloat16*)out);
+      auto go = [&](auto kern, int r) {
+        const unsigned gr = (unsigned)((rows + 8LL * r - 1) / (8LL * r));
+        launch_k(kern, dim3(gr), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, g, b, eps, (__nv_bfloat16*)out);
       };
+      if (nv <= 4 && rpw > 1) {  // (wide rows keep one row per warp: their loads already fill the warp)
+        switch (nv * 8 + rpw) {
+          case 10: go(layer_norm_bf16x2_kernel<1, 2>, 2); break;
+          case 12: go(layer_norm_bf16x2_kernel<1, 4>, 4); break;
+          case 18: go(layer_norm_bf16x2_kernel<2, 2>, 2); break;
+          case 20: go(layer_norm_bf16x2_kernel<2, 4>, 4); break;
+          case 26: go(layer_norm_bf16x2_kernel<3, 2>, 2); break;
+          case 28: go(layer_norm_bf16x2_kernel<3, 4>, 4); break;
+          case 34: go(layer_norm_bf16x2_kernel<4, 2>, 2); break;
+          default: go(layer_norm_bf16x2_kernel<4, 4>, 4); break;
+        }
+        return (int)cudaGetLastError();
+      }
       switch (nv) {
-        case 1: go(layer_norm_bf16x2_kernel<1>); break;
-        case 2: go(layer_norm_bf16x2_kernel<2>); break;
-        case 3: go(layer_norm_bf16x2_kernel<3>); break;
-        case 4: go(layer_norm_bf16x2_kernel<4>); break;
-        case 5: case 6: go(layer_norm_bf16x2_kernel<6>); break;
-        default: go(layer_norm_bf16x2_kernel<8>); break;
+        case 1: go(layer_norm_bf16x2_kernel<1, 1>, 1); break;
+        case 2: go(layer_norm_bf16x2_kernel<2, 1>, 1); break;
+        case 3: go(layer_norm_bf16x2_kernel<3, 1>, 1); break;
+        case 4: go(layer_norm_bf16x2_kernel<4, 1>, 1); break;
+        case 5: case 6: go(layer_norm_bf16x2_kernel<6, 1>, 1); break;
+        default: go(layer_norm_bf16x2_kernel<8, 1>, 1); break;
       }
       return (int)cudaGetLastError();
     }
