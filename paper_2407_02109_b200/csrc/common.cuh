@@ -379,6 +379,12 @@ PSCWIN_DEVICE float ex2_approx(float x) {
   return y;
 }
 
+PSCWIN_DEVICE float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 PSCWIN_DEVICE float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

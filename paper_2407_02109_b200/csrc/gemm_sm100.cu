@@ -610,12 +610,23 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // log1p(t): t (1 - t/2 + t^2/3 - t^3/4 + t^4/5) for t < 1/32 (truncation < t^6/6: 1e-9 relative), else
           // log(1 + t) on MUFU (the rounding of 1 + t costs <= 6e-8 / log1p(t) <= 2e-6 relative there): two MUFU
           // per element instead of three (no division)
+          // Packed fp32x2 (round 2: the epilogue was issue-bound, ncu r02n 67 % issue with the softplus lines at 37 %
+          // of the stall samples): per pair FMUL2 + 2 ex2, the polynomial as FFMA2s, FADD2 + 2 lg2 + FMUL2, selects
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float t = __expf(v[j]);
-            const float poly = t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 0.2f, -0.25f), 0.33333334f), -0.5f), 1.f);
-            const float lp = t < 0.03125f ? poly : __logf(1.f + t);
-            v[j] = v[j] > 20.f ? v[j] : lp;
+          for (int j = 0; j < 32; j += 2) {
+            const float2 x = make_float2(v[j], v[j + 1]);
+            const float2 xs = __fmul2_rn(x, make_float2(1.4426950408889634f, 1.4426950408889634f));
+            const float2 t = make_float2(ex2_approx(xs.x), ex2_approx(xs.y));
+            float2 q = __ffma2_rn(t, make_float2(0.2f, 0.2f), make_float2(-0.25f, -0.25f));
+            q = __ffma2_rn(t, q, make_float2(0.33333334f, 0.33333334f));
+            q = __ffma2_rn(t, q, make_float2(-0.5f, -0.5f));
+            q = __ffma2_rn(t, q, make_float2(1.f, 1.f));
+            q = __fmul2_rn(t, q);
+            const float2 u = __fadd2_rn(t, make_float2(1.f, 1.f));
+            const float2 l = __fmul2_rn(make_float2(lg2_approx(u.x), lg2_approx(u.y)),
+                                        make_float2(0.69314718055994531f, 0.69314718055994531f));
+            v[j] = x.x > 20.f ? x.x : (t.x < 0.03125f ? q.x : l.x);
+            v[j + 1] = x.y > 20.f ? x.y : (t.y < 0.03125f ? q.y : l.y);
           }
         }
         if (f32_tma) {
