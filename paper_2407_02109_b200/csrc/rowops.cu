@@ -89,14 +89,18 @@ __global__ void layer_norm_kernel(const T* __restrict__ x, long long rows, int C
 // RPW rows per warp: the loads of all RPW rows are issued up front, then the rows are normalised in turn (ncu r02n
 // shows long-scoreboard stalls of 11.7 warps per issue at one row per warp, but 2 / 4 rows per warp measured slower:
 // the occupancy they cost outweighs the loads in flight they add; RPW = 1 is the default).
+// rev: rows are visited last-first. The LayerNorm input is the residual stream the previous GEMM has just written in
+// row order, so its LAST rows are the ones still resident in L2; reading them first turns part of the read into L2 hits.
 template <int NV, int RPW>  // 16-byte vectors per lane: ceil(C / 256)
 __global__ void layer_norm_bf16x2_kernel(const __nv_bfloat16* __restrict__ x, long long rows, int C,
                                          const float* __restrict__ g, const float* __restrict__ b, float eps,
-                                         __nv_bfloat16* __restrict__ out) {
+                                         __nv_bfloat16* __restrict__ out, int rev) {
   pdl_trigger();
   pdl_wait();
-  const long long row0 = ((long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RPW;
-  if (row0 >= rows) return;
+  const long long wg = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nwg = (rows + RPW - 1) / RPW;
+  if (wg >= nwg) return;
+  const long long row0 = (rev ? nwg - 1 - wg : wg) * RPW;
   const int lane = threadIdx.x & 31;
   const int nvec = C / 8;
   uint4 vr[RPW][NV];
@@ -180,6 +184,7 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
   // 65536 x 768 (graph-timed, L2 flushed) 45.6 / 47.0 / 53.1 us for 1 / 2 / 4 rows per warp (profiles/r02/rowops_r02o.log)
   static const int rpw_knob = env_knob("PSCWIN_LN_RPW", 1);
   const int rpw = (rpw_knob == 2 || rpw_knob == 4) ? rpw_knob : 1;
+  static const int rev = env_knob("PSCWIN_LN_REV", 1);  // A/B knob: 0 = rows first-to-last
   if (is_f32) {
     if (C % 4 || C > 1024) return -1;
     launch_k(layer_norm_kernel<float>, dim3(grid), dim3(256), 0, stream, (const float*)x, rows, C, g, b, eps, (float*)out);
@@ -190,7 +195,8 @@ int launch_layer_norm(const void* x, long long rows, int C, const float* g, cons
       const int nv = (C / 8 + 31) / 32;
       auto go = [&](auto kern, int r) {
         const unsigned gr = (unsigned)((rows + 8LL * r - 1) / (8LL * r));
-        launch_k(kern, dim3(gr), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, g, b, eps, (__nv_bfloat16*)out);
+        launch_k(kern, dim3(gr), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, g, b, eps, (__nv_bfloat16*)out,
+                 rev);
       };
       if (nv <= 4 && rpw > 1) {  // (wide rows keep one row per warp: their loads already fill the warp)
         switch (nv * 8 + rpw) {
