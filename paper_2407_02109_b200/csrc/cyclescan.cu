@@ -49,6 +49,7 @@ struct ScanParams {
   // band mode (window-row sharding): the k-1 xin rows preceding this segment in the cycled sequence
   // (the previous rank's tail; rank 0: the global sequence tail) replace the local wrap-around; null = one segment
   const __nv_bfloat16* hist;
+  int conv_rev;  // conv_silu visits row groups last-first (A/B knob PSCWIN_CONV_REV)
 };
 
 // SiLU(x) = x / (1 + e^-x) with the fast division (MUFU rcp; -> 0 as e^-x overflows for very negative x)
@@ -74,7 +75,10 @@ __global__ void __launch_bounds__(256) conv_silu_kernel(ScanParams p) {
   const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)p.B * groups_img * dv) return;
   const int d0 = (int)(idx % dv) * 8;
-  const long long grp = idx / dv;
+  // row groups last-first (p.conv_rev): the in_proj GEMM has just written xin in row order, so its last rows are the
+  // L2-resident ones; and the x_proj GEMM, which reads v first-to-last, then finds the rows written last first
+  const long long ngrp = (long long)p.B * groups_img;
+  const long long grp = p.conv_rev ? ngrp - 1 - idx / dv : idx / dv;
   const int b = (int)(grp / groups_img);
   const int r0 = (int)(grp - (long long)b * groups_img) * CONV_T;
   const __nv_bfloat16* xb = p.xin + (long long)b * p.L * p.ld_x + d0;
@@ -1429,6 +1433,8 @@ static ScanParams make_scan_params(const ScanPlan& pl, int B, int L, int D, int 
   p.ld_out = ld_out;
   p.vec_out = (ld_out % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) ? 1 : 0;
   p.hist = nullptr;
+  static const int conv_rev = env_knob("PSCWIN_CONV_REV", 1);
+  p.conv_rev = conv_rev;
   return p;
 }
 
