@@ -188,9 +188,20 @@ struct LayerWs {
 // saves 19 us per LayerNorm but the folded epilogue (two more FMAs per element, s_n from shared memory, register
 // spills in the RoPE variant) makes the QKV GEMM 186 -> 213 us and in_proj 235 -> 272 us: the projections'
 // epilogues, not their tensor pipes, bound them once the LayerNorm work moves in.
-bool ln_fold_enabled() {
-  static const bool on = env_knob("PSCWIN_LN_FOLD", 0) != 0;
-  return on;
+// PSCWIN_LN_FOLD = 2 (default): LN1 folded into the QKV projection on every path (whole image, row bands,
+// multi-scale), LN_s -> in_proj and LN2 -> fc1 kept as LayerNorm passes; 1: all three folded (whole-image path);
+// 0: no folding. Measured at 4096^2 (profiles/r02/ln_fold_r02x.log, bench --breakdown): the row-stats pass
+// (33 us) replaces the LayerNorm (45 us) while the folded RoPE epilogue now costs the QKV GEMM < 1 us (the round-2
+// per-warp epilogue; 27 us with the round-1 epilogue, r02c); in_proj's folded epilogue still costs +14 us, more
+// than its LayerNorm saving, so LN_s stays a pass.
+// Folding applies to images of at least PSCWIN_LN_FOLD_MIN_T tokens (B H W of the WHOLE image, so whole-image, band
+// and multi-scale paths of one problem choose alike): at 1024^2 (4096 tokens) the weight fold on the side stream is
+// not hidden behind the short row-stats pass and the stage measured 0.372 -> 0.391 ms with it.
+int ln_fold_mode(long long tokens) {
+  static const int mode = env_knob("PSCWIN_LN_FOLD", 2);
+  static const int min_t = env_knob("PSCWIN_LN_FOLD_MIN_T", 16384);
+  if (tokens < min_t) return 0;
+  return (mode == 0 || mode == 1) ? mode : 2;
 }
 size_t fold_bytes(size_t N, size_t K) { return align256(N * K * 2) + align256(N * 4) * 2; }
 LnFold fold_at(void* ws, size_t off, size_t N, size_t K, size_t stats_off) {
@@ -207,6 +218,26 @@ int fold_launch(const LnFold& f, const void* W, int N, int K, const void* g, con
                 cudaStream_t s) {
   return launch_ln_fold(W, N, K, (const float*)g, (const float*)be, (const float*)bias, const_cast<void*>(f.wf),
                         const_cast<float*>(f.colsum), const_cast<float*>(f.bias), s);
+}
+
+// LN1 -> QKV on the band and multi-scale paths: LayerNorm pass + GEMM, or (ln_fold_mode() != 0) the weight fold on
+// the layer's stream, then the row statistics and the folded GEMM -- the same arithmetic as the whole-image forward,
+// so the three paths stay bit-identical. fold_ws: fold_bytes(3C, C) bytes; stats: [M] float2.
+int ln1_qkv(const pscwin_layer_weights* wt, float eps, const void* x, GemmArgs a, void* u, void* fold_ws,
+            float2* stats, long long image_tokens, cudaStream_t s) {
+  if (ln_fold_mode(image_tokens) == 0) return ln_gemm(x, (const float*)wt->ln1_g, (const float*)wt->ln1_b, eps, wt->w_qkv, a, u,
+                                          nullptr, s);
+  LnFold f;
+  uint8_t* b = reinterpret_cast<uint8_t*>(fold_ws);
+  const size_t N = a.N, K = a.K;
+  f.wf = b;
+  f.colsum = reinterpret_cast<const float*>(b + align256(N * K * 2));
+  f.bias = reinterpret_cast<const float*>(b + align256(N * K * 2) + align256(N * 4));
+  f.stats = stats;
+  f.ready = nullptr;
+  const int rc = fold_launch(f, wt->w_qkv, a.N, a.K, wt->ln1_g, wt->ln1_b, wt->b_qkv, s);
+  if (rc) return rc;
+  return ln_gemm(x, (const float*)wt->ln1_g, (const float*)wt->ln1_b, eps, wt->w_qkv, a, u, &f, s);
 }
 
 LayerWs plan_layer(const pscwin_layer_desc* d) {
@@ -541,7 +572,10 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   float* qkv_pad = reinterpret_cast<float*>(wsp(ws, L.qkv_pad));
   void* O = wsp(ws, L.O);
   const bool learn_pad = shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE;
-  const bool fold = ln_fold_enabled();
+  const int fold_mode = ln_fold_mode(T);
+  const bool fold = fold_mode != 0;                      // LN1 -> QKV
+  const bool fold_fc1 = fold_mode == 1;                  // LN2 -> fc1
+  const bool fold_in = fold_mode == 1 && d->cycle_scan;  // LN_s -> in_proj
   const int D2 = 2 * d->ssm_expand * C;
   // Weight-only work on the side stream, forked at the start of the layer: the LayerNorm folds of the projections
   // (cycle-scan in_proj, QKV, fc1) and the learnable pad token's projection + rotated tables. Each consumer waits
@@ -553,7 +587,7 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   LnFold f_fc1 = fold_at(ws, L.f_fc1, d->mlp_hidden, C, L.stats);
   if (fork && (cudaEventRecord(sd->fork, s) != cudaSuccess || cudaStreamWaitEvent(sd->s, sd->fork, 0) != cudaSuccess))
     return PSCWIN_ERR_CUDA;
-  if (fold && d->cycle_scan) {
+  if (fold_in) {
     if ((rc = fold_launch(f_in, wt->w_in, D2, C, wt->lns_g, wt->lns_b, nullptr, aux))) return status_from(rc);
     if (fork && cudaEventRecord(f_in.ready = sd->ev[0], aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
   }
@@ -568,14 +602,14 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
     if ((rc = launch_pad_tables(pa, aux))) return status_from(rc);
     if (cudaEventRecord(sd->join, aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
   }
-  if (fold && d->mlp_hidden > 0) {
+  if (fold_fc1 && d->mlp_hidden > 0) {
     if ((rc = fold_launch(f_fc1, wt->w_fc1, d->mlp_hidden, C, wt->ln2_g, wt->ln2_b, wt->b_fc1, aux)))
       return status_from(rc);
     if (fork && cudaEventRecord(f_fc1.ready = sd->ev[2], aux) != cudaSuccess) return PSCWIN_ERR_CUDA;
   }
   const void* x = x_in;
   if (d->cycle_scan) {
-    rc = cycle_scan_module(d, wt, fold ? &f_in : nullptr, x_in, x_out, ws, L.u, L.xz, L.g, L.scan,
+    rc = cycle_scan_module(d, wt, fold_in ? &f_in : nullptr, x_in, x_out, ws, L.u, L.xz, L.g, L.scan,
                            L.total - L.scan, s);
     if (rc) return rc;
     x = x_out;
@@ -602,7 +636,7 @@ int pscwin_forward(const pscwin_layer_desc* d, const pscwin_layer_weights* wt, c
   rc = launch_gemm_bf16(O, wt->w_o, a, s);
   if (rc) return status_from(rc);
   if (d->mlp_hidden > 0)
-    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, L.u), wsp(ws, L.h), s, fold ? &f_fc1 : nullptr);
+    return ffn_bf16(T, C, d->mlp_hidden, d->ln_eps, wt, x_out, wsp(ws, L.u), wsp(ws, L.h), s, fold_fc1 ? &f_fc1 : nullptr);
   return PSCWIN_OK;
 }
 
@@ -651,6 +685,7 @@ int check_ms(const pscwin_ms_desc* m, MsGeo* g) {
 
 struct MsWs {
   size_t u, qkv, qkv_pad, O, pad_tab, h, xz, g, scan, total;
+  size_t stats, fold;  // folded LN1 -> QKV: row statistics [T] float2, W' | s | c
 };
 
 MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
@@ -664,8 +699,10 @@ MsWs plan_ms(const pscwin_ms_desc* m, const MsGeo& g) {
     return o;
   };
   w.u = take(T * C * 2);
-  w.qkv = w.qkv_pad = w.O = w.pad_tab = w.h = w.xz = w.g = w.scan = 0;
+  w.qkv = w.qkv_pad = w.O = w.pad_tab = w.h = w.xz = w.g = w.scan = w.stats = w.fold = 0;
   if (m->attention) {
+    w.stats = take(T * sizeof(float2));
+    w.fold = take(fold_bytes(3 * C, C));
     w.qkv = take(T * 3 * C * 2);
     w.qkv_pad = take(3 * C * 4);
     w.O = take(T * C * 2);
@@ -760,8 +797,6 @@ int pscwin_ms_forward(const pscwin_ms_desc* m, const pscwin_layer_weights* wt, c
   __nv_bfloat16* qkv = reinterpret_cast<__nv_bfloat16*>(wsp(ws, P.qkv));
   float* qkv_pad = reinterpret_cast<float*>(wsp(ws, P.qkv_pad));
   __nv_bfloat16* O = reinterpret_cast<__nv_bfloat16*>(wsp(ws, P.O));
-  rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d.ln_eps, 0, u, s);
-  if (rc) return status_from(rc);
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = (int)T;
@@ -785,7 +820,7 @@ int pscwin_ms_forward(const pscwin_ms_desc* m, const pscwin_layer_weights* wt, c
     a.seg_HW[i] = g.H[i] * g.W[i];
     a.seg_W[i] = g.W[i];
   }
-  rc = launch_gemm_bf16(u, wt->w_qkv, a, s);
+  rc = ln1_qkv(wt, d.ln_eps, x, a, u, wsp(ws, P.fold), reinterpret_cast<float2*>(wsp(ws, P.stats)), T, s);
   if (rc) return status_from(rc);
   if (learn_pad) {
     rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, qkv_pad, s);
@@ -876,6 +911,7 @@ pscwin_layer_desc sub_desc(const pscwin_layer_desc* d, int rows, int sy) {
 struct BandWs {
   size_t u, qkv, qkv_pad, O, pad_tab, h, xz, g, x1, hist_send, hist_recv, rec_send, rec_recv, scan, total;
   size_t xzp, gs;  // window-major scan order: xz rows gathered into scan order, gated output in scan order
+  size_t stats, fold;  // folded LN1 -> QKV: row statistics [T] float2, W' | s | c
   size_t row_bytes_qkv;
   int D, N, R;
 };
@@ -893,6 +929,8 @@ BandWs plan_band(const pscwin_layer_desc* d, const pscwin_band* b, const BandGeo
   };
   w.row_bytes_qkv = Wd * 3 * C * 2;
   w.u = take(T * C * 2);
+  w.stats = take(T * sizeof(float2));
+  w.fold = take(fold_bytes(3 * C, C));
   w.qkv = take(Te * 3 * C * 2);
   w.qkv_pad = take(3 * C * 4);
   w.O = take(Te * C * 2);
@@ -1089,8 +1127,6 @@ int pscwin_band_attn_begin(const pscwin_layer_desc* d, const pscwin_band* b, con
   const int C = d->C;
   const void* x = d->cycle_scan ? wsp(ws, w.x1) : x_band;
   void* u = wsp(ws, w.u);
-  rc = launch_layer_norm(x, T, C, (const float*)wt->ln1_g, (const float*)wt->ln1_b, d->ln_eps, 0, u, s);
-  if (rc) return PSCWIN_ERR_CUDA;
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = (int)T;
@@ -1109,7 +1145,9 @@ int pscwin_band_attn_begin(const pscwin_layer_desc* d, const pscwin_band* b, con
   a.C = C;
   a.d_head = C / d->heads;
   a.tok0 = g.r0 * d->W;  // RoPE at global grid rows
-  if (launch_gemm_bf16(u, wt->w_qkv, a, s)) return PSCWIN_ERR_CUDA;
+  if (ln1_qkv(wt, d->ln_eps, x, a, u, wsp(ws, w.fold), reinterpret_cast<float2*>(wsp(ws, w.stats)),
+              (long long)d->B * d->H * d->W, s))
+    return PSCWIN_ERR_CUDA;
   if (shifted && d->pad_mode == PSCWIN_PAD_LEARNABLE) {
     rc = launch_pad_qkv(wt->pad, wt->w_qkv, (const float*)wt->b_qkv, C, 0, reinterpret_cast<float*>(wsp(ws, w.qkv_pad)),
                         s);

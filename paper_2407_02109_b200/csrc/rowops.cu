@@ -296,12 +296,15 @@ int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C
 //   ln_fold_kernel:   W' (bf16), s (from the rounded W' so x W'^T - mu s vanishes for a constant row) and c, from
 //                     the weights alone (weight-only work: it runs on the side stream, off the critical path).
 // ---------------------------------------------------------------------------------------------------------------
+// Rows are visited last-first (rev): x was just written first-to-last by the previous GEMM, so its last rows are the
+// L2-resident ones, and the projection that follows reads x first-to-last, i.e. the rows this kernel touched last.
 __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long rows, int C, float eps,
-                                 float2* __restrict__ stats) {
+                                 float2* __restrict__ stats, int rev) {
   pdl_trigger();
   pdl_wait();
-  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
+  const long long wg = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wg >= rows) return;
+  const long long row = rev ? rows - 1 - wg : wg;
   const int lane = threadIdx.x & 31;
   const int nvec = C / 8;
   const uint4* src = reinterpret_cast<const uint4*>(x + row * C);
@@ -309,7 +312,7 @@ __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long 
 #pragma unroll
   for (int k = 0; k < 8; ++k) {  // all loads in flight before any arithmetic
     const int i = lane + 32 * k;
-    if (i < nvec) v[k] = __ldcs(src + i);
+    if (i < nvec) v[k] = src[i];  // (normal caching: the projection re-reads x right after)
   }
   float sum = 0.f;
 #pragma unroll
@@ -388,8 +391,9 @@ int launch_row_stats(const void* x, long long rows, int C, float eps, float2* st
   if (rows == 0) return 0;
   if (C % 8 || C > 2048) return -1;
   PSCWIN_PROF("row_stats", stream);
+  static const int rev = env_knob("PSCWIN_LN_REV", 1);
   launch_k(row_stats_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C,
-           eps, stats);
+           eps, stats, rev);
   return (int)cudaGetLastError();
 }
 

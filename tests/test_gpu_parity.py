@@ -245,3 +245,59 @@ def test_layer_forward_unit_residual(pl, cfg):
     ref = oracle.pscwin_layer(x, w, cfg)
     assert rel_err(got, ref) < BF16_TOL
     assert layer_gate(got, x, ref, n_residual(cfg)) < 1.0
+
+
+_MC_CHILD = r'''
+import sys
+import numpy as np
+import torch
+import paper_2407_02109_b200 as pl
+g = torch.Generator(device="cuda").manual_seed(11)
+outs = []
+for M, K, N, bias, resid in [(4096, 768, 2304, True, False), (4173, 768, 768, True, True), (1536, 1536, 768, False, True),
+                             (1100, 768, 320, True, True), (2048, 768, 3072, False, False)]:
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda", generator=g) if bias else None
+    r = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16) if resid else None
+    outs.append(pl.linear(A, W, bias=b, residual=r).float().cpu().numpy())
+np.savez(sys.argv[1], *outs)
+'''
+
+
+def test_gemm_b_multicast_variant_bit_identical(pl, tmp_path):
+    # A/B variant PSCWIN_GEMM_MC=2 (B k-blocks multicast across two CTA pairs of a 4-CTA cluster; measured slower and
+    # off by default) computes every output with the same MMAs in the same order: bit-identical to the default,
+    # including ragged row super-tiles (4173, 1100 rows) and several column tiles
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "child.py"
+    script.write_text(_MC_CHILD)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for mc in ("1", "2"):
+        out = tmp_path / f"mc{mc}.npz"
+        env = dict(os.environ, PSCWIN_GEMM_MC=mc, PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+        subprocess.run([sys.executable, str(script), str(out)], env=env, check=True, timeout=600)
+        res[mc] = np.load(out)
+    for k in res["1"].files:
+        assert np.array_equal(res["1"][k], res["2"][k]), k
+
+
+def test_ln_fold_forced_on_small_layers(tmp_path):
+    # LN1 -> QKV folding (default for images of >= 16384 tokens, PSCWIN_LN_FOLD_MIN_T) forced onto the small parity
+    # cases: the layer tests against the oracle, band == whole-image bit-identity, the single-scale multi-scale layer
+    # == the layer, and the full-size sampled cases run it by default (4096^2, 2048^2 B = 8)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PSCWIN_LN_FOLD_MIN_T="0")
+    sel = ["tests/test_gpu_parity.py::test_layer_forward", "tests/test_gpu_scan.py::test_cycle_scan_layer_forward",
+           "tests/test_gpu_bands.py::test_bands_equal_whole_image", "tests/test_gpu_bands.py::test_bands_overlap_schedule_equals_whole_image",
+           "tests/test_gpu_bands.py::test_dist_forward_nccl_world1",
+           "tests/test_gpu_ms.py::test_ms_single_scale_equals_layer_forward", "tests/test_gpu_ms.py::test_ms_layer"]
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider", *sel],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
