@@ -384,7 +384,17 @@ AuxStream* aux_stream(int slot) {
   }
   AuxStream& a = tab[dev][slot];
   if (!a.ok) {
-    if (!a.s && cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) a.s = nullptr;
+    // PSCWIN_AUX_PRIO=1 (A/B knob) gives the side stream (short weight-only kernels a main-stream kernel waits for:
+    // LayerNorm weight fold, pad token projection / tables) the highest priority. Measured at 4096^2: the side kernels'
+    // event times drop (weight fold 32 -> 11 us, pad tables 118 -> 24 us) but the step does not change beyond the
+    // run-to-run spread (15.02 / 15.01 vs 14.87 / 15.07 ms, profiles/r02/aux_prio_r02aa.log): off by default.
+    static const int prio_on = env_knob("PSCWIN_AUX_PRIO", 0);
+    int lo = 0, hi = 0;
+    if (prio_on && cudaDeviceGetStreamPriorityRange(&lo, &hi) == cudaSuccess) {
+      if (!a.s && cudaStreamCreateWithPriority(&a.s, cudaStreamNonBlocking, hi) != cudaSuccess) a.s = nullptr;
+    } else if (!a.s && cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) {
+      a.s = nullptr;
+    }
     if (!a.fork && cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) a.fork = nullptr;
     if (!a.join && cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming) != cudaSuccess) a.join = nullptr;
     bool evs = true;

@@ -298,6 +298,7 @@ int launch_pad_qkv(const void* pad, const void* w_qkv, const float* b_qkv, int C
 // ---------------------------------------------------------------------------------------------------------------
 // Rows are visited last-first (rev): x was just written first-to-last by the previous GEMM, so its last rows are the
 // L2-resident ones, and the projection that follows reads x first-to-last, i.e. the rows this kernel touched last.
+template <int NV>  // 16-byte vectors per lane: ceil(C / 256)
 __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long rows, int C, float eps,
                                  float2* __restrict__ stats, int rev) {
   pdl_trigger();
@@ -308,15 +309,15 @@ __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long 
   const int lane = threadIdx.x & 31;
   const int nvec = C / 8;
   const uint4* src = reinterpret_cast<const uint4*>(x + row * C);
-  uint4 v[8];
+  uint4 v[NV];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {  // all loads in flight before any arithmetic
+  for (int k = 0; k < NV; ++k) {  // all loads in flight before any arithmetic
     const int i = lane + 32 * k;
     if (i < nvec) v[k] = src[i];  // (normal caching: the projection re-reads x right after)
   }
   float sum = 0.f;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < NV; ++k) {
     if (lane + 32 * k < nvec) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
 #pragma unroll
@@ -328,7 +329,7 @@ __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long 
   const float mean = sum / C;
   float sq = 0.f;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < NV; ++k) {
     if (lane + 32 * k < nvec) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
 #pragma unroll
@@ -392,8 +393,16 @@ int launch_row_stats(const void* x, long long rows, int C, float eps, float2* st
   if (C % 8 || C > 2048) return -1;
   PSCWIN_PROF("row_stats", stream);
   static const int rev = env_knob("PSCWIN_LN_REV", 1);
-  launch_k(row_stats_kernel, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C,
-           eps, stats, rev);
+  const int nv = (C / 8 + 31) / 32;
+  auto go = [&](auto kern) {
+    launch_k(kern, dim3((unsigned)((rows + 7) / 8)), dim3(256), 0, stream, (const __nv_bfloat16*)x, rows, C, eps, stats,
+             rev);
+  };
+  if (nv <= 1) go(row_stats_kernel<1>);
+  else if (nv == 2) go(row_stats_kernel<2>);
+  else if (nv == 3) go(row_stats_kernel<3>);
+  else if (nv == 4) go(row_stats_kernel<4>);
+  else go(row_stats_kernel<8>);
   return (int)cudaGetLastError();
 }
 
