@@ -807,8 +807,14 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
         return ((tiles + slots - 1) / slots) * (bn + 32);
       };
       p.BN = cost(256) <= cost(128) ? 256 : 128;
-      static const int bn_knob = env_knob("PSCWIN_GEMM_BN", 0);  // tuning knob for the multi-tile case: 128 or 256
-      if (bn_knob == 128 || bn_knob == 256) p.BN = bn_knob;
+      // 192-column tiles when they quantise better (N = 768: 4 tiles of 192 over the 74 pair slots at 4096^2 fill
+      // 13.8 of 14 waves against 10.4 of 11 with 256). PSCWIN_GEMM_BN192=1 (A/B knob) enables the candidate; off:
+      // the out-proj gains 2 us per launch but the 4096^2 step measured 0.13 ms SLOWER in alternating runs
+      // (14.94 / 14.96 vs 14.81 / 14.82 ms, profiles/r02/gemm_bn192_r02ab.log)
+      static const int bn192 = env_knob("PSCWIN_GEMM_BN192", 0);
+      if (bn192 && p.N % 192 == 0 && cost(192) < cost(p.BN)) p.BN = 192;
+      static const int bn_knob = env_knob("PSCWIN_GEMM_BN", 0);  // tuning knob for the multi-tile case: 128/192/256
+      if (bn_knob == 128 || bn_knob == 192 || bn_knob == 256) p.BN = bn_knob;
     }
   }
   if (pair && (p.BN % 16)) return -2;
