@@ -315,30 +315,35 @@ __global__ void row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long 
     const int i = lane + 32 * k;
     if (i < nvec) v[k] = src[i];  // (normal caching: the projection re-reads x right after)
   }
-  float sum = 0.f;
+  // packed fp32x2 arithmetic (ncu r02ac: the scalar form was issue-bound, 82 % issue): FADD2 sums, FADD2 centring,
+  // FFMA2 squares
+  float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     if (lane + 32 * k < nvec) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) sum += bf16_lo(w[j]) + bf16_hi(w[j]);
+      for (int j = 0; j < 4; ++j) s2 = __fadd2_rn(s2, make_float2(bf16_lo(w[j]), bf16_hi(w[j])));
     }
   }
+  float sum = s2.x + s2.y;
 #pragma unroll
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   const float mean = sum / C;
-  float sq = 0.f;
+  const float2 nm = make_float2(-mean, -mean);
+  float2 q2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     if (lane + 32 * k < nvec) {
       const uint32_t* w = reinterpret_cast<const uint32_t*>(&v[k]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float a = bf16_lo(w[j]) - mean, b = bf16_hi(w[j]) - mean;
-        sq = fmaf(a, a, fmaf(b, b, sq));
+        const float2 dv = __fadd2_rn(make_float2(bf16_lo(w[j]), bf16_hi(w[j])), nm);
+        q2 = __ffma2_rn(dv, dv, q2);
       }
     }
   }
+  float sq = q2.x + q2.y;
 #pragma unroll
   for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
   if (lane == 0) stats[row] = make_float2(mean, rsqrtf(sq / C + eps));
