@@ -40,7 +40,10 @@ typedef enum {
   PSCWIN_ERR_ALIGN = 3,       /* pointer not 16-byte aligned */
   PSCWIN_ERR_WORKSPACE = 4,   /* workspace missing or too small */
   PSCWIN_ERR_CUDA = 5,        /* CUDA launch / driver error */
-  PSCWIN_ERR_UNSUPPORTED = 6  /* valid per the paper but not implemented on this path (e.g. d_head 128) */
+  PSCWIN_ERR_UNSUPPORTED = 6, /* valid per the paper but not implemented on this path (e.g. d_head 128) */
+  PSCWIN_ERR_NCCL = 7,        /* an NCCL call failed, an asynchronous communicator error is pending, or the
+                                 communicator was aborted (pscwin_nccl_comm_check / _abort) */
+  PSCWIN_ERR_TIMEOUT = 8      /* pscwin_nccl_wait: the stream did not drain within the deadline (comm aborted) */
 } pscwin_status;
 
 typedef enum { PSCWIN_BF16 = 0, PSCWIN_F32 = 1 } pscwin_dtype;
@@ -308,11 +311,23 @@ int pscwin_band_out_proj(const pscwin_layer_desc* global_desc, const pscwin_band
  * and the out-proj (SURVEY §8(e) overlap). comm_stream NULL: everything on `stream`. Both streams must be usable
  * by the caller's CUDA graph capture (the call is capturable: the fork / join are event edges). Every rank of the
  * communicator must call it for the same layer. x_band, x_band_out [rows, W, C] bf16 (no alias). Workspace:
- * pscwin_dist_workspace_bytes (= pscwin_band_workspace_bytes). Errors: as the band phases; ERR_CUDA for an NCCL
- * failure. */
+ * pscwin_dist_workspace_bytes (= pscwin_band_workspace_bytes). Errors: as the band phases; PSCWIN_ERR_NCCL for an
+ * NCCL call that fails, or when the communicator already carries an asynchronous error (checked on entry). */
 int pscwin_nccl_get_unique_id(void* id_out /* host, 128 bytes */);
 int pscwin_nccl_comm_init(const void* id /* host, 128 bytes */, int32_t world, int32_t rank, void** comm_out);
 int pscwin_nccl_comm_destroy(void* comm);  /* after every CUDA graph holding its operations is destroyed */
+/* Failure detection for the multi-GPU path: a rank that dies or stalls leaves its peers' NCCL kernels
+ * spinning. pscwin_nccl_comm_check returns PSCWIN_ERR_NCCL if NCCL reports an asynchronous error on `comm`
+ * (ncclCommGetAsyncError; e.g. a remote failure or a previous abort), else PSCWIN_OK; host only, never blocks.
+ * pscwin_nccl_comm_abort aborts every outstanding operation on `comm` (ncclCommAbort; the communicator is freed and
+ * must not be used again, its stream's pending work completes with the operations cancelled).
+ * pscwin_nccl_wait polls `stream` (cudaStreamQuery) and `comm` (async error) every ~100 us until the stream has
+ * drained (PSCWIN_OK), an async error appears (the comm is aborted, PSCWIN_ERR_NCCL) or timeout_ms passes (the comm
+ * is aborted, PSCWIN_ERR_TIMEOUT); timeout_ms <= 0 waits without a deadline. A CUDA error on the stream gives
+ * PSCWIN_ERR_CUDA. After an abort the caller re-creates the communicator (pscwin_nccl_comm_init) to go on. */
+int pscwin_nccl_comm_check(void* comm);
+int pscwin_nccl_comm_abort(void* comm);
+int pscwin_nccl_wait(void* comm, void* stream, int64_t timeout_ms);
 size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* global_desc, int32_t row_begin, int32_t row_end,
                                    int32_t rank, int32_t world);
 int pscwin_dist_forward(const pscwin_layer_desc* global_desc, const pscwin_layer_weights* wts, const void* x_band,

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpscwin.so")
 
-OK, ERR_SHAPE, ERR_CONTRACT, ERR_ALIGN, ERR_WORKSPACE, ERR_CUDA, ERR_UNSUPPORTED = range(7)
+OK, ERR_SHAPE, ERR_CONTRACT, ERR_ALIGN, ERR_WORKSPACE, ERR_CUDA, ERR_UNSUPPORTED, ERR_NCCL, ERR_TIMEOUT = range(9)
 BF16, F32 = 0, 1
 PAD_LEARNABLE, PAD_MASKED = 0, 1
 CS_NONE, CS_SINGLE_SCALE, CS_MULTI_SCALE = 0, 1, 2
@@ -34,6 +34,7 @@ EXPORTS = [
     "pscwin_ms_window_count", "pscwin_ms_index_map", "pscwin_ms_workspace_bytes", "pscwin_ms_forward",
     "pscwin_patch_embed_workspace_bytes", "pscwin_patch_embed", "pscwin_resize_bilinear", "pscwin_neck_workspace_bytes",
     "pscwin_neck", "pscwin_nccl_get_unique_id", "pscwin_nccl_comm_init", "pscwin_nccl_comm_destroy",
+    "pscwin_nccl_comm_check", "pscwin_nccl_comm_abort", "pscwin_nccl_wait",
     "pscwin_dist_workspace_bytes", "pscwin_dist_forward",
 ]
 
@@ -202,6 +203,9 @@ def lib() -> ctypes.CDLL:
         "pscwin_nccl_get_unique_id": ([vp], ctypes.c_int),
         "pscwin_nccl_comm_init": ([vp, i32, i32, ctypes.POINTER(vp)], ctypes.c_int),
         "pscwin_nccl_comm_destroy": ([vp], ctypes.c_int),
+        "pscwin_nccl_comm_check": ([vp], ctypes.c_int),
+        "pscwin_nccl_comm_abort": ([vp], ctypes.c_int),
+        "pscwin_nccl_wait": ([vp, vp, ctypes.c_int64], ctypes.c_int),
         "pscwin_dist_workspace_bytes": ([ctypes.POINTER(LayerDesc), i32, i32, i32, i32], sz),
         "pscwin_dist_forward": ([ctypes.POINTER(LayerDesc), ctypes.POINTER(LayerWeights), vp, vp, i32, i32, vp, vp, sz,
                                  vp, vp], ctypes.c_int),

@@ -9,7 +9,7 @@ from typing import Dict, List
 
 import torch
 
-from ._lib import BandDesc, BandIO, LayerDesc, LayerWeights, check, lib
+from ._lib import ERR_NCCL, ERR_TIMEOUT, BandDesc, BandIO, LayerDesc, LayerWeights, check, lib
 from .api import _ptr, _stream
 from .dist import band_rows
 
@@ -174,6 +174,27 @@ class NcclComm:
         if self.ptr:
             lib().pscwin_nccl_comm_destroy(self.ptr)
             self.ptr = ctypes.c_void_p()
+
+    def check(self) -> None:
+        """Raise PscwinError(ERR_NCCL) if NCCL reports an asynchronous error on this communicator."""
+        check(lib().pscwin_nccl_comm_check(self.ptr), "nccl_comm_check")
+
+    def abort(self) -> None:
+        """ncclCommAbort: cancel every outstanding operation; the communicator cannot be used again."""
+        if self.ptr:
+            lib().pscwin_nccl_comm_abort(self.ptr)
+            self.ptr = ctypes.c_void_p()
+
+    def wait(self, stream=None, timeout_s: float = 0.0) -> None:
+        """Wait for `stream` (default: torch's current stream) to drain while watching the communicator: on an
+        asynchronous NCCL error or after timeout_s (> 0) seconds the communicator is aborted and PscwinError
+        (ERR_NCCL / ERR_TIMEOUT) raised -- a stalled or failed peer surfaces as an error instead of a hang."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = lib().pscwin_nccl_wait(self.ptr, s.cuda_stream, int(timeout_s * 1000))
+        if rc in (ERR_NCCL, ERR_TIMEOUT):
+            self.ptr = ctypes.c_void_p()  # aborted inside the library
+        check(rc, "nccl_wait")
 
 
 class DistLayer:

@@ -423,6 +423,8 @@ const char* pscwin_status_string(int st) {
     case PSCWIN_ERR_WORKSPACE: return "workspace too small";
     case PSCWIN_ERR_CUDA: return "CUDA error";
     case PSCWIN_ERR_UNSUPPORTED: return "unsupported on this path";
+    case PSCWIN_ERR_NCCL: return "NCCL error (failed call, asynchronous communicator error or aborted communicator)";
+    case PSCWIN_ERR_TIMEOUT: return "timed out waiting for the stream (communicator aborted)";
     default: return "unknown status";
   }
 }

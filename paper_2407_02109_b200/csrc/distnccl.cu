@@ -7,12 +7,15 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <chrono>
+#include <thread>
+
 #include "../../include/pscwin.h"
 #include "pscwin_internal.h"
 
 namespace {
 inline uint8_t* at(void* ws, uint64_t off) { return reinterpret_cast<uint8_t*>(ws) + off; }
-inline int nccl_ok(ncclResult_t r) { return r == ncclSuccess ? PSCWIN_OK : PSCWIN_ERR_CUDA; }
+inline int nccl_ok(ncclResult_t r) { return r == ncclSuccess ? PSCWIN_OK : PSCWIN_ERR_NCCL; }
 }  // namespace
 
 extern "C" {
@@ -20,7 +23,7 @@ extern "C" {
 int pscwin_nccl_get_unique_id(void* id_out) {
   if (!id_out) return PSCWIN_ERR_SHAPE;
   ncclUniqueId id;
-  if (ncclGetUniqueId(&id) != ncclSuccess) return PSCWIN_ERR_CUDA;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return PSCWIN_ERR_NCCL;
   memcpy(id_out, &id, sizeof(id));
   return PSCWIN_OK;
 }
@@ -30,7 +33,7 @@ int pscwin_nccl_comm_init(const void* id_in, int32_t world, int32_t rank, void**
   ncclUniqueId id;
   memcpy(&id, id_in, sizeof(id));
   ncclComm_t c = nullptr;
-  if (ncclCommInitRank(&c, world, id, rank) != ncclSuccess) return PSCWIN_ERR_CUDA;
+  if (ncclCommInitRank(&c, world, id, rank) != ncclSuccess) return PSCWIN_ERR_NCCL;
   *comm_out = c;
   return PSCWIN_OK;
 }
@@ -38,6 +41,38 @@ int pscwin_nccl_comm_init(const void* id_in, int32_t world, int32_t rank, void**
 int pscwin_nccl_comm_destroy(void* comm) {
   if (!comm) return PSCWIN_OK;
   return nccl_ok(ncclCommDestroy(reinterpret_cast<ncclComm_t>(comm)));
+}
+
+int pscwin_nccl_comm_check(void* comm) {
+  if (!comm) return PSCWIN_ERR_SHAPE;
+  ncclResult_t async = ncclSuccess;
+  if (ncclCommGetAsyncError(reinterpret_cast<ncclComm_t>(comm), &async) != ncclSuccess) return PSCWIN_ERR_NCCL;
+  return (async == ncclSuccess || async == ncclInProgress) ? PSCWIN_OK : PSCWIN_ERR_NCCL;
+}
+
+int pscwin_nccl_comm_abort(void* comm) {
+  if (!comm) return PSCWIN_ERR_SHAPE;
+  return nccl_ok(ncclCommAbort(reinterpret_cast<ncclComm_t>(comm)));
+}
+
+int pscwin_nccl_wait(void* comm, void* stream, int64_t timeout_ms) {
+  if (!comm) return PSCWIN_ERR_SHAPE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return PSCWIN_OK;
+    if (q != cudaErrorNotReady) return PSCWIN_ERR_CUDA;
+    if (pscwin_nccl_comm_check(comm) != PSCWIN_OK) {
+      ncclCommAbort(reinterpret_cast<ncclComm_t>(comm));
+      return PSCWIN_ERR_NCCL;
+    }
+    if (timeout_ms > 0 && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) {
+      ncclCommAbort(reinterpret_cast<ncclComm_t>(comm));
+      return PSCWIN_ERR_TIMEOUT;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
+  }
 }
 
 size_t pscwin_dist_workspace_bytes(const pscwin_layer_desc* d, int32_t row_begin, int32_t row_end, int32_t rank,
@@ -78,9 +113,12 @@ static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weight
                            size_t ws_bytes, void* stream, void* comm_stream) {
   if (!nccl_comm) return PSCWIN_ERR_SHAPE;
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(nccl_comm);
+  // a communicator that already carries an asynchronous error (a peer failed, or it was aborted) would hang or fail
+  // inside the enqueued operations: refuse up front
+  if (pscwin_nccl_comm_check(nccl_comm) != PSCWIN_OK) return PSCWIN_ERR_NCCL;
   int rank = 0, world = 1;
   if (ncclCommUserRank(comm, &rank) != ncclSuccess || ncclCommCount(comm, &world) != ncclSuccess)
-    return PSCWIN_ERR_CUDA;
+    return PSCWIN_ERR_NCCL;
   pscwin_band b;
   b.row_begin = row_begin;
   b.row_end = row_end;
@@ -98,10 +136,10 @@ static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weight
     rc = pscwin_band_scan_begin(d, &b, wt, x_band, ws, ws_bytes, stream);
     if (rc) return rc;
     // conv history ring: rank g -> g+1 (rank 0 receives the global sequence tail from the last rank)
-    if (ncclGroupStart() != ncclSuccess) return PSCWIN_ERR_CUDA;
+    if (ncclGroupStart() != ncclSuccess) return PSCWIN_ERR_NCCL;
     ncclSend(at(ws, io.hist_send), io.hist_bytes, ncclUint8, next, comm, s);
     ncclRecv(at(ws, io.hist_recv), io.hist_bytes, ncclUint8, prev, comm, s);
-    if (ncclGroupEnd() != ncclSuccess) return PSCWIN_ERR_CUDA;
+    if (ncclGroupEnd() != ncclSuccess) return PSCWIN_ERR_NCCL;
     rc = pscwin_band_scan_mid(d, &b, wt, ws, ws_bytes, stream);
     if (rc) return rc;
     // scan records: all-gather in rank order, then every rank folds them locally (band_scan_end)
@@ -122,12 +160,12 @@ static int dist_forward_on(const pscwin_layer_desc* d, const pscwin_layer_weight
       return PSCWIN_ERR_CUDA;
   }
   if (halo) {
-    if (ncclGroupStart() != ncclSuccess) return PSCWIN_ERR_CUDA;
+    if (ncclGroupStart() != ncclSuccess) return PSCWIN_ERR_NCCL;
     if (io.send_prev_bytes) ncclSend(at(ws, io.send_prev), io.send_prev_bytes, ncclUint8, rank - 1, comm, hs);
     if (io.send_next_bytes) ncclSend(at(ws, io.send_next), io.send_next_bytes, ncclUint8, rank + 1, comm, hs);
     if (io.recv_prev_bytes) ncclRecv(at(ws, io.recv_prev), io.recv_prev_bytes, ncclUint8, rank - 1, comm, hs);
     if (io.recv_next_bytes) ncclRecv(at(ws, io.recv_next), io.recv_next_bytes, ncclUint8, rank + 1, comm, hs);
-    if (ncclGroupEnd() != ncclSuccess) return PSCWIN_ERR_CUDA;
+    if (ncclGroupEnd() != ncclSuccess) return PSCWIN_ERR_NCCL;
   }
   if (ev) {
     if (cudaEventRecord(ev->join, c) != cudaSuccess) return PSCWIN_ERR_CUDA;

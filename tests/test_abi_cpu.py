@@ -142,3 +142,9 @@ def test_ms_workspace_and_contract(pl):
     assert pl.ms_workspace_bytes(bad) == 0
     none = pl.MSDesc.make(cfg, [(64, 64)], 0, 0)                                          # nothing to run
     assert pl.ms_workspace_bytes(none) == 0
+
+
+def test_status_strings_cover_nccl_errors():
+    import paper_2407_02109_b200._lib as L
+    for st in (L.ERR_NCCL, L.ERR_TIMEOUT):
+        assert L.lib().pscwin_status_string(st).decode() != "unknown status"

@@ -154,3 +154,42 @@ def test_dist_forward_nccl_world1(pl, i):
     code = _NCCL_CASE.format(root=root, tests=os.path.join(root, "tests"), i=i)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=240)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+_NCCL_WATCHDOG = r'''
+import sys
+sys.path.insert(0, {root!r})
+import torch
+import paper_2407_02109_b200 as pl
+from paper_2407_02109_b200.bands import NcclComm
+from paper_2407_02109_b200._lib import ERR_TIMEOUT, PscwinError
+c = NcclComm(0, 1)
+c.check()                                   # no asynchronous error on a fresh communicator
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    torch.cuda._sleep(3_000_000_000)        # a stream that does not drain (~1.5 s of spinning): a stalled peer
+try:
+    c.wait(s, timeout_s=0.05)
+    raise SystemExit("no timeout")
+except PscwinError as e:
+    assert e.status == ERR_TIMEOUT, e
+assert not c.ptr                            # the watchdog aborted the communicator
+torch.cuda.synchronize()
+c2 = NcclComm(0, 1)                         # a new communicator works after the abort
+c2.check()
+c2.wait(timeout_s=10.0)
+c2.abort()
+print("ok")
+'''
+
+
+def test_nccl_watchdog_times_out_and_aborts(pl):
+    # failure detection of the multi-GPU path (SURVEY §5): pscwin_nccl_wait turns a stream that never drains into
+    # PSCWIN_ERR_TIMEOUT and aborts the communicator instead of hanging; a fresh communicator works afterwards
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _NCCL_WATCHDOG.format(root=root)], capture_output=True, text=True,
+                       timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
