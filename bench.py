@@ -120,6 +120,15 @@ def scan_chunks(c):
 
 
 # ----------------------------------------------------------------------------------------------- roofline
+def _ln_fold(T: int):
+    """Which LayerNorms the library folds into the next projection for an image of T tokens (abi.cu ln_fold_mode):
+    (LN1 -> QKV folded, LN_s / LN2 folded too)."""
+    mode = int(os.environ.get("PSCWIN_LN_FOLD", "2"))
+    mode = mode if mode in (0, 1) else 2
+    on = mode != 0 and T >= int(os.environ.get("PSCWIN_LN_FOLD_MIN_T", "16384"))
+    return on, on and mode == 1
+
+
 def kernel_work(label: str, metas):
     """Algorithmic work of a kernel label over ONE step (DESIGN.md §6 "algorithmic work per unit x units"),
     summed over the layers that launch it: returns (bound, amount, unit_scale, unit) or None."""
@@ -170,7 +179,16 @@ def kernel_work(label: str, metas):
             tot += 2.0 * T * Hd * C
         elif label == "layer_norm":
             bound, scale, unit = "hbm", 1e9, "GB/s"
-            tot += (a + cs + (Hd > 0)) * 4.0 * T * C    # bf16 row read + write
+            f_attn, f_all = _ln_fold(T)
+            tot += (a * (not f_attn) + (cs + (Hd > 0)) * (not f_all)) * 4.0 * T * C    # bf16 row read + write
+        elif label == "row_stats":       # folded LayerNorm: bf16 row read, (mu, rstd) written
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            f_attn, f_all = _ln_fold(T)
+            tot += (a * f_attn + (cs + (Hd > 0)) * f_all) * T * (2.0 * C + 8.0)
+        elif label == "ln_fold":         # weight fold of W_qkv (and W_in / W_fc1 when all are folded): W read, W' written
+            bound, scale, unit = "hbm", 1e9, "GB/s"
+            f_attn, f_all = _ln_fold(T)
+            tot += a * f_attn * (4.0 * 3 * C * C + 8.0 * 3 * C) + f_all * (cs * 4.0 * 2 * D * C + (Hd > 0) * 4.0 * Hd * C)
         elif label == "conv_silu":
             bound, scale, unit = "hbm", 1e9, "GB/s"
             tot += cs * 4.0 * T * D                     # xin read + v write, bf16
