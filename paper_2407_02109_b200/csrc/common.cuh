@@ -43,7 +43,21 @@ PSCWIN_DEVICE void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 PSCWIN_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// PSCWIN_MBAR_SUSPEND_NS (compile-time A/B flag, default 0 = the hardware's own limit): suspend-time hint of the
+// try_wait loops, i.e. how long a waiting thread may sleep before re-testing (the phase completing wakes it)
+#ifndef PSCWIN_MBAR_SUSPEND_NS
+#define PSCWIN_MBAR_SUSPEND_NS 0
+#endif
 PSCWIN_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if PSCWIN_MBAR_SUSPEND_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "n"(PSCWIN_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
@@ -51,6 +65,7 @@ PSCWIN_DEVICE void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // non-blocking probe of an mbarrier phase (mbarrier.test_wait): true once the phase with this parity completed
@@ -201,15 +216,7 @@ PSCWIN_DEVICE void mbar_arrive_remote(uint32_t cluster_addr) {
 // arrivals after tcgen05 fences). Everything it orders is async-proxy work (TMA, UMMA, TMEM), which the mbarrier
 // itself orders, so the default .acquire.cta semantics suffice (as CUTLASS's cluster pipelines wait); the
 // .acquire.cluster form made every successful wait invalidate L1 (CCTL.IVALL), a top stall of the pair GEMMs.
-PSCWIN_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
+PSCWIN_DEVICE void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 // TMA load into this CTA's shared memory, completing bytes on an mbarrier of either CTA of the pair
 PSCWIN_DEVICE void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t bar_cluster_addr, int c0, int c1,
                                     uint64_t hint) {
