@@ -51,6 +51,16 @@ __host__ __device__ inline size_t gemm_stage_bytes(int BN, bool pair) {
 }
 }  // namespace
 
+// four per-column values (bias, LayerNorm column sums) at columns c..c+3 read through L1 (every lane of a warp reads
+// the same addresses: broadcast), zero past N
+__device__ __forceinline__ float4 bias_l1_4(const float* v, int c, int N) {
+  if (c + 4 <= N) return __ldg(reinterpret_cast<const float4*>(v + c));
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  float* rp = reinterpret_cast<float*>(&r);
+  for (int e = 0; e < 4 && c + e < N; ++e) rp[e] = __ldg(v + c + e);
+  return r;
+}
+
 __device__ __forceinline__ void rope_pair(float& a, float& b, float c, float s) {
   float x0 = a * c - b * s;
   float x1 = a * s + b * c;
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         ln_r = st.y;
         ln_nmr = -st.x * st.y;
       }
-      if (EK != EK_F32 && p.bias) {  // (f32 tiles read the bias straight from L1: no CTA-wide barrier there)
+      if (EK != EK_F32 && p.bias && !p.bias_l1) {  // (f32 tiles / bias_l1 read the bias straight from L1)
         if (etid < BN / 4) {
           const int c = n0 + 4 * etid;
           float4 b4 = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -412,7 +422,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // tile. Each box goes TMEM -> registers (the next box's TMEM load is in flight meanwhile) -> fused op ->
         // a 2 KB SW64 staging box (this warp's own double buffer, or the residual box in place) -> one TMA store
         // by the warp's lane 0. The only CTA-wide barrier is the one per tile that publishes the staged bias.
-        if (p.bias) named_bar_sync(1, 256);
+        if (p.bias && !p.bias_l1) named_bar_sync(1, 256);
         const int nbx = p.dbg_noepi ? 0 : (BN + 31) / 32;  // (timing probe: no epilogue work at all)
         // residual from global memory (L2-warm: the producer prefetched the tile): this thread's 64 bytes of row
         // `row` per box, loaded one box ahead (the first box's before the accumulator wait). (Measured: loading all
@@ -466,8 +476,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             if (ln) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
-                const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
-                const float4 s4 = *reinterpret_cast<const float4*>(sc + cl + j);
+                const float4 b4 = p.bias_l1 ? bias_l1_4(p.bias, col0 + j, p.N) : *reinterpret_cast<const float4*>(sb + cl + j);
+                const float4 s4 = p.bias_l1 ? bias_l1_4(p.ln_colsum, col0 + j, p.N)
+                                            : *reinterpret_cast<const float4*>(sc + cl + j);
                 v[j] = fmaf(v[j], ln_r, fmaf(ln_nmr, s4.x, b4.x));
                 v[j + 1] = fmaf(v[j + 1], ln_r, fmaf(ln_nmr, s4.y, b4.y));
                 v[j + 2] = fmaf(v[j + 2], ln_r, fmaf(ln_nmr, s4.z, b4.z));
@@ -476,7 +487,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             } else {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
-                const float4 b4 = *reinterpret_cast<const float4*>(sb + cl + j);
+                const float4 b4 = p.bias_l1 ? bias_l1_4(p.bias, col0 + j, p.N) : *reinterpret_cast<const float4*>(sb + cl + j);
                 v[j] += b4.x; v[j + 1] += b4.y; v[j + 2] += b4.z; v[j + 3] += b4.w;
               }
             }
@@ -848,6 +859,13 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
     p.stages = stages;
   }
   p.pair = pair ? 1 : 0;
+  // PSCWIN_GEMM_BIAS_L1=1 (A/B knob): bf16 epilogues read the bias (and LayerNorm column sums) through L1 instead of
+  // staging them in shared memory behind a CTA-wide barrier per tile (the out-proj's second stall reason in ncu
+  // r02d). Measured much slower (QKV 200 -> 266 us, out-proj 86.7 -> 92.8 us at 4096^2, gemm_bias_l1_r02al.log):
+  // the per-box global loads cost more than one barrier per tile; off
+  static const int bias_l1 = env_knob("PSCWIN_GEMM_BIAS_L1", 0);
+  p.bias_l1 = (bias_l1 && (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0 &&
+               (reinterpret_cast<uintptr_t>(p.ln_colsum) & 15) == 0) ? 1 : 0;
   CUtensorMap tmA, tmB, tmOut, tmRes;
   const CUtensorMapDataType in_t = p.tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const int esz = p.tf32 ? 4 : 2, bke = p.tf32 ? BK / 2 : BK;

@@ -54,6 +54,7 @@ struct GemmArgs {
   // B = W' = W diag(gamma), bias = c = W beta + b; the epilogue computes rstd_m (acc - mu_m s_n) + c_n
   const float2* ln_stats;  // [M] (mu, rstd) per A row, or null (no folding)
   const float* ln_colsum;  // [N] s_n = sum_k W'[n,k]
+  int bias_l1;  // bf16 epilogue reads bias / column sums through L1 (no per-tile staging barrier; set by the launcher)
 };
 
 // host helpers (abi.cu)
