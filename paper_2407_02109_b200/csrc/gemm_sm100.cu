@@ -818,12 +818,18 @@ int launch_gemm_bf16(const void* A, const void* Bw, const GemmArgs& args_in, cud
         return ((tiles + slots - 1) / slots) * (bn + 32);
       };
       p.BN = cost(256) <= cost(128) ? 256 : 128;
-      // 192-column tiles when they quantise better (N = 768: 4 tiles of 192 over the 74 pair slots at 4096^2 fill
-      // 13.8 of 14 waves against 10.4 of 11 with 256). PSCWIN_GEMM_BN192=1 (A/B knob) enables the candidate; off:
-      // the out-proj gains 2 us per launch but the 4096^2 step measured 0.13 ms SLOWER in alternating runs
-      // (14.94 / 14.96 vs 14.81 / 14.82 ms, profiles/r02/gemm_bn192_r02ab.log)
-      static const int bn192 = env_knob("PSCWIN_GEMM_BN192", 0);
-      if (bn192 && p.N % 192 == 0 && cost(192) < cost(p.BN)) p.BN = 192;
+      // 192-column tiles when they quantise better. Unrestricted (PSCWIN_GEMM_BN192=1) they also replace 256 at
+      // 4096^2 (N = 768: 13.8 of 14 rounds against 10.4 of 11), where the out-proj gains 2 us per launch but the step
+      // measured 0.13 ms SLOWER in alternating runs (gemm_bn192_r02ab.log); PSCWIN_GEMM_BN192=0 never uses them.
+      // The default rule below takes them only without extra rounds: 1024^2 stage 0.377 -> 0.370 ms (out-proj 20.0 ->
+      // 18.1 us), 4096^2 unchanged (gemm_bn192_rule_r02ao.log).
+      // Default (PSCWIN_GEMM_BN192 unset / 2): only when 192-column tiles need no more scheduling rounds than the
+      // current width (e.g. the 1024^2 out-proj: 64 pair tiles in one round instead of 48 wider ones), never when they
+      // add rounds (4096^2)
+      static const int bn192 = env_knob("PSCWIN_GEMM_BN192", 2);
+      auto rounds = [&](int bn) { return ((long long)m_tiles * ((p.N + bn - 1) / bn) + slots - 1) / slots; };
+      if (p.N % 192 == 0 && cost(192) < cost(p.BN) && (bn192 == 1 || (bn192 == 2 && rounds(192) <= rounds(p.BN))))
+        p.BN = 192;
       static const int bn_knob = env_knob("PSCWIN_GEMM_BN", 0);  // tuning knob for the multi-tile case: 128/192/256
       if (bn_knob == 128 || bn_knob == 192 || bn_knob == 256) p.BN = bn_knob;
     }
